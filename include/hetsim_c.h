@@ -1,0 +1,164 @@
+/*
+ * hetsim-b200 C ABI.
+ *
+ * Three layers, all plain C (no C++/torch types):
+ *
+ *  1. hs_query        — JSON-in/JSON-out access to the host C++ API
+ *                       (parse_spec, derive_components, classify_edges,
+ *                       ready_components, bottom_level_ranks, setup_cq,
+ *                       run_schedule). Replaces direct calls into the
+ *                       reference's C++ library (proj/include/hetsim/ headers).
+ *
+ *  2. hs_* CUDA layer — the thin layer the C++ executor calls for every device
+ *                       action. One CUDA stream per command
+ *                       queue, events for E_Q and inter-component edges,
+ *                       copies on the copy engines, sm_100a node kernels,
+ *                       host callbacks, graph capture. This is what the
+ *                       reference's simulator (`dispatch` -> platform_sim,
+ *                       SPEC.md:342-349 / 386-440) is replaced by.
+ *
+ *  3. hs_engine       — the dispatch entry point as a whole: a DAG template
+ *                       bound to host buffers and executed on one GPU for a
+ *                       stream of instances (dynamic Alg. 1 or captured graph).
+ *
+ * Conventions: every int-returning function returns 0 on success; non-zero
+ * means failure and hs_last_error() (thread-local) holds "<Errc>: message".
+ * No C++ exception crosses this boundary.
+ */
+#ifndef HETSIM_C_H_
+#define HETSIM_C_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---------------------------------------------------------------- status */
+#define HS_OK 0
+#define HS_ERR_INVALID 1 /* bad argument / input error (exit code 2 class)  */
+#define HS_ERR_CUDA 2    /* CUDA runtime / driver failure (DeviceError)      */
+#define HS_ERR_RUNTIME 3 /* scheduling runtime error (exit code 1 class)     */
+
+const char* hs_last_error(void);
+/* hetsim::Errc ordinal of the last failure on this thread, -1 if none. */
+int hs_last_errc(void);
+const char* hs_version(void);
+
+/* ------------------------------------------------------ 1. host queries */
+/* Returns a malloc'd JSON document {"ok":true,...} or {"ok":false,"errc":..}.
+ * Never NULL. Free with hs_free_string. */
+char* hs_query(const char* request_json);
+void hs_free_string(char* s);
+
+/* ------------------------------------------------------ 2. CUDA layer  */
+typedef struct hs_ctx* hs_ctx_t;
+typedef struct hs_stream* hs_stream_t;
+typedef struct hs_event* hs_event_t;
+typedef struct hs_graph* hs_graph_t;
+
+int hs_device_count(int* count);
+int hs_ctx_create(int gpu_ordinal, hs_ctx_t* out);
+int hs_ctx_destroy(hs_ctx_t ctx);
+int hs_ctx_sync(hs_ctx_t ctx);
+
+int hs_stream_create(hs_ctx_t ctx, int priority, hs_stream_t* out);
+int hs_stream_destroy(hs_stream_t s);
+int hs_stream_sync(hs_stream_t s);
+
+int hs_event_create(hs_ctx_t ctx, int timing, hs_event_t* out); /* timing=0 for E_Q deps */
+int hs_event_destroy(hs_event_t e);
+int hs_event_record(hs_event_t e, hs_stream_t s);
+int hs_stream_wait(hs_stream_t s, hs_event_t e);
+int hs_event_sync(hs_event_t e);
+int hs_event_elapsed_ns(hs_event_t from, hs_event_t to, int64_t* ns);
+
+int hs_malloc(hs_ctx_t ctx, size_t bytes, void** out);
+int hs_free(hs_ctx_t ctx, void* p);
+int hs_host_alloc(size_t bytes, void** out); /* pinned */
+int hs_host_free(void* p);
+int hs_host_pin(void* p, size_t bytes);
+int hs_host_unpin(void* p);
+
+int hs_memcpy_h2d(hs_stream_t s, void* dst, const void* src, size_t bytes);
+int hs_memcpy_d2h(hs_stream_t s, void* dst, const void* src, size_t bytes);
+int hs_memcpy_d2d(hs_stream_t s, void* dst, const void* src, size_t bytes);
+int hs_memcpy_peer(hs_stream_t s, void* dst, int dst_gpu, const void* src, int src_gpu, size_t bytes);
+int hs_memset(hs_stream_t s, void* dst, int value, size_t bytes);
+/* Strided copy of `height` rows of `width` bytes; kind 0=H2D 1=D2H 2=D2D 3=default. */
+int hs_memcpy_2d(hs_stream_t s, void* dst, size_t dpitch, const void* src, size_t spitch, size_t width,
+                 size_t height, int kind);
+
+/* DAG node operators (kernel "name" in the spec). Argument conventions
+ * (buffer positions / var-args) are listed in DESIGN.md §4. */
+typedef enum {
+  HS_OP_GEMM = 0,      /* C[M,N] = A[M,K] B[K,N]                  */
+  HS_OP_GEMM_NT = 1,   /* C[M,N] = A[M,K] B[N,K]^T                */
+  HS_OP_GEMM_RELU = 2, /* C = max(0, A B)                         */
+  HS_OP_TRANSPOSE = 3, /* B[C,R] = A[R,C]^T                       */
+  HS_OP_SCALE = 4,     /* B = A * s                               */
+  HS_OP_SOFTMAX = 5,   /* row softmax of (A * s)                  */
+  HS_OP_ADD = 6,       /* C = A + B                               */
+  HS_OP_ADD_LN = 7,    /* Y = LayerNorm(A + B) * gamma + beta     */
+  HS_OP_CONCAT = 8,    /* Y[:, i*c:(i+1)*c] = Z_i                 */
+  HS_OP_COUNT = 9
+} hs_op;
+
+typedef enum {
+  HS_MATH_TF32X3 = 0,   /* tcgen05 kind::tf32, 3-term split: fp32-accurate (default) */
+  HS_MATH_TF32 = 1,     /* tcgen05 kind::tf32, single term (fast, ~1e-3)            */
+  HS_MATH_FP32_SIMT = 2 /* CUDA-core fp32 FMA (diagnostic)                          */
+} hs_math;
+
+#define HS_MAX_INPUTS 16
+typedef struct {
+  const void* in[HS_MAX_INPUTS]; /* input-side buffers in ascending arg position     */
+  int64_t in_stride[HS_MAX_INPUTS]; /* per-instance stride in elements (0 = shared)  */
+  int n_in;
+  void* out;                        /* first output-side buffer                      */
+  int64_t out_stride;               /* per-instance stride in elements               */
+  int64_t dims[4];                  /* op-specific sizes             */
+  float fparam[2];                  /* [0] scale s, [1] layer-norm eps               */
+} hs_op_args;
+
+int hs_op_from_name(const char* name); /* -1 if unknown */
+int hs_launch(hs_stream_t s, int op, const hs_op_args* args, int math_mode, int batch);
+
+int hs_host_callback(hs_stream_t s, void (*fn)(void*), void* user);
+int hs_capture_begin(hs_stream_t s);
+int hs_capture_end(hs_stream_t s, hs_graph_t* out);
+int hs_graph_launch(hs_graph_t g, hs_stream_t s);
+int hs_graph_destroy(hs_graph_t g);
+/* Number of node-kernel launches issued through hs_launch so far (all threads). */
+int64_t hs_launch_count(void);
+
+/* ------------------------------------------------------ 3. engine */
+typedef struct hs_engine* hs_engine_t;
+
+/* config_json: {"spec": "<spec document>", "params": {..}, "gpu": 0,
+ *   "policy": "clustering"|"eager"|"heft", "mode": "graph"|"dynamic",
+ *   "batch": B, "slots": 2, "math": "tf32x3"|"tf32"|"simt",
+ *   "cpu_devices": [..], "trace": false} */
+int hs_engine_create(const char* config_json, hs_engine_t* out);
+int hs_engine_destroy(hs_engine_t e);
+
+/* Bind the isolated input (or isolated output) buffer (kernel, pos) to memory
+ * holding `count` instances laid out `stride_bytes` apart (0 = one copy shared
+ * by every instance; such inputs are uploaded once and stay resident).
+ * on_device != 0 means `ptr` is device memory on the engine's GPU. */
+int hs_engine_bind(hs_engine_t e, int kernel, int pos, void* ptr, int64_t stride_bytes, int on_device);
+
+/* Execute `n_instances` DAG instances (instances [first, first+n) of the
+ * bound arrays). Blocks until done. elapsed_ns (optional) = device time
+ * from the first to the last command, measured with CUDA events. */
+int hs_engine_run(hs_engine_t e, int64_t first, int64_t n_instances, int64_t* elapsed_ns);
+
+/* JSON introspection: what = "plan" | "stats" | "completions" | "trace". */
+int hs_engine_info(hs_engine_t e, const char* what, char** out_json);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HETSIM_C_H_ */

@@ -1,0 +1,541 @@
+"""TEST INFRASTRUCTURE ONLY — CPU restatement of the reference's algorithm.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
+reference legs may import this module; the product never does.
+
+Pinning:
+  * L0-L2 (expr, spec model, FRONT/END/IN, edge classes, ranks) are pinned
+    against the reference's own compiled sources (oracle/_ref, built by
+    oracle/Makefile from /root/reference/proj/src) and against the golden
+    fixtures in tests/golden/ made from it (tests/golden/make_golden.py).
+  * setup_cq / scheduler have NO reference implementation (cq_builder.hpp is
+    declaration-only; scheduler is prose in SPEC.md). They are restated here
+    from SPEC.md:199-368 and PAPER.md:191-197, 253-316 and pinned by the
+    paper's worked examples (Fig. 8 golden: SPEC.md:244, 561).
+  * Node kernels: plain C in oracle/kernels.c (PAPER.md:232-241 GEMM);
+    floating-point parity is unpinned by the reference (no numerics exist
+    there) — tolerance 1e-4 normwise per north_star.
+
+Each function cites the reference file:line it follows.
+"""
+from __future__ import annotations
+
+import ctypes
+import json
+import pathlib
+from collections import deque
+from fractions import Fraction
+
+import numpy as np
+
+HERE = pathlib.Path(__file__).resolve().parent
+LIBORACLE = HERE / "liboracle.so"
+LIBREF = HERE / "_ref" / "libhetsim_ref.so"
+
+
+# ============================================================================ expr (proj/src/expr.cpp:17-151)
+
+class OracleError(Exception):
+    def __init__(self, errc, msg=""):
+        super().__init__(f"{errc}: {msg}")
+        self.errc = errc
+
+
+def eval_expr(text: str, params: dict | None) -> int:
+    """Recursive descent: sum/product/unary; exact '/' (expr.cpp:74-88); ids -> 1 when params is None."""
+    pos = 0
+    s = text
+
+    def skip():
+        nonlocal pos
+        while pos < len(s) and s[pos] in " \t\n\r\f\v":
+            pos += 1
+
+    def peek():
+        skip()
+        return s[pos] if pos < len(s) else ""
+
+    def fit(v):
+        if v > 2**63 - 1 or v < -(2**63):
+            raise OracleError("NumericOverflow")
+        return v
+
+    def total():
+        nonlocal pos
+        v = prod()
+        while True:
+            c = peek()
+            if c == "+":
+                pos += 1
+                v = fit(v + prod())
+            elif c == "-":
+                pos += 1
+                v = fit(v - prod())
+            else:
+                return v
+
+    def prod():
+        nonlocal pos
+        v = unary()
+        while True:
+            c = peek()
+            if c == "*":
+                pos += 1
+                v = fit(v * unary())
+            elif c == "/":
+                pos += 1
+                d = unary()
+                if d == 0:
+                    raise OracleError("DivisionByZero")
+                q = abs(v) // abs(d)
+                if abs(v) % abs(d):
+                    raise OracleError("InexactDivision")
+                v = q if (v >= 0) == (d > 0) else -q
+            else:
+                return v
+
+    def unary():
+        nonlocal pos
+        c = peek()
+        if c == "(":
+            pos += 1
+            v = total()
+            if peek() != ")":
+                raise OracleError("MalformedSpec", "missing ')'")
+            pos += 1
+            return v
+        if c == "-":
+            pos += 1
+            return fit(-unary())
+        if c.isdigit() and c.isascii():
+            start = pos
+            while pos < len(s) and s[pos].isascii() and s[pos].isdigit():
+                pos += 1
+                if pos - start > 18:
+                    raise OracleError("NumericOverflow")
+            return int(s[start:pos])
+        if c and c.isascii() and (c.isalpha() or c == "_"):
+            start = pos
+            while pos < len(s) and s[pos].isascii() and (s[pos].isalnum() or s[pos] == "_"):
+                pos += 1
+            name = s[start:pos]
+            if params is None:
+                return 1
+            if name not in params:
+                raise OracleError("UnboundParameter", name)
+            return params[name]
+        raise OracleError("MalformedSpec", "unexpected character")
+
+    v = total()
+    skip()
+    if pos != len(s):
+        raise OracleError("MalformedSpec", "trailing input")
+    return v
+
+
+# ============================================================================ spec helpers
+
+class Spec:
+    """Parsed view of a (valid) spec document; validation is the product's job."""
+
+    def __init__(self, text: str, params: dict):
+        self.doc = json.loads(text)
+        self.params = dict(params)
+        self.kernels = {k["id"]: k for k in self.doc["kernels"]}
+        self.edges = [tuple(e) for e in self.doc.get("depends", [])]
+        self.tc = [list(c) for c in self.doc.get("tc", [])]
+        self.cq = {c["device"]: c["queues"] for c in self.doc.get("cq", [])}
+        self.comp_of = {k: i for i, comp in enumerate(self.tc) for k in comp}
+
+    def buffers(self, kid, side):
+        k = self.kernels[kid]
+        lists = (["inputBuffers", "ioBuffers"] if side == "in" else ["outputBuffers", "ioBuffers"])
+        out = [b for name in lists for b in k.get(name, [])]
+        return sorted(out, key=lambda b: b["pos"])
+
+    def bytes(self, kid, pos):
+        for name in ("inputBuffers", "outputBuffers", "ioBuffers"):
+            for b in self.kernels[kid].get(name, []):
+                if b["pos"] == pos:
+                    w = 8 if b["type"] in ("float64", "int64") else 4
+                    return eval_expr(str(b["size"]), self.params) * w
+        raise KeyError((kid, pos))
+
+    def topo_order(self):
+        """Kahn, ascending-id frontier (spec_model.cpp:125-151)."""
+        succ = {k: set() for k in self.kernels}
+        for s, _, d, _ in self.edges:
+            succ[s].add(d)
+        indeg = {k: 0 for k in self.kernels}
+        for s in succ:
+            for d in succ[s]:
+                indeg[d] += 1
+        ready = sorted(k for k, v in indeg.items() if v == 0)
+        order = []
+        while ready:
+            k = ready.pop(0)
+            order.append(k)
+            for d in sorted(succ[k]):
+                indeg[d] -= 1
+                if indeg[d] == 0:
+                    ready.append(d)
+                    ready.sort()
+        return order
+
+
+# ============================================================================ graph analysis (graph_analysis.cpp:18-133)
+
+def components(spec: Spec):
+    comps = []
+    for i, ks in enumerate(spec.tc):
+        members = set(ks)
+        front = {d for s, _, d, _ in spec.edges if d in members and s not in members}   # Def. 1, :18-27
+        end = {s for s, _, d, _ in spec.edges if s in members and d not in members}     # Def. 2, :29-38
+        comps.append({"id": i, "kernels": sorted(ks), "front": front, "end": end,
+                      "interior": set(ks) - front - end})                                # Def. 3, :40-48
+    return comps
+
+
+def edge_kinds(spec: Spec):
+    return ["intra" if spec.comp_of[s] == spec.comp_of[d] else "inter" for s, _, d, _ in spec.edges]  # :67-72
+
+
+def write_class(spec, kid, pos):  # graph_analysis.cpp:74-78: dependent iff the input has a producer
+    return "dependent" if any(d == kid and dp == pos for _, _, d, dp in spec.edges) else "isolated"
+
+
+def read_class(spec, kid, pos):  # :79-83: dependent iff the output has a consumer
+    return "dependent" if any(s == kid and sp == pos for s, sp, _, _ in spec.edges) else "isolated"
+
+
+def ranks(spec: Spec, times: dict):
+    """bottom_level_ranks (graph_analysis.cpp:112-123): t(k) + max(0, max succ rank)."""
+    succ = {k: set() for k in spec.kernels}
+    for s, _, d, _ in spec.edges:
+        succ[s].add(d)
+    r = {}
+    for k in reversed(spec.topo_order()):
+        r[k] = times[k] + max([Fraction(0)] + [r[s] for s in succ[k]])
+    return r
+
+
+def component_rank(comp, r):  # graph_analysis.cpp:125-133
+    src = comp["front"] if comp["front"] else comp["kernels"]
+    return max([Fraction(0)] + [r[k] for k in src])
+
+
+def frac_str(f: Fraction) -> str:
+    return str(f.numerator) if f.denominator == 1 else f"{f.numerator}/{f.denominator}"
+
+
+# ============================================================================ setup_cq
+
+def setup_cq(spec: Spec, comp_id: int, device: int, device_type: str, r: int) -> dict:
+    comp = components(spec)[comp_id]
+    kinds = edge_kinds(spec)
+    members = set(comp["kernels"])
+    # processing order: Kahn over the induced subgraph, smallest id first (cq_builder.hpp:72-74)
+    succ = {k: set() for k in members}
+    indeg = {k: 0 for k in members}
+    for s, _, d, _ in spec.edges:
+        if s in members and d in members and s != d and d not in succ[s]:
+            succ[s].add(d)
+            indeg[d] += 1
+    ready = sorted(k for k in members if indeg[k] == 0)
+    order = []
+    while ready:
+        k = ready.pop(0)
+        order.append(k)
+        for d in succ[k]:
+            indeg[d] -= 1
+            if indeg[d] == 0:
+                ready.append(d)
+        ready.sort()
+    queues = [[] for _ in range(r)]
+    cmds = []  # event-indexed
+    count = {"write": 0, "ndrange": 0, "read": 0}
+    prefix = {"write": "w", "ndrange": "e", "read": "r"}
+
+    def push(q, kind, kernel, buf=None, dependent=False, edge=-1):
+        count[kind] += 1
+        ev = len(cmds)
+        c = {"event": ev, "label": f"{prefix[kind]}{count[kind]}", "kind": kind, "kernel": kernel, "queue": q}
+        if buf is not None:
+            c.update({"buffer": list(buf), "dependent": int(dependent), "bytes": spec.bytes(*buf), "edge": edge})
+        cmds.append(c)
+        queues[q].append(ev)
+        return ev
+
+    nd_event = {}
+    deps = set()
+    for i, k in enumerate(order):
+        q = i % r
+        # enq: (a) dependent writes for FRONT kernels on inter in-edges
+        if k in comp["front"]:
+            for b in spec.buffers(k, "in"):
+                for ei, (s, sp, d, dp) in enumerate(spec.edges):
+                    if d == k and dp == b["pos"] and kinds[ei] == "inter":
+                        push(q, "write", k, (k, b["pos"]), True, ei)
+        # (b) isolated writes
+        for b in spec.buffers(k, "in"):
+            if write_class(spec, k, b["pos"]) == "isolated":
+                push(q, "write", k, (k, b["pos"]))
+        # (c) ndrange
+        nd_event[k] = push(q, "ndrange", k)
+        # (d) isolated reads
+        for b in spec.buffers(k, "out"):
+            if read_class(spec, k, b["pos"]) == "isolated":
+                push(q, "read", k, (k, b["pos"]))
+        # (e) dependent reads for END kernels, one per inter out-edge
+        if k in comp["end"]:
+            for b in spec.buffers(k, "out"):
+                for ei, (s, sp, d, dp) in enumerate(spec.edges):
+                    if s == k and sp == b["pos"] and kinds[ei] == "inter":
+                        push(q, "read", k, (k, b["pos"]), True, ei)
+        # set_dependencies: cross-queue pairs only
+        for c in cmds:
+            if c["kernel"] != k:
+                continue
+            if c["kind"] == "write" and c["queue"] != q:
+                deps.add((c["event"], nd_event[k]))
+            if c["kind"] == "read" and c["queue"] != q:
+                deps.add((nd_event[k], c["event"]))
+        for ei, (s, sp, d, dp) in enumerate(spec.edges):
+            if kinds[ei] != "intra":
+                continue
+            if d == k and s != k and s in nd_event and cmds[nd_event[s]]["queue"] != q:
+                deps.add((nd_event[s], nd_event[k]))
+            if s == k and d != k and d in nd_event and cmds[nd_event[d]]["queue"] != q:
+                deps.add((nd_event[k], nd_event[d]))
+    # set_callbacks
+    end_marks = set()
+    for c in cmds:
+        if c["kernel"] in comp["end"]:
+            if device_type == "gpu" and c["kind"] == "read" and c.get("dependent"):
+                end_marks.add(c["event"])
+            if device_type == "cpu" and c["kind"] == "ndrange":
+                end_marks.add(c["event"])
+    callbacks = set(end_marks) | {q[-1] for q in queues if q}
+    lab = lambda e: cmds[e]["label"]  # noqa: E731
+    return {
+        "component": comp_id, "device": device,
+        "queues": [[lab(e) for e in q] for q in queues],
+        "deps": [[lab(a), lab(b)] for a, b in sorted(deps)],
+        "callbacks": [lab(e) for e in sorted(callbacks)],
+        "end_marks": [lab(e) for e in sorted(end_marks)],
+        "commands": cmds,
+        "_terminal": [q[-1] for q in queues if q],
+        "_callbacks": sorted(callbacks),
+        "_end_marks": sorted(end_marks),
+    }
+
+
+# ============================================================================ scheduler
+
+def schedule(spec: Spec, policy="clustering", times=None, cpu_devices=(), replay=None) -> dict:
+    comps = components(spec)
+    devices = sorted(spec.cq)
+    dtype = {d: ("cpu" if d in cpu_devices else "gpu") for d in devices}
+    dev_pref = {c["id"]: spec.kernels[c["kernels"][0]]["dev"] for c in comps}
+
+    def t_of(k, dt):
+        if not times:
+            return Fraction(1)
+        return Fraction(times[dt][k])
+    rk = ranks(spec, {k: t_of(k, spec.kernels[k]["dev"]) for k in spec.kernels})
+    crank = [component_rank(c, rk) for c in comps]
+    cross = [sorted({s for s, _, d, _ in spec.edges if d in set(c["kernels"]) and spec.comp_of[s] != c["id"]})
+             for c in comps]
+    state = ["waiting"] * len(comps)
+    finished, finish_order = set(), []
+    F, A = set(), set(devices)
+    live = {}
+    dispatches, completions = [], []
+    pending = deque()
+    log = deque(replay) if replay is not None else None
+
+    def refresh():
+        for c in comps:
+            if state[c["id"]] == "waiting" and all(k in finished for k in cross[c["id"]]):
+                state[c["id"]] = "queued"
+                F.add(c["id"])
+
+    def select():
+        order = sorted(F, key=lambda c: (-crank[c], c))
+        if policy == "clustering":
+            for c in order:
+                for d in sorted(A):
+                    if dtype[d] == dev_pref[c]:
+                        return c, d
+            return None
+        if policy == "eager":
+            return order[0], min(A)
+        c = order[0]   # heft: minimal EFT over idle devices, ties lower id
+        best = None
+        for d in sorted(A):
+            eft = sum(t_of(k, dtype[d]) for k in comps[c]["kernels"])
+            if best is None or eft < best[0]:
+                best = (eft, d)
+        return c, best[1]
+
+    def finish(k):
+        if k not in finished:
+            finished.add(k)
+            finish_order.append(k)
+
+    refresh()
+    while len(finished) < len(spec.kernels):
+        while A and F:
+            pick = select()
+            if pick is None:
+                break
+            c, d = pick
+            q = setup_cq(spec, c, d, dtype[d], spec.cq[d])
+            F.discard(c)
+            A.discard(d)
+            state[c] = "dispatched"
+            live[c] = {"device": d, "q": q, "done": set()}
+            dispatches.append([c, d])
+            for ev in q["_callbacks"]:
+                pending.append((c, ev))
+        if len(finished) >= len(spec.kernels):
+            break
+        if not live:
+            raise OracleError("Deadlock")
+        if log is not None:
+            c, ev = log.popleft()
+        else:
+            c, ev = pending.popleft()
+        L = live[c]
+        q = L["q"]
+        completions.append([c, ev])
+        L["done"].add(ev)
+        for k in sorted(comps[c]["end"]):
+            marks = [e for e in q["_end_marks"] if q["commands"][e]["kernel"] == k]
+            if marks and all(e in L["done"] for e in marks):
+                finish(k)
+        if all(e in L["done"] for e in q["_terminal"]):
+            for k in comps[c]["kernels"]:
+                finish(k)
+            state[c] = "done"
+            A.add(L["device"])
+            del live[c]
+        refresh()
+    return {"dispatches": dispatches, "completions": completions, "kernel_finish_order": finish_order,
+            "component_ranks": [frac_str(x) for x in crank]}
+
+
+# ============================================================================ numeric kernels (oracle/kernels.c)
+
+_olib = None
+
+
+def olib():
+    global _olib
+    if _olib is None:
+        if not LIBORACLE.exists():
+            raise RuntimeError(f"{LIBORACLE} missing: run `make oracle`")
+        L = ctypes.CDLL(str(LIBORACLE))
+        i64, i32, f32, vp = ctypes.c_int64, ctypes.c_int, ctypes.c_float, ctypes.c_void_p
+        L.or_gemm.argtypes = [vp, i64, vp, i64, vp, i64, i32, i32, i32, i32, i32, i32]
+        L.or_gemm_f64.argtypes = [vp, i64, vp, i64, vp, i64, i32, i32, i32, i32, i32]
+        L.or_transpose.argtypes = [vp, i64, vp, i64, i32, i32, i32]
+        L.or_scale.argtypes = [vp, i64, vp, i64, i64, f32, i32]
+        L.or_add.argtypes = [vp, i64, vp, i64, vp, i64, i64, i32]
+        L.or_softmax.argtypes = [vp, i64, vp, i64, i32, i32, f32, i32]
+        L.or_add_layernorm.argtypes = [vp, i64, vp, i64, vp, i64, vp, i64, vp, i64, i32, i32, f32, i32]
+        L.or_concat.argtypes = [ctypes.POINTER(vp), ctypes.POINTER(i64), i32, vp, i64, i32, i32, i32]
+        L.or_max_threads.restype = i32
+        _olib = L
+    return _olib
+
+
+def _p(a):
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+def run_node(name, ins, strides, out, out_stride, vals, batch):
+    """Execute one node for `batch` instances. ins: list of float32 arrays; vals: var-arg values."""
+    L = olib()
+    if name in ("gemm", "gemm_nt", "gemm_relu"):
+        M, N, K = vals[:3]
+        L.or_gemm(_p(ins[0]), strides[0], _p(ins[1]), strides[1], _p(out), out_stride, M, N, K,
+                  int(name == "gemm_nt"), int(name == "gemm_relu"), batch)
+    elif name == "transpose":
+        L.or_transpose(_p(ins[0]), strides[0], _p(out), out_stride, vals[0], vals[1], batch)
+    elif name == "scale":
+        L.or_scale(_p(ins[0]), strides[0], _p(out), out_stride, vals[0], float(np.float32(vals[1] / vals[2])), batch)
+    elif name == "softmax":
+        s = float(np.float32(vals[2] / vals[3])) if len(vals) >= 4 else 1.0
+        L.or_softmax(_p(ins[0]), strides[0], _p(out), out_stride, vals[0], vals[1], s, batch)
+    elif name == "add":
+        L.or_add(_p(ins[0]), strides[0], _p(ins[1]), strides[1], _p(out), out_stride, vals[0], batch)
+    elif name == "add_layernorm":
+        L.or_add_layernorm(_p(ins[0]), strides[0], _p(ins[1]), strides[1], _p(ins[2]), strides[2], _p(ins[3]),
+                           strides[3], _p(out), out_stride, vals[0], vals[1], 1e-5, batch)
+    elif name == "concat":
+        n = len(ins)
+        ptrs = (ctypes.c_void_p * n)(*[a.ctypes.data for a in ins])
+        st = (ctypes.c_int64 * n)(*strides)
+        L.or_concat(ptrs, st, n, _p(out), out_stride, vals[0], vals[1], batch)
+    else:
+        raise ValueError(name)
+
+
+def run_dag(spec_text: str, params: dict, inputs: dict, n: int, keep=False):
+    """Execute the DAG on the CPU for n instances, kernels in topological order.
+
+    inputs: (kernel,pos) -> array of shape [n, elems] (per-instance) or [elems] (shared).
+    Returns {(kernel,pos): [n, elems]} for every isolated output (all buffers if keep).
+    """
+    spec = Spec(spec_text, params)
+    producer = {(d, dp): (s, sp) for s, sp, d, dp in spec.edges}
+    feeding = {(s, sp) for s, sp, _, _ in spec.edges}
+    bufs = {}
+    for k in spec.topo_order():
+        kd = spec.kernels[k]
+        ins, strides = [], []
+        for b in spec.buffers(k, "in"):
+            key = (k, b["pos"])
+            arr = bufs[producer[key]] if key in producer else np.ascontiguousarray(inputs[key], dtype=np.float32)
+            shared = arr.ndim == 1
+            ins.append(arr)
+            strides.append(0 if shared else arr.shape[1])
+        ob = spec.buffers(k, "out")[0]
+        elems = spec.bytes(k, ob["pos"]) // 4
+        out = np.empty((n, elems), dtype=np.float32)
+        vals = [eval_expr(str(v["value"]), params) for v in sorted(kd.get("varArguments", []), key=lambda v: v["pos"])]
+        run_node(kd["name"], ins, strides, out, elems, vals, n)
+        bufs[(k, ob["pos"])] = out
+    if keep:
+        return bufs
+    return {key: v for key, v in bufs.items() if key not in feeding}
+
+
+def max_threads() -> int:
+    return int(olib().or_max_threads())
+
+
+# ============================================================================ reference shim (oracle/_ref)
+
+_rlib = None
+
+
+def ref_available() -> bool:
+    return LIBREF.exists()
+
+
+def ref_query(request: dict) -> dict:
+    """Ask the reference's compiled L0-L2 (oracle/_ref/libhetsim_ref.so)."""
+    global _rlib
+    if _rlib is None:
+        L = ctypes.CDLL(str(LIBREF))
+        L.ref_query.restype = ctypes.c_void_p
+        L.ref_query.argtypes = [ctypes.c_char_p]
+        L.ref_free.argtypes = [ctypes.c_void_p]
+        _rlib = L
+    p = _rlib.ref_query(json.dumps(request).encode())
+    try:
+        return json.loads(ctypes.string_at(p).decode())
+    finally:
+        _rlib.ref_free(p)

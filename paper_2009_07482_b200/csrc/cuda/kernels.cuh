@@ -1,0 +1,44 @@
+// Launchers for the DAG node kernels (sm_100a). All pointers are device
+// pointers; every buffer carries a per-instance stride in elements (0 means
+// the buffer is shared by all `batch` instances, e.g. resident weights).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace hs {
+
+enum class GemmLayout { nn, nt };  // B is [K,N] row-major (nn) or [N,K] row-major (nt)
+
+struct GemmArgs {
+  const float* A;
+  int64_t sA;
+  const float* B;
+  int64_t sB;
+  float* C;
+  int64_t sC;
+  int M, N, K;
+  int batch;
+  GemmLayout layout;
+  bool relu;
+};
+
+// math: 0 = TF32x3 (tcgen05), 1 = TF32 (tcgen05), 2 = fp32 SIMT
+cudaError_t gemm_tcgen05(const GemmArgs& a, int terms, cudaStream_t s);
+cudaError_t gemm_simt(const GemmArgs& a, cudaStream_t s);
+// true when the tcgen05 path supports this shape/alignment
+bool gemm_tcgen05_supported(const GemmArgs& a);
+
+cudaError_t transpose(const float* A, int64_t sA, float* B, int64_t sB, int R, int C, int batch, cudaStream_t s);
+cudaError_t scale(const float* A, int64_t sA, float* B, int64_t sB, int64_t n, float f, int batch, cudaStream_t s);
+cudaError_t add(const float* A, int64_t sA, const float* B, int64_t sB, float* C, int64_t sC, int64_t n, int batch,
+                cudaStream_t s);
+cudaError_t softmax(const float* A, int64_t sA, float* B, int64_t sB, int rows, int cols, float f, int batch,
+                    cudaStream_t s);
+cudaError_t add_layernorm(const float* A, int64_t sA, const float* B, int64_t sB, const float* gamma, int64_t sG,
+                          const float* beta, int64_t sBt, float* Y, int64_t sY, int rows, int cols, float eps,
+                          int batch, cudaStream_t s);
+cudaError_t concat(const float* const* Z, const int64_t* sZ, int count, float* Y, int64_t sY, int rows, int cols_each,
+                   int batch, cudaStream_t s);
+
+}  // namespace hs

@@ -1,0 +1,675 @@
+// B200 executor / engine. See engine.hpp for the command -> CUDA mapping.
+//
+// Two execution modes over the same issue() path:
+//  * dynamic — Alg. 1 literally: the Scheduler calls CudaDispatch::dispatch
+//    for every (T, d) it selects; completions of callback-marked commands
+//    come back through cudaLaunchHostFunc -> MPSC queue -> Scheduler::cb.
+//    A logical device stays locked until its component's terminal commands
+//    complete.
+//  * graph   — the same Scheduler is run once against PlanExecutor to fix the
+//    dispatch sequence; issue() then records that sequence into a CUDA graph
+//    per instance slot (stream capture over the per-queue streams). Device
+//    exclusivity becomes an event join on the previous component's terminal
+//    commands, so no host round trip sits between components. Steady-state
+//    batches are copy-in -> graph launch -> copy-out on the slot's origin
+//    stream, slots alternating so that copies overlap compute.
+#include "engine.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+
+#include "../core/json.hpp"
+#include "hetsim/errors.hpp"
+
+extern "C" int hs__set_error(int status, int errc, const char* msg);
+
+namespace hetsim {
+
+namespace {
+
+void hs_ok(int r, const char* what) {
+  if (r == HS_OK) return;
+  const int errc = hs_last_errc();
+  std::string msg = std::string(what) + ": " + hs_last_error();
+  fail(errc == static_cast<int>(Errc::invalid_param) ? Errc::invalid_param : Errc::device_error, msg);
+}
+
+struct CbData {
+  Engine* engine;
+  Completion c;
+};
+
+void CUDART_CB_trampoline(void* p) {
+  auto* d = static_cast<CbData*>(p);
+  d->engine->push_completion(d->c);
+  delete d;
+}
+
+std::vector<long long> var_values(const KernelSpec& k, const ParamMap& params) {
+  std::vector<const VarArg*> vs;
+  for (const auto& v : k.var_args) vs.push_back(&v);
+  std::sort(vs.begin(), vs.end(), [](const VarArg* a, const VarArg* b) { return a->pos < b->pos; });
+  std::vector<long long> out;
+  for (const VarArg* v : vs) out.push_back(eval_expr(v->value, params));
+  return out;
+}
+
+}  // namespace
+
+// Executor used in dynamic mode: Alg. 1 dispatch -> Engine::issue.
+class CudaDispatch : public Executor {
+ public:
+  CudaDispatch(Engine& e, Engine::Slot& sl, int64_t first, int64_t n) : e_(e), sl_(sl), first_(first), n_(n) {}
+  void dispatch(const TaskComponent& t, const CommandQueueStructure& q) override {
+    e_.issue(sl_, t, q, -1, nullptr, false, first_, n_);
+  }
+  Completion wait_next() override { return e_.wait_completion(); }
+
+ private:
+  Engine& e_;
+  Engine::Slot& sl_;
+  int64_t first_, n_;
+};
+
+Engine::Engine(EngineConfig cfg) : cfg_(std::move(cfg)) {
+  if (cfg_.batch < 1) fail(Errc::invalid_param, "batch must be >= 1");
+  if (cfg_.slots < 1) cfg_.slots = 1;
+  g_ = parse_spec(cfg_.spec_text, cfg_.params);
+  platform_ = Platform::from_spec(g_, cfg_.cpu_devices, 1);
+  for (const auto& d : platform_.devices)
+    if (d.type == DeviceType::cpu)
+      fail(Errc::invalid_param, "device " + std::to_string(d.id) + " is a CPU device; the B200 executor has no CPU path");
+  sched_ = std::make_unique<Scheduler>(g_, platform_, Profiles{}, cfg_.policy);
+  build_nodes();
+  hs_ok(hs_ctx_create(cfg_.gpu, &ctx_), "hs_ctx_create");
+}
+
+Engine::~Engine() {
+  if (!ctx_) return;
+  hs_ctx_sync(ctx_);
+  for (auto& sl : slots_) {
+    hs_graph_destroy(sl.graph);
+    for (auto& [k, e] : sl.events) hs_event_destroy(e);
+    for (auto& [k, e] : sl.group_event) hs_event_destroy(e);
+    hs_event_destroy(sl.t_start);
+    hs_event_destroy(sl.t_end);
+    for (auto& [k, s] : sl.streams) hs_stream_destroy(s);
+    hs_stream_destroy(sl.origin);
+  }
+  for (void* p : allocations_) hs_free(ctx_, p);
+  hs_ctx_destroy(ctx_);
+}
+
+void Engine::build_nodes() {
+  for (const auto& k : g_.kernels) {
+    Node nd;
+    nd.op = hs_op_from_name(k.name.c_str());
+    if (nd.op < 0) fail(Errc::invalid_param, "kernel " + std::to_string(k.id) + ": no sm_100a operator '" + k.name + "'");
+    for (const auto* b : k.input_side()) nd.inputs.push_back({k.id, b->pos});
+    auto outs = k.output_side();
+    if (outs.empty()) fail(Errc::invalid_param, "kernel " + std::to_string(k.id) + " has no output buffer");
+    nd.output = {k.id, outs.front()->pos};
+    for (const auto* list : {&k.input_buffers, &k.output_buffers, &k.io_buffers})
+      for (const auto& b : *list) {
+        if (b.type != ElemType::f32)
+          fail(Errc::invalid_param, "kernel " + std::to_string(k.id) + ": only float32 buffers are supported");
+        bytes_[{k.id, b.pos}] = buffer_bytes(b, g_.params);
+      }
+    auto v = var_values(k, g_.params);
+    auto elems = [&](std::pair<int, int> key) { return bytes_.at(key) / 4; };
+    auto need = [&](bool ok, const char* what) {
+      if (!ok) fail(Errc::invalid_param, "kernel " + std::to_string(k.id) + " (" + k.name + "): " + what);
+    };
+    const size_t nin = nd.inputs.size();
+    switch (nd.op) {
+      case HS_OP_GEMM:
+      case HS_OP_GEMM_NT:
+      case HS_OP_GEMM_RELU:
+        need(v.size() >= 3 && nin == 2, "expects (A, B, C, M, N, K)");
+        for (int i = 0; i < 3; ++i) nd.dims[i] = v[size_t(i)];
+        need(elems(nd.inputs[0]) == v[0] * v[2], "A size != M*K");
+        need(elems(nd.inputs[1]) == v[1] * v[2], "B size != K*N");
+        need(elems(nd.output) == v[0] * v[1], "C size != M*N");
+        break;
+      case HS_OP_TRANSPOSE:
+        need(v.size() >= 2 && nin == 1, "expects (A, B, R, C)");
+        nd.dims[0] = v[0];
+        nd.dims[1] = v[1];
+        need(elems(nd.inputs[0]) == v[0] * v[1] && elems(nd.output) == v[0] * v[1], "size != R*C");
+        break;
+      case HS_OP_SCALE:
+        need(v.size() >= 3 && nin == 1 && v[2] != 0, "expects (A, B, n, num, den)");
+        nd.dims[0] = v[0];
+        nd.fparam[0] = float(double(v[1]) / double(v[2]));
+        need(elems(nd.inputs[0]) == v[0] && elems(nd.output) == v[0], "size != n");
+        break;
+      case HS_OP_SOFTMAX:
+        need(v.size() >= 2 && nin == 1, "expects (A, B, rows, cols[, num, den])");
+        nd.dims[0] = v[0];
+        nd.dims[1] = v[1];
+        nd.fparam[0] = v.size() >= 4 && v[3] != 0 ? float(double(v[2]) / double(v[3])) : 1.f;
+        need(elems(nd.inputs[0]) == v[0] * v[1] && elems(nd.output) == v[0] * v[1], "size != rows*cols");
+        need(v[1] <= 1024, "cols > 1024");
+        break;
+      case HS_OP_ADD:
+        need(v.size() >= 1 && nin == 2, "expects (A, B, C, n)");
+        nd.dims[0] = v[0];
+        need(elems(nd.inputs[0]) == v[0] && elems(nd.inputs[1]) == v[0] && elems(nd.output) == v[0], "size != n");
+        break;
+      case HS_OP_ADD_LN:
+        need(v.size() >= 2 && nin == 4, "expects (A, B, gamma, beta, Y, rows, cols)");
+        nd.dims[0] = v[0];
+        nd.dims[1] = v[1];
+        need(elems(nd.inputs[0]) == v[0] * v[1] && elems(nd.inputs[1]) == v[0] * v[1] &&
+                 elems(nd.output) == v[0] * v[1],
+             "size != rows*cols");
+        need(elems(nd.inputs[2]) == v[1] && elems(nd.inputs[3]) == v[1], "gamma/beta size != cols");
+        need(v[1] <= 1024, "cols > 1024");
+        break;
+      case HS_OP_CONCAT:
+        need(v.size() >= 2 && nin >= 1 && nin <= HS_MAX_INPUTS, "expects (Z0..Zn-1, Y, rows, cols_each)");
+        nd.dims[0] = v[0];
+        nd.dims[1] = v[1];
+        for (auto in : nd.inputs) need(elems(in) == v[0] * v[1], "input size != rows*cols_each");
+        need(elems(nd.output) == v[0] * v[1] * int64_t(nin), "output size != rows*cols_each*count");
+        break;
+      default: break;
+    }
+    nodes_[k.id] = nd;
+  }
+}
+
+void Engine::bind(int kernel, int pos, void* ptr, int64_t stride_bytes, bool on_device) {
+  if (planned_) fail(Errc::invalid_param, "bindings are frozen after the first run");
+  const BufferSpec* b = g_.kernel(kernel).buffer_at(pos);
+  if (!b) fail(Errc::invalid_param, "kernel " + std::to_string(kernel) + " has no buffer at position " + std::to_string(pos));
+  if (!ptr) fail(Errc::invalid_param, "null binding");
+  if (stride_bytes < 0) fail(Errc::invalid_param, "negative stride");
+  bindings_[{kernel, pos}] = Binding{ptr, stride_bytes, on_device};
+}
+
+void Engine::plan_buffers() {
+  auto producers = g_.producer_edge();
+  auto ec = sched_->edge_classes();
+  std::map<std::tuple<void*, int64_t, int64_t, bool>, int> dedupe;
+  for (const auto& k : g_.kernels) {
+    for (const auto* b : k.input_side()) {
+      std::pair<int, int> key{k.id, b->pos};
+      auto pe = producers.find(key);
+      if (pe != producers.end()) {
+        const DagEdge& e = g_.edges[size_t(pe->second)];
+        if (b->kind == BufferKind::io) io_copy_[key] = {e.src_kernel, e.src_pos};
+        else alias_[key] = {e.src_kernel, e.src_pos};
+        continue;
+      }
+      auto bi = bindings_.find(key);
+      if (bi == bindings_.end())
+        fail(Errc::invalid_param, "isolated input (" + std::to_string(k.id) + "," + std::to_string(b->pos) + ") is not bound");
+      Group gr;
+      gr.b = bi->second;
+      gr.bytes = bytes_.at(key);
+      gr.resident = gr.b.stride == 0;
+      gr.io = b->kind == BufferKind::io;
+      if (gr.io && gr.resident) fail(Errc::invalid_param, "an io buffer cannot be bound as shared (stride 0)");
+      if (!gr.io) {
+        auto dk = std::make_tuple(gr.b.ptr, gr.b.stride, gr.bytes, gr.b.on_device);
+        auto it = dedupe.find(dk);
+        if (it != dedupe.end()) {
+          group_of_[key] = it->second;
+          continue;
+        }
+        dedupe[dk] = int(groups_.size());
+      }
+      group_of_[key] = int(groups_.size());
+      groups_.push_back(gr);
+    }
+    for (const auto* b : k.output_side()) {
+      std::pair<int, int> key{k.id, b->pos};
+      if (ec.read_class.at(key) == CopyClass::isolated && bindings_.count(key)) outputs_.push_back(key);
+    }
+  }
+  // resident groups: one allocation per engine
+  for (size_t gi = 0; gi < groups_.size(); ++gi) {
+    if (!groups_[gi].resident) continue;
+    void* p = nullptr;
+    hs_ok(hs_malloc(ctx_, size_t(groups_[gi].bytes), &p), "hs_malloc");
+    allocations_.push_back(p);
+    device_bytes_ += groups_[gi].bytes;
+    resident_buf_[int(gi)] = p;
+  }
+  const int64_t B = cfg_.batch;
+  slots_.resize(size_t(cfg_.slots));
+  for (auto& sl : slots_) {
+    auto alloc = [&](int64_t bytes) {
+      void* p = nullptr;
+      hs_ok(hs_malloc(ctx_, size_t(bytes * B), &p), "hs_malloc");
+      allocations_.push_back(p);
+      device_bytes_ += bytes * B;
+      return p;
+    };
+    for (const auto& k : g_.kernels)
+      for (const auto* b : k.output_side()) sl.buf[{k.id, b->pos}] = alloc(bytes_.at({k.id, b->pos}));
+    for (size_t gi = 0; gi < groups_.size(); ++gi) {
+      if (groups_[gi].resident) continue;
+      if (groups_[gi].io) continue;  // io group lives in the (kernel,pos) output allocation
+      sl.group_buf[int(gi)] = alloc(groups_[gi].bytes);
+    }
+    for (const auto& [key, gi] : group_of_) {
+      if (groups_[size_t(gi)].io) sl.group_buf[gi] = sl.buf.at(key);
+      sl.buf[key] = groups_[size_t(gi)].resident ? resident_buf_.at(gi) : sl.group_buf.at(gi);
+    }
+    for (const auto& [key, src] : alias_) sl.buf[key] = sl.buf.at(src);
+    hs_ok(hs_stream_create(ctx_, 0, &sl.origin), "hs_stream_create");
+    hs_ok(hs_event_create(ctx_, 1, &sl.t_start), "hs_event_create");
+    hs_ok(hs_event_create(ctx_, 1, &sl.t_end), "hs_event_create");
+  }
+  launches_per_batch_ = int64_t(g_.kernels.size());
+}
+
+void Engine::upload_resident() {
+  if (resident_uploaded_) return;
+  hs_stream_t s = slots_.front().origin;
+  for (const auto& [gi, dst] : resident_buf_) {
+    const Group& gr = groups_[size_t(gi)];
+    hs_ok(hs_memcpy_2d(s, dst, size_t(gr.bytes), gr.b.ptr, size_t(gr.bytes), size_t(gr.bytes), 1, gr.b.on_device ? 2 : 0),
+          "resident upload");
+  }
+  hs_ok(hs_stream_sync(s), "resident upload sync");
+  resident_uploaded_ = true;
+}
+
+hs_stream_t Engine::stream(Slot& sl, int device, int queue) {
+  auto key = std::make_pair(device, queue);
+  auto it = sl.streams.find(key);
+  if (it != sl.streams.end()) return it->second;
+  hs_stream_t s = nullptr;
+  hs_ok(hs_stream_create(ctx_, 0, &s), "hs_stream_create");
+  sl.streams[key] = s;
+  return s;
+}
+
+hs_event_t Engine::event(Slot& sl, int comp, int ev) {
+  auto key = std::make_pair(comp, ev);
+  auto it = sl.events.find(key);
+  if (it != sl.events.end()) return it->second;
+  hs_event_t e = nullptr;
+  hs_ok(hs_event_create(ctx_, 0, &e), "hs_event_create");
+  sl.events[key] = e;
+  return e;
+}
+
+void Engine::copy_in(Slot& sl, hs_stream_t s, int gi, int64_t first, int64_t n) {
+  const Group& gr = groups_[size_t(gi)];
+  const char* src = static_cast<const char*>(gr.b.ptr) + first * gr.b.stride;
+  hs_ok(hs_memcpy_2d(s, sl.group_buf.at(gi), size_t(gr.bytes), src, size_t(gr.b.stride), size_t(gr.bytes), size_t(n),
+                     gr.b.on_device ? 2 : 0),
+        "copy-in");
+}
+
+void Engine::copy_out(Slot& sl, hs_stream_t s, int64_t first, int64_t n) {
+  for (const auto& key : outputs_) {
+    const Binding& b = bindings_.at(key);
+    const int64_t bytes = bytes_.at(key);
+    char* dst = static_cast<char*>(b.ptr) + first * b.stride;
+    hs_ok(hs_memcpy_2d(s, dst, size_t(b.stride ? b.stride : bytes), sl.buf.at(key), size_t(bytes), size_t(bytes),
+                       size_t(b.stride ? n : 1), b.on_device ? 2 : 1),
+          "copy-out");
+  }
+}
+
+void Engine::launch_node(Slot& sl, hs_stream_t s, int kernel) {
+  const Node& nd = nodes_.at(kernel);
+  for (const auto& in : nd.inputs) {
+    auto io = io_copy_.find(in);
+    if (io != io_copy_.end())
+      hs_ok(hs_memcpy_d2d(s, sl.buf.at(in), sl.buf.at(io->second), size_t(bytes_.at(in) * cfg_.batch)), "io copy");
+  }
+  hs_op_args a{};
+  a.n_in = int(nd.inputs.size());
+  for (size_t i = 0; i < nd.inputs.size(); ++i) {
+    const auto& key = nd.inputs[i];
+    a.in[i] = sl.buf.at(key);
+    auto gi = group_of_.find(key);
+    const bool shared = gi != group_of_.end() && groups_[size_t(gi->second)].resident;
+    a.in_stride[i] = shared ? 0 : bytes_.at(key) / 4;
+  }
+  a.out = sl.buf.at(nd.output);
+  a.out_stride = bytes_.at(nd.output) / 4;
+  for (int i = 0; i < 4; ++i) a.dims[i] = nd.dims[i];
+  a.fparam[0] = nd.fparam[0];
+  a.fparam[1] = nd.fparam[1];
+  hs_ok(hs_launch(s, nd.op, &a, cfg_.math, cfg_.batch), "hs_launch");
+}
+
+void Engine::issue(Slot& sl, const TaskComponent& t, const CommandQueueStructure& q, int prev_comp,
+                   const CommandQueueStructure* prev_q, bool graph, int64_t first, int64_t n) {
+  const int d = q.device;
+  std::set<int> dep_sources;
+  std::map<int, std::vector<int>> preds;
+  for (auto [a, b] : q.deps) {
+    dep_sources.insert(a);
+    preds[b].push_back(a);
+  }
+  // Device exclusivity in graph mode: every queue waits for the previous
+  // component's terminal commands on this logical device.
+  if (prev_q) {
+    for (size_t qi = 0; qi < q.queues.size(); ++qi) {
+      if (q.queues[qi].empty()) continue;
+      hs_stream_t s = stream(sl, d, int(qi));
+      for (int te : prev_q->terminal_events()) hs_ok(hs_stream_wait(s, event(sl, prev_comp, te)), "exclusivity wait");
+    }
+  }
+  // Commands in global enqueue order: every E_Q / inter-edge source is
+  // recorded on the host before any stream waits on it.
+  for (int ev = 0; ev < q.event_count; ++ev) {
+    const auto [qi, idx] = q.event_pos[size_t(ev)];
+    const Command& c = q.queues[size_t(qi)][size_t(idx)];
+    hs_stream_t s = stream(sl, d, qi);
+    auto pit = preds.find(ev);
+    if (pit != preds.end())
+      for (int p : pit->second) hs_ok(hs_stream_wait(s, event(sl, t.id, p)), "E_Q wait");
+    bool record = dep_sources.count(ev) || q.callbacks.count(ev);
+    switch (c.kind) {
+      case CmdKind::write: {
+        const std::pair<int, int> key{c.buffer->kernel, c.buffer->pos};
+        if (c.dependent) {
+          auto src = sl.edge_event.find(c.edge);
+          if (src == sl.edge_event.end())
+            fail(Errc::deadlock, "dependent write for edge " + std::to_string(c.edge) + " issued before its producer");
+          hs_ok(hs_stream_wait(s, event(sl, src->second.first, src->second.second)), "inter-edge wait");
+          auto io = io_copy_.find(key);
+          if (io != io_copy_.end())
+            hs_ok(hs_memcpy_d2d(s, sl.buf.at(key), sl.buf.at(io->second), size_t(bytes_.at(key) * cfg_.batch)),
+                  "dependent write");
+        } else if (!graph) {
+          const int gi = group_of_.at(key);
+          if (!groups_[size_t(gi)].resident) {
+            if (!sl.group_done.count(gi)) {
+              copy_in(sl, s, gi, first, n);
+              auto ge = sl.group_event.find(gi);
+              hs_event_t e = nullptr;
+              if (ge == sl.group_event.end()) {
+                hs_ok(hs_event_create(ctx_, 0, &e), "hs_event_create");
+                sl.group_event[gi] = e;
+              } else {
+                e = ge->second;
+              }
+              hs_ok(hs_event_record(e, s), "group record");
+              sl.group_done.insert(gi);
+            } else {
+              hs_ok(hs_stream_wait(s, sl.group_event.at(gi)), "group wait");
+            }
+          }
+        }
+        break;
+      }
+      case CmdKind::ndrange:
+        launch_node(sl, s, c.kernel);
+        break;
+      case CmdKind::read:
+        if (c.dependent) {
+          sl.edge_event[c.edge] = {t.id, ev};
+          record = true;
+        } else if (!graph) {
+          const std::pair<int, int> key{c.buffer->kernel, c.buffer->pos};
+          if (bindings_.count(key)) {
+            const Binding& b = bindings_.at(key);
+            const int64_t bytes = bytes_.at(key);
+            hs_ok(hs_memcpy_2d(s, static_cast<char*>(b.ptr) + first * b.stride, size_t(b.stride ? b.stride : bytes),
+                               sl.buf.at(key), size_t(bytes), size_t(bytes), size_t(b.stride ? n : 1),
+                               b.on_device ? 2 : 1),
+                  "isolated read");
+          }
+        }
+        break;
+    }
+    if (record) hs_ok(hs_event_record(event(sl, t.id, ev), s), "event record");
+    if (!graph && q.callbacks.count(ev))
+      hs_ok(hs_host_callback(s, &CUDART_CB_trampoline, new CbData{this, {t.id, ev}}), "host callback");
+  }
+}
+
+void Engine::capture(Slot& sl) {
+  // Every stream the plan touches joins the capture through a fork event.
+  std::set<std::pair<int, int>> used;
+  for (size_t i = 0; i < plan_.dispatches.size(); ++i) {
+    const auto& q = plan_.structures[i];
+    for (size_t qi = 0; qi < q.queues.size(); ++qi) used.insert({q.device, int(qi)});
+  }
+  for (auto [d, qi] : used) stream(sl, d, qi);  // create before capture
+  hs_ok(hs_capture_begin(sl.origin), "capture begin");
+  hs_event_t fork = event(sl, -1, 0);
+  hs_ok(hs_event_record(fork, sl.origin), "fork record");
+  for (auto [d, qi] : used) hs_ok(hs_stream_wait(stream(sl, d, qi), fork), "fork wait");
+  std::map<int, int> last_on_device;  // logical device -> index into plan_
+  for (size_t i = 0; i < plan_.dispatches.size(); ++i) {
+    const auto& rec = plan_.dispatches[i];
+    const auto& q = plan_.structures[i];
+    auto prev = last_on_device.find(rec.device);
+    const CommandQueueStructure* pq = prev == last_on_device.end() ? nullptr : &plan_.structures[size_t(prev->second)];
+    int pc = prev == last_on_device.end() ? -1 : plan_.dispatches[size_t(prev->second)].component;
+    issue(sl, sched_->components()[size_t(rec.component)], q, pc, pq, true, 0, cfg_.batch);
+    last_on_device[rec.device] = int(i);
+  }
+  int j = 0;
+  for (auto [d, qi] : used) {
+    hs_event_t e = event(sl, -2, j++);
+    hs_ok(hs_event_record(e, stream(sl, d, qi)), "join record");
+    hs_ok(hs_stream_wait(sl.origin, e), "join wait");
+  }
+  hs_ok(hs_capture_end(sl.origin, &sl.graph), "capture end");
+}
+
+void Engine::push_completion(const Completion& c) {
+  {
+    std::lock_guard<std::mutex> lk(mu_);
+    done_q_.push_back(c);
+  }
+  cv_.notify_one();
+}
+
+Completion Engine::wait_completion() {
+  std::unique_lock<std::mutex> lk(mu_);
+  if (!cv_.wait_for(lk, std::chrono::seconds(120), [&] { return !done_q_.empty(); }))
+    fail(Errc::deadlock, "no completion callback within 120 s");
+  Completion c = done_q_.front();
+  done_q_.pop_front();
+  last_log_.push_back(c);
+  return c;
+}
+
+void Engine::run_dynamic(Slot& sl, int64_t first, int64_t n) {
+  sl.group_done.clear();
+  sl.edge_event.clear();
+  last_log_.clear();
+  {
+    std::lock_guard<std::mutex> lk(mu_);
+    done_q_.clear();
+  }
+  CudaDispatch ex(*this, sl, first, n);
+  ScheduleResult r = sched_->run(ex);
+  last_dispatches_ = r.dispatches;
+}
+
+void Engine::run(int64_t first, int64_t n, int64_t* elapsed_ns) {
+  if (n < 1) fail(Errc::invalid_param, "n_instances must be >= 1");
+  if (!planned_) {
+    plan_buffers();
+    if (cfg_.graph_mode) {
+      PlanExecutor pe;
+      plan_ = sched_->run(pe);
+      for (auto& sl : slots_) capture(sl);
+    }
+    planned_ = true;
+  }
+  upload_resident();
+  const int64_t B = cfg_.batch;
+  const int64_t nb = (n + B - 1) / B;
+  Slot& s0 = slots_.front();
+  // Every stream that can carry work starts after t_start.
+  hs_ok(hs_event_record(s0.t_start, s0.origin), "start record");
+  for (size_t i = 1; i < slots_.size(); ++i) hs_ok(hs_stream_wait(slots_[i].origin, s0.t_start), "start wait");
+  if (cfg_.graph_mode) {
+    for (int64_t b = 0; b < nb; ++b) {
+      Slot& sl = slots_[size_t(b % int64_t(slots_.size()))];
+      const int64_t f = first + b * B, cnt = std::min(B, n - b * B);
+      for (size_t gi = 0; gi < groups_.size(); ++gi)
+        if (!groups_[gi].resident) copy_in(sl, sl.origin, int(gi), f, cnt);
+      hs_ok(hs_graph_launch(sl.graph, sl.origin), "graph launch");
+      copy_out(sl, sl.origin, f, cnt);
+    }
+  } else {
+    for (auto& [k, s] : s0.streams) hs_ok(hs_stream_wait(s, s0.t_start), "start wait");
+    for (int64_t b = 0; b < nb; ++b) {
+      const int64_t f = first + b * B, cnt = std::min(B, n - b * B);
+      run_dynamic(s0, f, cnt);
+    }
+    // join every queue stream back into the origin
+    int j = 0;
+    for (auto& [k, s] : s0.streams) {
+      hs_event_t e = event(s0, -3, j++);
+      hs_ok(hs_event_record(e, s), "join record");
+      hs_ok(hs_stream_wait(s0.origin, e), "join wait");
+    }
+  }
+  for (size_t i = 1; i < slots_.size(); ++i) {
+    hs_ok(hs_event_record(slots_[i].t_end, slots_[i].origin), "end record");
+    hs_ok(hs_stream_wait(s0.origin, slots_[i].t_end), "end wait");
+  }
+  hs_ok(hs_event_record(s0.t_end, s0.origin), "end record");
+  hs_ok(hs_event_sync(s0.t_end), "end sync");
+  if (elapsed_ns) hs_ok(hs_event_elapsed_ns(s0.t_start, s0.t_end, elapsed_ns), "elapsed");
+  ++runs_;
+  batches_run_ += nb;
+}
+
+std::string Engine::info(const std::string& what) const {
+  using json::Value;
+  Value out = Value::make_object();
+  auto pairs = [](const auto& v, auto a, auto b) {
+    Value arr = Value::make_array();
+    for (const auto& x : v) {
+      Value p = Value::make_array();
+      p.push_back(Value::of(static_cast<long long>(x.*a)));
+      p.push_back(Value::of(static_cast<long long>(x.*b)));
+      arr.push_back(std::move(p));
+    }
+    return arr;
+  };
+  if (what == "plan") {
+    out.set("mode", Value::of(std::string(cfg_.graph_mode ? "graph" : "dynamic")));
+    out.set("batch", Value::of(static_cast<long long>(cfg_.batch)));
+    out.set("slots", Value::of(static_cast<long long>(cfg_.slots)));
+    out.set("kernels", Value::of(static_cast<long long>(g_.kernels.size())));
+    out.set("edges", Value::of(static_cast<long long>(g_.edges.size())));
+    out.set("components", Value::of(static_cast<long long>(sched_->components().size())));
+    out.set("dispatches", pairs(plan_.dispatches, &DispatchRecord::component, &DispatchRecord::device));
+    long long streams = 0;
+    for (const auto& sl : slots_) streams += static_cast<long long>(sl.streams.size());
+    out.set("streams", Value::of(streams));
+    out.set("device_bytes", Value::of(static_cast<long long>(device_bytes_)));
+    out.set("resident_groups", Value::of(static_cast<long long>(resident_buf_.size())));
+    out.set("instance_groups", Value::of(static_cast<long long>(groups_.size() - resident_buf_.size())));
+    out.set("aliased_inputs", Value::of(static_cast<long long>(alias_.size())));
+  } else if (what == "stats") {
+    out.set("launches_per_batch", Value::of(static_cast<long long>(launches_per_batch_)));
+    out.set("runs", Value::of(static_cast<long long>(runs_)));
+    out.set("batches", Value::of(static_cast<long long>(batches_run_)));
+  } else if (what == "completions") {
+    out.set("completions", pairs(last_log_, &Completion::component, &Completion::event));
+    out.set("dispatches", pairs(last_dispatches_, &DispatchRecord::component, &DispatchRecord::device));
+  } else {
+    fail(Errc::invalid_param, "unknown info '" + what + "'");
+  }
+  return json::dump(out, -1);
+}
+
+}  // namespace hetsim
+
+// ------------------------------------------------------------------ C ABI
+namespace {
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return HS_OK;
+  } catch (const hetsim::Error& e) {
+    const int status = hetsim::exit_code_for(e.code()) == 2 ? HS_ERR_INVALID
+                       : e.code() == hetsim::Errc::device_error ? HS_ERR_CUDA
+                                                                : HS_ERR_RUNTIME;
+    return hs__set_error(status, static_cast<int>(e.code()), e.what());
+  } catch (const std::exception& e) {
+    return hs__set_error(HS_ERR_RUNTIME, -1, e.what());
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int hs_engine_create(const char* config_json, hs_engine_t* out) {
+  return guarded([&] {
+    using namespace hetsim;
+    if (!out) fail(Errc::invalid_param, "null out");
+    json::Value c;
+    try {
+      c = json::parse(config_json ? config_json : "");
+    } catch (const std::exception& e) {
+      fail(Errc::malformed_spec, std::string("engine config: ") + e.what());
+    }
+    EngineConfig cfg;
+    cfg.spec_text = c.at("spec").as_string();
+    if (const json::Value* p = c.find("params"))
+      for (const auto& [k, v] : p->object_items()) cfg.params[k] = v.as_int64();
+    if (const json::Value* v = c.find("gpu")) cfg.gpu = v->as_int();
+    if (const json::Value* v = c.find("policy")) cfg.policy = policy_from_name(v->as_string());
+    if (const json::Value* v = c.find("mode")) {
+      if (v->as_string() != "graph" && v->as_string() != "dynamic") fail(Errc::invalid_param, "mode must be graph|dynamic");
+      cfg.graph_mode = v->as_string() == "graph";
+    }
+    if (const json::Value* v = c.find("batch")) cfg.batch = v->as_int();
+    if (const json::Value* v = c.find("slots")) cfg.slots = v->as_int();
+    if (const json::Value* v = c.find("math")) {
+      const std::string m = v->as_string();
+      if (m == "tf32x3") cfg.math = HS_MATH_TF32X3;
+      else if (m == "tf32") cfg.math = HS_MATH_TF32;
+      else if (m == "simt") cfg.math = HS_MATH_FP32_SIMT;
+      else fail(Errc::invalid_param, "math must be tf32x3|tf32|simt");
+    }
+    if (const json::Value* v = c.find("cpu_devices"))
+      for (const json::Value* x : v->items()) cfg.cpu_devices.insert(x->as_int());
+    *out = reinterpret_cast<hs_engine_t>(new Engine(std::move(cfg)));
+  });
+}
+
+int hs_engine_destroy(hs_engine_t e) {
+  return guarded([&] { delete reinterpret_cast<hetsim::Engine*>(e); });
+}
+
+int hs_engine_bind(hs_engine_t e, int kernel, int pos, void* ptr, int64_t stride_bytes, int on_device) {
+  return guarded([&] {
+    if (!e) hetsim::fail(hetsim::Errc::invalid_param, "null engine");
+    reinterpret_cast<hetsim::Engine*>(e)->bind(kernel, pos, ptr, stride_bytes, on_device != 0);
+  });
+}
+
+int hs_engine_run(hs_engine_t e, int64_t first, int64_t n, int64_t* elapsed_ns) {
+  return guarded([&] {
+    if (!e) hetsim::fail(hetsim::Errc::invalid_param, "null engine");
+    reinterpret_cast<hetsim::Engine*>(e)->run(first, n, elapsed_ns);
+  });
+}
+
+int hs_engine_info(hs_engine_t e, const char* what, char** out_json) {
+  return guarded([&] {
+    if (!e || !what || !out_json) hetsim::fail(hetsim::Errc::invalid_param, "null argument");
+    std::string s = reinterpret_cast<hetsim::Engine*>(e)->info(what);
+    char* buf = static_cast<char*>(std::malloc(s.size() + 1));
+    std::memcpy(buf, s.c_str(), s.size() + 1);
+    *out_json = buf;
+  });
+}
+
+}  // extern "C"

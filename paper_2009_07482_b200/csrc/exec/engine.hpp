@@ -1,0 +1,139 @@
+// B200 executor: runs Alg. 1's dispatch(T, Q) on CUDA streams through the
+// hs_* C ABI, and packages a DAG template + buffer bindings as an engine that
+// executes a stream of instances (include/hetsim_c.h §3).
+//
+// Mapping:
+//   queue i of a component on logical device d -> stream S[slot][d][i]
+//   E_Q pair (a, b)                              -> record ev(a); S(b) waits ev(a)
+//   inter edge (dependent read -> write)         -> record on the producer's read,
+//                                                   consumer's write waits (data stays
+//                                                   in HBM: the consumer aliases it)
+//   callback mark                                -> cudaLaunchHostFunc (dynamic) /
+//                                                   exclusivity join (graph)
+//   ndrange                                      -> hs_launch (sm_100a kernels), one
+//                                                   launch for all `batch` instances
+//   isolated write/read                          -> H2D/D2H on the copy engines
+#pragma once
+
+#include <condition_variable>
+#include <deque>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "hetsim/cq_builder.hpp"
+#include "hetsim/scheduler.hpp"
+#include "hetsim/spec_model.hpp"
+#include "hetsim_c.h"
+
+namespace hetsim {
+
+struct EngineConfig {
+  std::string spec_text;
+  ParamMap params;
+  int gpu = 0;
+  Policy policy = Policy::clustering;
+  bool graph_mode = true;
+  int batch = 1;
+  int slots = 2;
+  int math = HS_MATH_TF32X3;
+  std::set<int> cpu_devices;
+};
+
+class Engine {
+ public:
+  explicit Engine(EngineConfig cfg);
+  ~Engine();
+  Engine(const Engine&) = delete;
+  Engine& operator=(const Engine&) = delete;
+
+  void bind(int kernel, int pos, void* ptr, int64_t stride_bytes, bool on_device);
+  void run(int64_t first, int64_t n, int64_t* elapsed_ns);
+  std::string info(const std::string& what) const;
+
+  // Completion delivery from CUDA host callbacks (any thread).
+  void push_completion(const Completion& c);
+
+ private:
+  struct Node {
+    int op = -1;
+    std::vector<std::pair<int, int>> inputs;  // (kernel,pos) in arg order
+    std::pair<int, int> output{-1, -1};
+    int64_t dims[4] = {0, 0, 0, 0};
+    float fparam[2] = {1.f, 1e-5f};
+  };
+  struct Binding {
+    void* ptr = nullptr;
+    int64_t stride = 0;  // bytes between instances; 0 = shared
+    bool on_device = false;
+  };
+  struct Group {  // one device allocation fed by one isolated binding (deduplicated)
+    Binding b;
+    int64_t bytes = 0;  // per instance
+    bool resident = false;
+    bool io = false;
+  };
+  struct Slot {
+    std::map<std::pair<int, int>, void*> buf;  // (kernel,pos) -> device base for this slot
+    std::map<int, void*> group_buf;            // per-instance groups
+    hs_stream_t origin = nullptr;
+    std::map<std::pair<int, int>, hs_stream_t> streams;  // (device, queue)
+    std::map<std::pair<int, int>, hs_event_t> events;    // (component, event)
+    std::map<int, std::pair<int, int>> edge_event;       // edge -> (component, event) of its dependent read
+    std::map<int, hs_event_t> group_event;
+    std::set<int> group_done;
+    hs_graph_t graph = nullptr;
+    hs_event_t t_start = nullptr, t_end = nullptr;
+  };
+
+  void build_nodes();
+  void plan_buffers();
+  void upload_resident();
+  void capture(Slot& sl);
+  hs_stream_t stream(Slot& sl, int device, int queue);
+  hs_event_t event(Slot& sl, int comp, int ev);
+  void issue(Slot& sl, const TaskComponent& t, const CommandQueueStructure& q, int prev_comp,
+             const CommandQueueStructure* prev_q, bool graph, int64_t first, int64_t n);
+  void launch_node(Slot& sl, hs_stream_t s, int kernel);
+  void copy_in(Slot& sl, hs_stream_t s, int group, int64_t first, int64_t n);
+  void copy_out(Slot& sl, hs_stream_t s, int64_t first, int64_t n);
+  void run_dynamic(Slot& sl, int64_t first, int64_t n);
+  Completion wait_completion();
+
+  friend class CudaDispatch;
+
+  EngineConfig cfg_;
+  DagSpec g_;
+  Platform platform_;
+  std::unique_ptr<Scheduler> sched_;
+  ScheduleResult plan_;
+  std::map<int, Node> nodes_;
+  std::map<std::pair<int, int>, Binding> bindings_;
+  std::vector<Group> groups_;
+  std::map<std::pair<int, int>, int> group_of_;                 // isolated input (kernel,pos) -> group
+  std::map<std::pair<int, int>, std::pair<int, int>> alias_;    // input (kernel,pos) -> producer (kernel,pos)
+  std::map<std::pair<int, int>, std::pair<int, int>> io_copy_;  // io input fed by an edge -> producer
+  std::map<std::pair<int, int>, int64_t> bytes_;                // (kernel,pos) -> bytes per instance
+  std::vector<std::pair<int, int>> outputs_;                    // isolated outputs with a binding
+  std::map<int, void*> resident_buf_;
+  hs_ctx_t ctx_ = nullptr;
+  std::vector<Slot> slots_;
+  bool planned_ = false;
+  bool resident_uploaded_ = false;
+  int64_t device_bytes_ = 0;
+  int64_t launches_per_batch_ = 0;
+  int64_t runs_ = 0, batches_run_ = 0;
+  std::vector<void*> allocations_;
+
+  // dynamic-mode completion queue (MPSC: CUDA callback threads -> scheduler thread)
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::deque<Completion> done_q_;
+  std::vector<Completion> last_log_;
+  std::vector<DispatchRecord> last_dispatches_;
+};
+
+}  // namespace hetsim

@@ -1,0 +1,91 @@
+"""The dispatch entry point as a Python object: a DAG template executed on one
+B200 through the native engine (include/hetsim_c.h §3).
+
+    eng = Engine(spec_text, params, batch=64, mode="graph")
+    eng.bind(kernel, pos, host_array)                # per-instance input/output
+    eng.bind(kernel, pos, weights, shared=True)      # resident weights (stride 0)
+    ns = eng.run(first=0, n=4096)
+
+Arrays may be numpy arrays or torch tensors (CPU, ideally pinned; or CUDA
+tensors on the engine's GPU with on_device=True). The engine keeps a reference
+to every bound array.
+"""
+from __future__ import annotations
+
+import ctypes
+import json
+
+from ._native import HetsimError, check, lib
+
+
+def _ptr_and_nbytes(arr):
+    if hasattr(arr, "data_ptr"):  # torch
+        return int(arr.data_ptr()), int(arr.numel() * arr.element_size()), bool(arr.is_cuda)
+    if not arr.flags["C_CONTIGUOUS"]:
+        raise ValueError("bound arrays must be C-contiguous")
+    return int(arr.ctypes.data), int(arr.nbytes), False
+
+
+class Engine:
+    def __init__(self, spec_text: str, params: dict | None = None, *, gpu: int = 0, policy: str = "clustering",
+                 mode: str = "graph", batch: int = 1, slots: int = 2, math: str = "tf32x3", cpu_devices=()):
+        cfg = {"spec": spec_text, "params": dict(params or {}), "gpu": gpu, "policy": policy, "mode": mode,
+               "batch": batch, "slots": slots, "math": math, "cpu_devices": list(cpu_devices)}
+        self._lib = lib()
+        h = ctypes.c_void_p()
+        check(self._lib.hs_engine_create(json.dumps(cfg).encode(), ctypes.byref(h)), "hs_engine_create")
+        self._h = h
+        self._keep = []
+        self.batch = batch
+        self.mode = mode
+
+    def bind(self, kernel: int, pos: int, arr, *, shared: bool = False, stride_bytes: int | None = None):
+        ptr, nbytes, on_dev = _ptr_and_nbytes(arr)
+        if stride_bytes is None:
+            if shared:
+                stride_bytes = 0
+            else:
+                shape = tuple(arr.shape)
+                stride_bytes = nbytes // shape[0] if shape and shape[0] else nbytes
+        check(self._lib.hs_engine_bind(self._h, kernel, pos, ctypes.c_void_p(ptr), stride_bytes, int(on_dev)),
+              "hs_engine_bind")
+        self._keep.append(arr)
+
+    def run(self, first: int = 0, n: int = 1) -> int:
+        ns = ctypes.c_int64(0)
+        check(self._lib.hs_engine_run(self._h, first, n, ctypes.byref(ns)), "hs_engine_run")
+        return ns.value
+
+    def info(self, what: str = "plan") -> dict:
+        p = ctypes.c_void_p()
+        check(self._lib.hs_engine_info(self._h, what.encode(), ctypes.byref(p)), "hs_engine_info")
+        try:
+            return json.loads(ctypes.string_at(p).decode())
+        finally:
+            self._lib.hs_free_string(p)
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            self._lib.hs_engine_destroy(self._h)
+            self._h = ctypes.c_void_p()
+        self._keep.clear()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+def launch_count() -> int:
+    """Node kernels launched through hs_launch in this process (graph replays not included)."""
+    return int(lib().hs_launch_count())
+
+
+__all__ = ["Engine", "HetsimError", "launch_count"]

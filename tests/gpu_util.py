@@ -1,0 +1,51 @@
+"""Helpers for GPU parity tests: run one node operator through the C ABI
+(hs_launch) on torch-allocated device memory, and compare with the oracle."""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from paper_2009_07482_b200 import _native
+
+OPS = {"gemm": 0, "gemm_nt": 1, "gemm_relu": 2, "transpose": 3, "scale": 4, "softmax": 5, "add": 6,
+       "add_layernorm": 7, "concat": 8}
+MATH = {"tf32x3": 0, "tf32": 1, "simt": 2}
+
+_ctx = None
+_stream = None
+
+
+def stream():
+    global _ctx, _stream
+    L = _native.lib()
+    if _stream is None:
+        ctx = ctypes.c_void_p()
+        _native.check(L.hs_ctx_create(0, ctypes.byref(ctx)))
+        s = ctypes.c_void_p()
+        _native.check(L.hs_stream_create(ctx, 0, ctypes.byref(s)))
+        _ctx, _stream = ctx, s
+    return _stream
+
+
+def launch(op, inputs, out, dims, fparam=(1.0, 1e-5), math="tf32x3", batch=1, strides=None, out_stride=None):
+    """inputs/out: torch CUDA float32 tensors shaped [batch, elems] or [elems] (shared)."""
+    L = _native.lib()
+    a = _native.OpArgs()
+    a.n_in = len(inputs)
+    for i, t in enumerate(inputs):
+        a.in_[i] = t.data_ptr()
+        a.in_stride[i] = (strides[i] if strides else (0 if t.dim() == 1 else t.shape[-1]))
+    a.out = out.data_ptr()
+    a.out_stride = out_stride if out_stride is not None else out.shape[-1]
+    for i, d in enumerate(dims):
+        a.dims[i] = d
+    a.fparam[0], a.fparam[1] = fparam
+    _native.check(L.hs_launch(stream(), OPS[op], ctypes.byref(a), MATH[math], batch), f"hs_launch({op})")
+    _native.check(L.hs_stream_sync(stream()), "sync")
+
+
+def normwise(y, ref):
+    y = np.asarray(y, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    return float(np.max(np.abs(y - ref)) / max(np.max(np.abs(ref)), 1e-30))

@@ -1,0 +1,146 @@
+"""Per-operator parity on the B200: sm_100a kernels (through hs_launch) vs the
+CPU oracle (oracle/kernels.c) on identical seeded inputs.
+
+Tolerances (north_star): GEMM in 3xTF32 mode <= 1e-4 normwise relative error
+per output; transpose / concat / scale-by-1/8 / add are bit-exact; softmax and
+add+LayerNorm differ from the sequential oracle only by summation order
+(<= 1e-5 normwise).
+"""
+import numpy as np
+import pytest
+
+from paper_2009_07482_b200.workloads import uniform
+
+pytestmark = pytest.mark.gpu
+
+TOL_TF32X3 = 1e-4
+
+
+def _t(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def _rand(uid, shape, seed=11):
+    n = int(np.prod(shape))
+    return uniform(seed, uid, n).reshape(shape)
+
+
+GEMM_CASES = [
+    # (M, N, K, op, batch, shared_B)
+    (256, 256, 256, "gemm", 1, False),      # C1 fork-join
+    (128, 64, 512, "gemm", 4, True),        # C3 Q/K/V projection (shared weight)
+    (128, 128, 64, "gemm", 3, False),       # C3 QK^T via transpose
+    (128, 128, 64, "gemm_nt", 2, False),    # C2 QK^T
+    (128, 64, 128, "gemm", 2, False),       # PV
+    (128, 64, 64, "gemm", 2, True),         # C W_h
+    (128, 2048, 512, "gemm_relu", 2, True),  # FFN1
+    (128, 512, 2048, "gemm", 2, True),      # FFN2
+    (100, 72, 36, "gemm", 2, False),        # ragged M/N/K tails
+    (130, 200, 44, "gemm_nt", 1, False),
+    (64, 8, 4, "gemm", 1, False),
+]
+
+
+@pytest.mark.parametrize("M,N,K,op,batch,shared", GEMM_CASES)
+@pytest.mark.parametrize("math", ["tf32x3", "simt"])
+def test_gemm_parity(M, N, K, op, batch, shared, math, oracle_mod):
+    from tests.gpu_util import launch, normwise
+    import torch
+    A = _rand(1, (batch, M * K))
+    Bshape = (N * K,) if shared else (batch, N * K)
+    B = _rand(2, Bshape) * np.float32(1.0 / np.sqrt(K))
+    ref = np.empty((batch, M * N), np.float32)
+    oracle_mod.run_node(op, [A, B.astype(np.float32)], [M * K, 0 if shared else N * K], ref, M * N, [M, N, K], batch)
+    out = torch.full((batch, M * N), float("nan"), device="cuda")
+    launch(op, [_t(A), _t(B.astype(np.float32))], out, [M, N, K], math=math, batch=batch)
+    y = out.cpu().numpy()
+    assert np.isfinite(y).all()
+    for b in range(batch):
+        err = normwise(y[b], ref[b])
+        assert err <= (TOL_TF32X3 if math == "tf32x3" else 1e-5), (b, err)
+
+
+def test_gemm_tf32_single_term_is_coarser(oracle_mod):
+    """The 1-term TF32 mode is visibly less accurate than 3xTF32 (sanity of the split)."""
+    from tests.gpu_util import launch, normwise
+    import torch
+    M, N, K = 128, 128, 2048
+    A, B = _rand(3, (1, M * K)), _rand(4, (1, K * N))
+    ref = np.empty((1, M * N), np.float32)
+    oracle_mod.run_node("gemm", [A, B], [M * K, K * N], ref, M * N, [M, N, K], 1)
+    errs = {}
+    for math in ("tf32", "tf32x3"):
+        out = torch.empty((1, M * N), device="cuda")
+        launch("gemm", [_t(A), _t(B)], out, [M, N, K], math=math)
+        errs[math] = normwise(out.cpu().numpy(), ref)
+    assert errs["tf32x3"] <= TOL_TF32X3
+    assert errs["tf32x3"] * 10 < errs["tf32"], errs
+
+
+@pytest.mark.parametrize("R,C,batch", [(128, 64, 3), (64, 128, 1), (37, 45, 2)])
+def test_transpose_bit_exact(R, C, batch, oracle_mod):
+    from tests.gpu_util import launch
+    import torch
+    A = _rand(5, (batch, R * C))
+    ref = np.empty_like(A)
+    oracle_mod.run_node("transpose", [A], [R * C], ref, R * C, [R, C], batch)
+    out = torch.empty((batch, R * C), device="cuda")
+    launch("transpose", [_t(A)], out, [R, C], batch=batch)
+    assert np.array_equal(out.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("n,batch", [(128 * 128, 2), (1001, 3)])
+def test_scale_and_add_bit_exact(n, batch, oracle_mod):
+    from tests.gpu_util import launch
+    import torch
+    A, B = _rand(6, (batch, n)), _rand(7, (batch, n))
+    ref = np.empty_like(A)
+    oracle_mod.run_node("scale", [A], [n], ref, n, [n, 1, 8], batch)
+    out = torch.empty((batch, n), device="cuda")
+    launch("scale", [_t(A)], out, [n], fparam=(0.125, 1e-5), batch=batch)
+    assert np.array_equal(out.cpu().numpy(), ref)
+    oracle_mod.run_node("add", [A, B], [n, n], ref, n, [n], batch)
+    launch("add", [_t(A), _t(B)], out, [n], batch=batch)
+    assert np.array_equal(out.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("rows,cols,batch,num,den", [(128, 128, 3, 1, 8), (128, 512, 1, 1, 1), (17, 100, 2, 1, 1)])
+def test_softmax(rows, cols, batch, num, den, oracle_mod):
+    from tests.gpu_util import launch, normwise
+    import torch
+    A = _rand(8, (batch, rows * cols)) * np.float32(4)
+    ref = np.empty_like(A)
+    oracle_mod.run_node("softmax", [A], [rows * cols], ref, rows * cols, [rows, cols, num, den], batch)
+    out = torch.empty((batch, rows * cols), device="cuda")
+    launch("softmax", [_t(A)], out, [rows, cols], fparam=(num / den, 1e-5), batch=batch)
+    y = out.cpu().numpy()
+    assert normwise(y, ref) <= 1e-5
+    assert np.allclose(y.reshape(-1, cols).sum(axis=1), 1.0, atol=1e-5)
+
+
+@pytest.mark.parametrize("rows,cols,batch", [(128, 512, 2), (9, 96, 3)])
+def test_add_layernorm(rows, cols, batch, oracle_mod):
+    from tests.gpu_util import launch, normwise
+    import torch
+    A, B = _rand(9, (batch, rows * cols)), _rand(10, (batch, rows * cols))
+    g = (1 + 0.1 * _rand(12, (cols,))).astype(np.float32)
+    be = (0.1 * _rand(13, (cols,))).astype(np.float32)
+    ref = np.empty_like(A)
+    oracle_mod.run_node("add_layernorm", [A, B, g, be], [rows * cols, rows * cols, 0, 0], ref, rows * cols,
+                        [rows, cols], batch)
+    out = torch.empty((batch, rows * cols), device="cuda")
+    launch("add_layernorm", [_t(A), _t(B), _t(g), _t(be)], out, [rows, cols], fparam=(1.0, 1e-5), batch=batch)
+    assert normwise(out.cpu().numpy(), ref) <= 1e-5
+
+
+@pytest.mark.parametrize("count,rows,cols,batch", [(8, 128, 64, 2), (3, 5, 7, 2)])
+def test_concat_bit_exact(count, rows, cols, batch, oracle_mod):
+    from tests.gpu_util import launch
+    import torch
+    Z = [_rand(20 + i, (batch, rows * cols)) for i in range(count)]
+    ref = np.empty((batch, rows * cols * count), np.float32)
+    oracle_mod.run_node("concat", Z, [rows * cols] * count, ref, rows * cols * count, [rows, cols], batch)
+    out = torch.empty((batch, rows * cols * count), device="cuda")
+    launch("concat", [_t(z) for z in Z], out, [rows, cols], batch=batch)
+    assert np.array_equal(out.cpu().numpy(), ref)
