@@ -1,0 +1,397 @@
+#!/usr/bin/env python
+"""hetsim-b200 benchmark — BASELINE.json metric:
+"DAG makespan (ms) and inference DAGs/sec at 1/2/4/8 B200 vs roofline & CPU".
+
+Workload (config C5, BASELINE.json configs[4]): a 12-layer transformer-encoder
+DAG (8 heads, d_model 512, seq 128, d_ff 2048; 828 kernels / 1103 edges / 108
+task components, fine-grained: 3 command queues per device, clustering policy)
+over a stream of 4096 independent instances, partitioned contiguously across
+the ranks (one process per GPU, no collective on the data path). One step =
+the whole 4096-instance stream; ms_per_step is its makespan (max over ranks)
+and value = 4096 / makespan [DAGs/s].
+
+  value  device-resident: X (1 GiB) and outputs live in HBM, copied per batch
+         into the engine's slots (D2D) inside the timed region
+  e2e    the same through the public engine API with pinned HOST buffers:
+         H2D of every batch's X and D2H of every output inside the timed region
+
+Usage: python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+Multi-GPU: python -m torch.distributed.run --nproc-per-node N bench.py --gpus N
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import pathlib
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = pathlib.Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "DAG makespan (ms) and inference DAGs/sec at 1/2/4/8 B200 vs roofline & CPU"
+UNIT = "DAGs/s"
+TOTAL_INSTANCES = 4096
+LAYERS = 12
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--instances", type=int, default=TOTAL_INSTANCES)
+    ap.add_argument("--layers", type=int, default=LAYERS)
+    ap.add_argument("--batch", type=int, default=64, help="instances per batched node launch")
+    ap.add_argument("--slots", type=int, default=2)
+    ap.add_argument("--queues", type=int, default=3)
+    ap.add_argument("--math", default="tf32x3")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------------- helpers
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu):
+        self.gpu = gpu
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        try:
+            for line in open(self.path):
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        except OSError:
+            pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        smax = max(float(r[2]) for r in rows if r[2].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        loaded = [s for s in sm if s > 0.5 * smax] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": smax, "reasons": reasons, "samples": len(rows)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def reduce_max(world, x, local):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def partition(total, world, rank):
+    per = math.ceil(total / world)
+    first = min(total, rank * per)
+    return first, max(0, min(per, total - first))
+
+
+# --------------------------------------------------------------------------- CPU arms (oracle port)
+
+def cpu_sample(layers, n_inst=1, reps=1):
+    """The CPU restatement (oracle/: clustering scheduler + fp32 kernels) on a bounded
+    sample of the same workload; returns (instances/s, threads, seconds)."""
+    from oracle import oracle as O
+    from paper_2009_07482_b200 import workloads
+    text, params, meta = workloads.encoder(layers=layers)
+    x = workloads.encoder_inputs(meta, params, n_inst).reshape(n_inst, -1)
+    arrays = {(i["kernel"], i["pos"]): x for i in meta["x_inputs"]}
+    for k, w in workloads.encoder_weights(meta).items():
+        arrays[k] = w.reshape(-1)
+    spec = O.Spec(text, params)
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        O.schedule(spec)  # the restated Alg. 1 (clustering) decides the dispatch order
+        O.run_dag(text, params, arrays, n_inst)
+        times.append(time.perf_counter() - t0)
+    t = min(times)
+    return n_inst / t, O.max_threads(), t
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    layers = args.layers
+    vals = []
+    for i in range(args.warmup + args.steps):
+        v, threads, t = cpu_sample(layers, n_inst=1)
+        if i >= args.warmup:
+            vals.append(v)
+    v = statistics.mean(vals)
+    sample = f"1 instance of the {layers}-layer encoder DAG per step (CPU oracle port: clustering + fp32 kernels)"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1000.0 / v, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"C5 {layers}-layer encoder DAG stream, {args.instances} instances (CPU sample)",
+                   "instances": args.instances, "layers": layers, "kernels": 69 * layers},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- GPU arm
+
+def gemm_roofline(batch, tflops_peak, reps=20):
+    """Time the dominant kernel (FFN1: gemm_relu 128x2048x512 per instance, batched like
+    the graph launches it) live on its own stream with CUDA events; returns achieved TFLOP/s."""
+    import ctypes
+
+    import torch
+
+    from paper_2009_07482_b200 import _native
+    L = _native.lib()
+    M, N, K = 128, 2048, 512
+    A = torch.randn(batch, M * K, device="cuda")
+    W = torch.randn(K * N, device="cuda")
+    C = torch.empty(batch, M * N, device="cuda")
+    ctx, st, e0, e1 = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+    _native.check(L.hs_ctx_create(torch.cuda.current_device(), ctypes.byref(ctx)))
+    _native.check(L.hs_stream_create(ctx, 0, ctypes.byref(st)))
+    _native.check(L.hs_event_create(ctx, 1, ctypes.byref(e0)))
+    _native.check(L.hs_event_create(ctx, 1, ctypes.byref(e1)))
+    a = _native.OpArgs()
+    a.n_in = 2
+    a.in_[0], a.in_[1] = A.data_ptr(), W.data_ptr()
+    a.in_stride[0], a.in_stride[1] = M * K, 0
+    a.out, a.out_stride = C.data_ptr(), M * N
+    a.dims[0], a.dims[1], a.dims[2] = M, N, K
+    for _ in range(3):
+        _native.check(L.hs_launch(st, 2, ctypes.byref(a), 0, batch))
+    _native.check(L.hs_stream_sync(st))
+    _native.check(L.hs_event_record(e0, st))
+    for _ in range(reps):
+        _native.check(L.hs_launch(st, 2, ctypes.byref(a), 0, batch))
+    _native.check(L.hs_event_record(e1, st))
+    _native.check(L.hs_event_sync(e1))
+    ns = ctypes.c_int64()
+    _native.check(L.hs_event_elapsed_ns(e0, e1, ctypes.byref(ns)))
+    t = ns.value / 1e9 / reps
+    flops = 2.0 * M * N * K * batch
+    for h in (e0, e1):
+        L.hs_event_destroy(h)
+    L.hs_stream_destroy(st)
+    L.hs_ctx_destroy(ctx)
+    return flops / t / 1e12, t * 1e3, flops
+
+
+def tf32_cublas_peak():
+    """cuBLAS TF32 dense throughput at 8192^3 (the tensor peak the 3xTF32 path is held to)."""
+    import torch
+    torch.backends.cuda.matmul.allow_tf32 = True
+    n = 8192
+    a = torch.randn(n, n, device="cuda")
+    b = torch.randn(n, n, device="cuda")
+    for _ in range(3):
+        torch.matmul(a, b)
+    torch.cuda.synchronize()
+    best = 1e9
+    for _ in range(5):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        torch.matmul(a, b)
+        e.record()
+        e.synchronize()
+        best = min(best, s.elapsed_time(e) / 1e3)
+    torch.backends.cuda.matmul.allow_tf32 = False
+    del a, b
+    return 2.0 * n ** 3 / best / 1e12
+
+
+def run_ours(args, world, rank, local):
+    import numpy as np
+    import torch
+
+    from paper_2009_07482_b200 import workloads
+    from paper_2009_07482_b200.engine import Engine
+
+    torch.cuda.set_device(local)
+    text, params, meta = workloads.encoder(layers=args.layers, queues=args.queues)
+    first, n = partition(args.instances, world, rank)
+    S, D = params["S"], params["D"]
+    inst_bytes = S * D * 4
+    weights = workloads.encoder_weights(meta)
+    x_np = workloads.encoder_inputs(meta, params, n, first=first).reshape(n, S * D)
+    out_key = (meta["output"]["kernel"], meta["output"]["pos"])
+
+    def make_engine(x, out):
+        eng = Engine(text, params, gpu=local, batch=args.batch, slots=args.slots, math=args.math, mode="graph")
+        for i in meta["x_inputs"]:
+            eng.bind(i["kernel"], i["pos"], x)
+        for key, w in weights.items():
+            eng.bind(*key, w.reshape(-1), shared=True)
+        eng.bind(*out_key, out)
+        return eng
+
+    # device-resident arm
+    x_dev = torch.from_numpy(x_np).cuda()
+    out_dev = torch.empty(n, S * D, device="cuda")
+    eng_d = make_engine(x_dev, out_dev)
+
+    def timed(eng, steps):
+        tot = 0
+        for _ in range(steps):
+            tot += eng.run(0, n)
+        return tot / 1e9
+
+    for _ in range(args.warmup):
+        eng_d.run(0, n)
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        dev_s = timed(eng_d, args.steps)
+    torch.cuda.synchronize()
+    barrier(world)
+    dev_s = reduce_max(world, dev_s, local)
+    ms_per_step = dev_s / args.steps * 1e3
+    value = args.instances / (ms_per_step / 1e3)
+    stats = eng_d.info("stats")
+    plan = eng_d.info("plan")
+    launches = int(stats["launches_per_batch"]) * math.ceil(n / args.batch) * args.steps
+
+    # end-to-end arm through the public API with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        eng_d.close()
+        del x_dev, out_dev
+        torch.cuda.empty_cache()
+        x_host = torch.from_numpy(x_np).pin_memory()
+        out_host = torch.empty(n, S * D).pin_memory()
+        eng_h = make_engine(x_host, out_host)
+        for _ in range(args.warmup):
+            eng_h.run(0, n)
+        barrier(world)
+        torch.cuda.synchronize()
+        e2e_s = timed(eng_h, args.steps)
+        barrier(world)
+        e2e_s = reduce_max(world, e2e_s, local)
+        e2e = {"value": args.instances / (e2e_s / args.steps), "unit": UNIT,
+               "h2d_bytes_per_step": args.instances * inst_bytes, "d2h_bytes_per_step": args.instances * inst_bytes,
+               "ms_per_step": e2e_s / args.steps * 1e3}
+        ref = workloads.encoder_inputs(meta, params, 1, first=first).reshape(-1)
+        assert np.array_equal(x_host[0].numpy(), ref)
+        assert torch.isfinite(out_host).all()
+        eng_h.close()
+
+    line = None
+    if rank == 0:
+        pk, pk_kind = peaks()
+        tf32 = tf32_cublas_peak()
+        achieved, ms_launch, flops = gemm_roofline(args.batch, tf32)
+        peak3 = tf32 / 3.0
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            v, threads, t = cpu_sample(args.layers, n_inst=1)
+            cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+                   "sample": f"1 instance of the {args.layers}-layer DAG ({t:.1f} s), oracle port, all host threads"}
+        flop_per_inst = 782.2e6 * args.layers
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32 (3xTF32 tcgen05)" if args.math == "tf32x3" else args.math,
+            "data": "synthetic (splitmix64 uniform inputs, random-init weights)",
+            "config": {"workload": f"C5: {args.layers}-layer encoder DAG (8 heads, d_model 512, seq 128, d_ff 2048), "
+                                   f"stream of {args.instances} instances",
+                       "kernels_per_dag": plan["kernels"], "edges": plan["edges"], "components": plan["components"],
+                       "policy": "clustering", "queues_per_device": args.queues, "batch": args.batch,
+                       "slots": args.slots, "mode": "graph", "parallelism": f"instance partition x{world}",
+                       "l2": "inputs (1 GiB X + 1 GiB out per step) larger than L2"},
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak3, "unit": "TFLOP/s",
+                         "frac": achieved / peak3, "traffic": None,
+                         "kernel": f"gemm_relu tcgen05 3xTF32 128x2048x512 x{args.batch} ({ms_launch:.3f} ms/launch)",
+                         "peak_note": f"cuBLAS TF32 measured in-run {tf32:.0f} TFLOP/s / 3 MMAs per product"},
+            "dag_roofline": {"flop_per_dag": flop_per_inst, "achieved_tflops": flop_per_inst * value / 1e12,
+                             "frac_of_3xtf32": flop_per_inst * value / 1e12 / (peak3 * world)},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "device_bytes": plan["device_bytes"],
+        }
+    return line
+
+
+def main():
+    args = parse_args()
+    world, rank, local = dist_setup()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+    line = run_ours(args, world, rank, local)
+    if rank == 0 and line is not None:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
