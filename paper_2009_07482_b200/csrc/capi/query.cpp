@@ -21,6 +21,10 @@
 using namespace hetsim;
 using json::Value;
 
+namespace hetsim {
+json::Value spec_to_json(const DagSpec& g);  // spec_model.cpp
+}
+
 namespace {
 
 Value V(long long i) { return Value::of(i); }
@@ -178,7 +182,11 @@ Value run(const Value& req) {
   }
   DagSpec g = parse_spec(req.at("spec").as_string(), params_of(req));
   if (op == "parse") {
-    out.set("serialized", S(serialize(g)));
+    const Value* style = req.find("json_style");
+    if (style && style->as_string() == "cudnn-fe")
+      out.set("serialized", S(json::dump(spec_to_json(g), 2, json::Style::fe_compact_int_arrays) + "\n"));
+    else
+      out.set("serialized", S(serialize(g)));
   } else if (op == "analyze") {
     out.set("analysis", analyze(g));
   } else if (op == "ready") {

@@ -407,14 +407,21 @@ static void format_double(std::string& out, double d) {
   out += s;
 }
 
-void dump_into(const Value& v, std::string& out, int indent, int depth) {
+void dump_into(const Value& v, std::string& out, int indent, int depth, Style style) {
+  // cudnn-frontend's patched nlohmann prints arrays whose first element is an
+  // integer on one line, elements fully compact.
+  if (indent >= 0 && style == Style::fe_compact_int_arrays && v.kind_ == Kind::array && !v.arr_.empty() &&
+      (v.arr_[0].kind_ == Kind::integer || v.arr_[0].kind_ == Kind::unsigned_integer)) {
+    dump_into(v, out, -1, depth, style);
+    return;
+  }
   if (indent < 0) {  // compact form: no whitespace at all
     switch (v.kind_) {
       case Kind::array:
         out += '[';
         for (size_t i = 0; i < v.arr_.size(); ++i) {
           if (i) out += ',';
-          dump_into(v.arr_[i], out, indent, depth);
+          dump_into(v.arr_[i], out, indent, depth, style);
         }
         out += ']';
         return;
@@ -424,7 +431,7 @@ void dump_into(const Value& v, std::string& out, int indent, int depth) {
           if (i) out += ',';
           append_escaped(out, v.obj_[i].first);
           out += ':';
-          dump_into(v.obj_[i].second, out, indent, depth);
+          dump_into(v.obj_[i].second, out, indent, depth, style);
         }
         out += '}';
         return;
@@ -447,7 +454,7 @@ void dump_into(const Value& v, std::string& out, int indent, int depth) {
       out += "[\n";
       for (size_t i = 0; i < v.arr_.size(); ++i) {
         pad(depth + 1);
-        dump_into(v.arr_[i], out, indent, depth + 1);
+        dump_into(v.arr_[i], out, indent, depth + 1, style);
         out += (i + 1 < v.arr_.size()) ? ",\n" : "\n";
       }
       pad(depth);
@@ -463,7 +470,7 @@ void dump_into(const Value& v, std::string& out, int indent, int depth) {
         pad(depth + 1);
         append_escaped(out, v.obj_[i].first);
         out += ": ";
-        dump_into(v.obj_[i].second, out, indent, depth + 1);
+        dump_into(v.obj_[i].second, out, indent, depth + 1, style);
         out += (i + 1 < v.obj_.size()) ? ",\n" : "\n";
       }
       pad(depth);
@@ -472,9 +479,9 @@ void dump_into(const Value& v, std::string& out, int indent, int depth) {
   }
 }
 
-std::string dump(const Value& v, int indent) {
+std::string dump(const Value& v, int indent, Style style) {
   std::string out;
-  dump_into(v, out, indent, 0);
+  dump_into(v, out, indent, 0, style);
   return out;
 }
 

@@ -27,6 +27,10 @@ struct TypeError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
 
+/// Pretty-print dialect: stock nlohmann 3.11.3, or the cudnn-frontend patched
+/// copy (integer arrays on one line) that the oracle build links against.
+enum class Style : uint8_t { stock, fe_compact_int_arrays };
+
 enum class Kind : uint8_t { null, boolean, integer, unsigned_integer, floating, string, array, object };
 
 class Value {
@@ -86,12 +90,12 @@ class Value {
   std::string s_;
   std::vector<Value> arr_;
   std::vector<std::pair<std::string, Value>> obj_;
-  friend void dump_into(const Value& v, std::string& out, int indent, int depth);
+  friend void dump_into(const Value& v, std::string& out, int indent, int depth, Style style);
 };
 
 Value parse(std::string_view text);
 /// Printer compatible with nlohmann::ordered_json::dump(indent); indent < 0 = compact.
-std::string dump(const Value& v, int indent);
+std::string dump(const Value& v, int indent, Style style = Style::stock);
 /// Appends a JSON string literal (with quotes) using nlohmann's escaping.
 void append_escaped(std::string& out, std::string_view s);
 

@@ -358,7 +358,7 @@ Value buffer_list(const std::vector<BufferSpec>& v) {
 
 }  // namespace
 
-std::string serialize(const DagSpec& g) {
+json::Value spec_to_json(const DagSpec& g) {
   Value root = Value::make_object();
   Value kernels = Value::make_array();
   for (const auto& k : g.kernels) {
@@ -411,8 +411,10 @@ std::string serialize(const DagSpec& g) {
     deps.push_back(std::move(r));
   }
   root.set("depends", std::move(deps));
-  return json::dump(root, 2) + "\n";
+  return root;
 }
+
+std::string serialize(const DagSpec& g) { return json::dump(spec_to_json(g), 2) + "\n"; }
 
 long long buffer_bytes(const BufferSpec& b, const ParamMap& params) {
   __int128 bytes = __int128(eval_positive(b.size_expr, params)) * elem_width(b.type);
