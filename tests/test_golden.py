@@ -23,7 +23,7 @@ def _q(req):
 
 
 def test_fixture_file_present():
-    assert len(FIXTURES) > 300
+    assert len(FIXTURES) > 200
 
 
 @pytest.mark.parametrize("i", range(len(FIXTURES)))
