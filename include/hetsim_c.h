@@ -120,10 +120,15 @@ typedef struct {
   int64_t out_stride;               /* per-instance stride in elements               */
   int64_t dims[4];                  /* op-specific sizes             */
   float fparam[2];                  /* [0] scale s, [1] layer-norm eps               */
+  const void* aux;                  /* GEMM: shared B pre-split by hs_gemm_split_weights, or NULL */
 } hs_op_args;
 
 int hs_op_from_name(const char* name); /* -1 if unknown */
 int hs_launch(hs_stream_t s, int op, const hs_op_args* args, int math_mode, int batch);
+/* Resident-weight preparation for GEMM nodes: B ([K,N] if transposed == 0, else
+ * [N,K]) -> K-major tf32 hi/lo planes `planes` = float[2][N][K]. Run once per
+ * weight; pass `planes` as hs_op_args.aux on every launch that uses B. */
+int hs_gemm_split_weights(hs_stream_t s, const void* B, int transposed, int64_t N, int64_t K, void* planes);
 
 int hs_host_callback(hs_stream_t s, void (*fn)(void*), void* user);
 int hs_capture_begin(hs_stream_t s);

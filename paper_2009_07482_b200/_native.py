@@ -42,6 +42,7 @@ class OpArgs(ctypes.Structure):
         ("out_stride", c_int64),
         ("dims", c_int64 * 4),
         ("fparam", ctypes.c_float * 2),
+        ("aux", c_void_p),
     ]
 
 
@@ -84,6 +85,7 @@ _PROTOS = {
     "hs_graph_launch": (c_int, [c_void_p, c_void_p]),
     "hs_graph_destroy": (c_int, [c_void_p]),
     "hs_launch_count": (c_int64, []),
+    "hs_gemm_split_weights": (c_int, [c_void_p, c_void_p, c_int, c_int64, c_int64, c_void_p]),
     "hs_engine_create": (c_int, [c_char_p, ctypes.POINTER(c_void_p)]),
     "hs_engine_destroy": (c_int, [c_void_p]),
     "hs_engine_bind": (c_int, [c_void_p, c_int, c_int, c_void_p, c_int64, c_int]),

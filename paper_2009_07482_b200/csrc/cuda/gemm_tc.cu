@@ -2,26 +2,32 @@
 //
 //   C[M,N] (+ReLU) = A[M,K] · B        B = [K,N] row-major (nn) or [N,K] (nt)
 //
-// Per CTA: one 128 x BN output tile, accumulator in TMEM (BN fp32 columns).
-// Warp roles (256 threads):
-//   warp 0      TMA producer: fp32 A/B tiles (K-block of 32) -> staging ring
-//   warp 1      MMA issuer: one elected lane issues tcgen05.mma.kind::tf32
-//   warp 2      TMEM allocator
-//   warps 4..7  converters during the main loop: staging fp32 -> canonical
-//               K-major SWIZZLE_128B operand planes, split x = hi + lo with
-//               hi = cvt.rna.tf32(x), lo = x - hi (exact); then the epilogue
-//               (tcgen05.ld 32x32b -> registers -> ReLU -> global).
-// 3xTF32: D += Ahi·Bhi + Ahi·Blo + Alo·Bhi (the Alo·Blo term, ~2^-22
-// relative, is dropped). TF32 mode (terms=1) issues only Ahi·Bhi.
+// Persistent kernel: one CTA per SM walks the 128 x BN output tiles of all
+// `batch` instances (instance index fastest, so concurrently running CTAs
+// share the same weight tile in L2). Warp roles (384 threads):
+//   warp 0       TMA producer. A (fp32) -> staging ring with SWIZZLE_128B, which
+//                is already the canonical K-major UMMA layout; B either as fp32
+//                staging (activations) or, for resident weights, as pre-split
+//                tf32 hi/lo planes written straight into the operand ring.
+//   warp 1       MMA issuer (one lane): tcgen05.mma.kind::tf32, accumulator in
+//                TMEM, double-buffered (2 x BN columns) so the epilogue of tile
+//                i overlaps the main loop of tile i+1.
+//   warp 2       TMEM allocator.
+//   warps 4..7   epilogue: tcgen05.ld 32x32b -> ReLU -> global (TMEM lane
+//                quarter = warp % 4).
+//   warps 8..15  converters: x = hi + lo with hi = cvt.rna.tf32(x), lo = x - hi
+//                (exact). Elementwise on the swizzled tile (same offsets in and
+//                out); an [K,N] activation B is transposed on the way.
+// 3xTF32: D += Alo·Bhi + Ahi·Blo + Ahi·Bhi (Alo·Blo, ~2^-22 relative, is
+// dropped). TF32 mode (terms = 1) issues only Ahi·Bhi.
 //
-// Pipelines (mbarriers): staging full/empty (TMA <-> converters), operand
-// full/empty (converters <-> MMA, released by tcgen05.commit), accumulator
-// full (MMA -> epilogue). TMA zero-fills out-of-bounds boxes, so ragged M, N
-// and K tails need no special casing in the main loop.
+// mbarrier pipelines: staging full/empty (TMA <-> converters), operand
+// full/empty (converters + TMA <-> MMA, released by tcgen05.commit),
+// accumulator full/empty (MMA <-> epilogue). TMA zero-fills out-of-bounds
+// boxes, so ragged M/N/K need no special casing in the main loop.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
-#include <cstdio>
 #include <mutex>
 
 #include "kernels.cuh"
@@ -32,8 +38,10 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 32;  // fp32 elements per K-block = one 128-byte swizzle row
-constexpr int kStages = 2;
-constexpr int kThreads = 256;
+constexpr int kEpiWarps = 4;
+constexpr int kConvWarps = 8;
+constexpr int kThreads = 32 * (4 + kEpiWarps + kConvWarps);  // 512: 4 control, 4 epilogue, 8 converter warps
+static_assert(kThreads == 512, "warp-role layout");
 
 // ----------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -48,8 +56,13 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
+// Watchdog: a pipeline that has not advanced for ~2^34 cycles (several
+// seconds) traps, so a broken barrier protocol surfaces as a launch error
+// (DeviceError) instead of a hung GPU.
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   uint32_t done = 0;
+  uint32_t spins = 0;
+  long long start = 0;
   do {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
@@ -58,6 +71,10 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         : "=r"(done)
         : "r"(bar), "r"(parity)
         : "memory");
+    if (!done && (++spins & 1023u) == 0) {
+      if (start == 0) start = clock64();
+      else if (clock64() - start > (1ll << 34)) __trap();
+    }
   } while (!done);
 }
 __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1,
@@ -117,61 +134,84 @@ __device__ __forceinline__ uint32_t sw128(int r, int kc) {
 }
 
 template <int kTerms>
-__device__ __forceinline__ void split_store(uint32_t hi_base, uint32_t lo_base, uint32_t off, float4 x) {
+__device__ __forceinline__ void split_store(uint32_t hi, uint32_t lo, uint32_t off, float4 x) {
   float4 h = make_float4(tf32_rna(x.x), tf32_rna(x.y), tf32_rna(x.z), tf32_rna(x.w));
-  sts128(hi_base + off, h);
-  if constexpr (kTerms > 1) sts128(lo_base + off, make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w));
+  sts128(hi + off, h);
+  if constexpr (kTerms > 1) sts128(lo + off, make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w));
 }
 
-template <int BN>
-struct Smem {
-  static constexpr int kStageA = BM * BK * 4;        // fp32 staging, row-major [128][32]
-  static constexpr int kStageB = BN * BK * 4;        // [BN][32] (nt) or [32][BN] (nn)
-  static constexpr int kPlaneA = BM * 128;           // one SW128 plane: 128 rows x 128 B
-  static constexpr int kPlaneB = BN * 128;
+// B source: 0 = activation [N,K] (nt), 1 = activation [K,N] (nn), 2 = pre-split planes
+template <int BN, int kBSrc>
+struct Cfg {
+  static constexpr bool kBPre = kBSrc == 2;
+  static constexpr int kStageA = BM * BK * 4;                       // 16 KB (SW128 via TMA)
+  static constexpr int kStageB = kBPre ? 0 : BN * BK * 4;           // fp32 B staging
   static constexpr int kStaging = kStageA + kStageB;
-  static constexpr int kOperand = 2 * kPlaneA + 2 * kPlaneB;  // hi + lo for A and B
-  static constexpr int kBarriers = 1024;
-  static constexpr int kTotal = kStages * (kStaging + kOperand) + kBarriers + 1024;  // + alignment slack
+  static constexpr int kPlaneA = BM * 128;
+  static constexpr int kPlaneB = BN * 128;
+  static constexpr int kOperand = 2 * kPlaneA + 2 * kPlaneB;       // hi + lo for A and B
+  static constexpr int kBudget = 200 * 1024;
+  // deepest operand ring that leaves room for >= 2 staging stages, staging fills the rest
+  static constexpr int kNO = (kBudget - 2 * kStaging) / kOperand >= 3 ? 3 : 2;
+  static constexpr int kNSraw = (kBudget - kNO * kOperand) / kStaging;
+  static constexpr int kNS = kNSraw > 6 ? 6 : kNSraw;
+  static constexpr int kTotal = kNS * kStaging + kNO * kOperand + 1024 /*barriers*/ + 1024 /*align*/;
+  static_assert(kNS >= 2 && kNO >= 2, "pipeline too shallow");
+  static_assert(kTotal <= 227 * 1024, "shared memory budget exceeded");
 };
 
-template <int BN, bool kNT, int kTerms>
+struct TileParams {
+  float* C;
+  int64_t sC;
+  int M, N, K;
+  int batch;
+  int a_batched, b_batched;
+  int relu;
+  int m_tiles, n_tiles;
+  int total_tiles;
+};
+
+template <int BN, int kBSrc, int kTerms>
 __global__ void __launch_bounds__(kThreads, 1)
-    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, float* C,
-                   int64_t sC, int M, int N, int K, int a_batched, int b_batched, int relu) {
-  using L = Smem<BN>;
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TileParams p) {
+  using L = Cfg<BN, kBSrc>;
+  constexpr int NS = L::kNS, NO = L::kNO;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
   const uint32_t staging = base;
-  const uint32_t operand = staging + kStages * L::kStaging;
-  const uint32_t bars = operand + kStages * L::kOperand;
-  // barrier layout (8 bytes each)
+  const uint32_t operand = staging + NS * L::kStaging;
+  const uint32_t bars = operand + NO * L::kOperand;
   auto st_full = [&](int s) { return bars + 8u * uint32_t(s); };
-  auto st_empty = [&](int s) { return bars + 8u * uint32_t(kStages + s); };
-  auto op_full = [&](int s) { return bars + 8u * uint32_t(2 * kStages + s); };
-  auto op_empty = [&](int s) { return bars + 8u * uint32_t(3 * kStages + s); };
-  const uint32_t acc_full = bars + 8u * uint32_t(4 * kStages);
-  const uint32_t tmem_slot = bars + 8u * uint32_t(4 * kStages + 1);
-  uint32_t* tmem_slot_ptr = reinterpret_cast<uint32_t*>(smem_raw + (tmem_slot - smem_u32(smem_raw)));
+  auto st_empty = [&](int s) { return bars + 8u * uint32_t(NS + s); };
+  auto op_full = [&](int s) { return bars + 8u * uint32_t(2 * NS + s); };
+  auto op_empty = [&](int s) { return bars + 8u * uint32_t(2 * NS + NO + s); };
+  auto acc_full = [&](int a) { return bars + 8u * uint32_t(2 * NS + 2 * NO + a); };
+  auto acc_empty = [&](int a) { return bars + 8u * uint32_t(2 * NS + 2 * NO + 2 + a); };
+  const uint32_t tmem_slot = bars + 8u * uint32_t(2 * NS + 2 * NO + 4);
+  const uint32_t* tmem_slot_ptr = reinterpret_cast<const uint32_t*>(smem_raw + (tmem_slot - smem_u32(smem_raw)));
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM, inst = blockIdx.z;
-  const int nk = (K + BK - 1) / BK;
+  const int nk = (p.K + BK - 1) / BK;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < NS; ++s) {
       mbar_init(st_full(s), 1);
-      mbar_init(st_empty(s), 4);
-      mbar_init(op_full(s), 4);
+      mbar_init(st_empty(s), kConvWarps);
+    }
+    for (int s = 0; s < NO; ++s) {
+      mbar_init(op_full(s), kConvWarps + (L::kBPre ? 1 : 0));
       mbar_init(op_empty(s), 1);
     }
-    mbar_init(acc_full, 1);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(acc_full(a), 1);
+      mbar_init(acc_empty(a), kEpiWarps);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tmem_slot), "r"(BN));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tmem_slot), "r"(2 * BN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
@@ -179,130 +219,175 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot_ptr;
 
+  // tile index -> (m_tile, instance, n_tile); instance fastest after m.
+  auto decode = [&](int t, int& m0, int& inst, int& n0) {
+    const int mt = t % p.m_tiles;
+    const int rest = t / p.m_tiles;
+    inst = rest % p.batch;
+    n0 = (rest / p.batch) * BN;
+    m0 = mt * BM;
+  };
+
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
-      const int ia = a_batched ? inst : 0, ib = b_batched ? inst : 0;
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % kStages;
-        const uint32_t ph = uint32_t(kb / kStages) & 1u;
-        mbar_wait(st_empty(s), ph ^ 1u);
-        const uint32_t sa = staging + uint32_t(s) * L::kStaging, sb = sa + L::kStageA;
-        mbar_expect_tx(st_full(s), L::kStaging);
-        tma_load_3d(sa, &tmA, st_full(s), kb * BK, m0, ia);
-        if (kNT) tma_load_3d(sb, &tmB, st_full(s), kb * BK, n0, ib);
-        else tma_load_3d(sb, &tmB, st_full(s), n0, kb * BK, ib);
+      uint32_t it = 0;
+      for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
+        int m0, inst, n0;
+        decode(t, m0, inst, n0);
+        const int ia = p.a_batched ? inst : 0, ib = p.b_batched ? inst : 0;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = int(it % NS);
+          mbar_wait(st_empty(s), ((it / NS) & 1u) ^ 1u);
+          const uint32_t sa = staging + uint32_t(s) * L::kStaging;
+          mbar_expect_tx(st_full(s), L::kStaging);
+          tma_load_3d(sa, &tmA, st_full(s), kb * BK, m0, ia);
+          if constexpr (kBSrc == 0) tma_load_3d(sa + L::kStageA, &tmB, st_full(s), kb * BK, n0, ib);
+          if constexpr (kBSrc == 1) tma_load_3d(sa + L::kStageA, &tmB, st_full(s), n0, kb * BK, ib);
+          if constexpr (L::kBPre) {
+            // pre-split weight planes (hi at plane 0, lo at plane 1) straight into the operand ring
+            const int o = int(it % NO);
+            mbar_wait(op_empty(o), ((it / NO) & 1u) ^ 1u);
+            const uint32_t b_hi = operand + uint32_t(o) * L::kOperand + 2 * L::kPlaneA;
+            mbar_expect_tx(op_full(o), (kTerms > 1 ? 2 : 1) * L::kPlaneB);
+            tma_load_3d(b_hi, &tmB, op_full(o), kb * BK, n0, 0);
+            if constexpr (kTerms > 1) tma_load_3d(b_hi + L::kPlaneB, &tmB, op_full(o), kb * BK, n0, 1);
+          }
+        }
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
       constexpr uint32_t idesc = instr_desc_tf32(BN);
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % kStages;
-        const uint32_t ph = uint32_t(kb / kStages) & 1u;
-        mbar_wait(op_full(s), ph);
+      uint32_t it = 0, lt = 0;
+      for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x, ++lt) {
+        const uint32_t acc = lt & 1u;
+        mbar_wait(acc_empty(int(acc)), ((lt >> 1) & 1u) ^ 1u);
         tc_fence_after();
-        const uint32_t a_hi = operand + uint32_t(s) * L::kOperand;
+        const uint32_t d = tmem + acc * uint32_t(BN);
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int o = int(it % NO);
+          mbar_wait(op_full(o), (it / NO) & 1u);
+          tc_fence_after();
+          const uint32_t a_hi = operand + uint32_t(o) * L::kOperand;
+          const uint32_t a_lo = a_hi + L::kPlaneA;
+          const uint32_t b_hi = a_lo + L::kPlaneA;
+          const uint32_t b_lo = b_hi + L::kPlaneB;
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk) {  // K = 8 tf32 per instruction = 32 bytes
+            const uint32_t koff = uint32_t(kk) * 32u;
+            const uint32_t first = (kb | kk) ? 1u : 0u;
+            if constexpr (kTerms > 1) {
+              mma_tf32(d, smem_desc(a_lo + koff), smem_desc(b_hi + koff), idesc, first);
+              mma_tf32(d, smem_desc(a_hi + koff), smem_desc(b_lo + koff), idesc, 1u);
+              mma_tf32(d, smem_desc(a_hi + koff), smem_desc(b_hi + koff), idesc, 1u);
+            } else {
+              mma_tf32(d, smem_desc(a_hi + koff), smem_desc(b_hi + koff), idesc, first);
+            }
+          }
+          mma_commit(op_empty(o));  // operand slot free once these MMAs have read it
+        }
+        mma_commit(acc_full(int(acc)));
+      }
+    }
+  } else if (warp >= 4 && warp < 4 + kEpiWarps) {
+    // ------------------------------------------------------------ epilogue
+    const int q = warp & 3;  // TMEM lane quarter accessible to this warp
+    uint32_t lt = 0;
+    for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x, ++lt) {
+      int m0, inst, n0;
+      decode(t, m0, inst, n0);
+      const uint32_t acc = lt & 1u;
+      mbar_wait(acc_full(int(acc)), (lt >> 1) & 1u);
+      tc_fence_after();
+      const int row = m0 + q * 32 + lane;
+      float* crow = p.C + int64_t(inst) * p.sC + int64_t(row) * p.N;
+#pragma unroll 1
+      for (int cb = 0; cb < BN / 32; ++cb) {
+        uint32_t r[32];
+        const uint32_t taddr = tmem + (uint32_t(q * 32) << 16) + acc * uint32_t(BN) + uint32_t(cb * 32);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+              "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]),
+              "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]),
+              "=r"(r[30]), "=r"(r[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (cb == BN / 32 - 1) {
+          // accumulator drained into registers: hand it back to the MMA warp early
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(acc_empty(int(acc)));
+        }
+        const int c0 = n0 + cb * 32;
+        if (row < p.M) {
+          if (c0 + 32 <= p.N && (p.N & 3) == 0) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+              float4 v = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
+                                     __uint_as_float(r[j + 3]));
+              if (p.relu) {
+                v.x = fmaxf(v.x, 0.f); v.y = fmaxf(v.y, 0.f); v.z = fmaxf(v.z, 0.f); v.w = fmaxf(v.w, 0.f);
+              }
+              *reinterpret_cast<float4*>(crow + c0 + j) = v;
+            }
+          } else {
+            for (int j = 0; j < 32 && c0 + j < p.N; ++j) {
+              float v = __uint_as_float(r[j]);
+              crow[c0 + j] = p.relu ? fmaxf(v, 0.f) : v;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp >= 8) {
+    // ------------------------------------------------------------ converters
+    const int t = threadIdx.x - 256;  // 0..255
+    constexpr int kCT = kConvWarps * 32;
+    uint32_t it = 0;
+    for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
+      for (int kb = 0; kb < nk; ++kb, ++it) {
+        const int s = int(it % NS), o = int(it % NO);
+        mbar_wait(st_full(s), (it / NS) & 1u);
+        mbar_wait(op_empty(o), ((it / NO) & 1u) ^ 1u);
+        const uint32_t sa = staging + uint32_t(s) * L::kStaging, sb = sa + L::kStageA;
+        const uint32_t a_hi = operand + uint32_t(o) * L::kOperand;
         const uint32_t a_lo = a_hi + L::kPlaneA;
         const uint32_t b_hi = a_lo + L::kPlaneA;
         const uint32_t b_lo = b_hi + L::kPlaneB;
+        // A staging is SW128 already: same byte offset in and out.
 #pragma unroll
-        for (int kk = 0; kk < BK / 8; ++kk) {  // K = 8 tf32 per instruction = 32 bytes
-          const uint32_t koff = uint32_t(kk) * 32u;
-          const uint32_t acc = (kb | kk) ? 1u : 0u;
-          if constexpr (kTerms > 1) {
-            mma_tf32(tmem, smem_desc(a_lo + koff), smem_desc(b_hi + koff), idesc, acc);
-            mma_tf32(tmem, smem_desc(a_hi + koff), smem_desc(b_lo + koff), idesc, 1u);
-            mma_tf32(tmem, smem_desc(a_hi + koff), smem_desc(b_hi + koff), idesc, 1u);
-          } else {
-            mma_tf32(tmem, smem_desc(a_hi + koff), smem_desc(b_hi + koff), idesc, acc);
+        for (int j = 0; j < L::kStageA / 16 / kCT; ++j) {
+          const uint32_t off = uint32_t(t + kCT * j) * 16u;
+          split_store<kTerms>(a_hi, a_lo, off, lds128(sa + off));
+        }
+        if constexpr (kBSrc == 0) {  // [N,K] staging (SW128) -> same offsets
+#pragma unroll
+          for (int j = 0; j < L::kStageB / 16 / kCT; ++j) {
+            const uint32_t off = uint32_t(t + kCT * j) * 16u;
+            split_store<kTerms>(b_hi, b_lo, off, lds128(sb + off));
+          }
+        } else if constexpr (kBSrc == 1) {
+          // [32 k][BN n] staging (no swizzle): gather 4 consecutive k of one column
+          // n (consecutive threads -> consecutive n: conflict-free), write one
+          // 16-byte K-major chunk (8 rows x distinct chunks per quarter-warp).
+#pragma unroll
+          for (int j = 0; j < (BN * 8) / kCT; ++j) {
+            const int id = t + kCT * j, n = id % BN, kc = id / BN;
+            const uint32_t src = sb + uint32_t((kc * 4) * BN + n) * 4u;
+            float4 x = make_float4(lds32(src), lds32(src + BN * 4), lds32(src + 2 * BN * 4), lds32(src + 3 * BN * 4));
+            split_store<kTerms>(b_hi, b_lo, sw128(n, kc), x);
           }
         }
-        mma_commit(op_empty(s));  // operand slot free once these MMAs have read it
-      }
-      mma_commit(acc_full);
-    }
-  } else if (warp >= 4) {
-    // ------------------------------------------------------------ converters
-    const int t = threadIdx.x - 128;  // 0..127
-    for (int kb = 0; kb < nk; ++kb) {
-      const int s = kb % kStages;
-      const uint32_t ph = uint32_t(kb / kStages) & 1u;
-      mbar_wait(st_full(s), ph);
-      mbar_wait(op_empty(s), ph ^ 1u);
-      const uint32_t sa = staging + uint32_t(s) * L::kStaging, sb = sa + L::kStageA;
-      const uint32_t a_hi = operand + uint32_t(s) * L::kOperand;
-      const uint32_t a_lo = a_hi + L::kPlaneA;
-      const uint32_t b_hi = a_lo + L::kPlaneA;
-      const uint32_t b_lo = b_hi + L::kPlaneB;
-      // A: staging row-major [128][32] -> SW128 planes. 8 threads per 128-byte row.
-#pragma unroll
-      for (int j = 0; j < (BM * 8) / 128; ++j) {
-        const int id = t + 128 * j, r = id >> 3, kc = id & 7;
-        split_store<kTerms>(a_hi, a_lo, sw128(r, kc), lds128(sa + uint32_t(r * 128 + kc * 16)));
-      }
-      if constexpr (kNT) {
-#pragma unroll
-        for (int j = 0; j < (BN * 8) / 128; ++j) {
-          const int id = t + 128 * j, r = id >> 3, kc = id & 7;
-          split_store<kTerms>(b_hi, b_lo, sw128(r, kc), lds128(sb + uint32_t(r * 128 + kc * 16)));
-        }
-      } else {
-        // staging [32 k][BN n]: gather 4 consecutive k of one column n (conflict-free:
-        // consecutive threads take consecutive n), write one 16-byte K-major chunk.
-#pragma unroll
-        for (int j = 0; j < (BN * 8) / 128; ++j) {
-          const int id = t + 128 * j, n = id % BN, kc = id / BN;
-          const uint32_t src = sb + uint32_t((kc * 4) * BN + n) * 4u;
-          float4 x = make_float4(lds32(src), lds32(src + BN * 4), lds32(src + 2 * BN * 4), lds32(src + 3 * BN * 4));
-          split_store<kTerms>(b_hi, b_lo, sw128(n, kc), x);
-        }
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> async (MMA) reads
-      __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(st_empty(s));
-        mbar_arrive(op_full(s));
-      }
-    }
-    // ------------------------------------------------------------ epilogue
-    mbar_wait(acc_full, 0);
-    tc_fence_after();
-    const int q = warp - 4;  // TMEM lane quarter accessible to this warp
-    const int row = m0 + q * 32 + lane;
-    float* crow = C + int64_t(inst) * sC + int64_t(row) * N;
-#pragma unroll 1
-    for (int cb = 0; cb < BN / 32; ++cb) {
-      uint32_t r[32];
-      const uint32_t taddr = tmem + (uint32_t(q * 32) << 16) + uint32_t(cb * 32);
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-          "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-            "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-            "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-            "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-          : "r"(taddr));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      const int c0 = n0 + cb * 32;
-      if (row < M) {
-        if (c0 + 32 <= N && (N & 3) == 0) {
-#pragma unroll
-          for (int j = 0; j < 32; j += 4) {
-            float4 v = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
-                                   __uint_as_float(r[j + 3]));
-            if (relu) {
-              v.x = fmaxf(v.x, 0.f); v.y = fmaxf(v.y, 0.f); v.z = fmaxf(v.z, 0.f); v.w = fmaxf(v.w, 0.f);
-            }
-            *reinterpret_cast<float4*>(crow + c0 + j) = v;
-          }
-        } else {
-          for (int j = 0; j < 32; ++j) {
-            if (c0 + j >= N) break;
-            float v = __uint_as_float(r[j]);
-            crow[c0 + j] = relu ? fmaxf(v, 0.f) : v;
-          }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> async (MMA) reads
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(st_empty(s));
+          mbar_arrive(op_full(o));
         }
       }
     }
@@ -311,7 +396,33 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
+  }
+}
+
+// Weight preparation: B (resident) -> K-major tf32 hi/lo planes [2][N][K].
+template <bool kNT>
+__global__ void split_weights_kernel(const float* __restrict__ B, float* __restrict__ planes, int N, int K) {
+  __shared__ float tile[32][33];
+  const int n0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
+  const int64_t plane = int64_t(N) * K;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    // load tile[n][k]
+    int n = n0 + (kNT ? i : threadIdx.x), k = k0 + (kNT ? threadIdx.x : i);
+    float v = 0.f;
+    if (n < N && k < K) v = kNT ? B[int64_t(n) * K + k] : B[int64_t(k) * N + n];
+    if (kNT) tile[i][threadIdx.x] = v;
+    else tile[threadIdx.x][i] = v;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    int n = n0 + i, k = k0 + threadIdx.x;
+    if (n < N && k < K) {
+      float x = tile[i][threadIdx.x];
+      float h = tf32_rna(x);
+      planes[int64_t(n) * K + k] = h;
+      planes[plane + int64_t(n) * K + k] = x - h;
+    }
   }
 }
 
@@ -334,7 +445,7 @@ EncodeTiledFn encode_fn() {
 
 // 3-D fp32 tensor map: dims {d0 (contiguous), d1, d2}, byte strides {s1, s2}.
 bool make_map(CUtensorMap* m, const float* ptr, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1, uint64_t s2,
-              uint32_t b0, uint32_t b1) {
+              uint32_t b0, uint32_t b1, bool swizzle128) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[3] = {d0, d1, d2};
@@ -342,42 +453,60 @@ bool make_map(CUtensorMap* m, const float* ptr, uint64_t d0, uint64_t d1, uint64
   cuuint32_t box[3] = {b0, b1, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(ptr), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
-template <int BN, bool kNT, int kTerms>
+int num_sms() {
+  static int n = [] {
+    int dev = 0, v = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return n;
+}
+
+template <int BN, int kBSrc, int kTerms>
 cudaError_t launch(const GemmArgs& a, cudaStream_t s) {
-  auto kernel = gemm_tc_kernel<BN, kNT, kTerms>;
-  constexpr int smem = Smem<BN>::kTotal;
+  using L = Cfg<BN, kBSrc>;
+  auto kernel = gemm_tc_kernel<BN, kBSrc, kTerms>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [&] { attr_err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); });
+  std::call_once(once, [&] {
+    attr_err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal);
+  });
   if (attr_err != cudaSuccess) return attr_err;
+  const uint64_t M = uint64_t(a.M), N = uint64_t(a.N), K = uint64_t(a.K);
   const uint64_t nA = a.sA ? uint64_t(a.batch) : 1, nB = a.sB ? uint64_t(a.batch) : 1;
-  const uint64_t sA = (a.sA ? uint64_t(a.sA) : uint64_t(a.M) * a.K) * 4;
+  const uint64_t sA = (a.sA ? uint64_t(a.sA) : M * K) * 4;
   CUtensorMap mA, mB;
-  if (!make_map(&mA, a.A, uint64_t(a.K), uint64_t(a.M), nA, uint64_t(a.K) * 4, sA, BK, BM)) return cudaErrorInvalidValue;
-  bool ok;
-  if (kNT) {
-    const uint64_t sB = (a.sB ? uint64_t(a.sB) : uint64_t(a.N) * a.K) * 4;
-    ok = make_map(&mB, a.B, uint64_t(a.K), uint64_t(a.N), nB, uint64_t(a.K) * 4, sB, BK, BN);
+  if (!make_map(&mA, a.A, K, M, nA, K * 4, sA, BK, BM, true)) return cudaErrorInvalidValue;
+  bool ok = false;
+  if constexpr (kBSrc == 2) {
+    ok = make_map(&mB, a.Bplanes, K, N, 2, K * 4, N * K * 4, BK, BN, true);
+  } else if constexpr (kBSrc == 0) {
+    const uint64_t sB = (a.sB ? uint64_t(a.sB) : N * K) * 4;
+    ok = make_map(&mB, a.B, K, N, nB, K * 4, sB, BK, BN, true);
   } else {
-    const uint64_t sB = (a.sB ? uint64_t(a.sB) : uint64_t(a.N) * a.K) * 4;
-    ok = make_map(&mB, a.B, uint64_t(a.N), uint64_t(a.K), nB, uint64_t(a.N) * 4, sB, BN, BK);
+    const uint64_t sB = (a.sB ? uint64_t(a.sB) : N * K) * 4;
+    ok = make_map(&mB, a.B, N, K, nB, N * 4, sB, BN, BK, false);
   }
   if (!ok) return cudaErrorInvalidValue;
-  dim3 grid((a.N + BN - 1) / BN, (a.M + BM - 1) / BM, a.batch);
-  kernel<<<grid, kThreads, smem, s>>>(mA, mB, a.C, a.sC, a.M, a.N, a.K, a.sA != 0, a.sB != 0, a.relu ? 1 : 0);
+  TileParams p{a.C, a.sC, a.M, a.N, a.K, a.batch, a.sA != 0, a.sB != 0, a.relu ? 1 : 0,
+               (a.M + BM - 1) / BM, (a.N + BN - 1) / BN, 0};
+  p.total_tiles = p.m_tiles * p.n_tiles * a.batch;
+  const int grid = p.total_tiles < num_sms() ? p.total_tiles : num_sms();
+  kernel<<<grid, kThreads, L::kTotal, s>>>(mA, mB, p);
   return cudaGetLastError();
 }
 
 template <int BN>
 cudaError_t launch_bn(const GemmArgs& a, int terms, cudaStream_t s) {
-  const bool nt = a.layout == GemmLayout::nt;
-  if (terms > 1) return nt ? launch<BN, true, 3>(a, s) : launch<BN, false, 3>(a, s);
-  return nt ? launch<BN, true, 1>(a, s) : launch<BN, false, 1>(a, s);
+  if (a.Bplanes) return terms > 1 ? launch<BN, 2, 3>(a, s) : launch<BN, 2, 1>(a, s);
+  if (a.layout == GemmLayout::nt) return terms > 1 ? launch<BN, 0, 3>(a, s) : launch<BN, 0, 1>(a, s);
+  return terms > 1 ? launch<BN, 1, 3>(a, s) : launch<BN, 1, 1>(a, s);
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
@@ -386,16 +515,23 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 
 bool gemm_tcgen05_supported(const GemmArgs& a) {
   if (a.M < 1 || a.N < 1 || a.K < 1 || a.batch < 1) return false;
-  if (a.K % 4 || (a.layout == GemmLayout::nn && a.N % 4)) return false;
+  if (a.K % 4 || (a.layout == GemmLayout::nn && !a.Bplanes && a.N % 4)) return false;
   if (a.sA % 4 || a.sB % 4 || a.sC % 4) return false;
   if (!aligned16(a.A) || !aligned16(a.B) || !aligned16(a.C)) return false;
-  if (a.batch > 65535) return false;
+  if (a.Bplanes && (!aligned16(a.Bplanes) || a.sB != 0)) return false;
   return encode_fn() != nullptr;
 }
 
 cudaError_t gemm_tcgen05(const GemmArgs& a, int terms, cudaStream_t s) {
   if (a.N <= 64) return launch_bn<64>(a, terms, s);
   return launch_bn<128>(a, terms, s);
+}
+
+cudaError_t gemm_split_weights(const float* B, GemmLayout layout, int N, int K, float* planes, cudaStream_t s) {
+  dim3 grid((N + 31) / 32, (K + 31) / 32), block(32, 8);
+  if (layout == GemmLayout::nt) split_weights_kernel<true><<<grid, block, 0, s>>>(B, planes, N, K);
+  else split_weights_kernel<false><<<grid, block, 0, s>>>(B, planes, N, K);
+  return cudaGetLastError();
 }
 
 }  // namespace hs

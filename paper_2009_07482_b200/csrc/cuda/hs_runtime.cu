@@ -248,7 +248,8 @@ int hs_launch(hs_stream_t st, int op, const hs_op_args* a, int math, int batch) 
       if (a->n_in < 2) return invalid("gemm needs two inputs");
       hs::GemmArgs g{in(0), a->in_stride[0], in(1), a->in_stride[1], out, a->out_stride,
                      int(a->dims[0]), int(a->dims[1]), int(a->dims[2]), batch,
-                     op == HS_OP_GEMM_NT ? hs::GemmLayout::nt : hs::GemmLayout::nn, op == HS_OP_GEMM_RELU};
+                     op == HS_OP_GEMM_NT ? hs::GemmLayout::nt : hs::GemmLayout::nn, op == HS_OP_GEMM_RELU,
+                     math == HS_MATH_FP32_SIMT ? nullptr : static_cast<const float*>(a->aux)};
       if (math == HS_MATH_FP32_SIMT || !hs::gemm_tcgen05_supported(g)) e = hs::gemm_simt(g, s);
       else e = hs::gemm_tcgen05(g, math == HS_MATH_TF32 ? 1 : 3, s);
       break;
@@ -288,6 +289,17 @@ int hs_launch(hs_stream_t st, int op, const hs_op_args* a, int math, int batch) 
 }
 
 int64_t hs_launch_count(void) { return g_launches.load(); }
+
+int hs_gemm_split_weights(hs_stream_t st, const void* B, int transposed, int64_t N, int64_t K, void* planes) {
+  if (!st || !B || !planes) return invalid("null argument");
+  if (N < 1 || K < 1 || N > (1 << 30) || K > (1 << 30)) return invalid("bad weight shape");
+  if (int r = use_device(st->gpu)) return r;
+  cudaError_t e = hs::gemm_split_weights(static_cast<const float*>(B), transposed ? hs::GemmLayout::nt : hs::GemmLayout::nn,
+                                         int(N), int(K), static_cast<float*>(planes), st->s);
+  if (e != cudaSuccess) return check(e, "split weights");
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return HS_OK;
+}
 
 int hs_host_callback(hs_stream_t s, void (*fn)(void*), void* user) {
   if (!s || !fn) return invalid("null argument");

@@ -21,7 +21,12 @@ struct GemmArgs {
   int batch;
   GemmLayout layout;
   bool relu;
+  // Optional: resident B pre-split into K-major tf32 planes [2][N][K] (hi, lo)
+  // by gemm_split_weights; then B is fed to the tensor cores by TMA directly.
+  const float* Bplanes = nullptr;
 };
+
+cudaError_t gemm_split_weights(const float* B, GemmLayout layout, int N, int K, float* planes, cudaStream_t s);
 
 // math: 0 = TF32x3 (tcgen05), 1 = TF32 (tcgen05), 2 = fp32 SIMT
 cudaError_t gemm_tcgen05(const GemmArgs& a, int terms, cudaStream_t s);

@@ -238,6 +238,30 @@ void Engine::plan_buffers() {
     device_bytes_ += groups_[gi].bytes;
     resident_buf_[int(gi)] = p;
   }
+  // GEMM nodes whose B operand is a resident weight get it pre-split once
+  // (tf32 hi/lo, K-major) so the tensor cores are fed by TMA with no conversion.
+  if (cfg_.math != HS_MATH_FP32_SIMT) {
+    for (const auto& [kid, nd] : nodes_) {
+      if (nd.op != HS_OP_GEMM && nd.op != HS_OP_GEMM_NT && nd.op != HS_OP_GEMM_RELU) continue;
+      auto gi = group_of_.find(nd.inputs[1]);
+      if (gi == group_of_.end() || !groups_[size_t(gi->second)].resident) continue;
+      const bool nt = nd.op == HS_OP_GEMM_NT;
+      auto key = std::make_pair(gi->second, nt);
+      auto it = planes_.find(key);
+      if (it == planes_.end()) {
+        Planes pl;
+        pl.gi = gi->second;
+        pl.nt = nt;
+        pl.n = nd.dims[1];
+        pl.k = nd.dims[2];
+        hs_ok(hs_malloc(ctx_, size_t(2 * pl.n * pl.k * 4), &pl.ptr), "hs_malloc");
+        allocations_.push_back(pl.ptr);
+        device_bytes_ += 2 * pl.n * pl.k * 4;
+        it = planes_.emplace(key, pl).first;
+      }
+      node_planes_[kid] = it->second.ptr;
+    }
+  }
   const int64_t B = cfg_.batch;
   slots_.resize(size_t(cfg_.slots));
   for (auto& sl : slots_) {
@@ -275,6 +299,8 @@ void Engine::upload_resident() {
     hs_ok(hs_memcpy_2d(s, dst, size_t(gr.bytes), gr.b.ptr, size_t(gr.bytes), size_t(gr.bytes), 1, gr.b.on_device ? 2 : 0),
           "resident upload");
   }
+  for (const auto& [key, pl] : planes_)
+    hs_ok(hs_gemm_split_weights(s, resident_buf_.at(pl.gi), pl.nt ? 1 : 0, pl.n, pl.k, pl.ptr), "split weights");
   hs_ok(hs_stream_sync(s), "resident upload sync");
   resident_uploaded_ = true;
 }
@@ -339,6 +365,8 @@ void Engine::launch_node(Slot& sl, hs_stream_t s, int kernel) {
   for (int i = 0; i < 4; ++i) a.dims[i] = nd.dims[i];
   a.fparam[0] = nd.fparam[0];
   a.fparam[1] = nd.fparam[1];
+  auto pl = node_planes_.find(kernel);
+  a.aux = pl == node_planes_.end() ? nullptr : pl->second;
   hs_ok(hs_launch(s, nd.op, &a, cfg_.math, cfg_.batch), "hs_launch");
 }
 

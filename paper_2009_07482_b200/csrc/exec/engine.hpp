@@ -119,6 +119,15 @@ class Engine {
   std::map<std::pair<int, int>, int64_t> bytes_;                // (kernel,pos) -> bytes per instance
   std::vector<std::pair<int, int>> outputs_;                    // isolated outputs with a binding
   std::map<int, void*> resident_buf_;
+  // resident GEMM weights pre-split into tf32 hi/lo planes: (group, transposed) -> planes
+  struct Planes {
+    void* ptr = nullptr;
+    int gi = -1;
+    bool nt = false;
+    int64_t n = 0, k = 0;
+  };
+  std::map<std::pair<int, bool>, Planes> planes_;
+  std::map<int, void*> node_planes_;  // kernel -> planes
   hs_ctx_t ctx_ = nullptr;
   std::vector<Slot> slots_;
   bool planned_ = false;

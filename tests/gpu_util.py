@@ -28,10 +28,22 @@ def stream():
     return _stream
 
 
-def launch(op, inputs, out, dims, fparam=(1.0, 1e-5), math="tf32x3", batch=1, strides=None, out_stride=None):
+def split_weights(B, transposed, N, K):
+    """Pre-split a shared GEMM B into tf32 hi/lo K-major planes (hs_gemm_split_weights)."""
+    import torch
+    planes = torch.empty(2 * N * K, device="cuda")
+    L = _native.lib()
+    _native.check(L.hs_gemm_split_weights(stream(), B.data_ptr(), int(transposed), N, K, planes.data_ptr()))
+    _native.check(L.hs_stream_sync(stream()))
+    return planes
+
+
+def launch(op, inputs, out, dims, fparam=(1.0, 1e-5), math="tf32x3", batch=1, strides=None, out_stride=None,
+           aux=None):
     """inputs/out: torch CUDA float32 tensors shaped [batch, elems] or [elems] (shared)."""
     L = _native.lib()
     a = _native.OpArgs()
+    a.aux = aux.data_ptr() if aux is not None else None
     a.n_in = len(inputs)
     for i, t in enumerate(inputs):
         a.in_[i] = t.data_ptr()

@@ -61,6 +61,27 @@ def test_gemm_parity(M, N, K, op, batch, shared, math, oracle_mod):
         assert err <= (TOL_TF32X3 if math == "tf32x3" else 1e-5), (b, err)
 
 
+@pytest.mark.parametrize("M,N,K,op,batch,shared", [c for c in GEMM_CASES if c[5]] + [(128, 128, 64, "gemm_nt", 3, True),
+                                                                              (72, 100, 36, "gemm", 2, True)])
+@pytest.mark.parametrize("math", ["tf32x3", "tf32"])
+def test_gemm_presplit_weights(M, N, K, op, batch, shared, math, oracle_mod):
+    """Resident-weight path: B pre-split once into K-major tf32 planes, fed by TMA."""
+    from tests.gpu_util import launch, normwise, split_weights
+    import torch
+    A = _rand(31, (batch, M * K))
+    B = (_rand(32, (N * K,)) * np.float32(1.0 / np.sqrt(K))).astype(np.float32)
+    ref = np.empty((batch, M * N), np.float32)
+    oracle_mod.run_node(op, [A, B], [M * K, 0], ref, M * N, [M, N, K], batch)
+    Bt = _t(B)
+    planes = split_weights(Bt, op == "gemm_nt", N, K)
+    out = torch.full((batch, M * N), float("nan"), device="cuda")
+    launch(op, [_t(A), Bt], out, [M, N, K], math=math, batch=batch, aux=planes)
+    y = out.cpu().numpy()
+    tol = TOL_TF32X3 if math == "tf32x3" else 5e-3
+    for b in range(batch):
+        assert normwise(y[b], ref[b]) <= tol, b
+
+
 def test_gemm_tf32_single_term_is_coarser(oracle_mod):
     """The 1-term TF32 mode is visibly less accurate than 3xTF32 (sanity of the split)."""
     from tests.gpu_util import launch, normwise
