@@ -4,11 +4,11 @@
 //
 // Persistent kernel: one CTA per SM walks the 128 x BN output tiles of all
 // `batch` instances (instance index fastest, so concurrently running CTAs
-// share the same weight tile in L2). Warp roles (384 threads):
-//   warp 0       TMA producer. A (fp32) -> staging ring with SWIZZLE_128B, which
-//                is already the canonical K-major UMMA layout; B either as fp32
-//                staging (activations) or, for resident weights, as pre-split
-//                tf32 hi/lo planes written straight into the operand ring.
+// share the same weight tile in L2). Warp roles (512 threads):
+//   warp 0       TMA producer. A (fp32) -> staging ring (SWIZZLE_128B); B either
+//                as fp32 staging (activations) or, for resident weights, as
+//                pre-split tf32 hi/lo planes (SW128, the canonical K-major UMMA
+//                layout) written straight into the shared-memory operand ring.
 //   warp 1       MMA issuer (one lane): tcgen05.mma.kind::tf32, accumulator in
 //                TMEM, double-buffered (2 x BN columns) so the epilogue of tile
 //                i overlaps the main loop of tile i+1.
@@ -16,8 +16,10 @@
 //   warps 4..7   epilogue: tcgen05.ld 32x32b -> ReLU -> global (TMEM lane
 //                quarter = warp % 4).
 //   warps 8..15  converters: x = hi + lo with hi = cvt.rna.tf32(x), lo = x - hi
-//                (exact). Elementwise on the swizzled tile (same offsets in and
-//                out); an [K,N] activation B is transposed on the way.
+//                (exact). The split A goes to TMEM (tcgen05.st; the MMA reads A
+//                from TMEM), so shared memory only carries B: this is what keeps
+//                the kernel off the shared-memory bandwidth ceiling. Activation
+//                B is split into shared memory (transposed when it is [K,N]).
 // 3xTF32: D += Alo·Bhi + Ahi·Blo + Ahi·Bhi (Alo·Blo, ~2^-22 relative, is
 // dropped). TF32 mode (terms = 1) issues only Ahi·Bhi.
 //
@@ -144,15 +146,17 @@ __device__ __forceinline__ void split_store(uint32_t hi, uint32_t lo, uint32_t o
 template <int BN, int kBSrc>
 struct Cfg {
   static constexpr bool kBPre = kBSrc == 2;
-  static constexpr int kStageA = BM * BK * 4;                       // 16 KB (SW128 via TMA)
-  static constexpr int kStageB = kBPre ? 0 : BN * BK * 4;           // fp32 B staging
+  static constexpr int kStageA = BM * BK * 4;              // 16 KB fp32 A tile (SW128 via TMA)
+  static constexpr int kStageB = kBPre ? 0 : BN * BK * 4;  // fp32 B staging (activations only)
   static constexpr int kStaging = kStageA + kStageB;
-  static constexpr int kPlaneA = BM * 128;
-  static constexpr int kPlaneB = BN * 128;
-  static constexpr int kOperand = 2 * kPlaneA + 2 * kPlaneB;       // hi + lo for A and B
+  static constexpr int kPlaneB = BN * 128;                 // one SW128 tf32 plane of B
+  static constexpr int kOperand = 2 * kPlaneB;             // B hi + lo (A lives in TMEM)
+  // TMEM (512 columns): two BN-wide fp32 accumulators + kNO A stages of 64
+  // columns (32 hi + 32 lo tf32 columns, one row per lane).
+  static constexpr int kAccCols = 2 * BN;
+  static constexpr int kNOtm = (512 - kAccCols) / 64;
+  static constexpr int kNO = kNOtm < 4 ? kNOtm : 4;
   static constexpr int kBudget = 200 * 1024;
-  // deepest operand ring that leaves room for >= 2 staging stages, staging fills the rest
-  static constexpr int kNO = (kBudget - 2 * kStaging) / kOperand >= 3 ? 3 : 2;
   static constexpr int kNSraw = (kBudget - kNO * kOperand) / kStaging;
   static constexpr int kNS = kNSraw > 6 ? 6 : kNSraw;
   static constexpr int kTotal = kNS * kStaging + kNO * kOperand + 1024 /*barriers*/ + 1024 /*align*/;
@@ -170,6 +174,26 @@ struct TileParams {
   int m_tiles, n_tiles;
   int total_tiles;
 };
+
+// D[tmem] (+)= A[tmem] · B[smem]; A is K-major in TMEM (lane = row, column = k).
+__device__ __forceinline__ void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc,
+                                            uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, {%5, %6, %7, %8}, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(b), "r"(idesc), "r"(acc), "r"(0u), "r"(0u), "r"(0u), "r"(0u)
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
 
 template <int BN, int kBSrc, int kTerms>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -211,13 +235,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tmem_slot), "r"(2 * BN));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tmem_slot), "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot_ptr;
+  const uint32_t tmem_a = tmem + uint32_t(L::kAccCols);  // A stages start after the accumulators
 
   // tile index -> (m_tile, instance, n_tile); instance fastest after m.
   auto decode = [&](int t, int& m0, int& inst, int& n0) {
@@ -248,7 +273,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             // pre-split weight planes (hi at plane 0, lo at plane 1) straight into the operand ring
             const int o = int(it % NO);
             mbar_wait(op_empty(o), ((it / NO) & 1u) ^ 1u);
-            const uint32_t b_hi = operand + uint32_t(o) * L::kOperand + 2 * L::kPlaneA;
+            const uint32_t b_hi = operand + uint32_t(o) * L::kOperand;
             mbar_expect_tx(op_full(o), (kTerms > 1 ? 2 : 1) * L::kPlaneB);
             tma_load_3d(b_hi, &tmB, op_full(o), kb * BK, n0, 0);
             if constexpr (kTerms > 1) tma_load_3d(b_hi + L::kPlaneB, &tmB, op_full(o), kb * BK, n0, 1);
@@ -270,23 +295,23 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int o = int(it % NO);
           mbar_wait(op_full(o), (it / NO) & 1u);
           tc_fence_after();
-          const uint32_t a_hi = operand + uint32_t(o) * L::kOperand;
-          const uint32_t a_lo = a_hi + L::kPlaneA;
-          const uint32_t b_hi = a_lo + L::kPlaneA;
+          const uint32_t a_hi = tmem_a + uint32_t(o) * 64u;
+          const uint32_t a_lo = a_hi + 32u;
+          const uint32_t b_hi = operand + uint32_t(o) * L::kOperand;
           const uint32_t b_lo = b_hi + L::kPlaneB;
 #pragma unroll
-          for (int kk = 0; kk < BK / 8; ++kk) {  // K = 8 tf32 per instruction = 32 bytes
-            const uint32_t koff = uint32_t(kk) * 32u;
+          for (int kk = 0; kk < BK / 8; ++kk) {  // K = 8 tf32 per instruction
+            const uint32_t kcol = uint32_t(kk) * 8u, koff = uint32_t(kk) * 32u;
             const uint32_t first = (kb | kk) ? 1u : 0u;
             if constexpr (kTerms > 1) {
-              mma_tf32(d, smem_desc(a_lo + koff), smem_desc(b_hi + koff), idesc, first);
-              mma_tf32(d, smem_desc(a_hi + koff), smem_desc(b_lo + koff), idesc, 1u);
-              mma_tf32(d, smem_desc(a_hi + koff), smem_desc(b_hi + koff), idesc, 1u);
+              mma_tf32_ts(d, a_lo + kcol, smem_desc(b_hi + koff), idesc, first);
+              mma_tf32_ts(d, a_hi + kcol, smem_desc(b_lo + koff), idesc, 1u);
+              mma_tf32_ts(d, a_hi + kcol, smem_desc(b_hi + koff), idesc, 1u);
             } else {
-              mma_tf32(d, smem_desc(a_hi + koff), smem_desc(b_hi + koff), idesc, first);
+              mma_tf32_ts(d, a_hi + kcol, smem_desc(b_hi + koff), idesc, first);
             }
           }
-          mma_commit(op_empty(o));  // operand slot free once these MMAs have read it
+          mma_commit(op_empty(o));  // operand slot (TMEM A + smem B) free once these MMAs have read it
         }
         mma_commit(acc_full(int(acc)));
       }
@@ -346,25 +371,40 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 8) {
     // ------------------------------------------------------------ converters
-    const int t = threadIdx.x - 256;  // 0..255
+    // A: warp w owns TMEM lane quarter w % 4 (rows 32q..32q+31) and k-half
+    // h = (w - 8) / 4: each thread splits 16 k-values of its row and writes
+    // them with tcgen05.st (hi -> columns [0,32), lo -> [32,64) of the stage).
+    const int t = threadIdx.x - 256;  // 0..255 (B conversion index)
     constexpr int kCT = kConvWarps * 32;
+    const int q = warp & 3, h = (warp - 8) >> 2;
+    const int row = q * 32 + lane;
     uint32_t it = 0;
     for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
       for (int kb = 0; kb < nk; ++kb, ++it) {
         const int s = int(it % NS), o = int(it % NO);
         mbar_wait(st_full(s), (it / NS) & 1u);
         mbar_wait(op_empty(o), ((it / NO) & 1u) ^ 1u);
+        tc_fence_after();
         const uint32_t sa = staging + uint32_t(s) * L::kStaging, sb = sa + L::kStageA;
-        const uint32_t a_hi = operand + uint32_t(o) * L::kOperand;
-        const uint32_t a_lo = a_hi + L::kPlaneA;
-        const uint32_t b_hi = a_lo + L::kPlaneA;
-        const uint32_t b_lo = b_hi + L::kPlaneB;
-        // A staging is SW128 already: same byte offset in and out.
+        {
+          uint32_t hi[16], lo[16];
 #pragma unroll
-        for (int j = 0; j < L::kStageA / 16 / kCT; ++j) {
-          const uint32_t off = uint32_t(t + kCT * j) * 16u;
-          split_store<kTerms>(a_hi, a_lo, off, lds128(sa + off));
+          for (int c = 0; c < 4; ++c) {
+            float4 x = lds128(sa + sw128(row, 4 * h + c));
+            const float xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float hv = tf32_rna(xs[e]);
+              hi[4 * c + e] = __float_as_uint(hv);
+              lo[4 * c + e] = __float_as_uint(xs[e] - hv);
+            }
+          }
+          const uint32_t ta = tmem_a + (uint32_t(q * 32) << 16) + uint32_t(o) * 64u + uint32_t(16 * h);
+          tmem_st16(ta, hi);
+          if constexpr (kTerms > 1) tmem_st16(ta + 32u, lo);
         }
+        const uint32_t b_hi = operand + uint32_t(o) * L::kOperand;
+        const uint32_t b_lo = b_hi + L::kPlaneB;
         if constexpr (kBSrc == 0) {  // [N,K] staging (SW128) -> same offsets
 #pragma unroll
           for (int j = 0; j < L::kStageB / 16 / kCT; ++j) {
@@ -383,7 +423,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             split_store<kTerms>(b_hi, b_lo, sw128(n, kc), x);
           }
         }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> async (MMA) reads
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        if constexpr (!L::kBPre) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        tc_fence_before();
         __syncwarp();
         if (lane == 0) {
           mbar_arrive(st_empty(s));
@@ -396,7 +438,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
   }
 }
 
