@@ -51,6 +51,7 @@ def parse_args():
     ap.add_argument("--batch", type=int, default=64, help="instances per batched node launch")
     ap.add_argument("--slots", type=int, default=2)
     ap.add_argument("--queues", type=int, default=3)
+    ap.add_argument("--devices", type=int, default=1, help="logical devices in the cq map (all on this GPU)")
     ap.add_argument("--math", default="tf32x3")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -274,7 +275,7 @@ def run_ours(args, world, rank, local):
     from paper_2009_07482_b200.engine import Engine
 
     torch.cuda.set_device(local)
-    text, params, meta = workloads.encoder(layers=args.layers, queues=args.queues)
+    text, params, meta = workloads.encoder(layers=args.layers, queues=args.queues, devices=args.devices)
     first, n = partition(args.instances, world, rank)
     S, D = params["S"], params["D"]
     inst_bytes = S * D * 4
@@ -361,7 +362,7 @@ def run_ours(args, world, rank, local):
             "config": {"workload": f"C5: {args.layers}-layer encoder DAG (8 heads, d_model 512, seq 128, d_ff 2048), "
                                    f"stream of {args.instances} instances",
                        "kernels_per_dag": plan["kernels"], "edges": plan["edges"], "components": plan["components"],
-                       "policy": "clustering", "queues_per_device": args.queues, "batch": args.batch,
+                       "policy": "clustering", "queues_per_device": args.queues, "logical_devices": args.devices, "batch": args.batch,
                        "slots": args.slots, "mode": "graph", "parallelism": f"instance partition x{world}",
                        "l2": "inputs (1 GiB X + 1 GiB out per step) larger than L2"},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak3, "unit": "TFLOP/s",

@@ -41,8 +41,16 @@ namespace {
 constexpr int BM = 128;
 constexpr int BK = 32;  // fp32 elements per K-block = one 128-byte swizzle row
 constexpr int kEpiWarps = 4;
-constexpr int kConvWarps = 8;
-constexpr int kThreads = 32 * (4 + kEpiWarps + kConvWarps);  // 512: 4 control, 4 epilogue, 8 converter warps
+// Converters work in groups of 4 warps (one per TMEM lane quarter); group g
+// handles the K-blocks with it % kConvGroups == g, so kConvGroups K-blocks are
+// split concurrently and the per-block latency chain (smem load -> split ->
+// tcgen05.st -> wait::st -> arrive) is overlapped instead of serialised.
+// Stage counts are multiples of kConvGroups so each group revisits only its
+// own slots, one phase at a time (a parity wait two phases ahead would alias).
+constexpr int kConvGroups = 2;
+constexpr int kGroupWarps = 4;
+constexpr int kConvWarps = kConvGroups * kGroupWarps;
+constexpr int kThreads = 32 * (4 + kEpiWarps + kConvWarps);  // 4 control + 4 epilogue + 8 converter warps
 static_assert(kThreads == 512, "warp-role layout");
 
 // ----------------------------------------------------------------- PTX helpers
@@ -155,10 +163,13 @@ struct Cfg {
   // columns (32 hi + 32 lo tf32 columns, one row per lane).
   static constexpr int kAccCols = 2 * BN;
   static constexpr int kNOtm = (512 - kAccCols) / 64;
-  static constexpr int kNO = kNOtm < 4 ? kNOtm : 4;
+  static constexpr int kNOcap = kNOtm < 4 ? kNOtm : 4;
+  static constexpr int kNO = kNOcap - kNOcap % kConvGroups;
   static constexpr int kBudget = 200 * 1024;
   static constexpr int kNSraw = (kBudget - kNO * kOperand) / kStaging;
-  static constexpr int kNS = kNSraw > 6 ? 6 : kNSraw;
+  static constexpr int kNScap = kNSraw > 6 ? 6 : kNSraw;
+  static constexpr int kNS = kNScap - kNScap % kConvGroups;
+  static_assert(kNS % kConvGroups == 0 && kNO % kConvGroups == 0, "stage rings must divide among groups");
   static constexpr int kTotal = kNS * kStaging + kNO * kOperand + 1024 /*barriers*/ + 1024 /*align*/;
   static_assert(kNS >= 2 && kNO >= 2, "pipeline too shallow");
   static_assert(kTotal <= 227 * 1024, "shared memory budget exceeded");
@@ -220,10 +231,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(st_full(s), 1);
-      mbar_init(st_empty(s), kConvWarps);
+      mbar_init(st_empty(s), kGroupWarps);
     }
     for (int s = 0; s < NO; ++s) {
-      mbar_init(op_full(s), kConvWarps + (L::kBPre ? 1 : 0));
+      mbar_init(op_full(s), kGroupWarps + (L::kBPre ? 1 : 0));
       mbar_init(op_empty(s), 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -371,26 +382,30 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 8) {
     // ------------------------------------------------------------ converters
-    // A: warp w owns TMEM lane quarter w % 4 (rows 32q..32q+31) and k-half
-    // h = (w - 8) / 4: each thread splits 16 k-values of its row and writes
-    // them with tcgen05.st (hi -> columns [0,32), lo -> [32,64) of the stage).
-    const int t = threadIdx.x - 256;  // 0..255 (B conversion index)
-    constexpr int kCT = kConvWarps * 32;
-    const int q = warp & 3, h = (warp - 8) >> 2;
+    // A: warp w of group g owns TMEM lane quarter w % 4 (rows 32q..32q+31);
+    // each thread splits the 32 k-values of its row and writes them with
+    // tcgen05.st (hi -> columns [0,32), lo -> [32,64) of the stage).
+    const int g = (warp - 8) / kGroupWarps;
+    const int t = threadIdx.x - 256 - g * kGroupWarps * 32;  // 0..127 within the group (B conversion index)
+    constexpr int kCT = kGroupWarps * 32;
+    const int q = warp & 3;
     const int row = q * 32 + lane;
     uint32_t it = 0;
     for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
       for (int kb = 0; kb < nk; ++kb, ++it) {
+        if (int(it % kConvGroups) != g) continue;
         const int s = int(it % NS), o = int(it % NO);
         mbar_wait(st_full(s), (it / NS) & 1u);
         mbar_wait(op_empty(o), ((it / NO) & 1u) ^ 1u);
         tc_fence_after();
         const uint32_t sa = staging + uint32_t(s) * L::kStaging, sb = sa + L::kStageA;
-        {
+        const uint32_t ta = tmem_a + (uint32_t(q * 32) << 16) + uint32_t(o) * 64u;
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
           uint32_t hi[16], lo[16];
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
-            float4 x = lds128(sa + sw128(row, 4 * h + c));
+            float4 x = lds128(sa + sw128(row, 4 * hh + c));
             const float xs[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
@@ -399,9 +414,8 @@ __global__ void __launch_bounds__(kThreads, 1)
               lo[4 * c + e] = __float_as_uint(xs[e] - hv);
             }
           }
-          const uint32_t ta = tmem_a + (uint32_t(q * 32) << 16) + uint32_t(o) * 64u + uint32_t(16 * h);
-          tmem_st16(ta, hi);
-          if constexpr (kTerms > 1) tmem_st16(ta + 32u, lo);
+          tmem_st16(ta + uint32_t(16 * hh), hi);
+          if constexpr (kTerms > 1) tmem_st16(ta + 32u + uint32_t(16 * hh), lo);
         }
         const uint32_t b_hi = operand + uint32_t(o) * L::kOperand;
         const uint32_t b_lo = b_hi + L::kPlaneB;
