@@ -121,6 +121,12 @@ typedef struct {
   int64_t dims[4];                  /* op-specific sizes             */
   float fparam[2];                  /* [0] scale s, [1] layer-norm eps               */
   const void* aux;                  /* GEMM: shared B pre-split by hs_gemm_split_weights, or NULL */
+  /* Grouped GEMM launch (n_out > 1): n_out sibling GEMMs sharing A and dims
+   * M, K, each with N = dims[1] columns; aux holds their planes concatenated
+   * along N; member m writes outs[m] (per-instance stride out_strides[m]). */
+  int n_out;
+  void* outs[4];
+  int64_t out_strides[4];
 } hs_op_args;
 
 int hs_op_from_name(const char* name); /* -1 if unknown */
@@ -129,6 +135,10 @@ int hs_launch(hs_stream_t s, int op, const hs_op_args* args, int math_mode, int 
  * [N,K]) -> K-major tf32 hi/lo planes `planes` = float[2][N][K]. Run once per
  * weight; pass `planes` as hs_op_args.aux on every launch that uses B. */
 int hs_gemm_split_weights(hs_stream_t s, const void* B, int transposed, int64_t N, int64_t K, void* planes);
+/* Same, writing hi at planes[n*K+k] and lo at planes[plane_stride + n*K+k] (elements):
+ * used to lay several weights side by side for a grouped launch. */
+int hs_gemm_split_weights_strided(hs_stream_t s, const void* B, int transposed, int64_t N, int64_t K, void* planes,
+                                  int64_t plane_stride);
 
 int hs_host_callback(hs_stream_t s, void (*fn)(void*), void* user);
 int hs_capture_begin(hs_stream_t s);

@@ -43,6 +43,9 @@ class OpArgs(ctypes.Structure):
         ("dims", c_int64 * 4),
         ("fparam", ctypes.c_float * 2),
         ("aux", c_void_p),
+        ("n_out", c_int),
+        ("outs", c_void_p * 4),
+        ("out_strides", c_int64 * 4),
     ]
 
 
@@ -86,6 +89,7 @@ _PROTOS = {
     "hs_graph_destroy": (c_int, [c_void_p]),
     "hs_launch_count": (c_int64, []),
     "hs_gemm_split_weights": (c_int, [c_void_p, c_void_p, c_int, c_int64, c_int64, c_void_p]),
+    "hs_gemm_split_weights_strided": (c_int, [c_void_p, c_void_p, c_int, c_int64, c_int64, c_void_p, c_int64]),
     "hs_engine_create": (c_int, [c_char_p, ctypes.POINTER(c_void_p)]),
     "hs_engine_destroy": (c_int, [c_void_p]),
     "hs_engine_bind": (c_int, [c_void_p, c_int, c_int, c_void_p, c_int64, c_int]),

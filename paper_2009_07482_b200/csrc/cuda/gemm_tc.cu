@@ -40,6 +40,9 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 32;  // fp32 elements per K-block = one 128-byte swizzle row
+#ifndef HS_SMEM_BUDGET_KB
+#define HS_SMEM_BUDGET_KB 200
+#endif
 constexpr int kEpiWarps = 4;
 // Converters work in groups of 4 warps (one per TMEM lane quarter); group g
 // handles the K-blocks with it % kConvGroups == g, so kConvGroups K-blocks are
@@ -161,11 +164,16 @@ struct Cfg {
   static constexpr int kOperand = 2 * kPlaneB;             // B hi + lo (A lives in TMEM)
   // TMEM (512 columns): two BN-wide fp32 accumulators + kNO A stages of 64
   // columns (32 hi + 32 lo tf32 columns, one row per lane).
-  static constexpr int kAccCols = 2 * BN;
+  // Double-buffer the accumulator only when that still leaves room for 4 A
+  // stages (BN <= 128); wider tiles trade epilogue overlap for pipeline depth.
+  static constexpr int kAccBufs = (2 * BN + 4 * 64 <= 512) ? 2 : 1;
+  static constexpr int kAccCols = kAccBufs * BN;
+  static constexpr int kBudget = HS_SMEM_BUDGET_KB * 1024;  // + barriers/alignment stays under the 227 KB opt-in limit
   static constexpr int kNOtm = (512 - kAccCols) / 64;
-  static constexpr int kNOcap = kNOtm < 4 ? kNOtm : 4;
+  static constexpr int kNOsm = (kBudget - 2 * kStaging) / kOperand;
+  static constexpr int kNOmin = kNOtm < kNOsm ? kNOtm : kNOsm;
+  static constexpr int kNOcap = kNOmin < 4 ? kNOmin : 4;
   static constexpr int kNO = kNOcap - kNOcap % kConvGroups;
-  static constexpr int kBudget = 200 * 1024;
   static constexpr int kNSraw = (kBudget - kNO * kOperand) / kStaging;
   static constexpr int kNScap = kNSraw > 6 ? 6 : kNSraw;
   static constexpr int kNS = kNScap - kNScap % kConvGroups;
@@ -184,6 +192,11 @@ struct TileParams {
   int relu;
   int m_tiles, n_tiles;
   int total_tiles;
+  // Grouped launch (n_out > 0): N = n_out * Nm columns, member m owns columns
+  // [m*Nm, (m+1)*Nm) and writes its own output Cs[m] (row stride Nm).
+  int n_out, Nm;
+  float* Cs[4];
+  int64_t sCs[4];
 };
 
 // D[tmem] (+)= A[tmem] · B[smem]; A is K-major in TMEM (lane = row, column = k).
@@ -298,8 +311,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr uint32_t idesc = instr_desc_tf32(BN);
       uint32_t it = 0, lt = 0;
       for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x, ++lt) {
-        const uint32_t acc = lt & 1u;
-        mbar_wait(acc_empty(int(acc)), ((lt >> 1) & 1u) ^ 1u);
+        const uint32_t acc = lt % uint32_t(L::kAccBufs);
+        mbar_wait(acc_empty(int(acc)), ((lt / uint32_t(L::kAccBufs)) & 1u) ^ 1u);
         tc_fence_after();
         const uint32_t d = tmem + acc * uint32_t(BN);
         for (int kb = 0; kb < nk; ++kb, ++it) {
@@ -334,11 +347,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x, ++lt) {
       int m0, inst, n0;
       decode(t, m0, inst, n0);
-      const uint32_t acc = lt & 1u;
-      mbar_wait(acc_full(int(acc)), (lt >> 1) & 1u);
+      const uint32_t acc = lt % uint32_t(L::kAccBufs);
+      mbar_wait(acc_full(int(acc)), (lt / uint32_t(L::kAccBufs)) & 1u);
       tc_fence_after();
       const int row = m0 + q * 32 + lane;
-      float* crow = p.C + int64_t(inst) * p.sC + int64_t(row) * p.N;
 #pragma unroll 1
       for (int cb = 0; cb < BN / 32; ++cb) {
         uint32_t r[32];
@@ -359,9 +371,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(acc_empty(int(acc)));
         }
-        const int c0 = n0 + cb * 32;
+        // destination of this 32-column chunk: the single C, or member m's C
+        int c0 = n0 + cb * 32, ncols = p.N;
+        float* crow;
+        if (p.n_out > 0) {
+          const int m = c0 / p.Nm;
+          c0 -= m * p.Nm;
+          ncols = p.Nm;
+          crow = p.Cs[m] + int64_t(inst) * p.sCs[m] + int64_t(row) * p.Nm;
+        } else {
+          crow = p.C + int64_t(inst) * p.sC + int64_t(row) * p.N;
+        }
         if (row < p.M) {
-          if (c0 + 32 <= p.N && (p.N & 3) == 0) {
+          if (c0 + 32 <= ncols && (ncols & 3) == 0) {
 #pragma unroll
             for (int j = 0; j < 32; j += 4) {
               float4 v = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
@@ -372,7 +394,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               *reinterpret_cast<float4*>(crow + c0 + j) = v;
             }
           } else {
-            for (int j = 0; j < 32 && c0 + j < p.N; ++j) {
+            for (int j = 0; j < 32 && c0 + j < ncols; ++j) {
               float v = __uint_as_float(r[j]);
               crow[c0 + j] = p.relu ? fmaxf(v, 0.f) : v;
             }
@@ -458,10 +480,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // Weight preparation: B (resident) -> K-major tf32 hi/lo planes [2][N][K].
 template <bool kNT>
-__global__ void split_weights_kernel(const float* __restrict__ B, float* __restrict__ planes, int N, int K) {
+__global__ void split_weights_kernel(const float* __restrict__ B, float* __restrict__ planes, int N, int K,
+                                     int64_t plane) {
   __shared__ float tile[32][33];
   const int n0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
-  const int64_t plane = int64_t(N) * K;
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
     // load tile[n][k]
     int n = n0 + (kNT ? i : threadIdx.x), k = k0 + (kNT ? threadIdx.x : i);
@@ -550,8 +572,24 @@ cudaError_t launch(const GemmArgs& a, cudaStream_t s) {
     ok = make_map(&mB, a.B, N, K, nB, N * 4, sB, BN, BK, false);
   }
   if (!ok) return cudaErrorInvalidValue;
-  TileParams p{a.C, a.sC, a.M, a.N, a.K, a.batch, a.sA != 0, a.sB != 0, a.relu ? 1 : 0,
-               (a.M + BM - 1) / BM, (a.N + BN - 1) / BN, 0};
+  TileParams p{};
+  p.C = a.C;
+  p.sC = a.sC;
+  p.M = a.M;
+  p.N = a.N;
+  p.K = a.K;
+  p.batch = a.batch;
+  p.a_batched = a.sA != 0;
+  p.b_batched = a.sB != 0;
+  p.relu = a.relu ? 1 : 0;
+  p.m_tiles = (a.M + BM - 1) / BM;
+  p.n_tiles = (a.N + BN - 1) / BN;
+  p.n_out = a.n_out > 1 ? a.n_out : 0;
+  p.Nm = p.n_out ? a.N / a.n_out : a.N;
+  for (int i = 0; i < p.n_out; ++i) {
+    p.Cs[i] = a.Cs[i];
+    p.sCs[i] = a.sCs[i];
+  }
   p.total_tiles = p.m_tiles * p.n_tiles * a.batch;
   const int grid = p.total_tiles < num_sms() ? p.total_tiles : num_sms();
   kernel<<<grid, kThreads, L::kTotal, s>>>(mA, mB, p);
@@ -579,14 +617,23 @@ bool gemm_tcgen05_supported(const GemmArgs& a) {
 }
 
 cudaError_t gemm_tcgen05(const GemmArgs& a, int terms, cudaStream_t s) {
+  if (a.n_out > 1) {
+    // grouped launch: one tile covers every member (a.N = total columns)
+    if (!a.Bplanes || a.N % a.n_out || (a.N / a.n_out) % 32 || a.n_out > 4) return cudaErrorInvalidValue;
+    if (a.N == 128) return launch_bn<128>(a, terms, s);
+    if (a.N == 192) return launch_bn<192>(a, terms, s);
+    return cudaErrorInvalidValue;
+  }
   if (a.N <= 64) return launch_bn<64>(a, terms, s);
   return launch_bn<128>(a, terms, s);
 }
 
-cudaError_t gemm_split_weights(const float* B, GemmLayout layout, int N, int K, float* planes, cudaStream_t s) {
+cudaError_t gemm_split_weights(const float* B, GemmLayout layout, int N, int K, float* planes, int64_t plane_stride,
+                               cudaStream_t s) {
+  const int64_t plane = plane_stride > 0 ? plane_stride : int64_t(N) * K;
   dim3 grid((N + 31) / 32, (K + 31) / 32), block(32, 8);
-  if (layout == GemmLayout::nt) split_weights_kernel<true><<<grid, block, 0, s>>>(B, planes, N, K);
-  else split_weights_kernel<false><<<grid, block, 0, s>>>(B, planes, N, K);
+  if (layout == GemmLayout::nt) split_weights_kernel<true><<<grid, block, 0, s>>>(B, planes, N, K, plane);
+  else split_weights_kernel<false><<<grid, block, 0, s>>>(B, planes, N, K, plane);
   return cudaGetLastError();
 }
 

@@ -250,7 +250,20 @@ int hs_launch(hs_stream_t st, int op, const hs_op_args* a, int math, int batch) 
                      int(a->dims[0]), int(a->dims[1]), int(a->dims[2]), batch,
                      op == HS_OP_GEMM_NT ? hs::GemmLayout::nt : hs::GemmLayout::nn, op == HS_OP_GEMM_RELU,
                      math == HS_MATH_FP32_SIMT ? nullptr : static_cast<const float*>(a->aux)};
-      if (math == HS_MATH_FP32_SIMT || !hs::gemm_tcgen05_supported(g)) e = hs::gemm_simt(g, s);
+      if (a->n_out > 1) {
+        // grouped launch of sibling GEMMs (tcgen05 only; the caller checked eligibility)
+        if (a->n_out > 4 || !a->aux || math == HS_MATH_FP32_SIMT) return invalid("bad grouped GEMM launch");
+        g.n_out = a->n_out;
+        g.N = int(a->dims[1]) * a->n_out;
+        for (int i = 0; i < a->n_out; ++i) {
+          g.Cs[i] = static_cast<float*>(a->outs[i]);
+          g.sCs[i] = a->out_strides[i];
+        }
+        g.C = g.Cs[0];
+        g.sC = g.sCs[0];
+        if (!hs::gemm_tcgen05_supported(g)) return invalid("grouped GEMM shape not supported");
+        e = hs::gemm_tcgen05(g, math == HS_MATH_TF32 ? 1 : 3, s);
+      } else if (math == HS_MATH_FP32_SIMT || !hs::gemm_tcgen05_supported(g)) e = hs::gemm_simt(g, s);
       else e = hs::gemm_tcgen05(g, math == HS_MATH_TF32 ? 1 : 3, s);
       break;
     }
@@ -291,11 +304,17 @@ int hs_launch(hs_stream_t st, int op, const hs_op_args* a, int math, int batch) 
 int64_t hs_launch_count(void) { return g_launches.load(); }
 
 int hs_gemm_split_weights(hs_stream_t st, const void* B, int transposed, int64_t N, int64_t K, void* planes) {
+  return hs_gemm_split_weights_strided(st, B, transposed, N, K, planes, N * K);
+}
+
+int hs_gemm_split_weights_strided(hs_stream_t st, const void* B, int transposed, int64_t N, int64_t K, void* planes,
+                                  int64_t plane_stride) {
   if (!st || !B || !planes) return invalid("null argument");
   if (N < 1 || K < 1 || N > (1 << 30) || K > (1 << 30)) return invalid("bad weight shape");
+  if (plane_stride < N * K) return invalid("plane stride smaller than one plane");
   if (int r = use_device(st->gpu)) return r;
   cudaError_t e = hs::gemm_split_weights(static_cast<const float*>(B), transposed ? hs::GemmLayout::nt : hs::GemmLayout::nn,
-                                         int(N), int(K), static_cast<float*>(planes), st->s);
+                                         int(N), int(K), static_cast<float*>(planes), plane_stride, st->s);
   if (e != cudaSuccess) return check(e, "split weights");
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return HS_OK;

@@ -24,9 +24,16 @@ struct GemmArgs {
   // Optional: resident B pre-split into K-major tf32 planes [2][N][K] (hi, lo)
   // by gemm_split_weights; then B is fed to the tensor cores by TMA directly.
   const float* Bplanes = nullptr;
+  // Grouped launch of n_out sibling GEMMs sharing A: N is the total column
+  // count, Bplanes their concatenated planes, member m writes Cs[m] (stride sCs[m]).
+  int n_out = 0;
+  float* Cs[4] = {nullptr, nullptr, nullptr, nullptr};
+  int64_t sCs[4] = {0, 0, 0, 0};
 };
 
-cudaError_t gemm_split_weights(const float* B, GemmLayout layout, int N, int K, float* planes, cudaStream_t s);
+// planes: hi at planes[n*K + k], lo at planes[plane_stride + n*K + k]
+cudaError_t gemm_split_weights(const float* B, GemmLayout layout, int N, int K, float* planes, int64_t plane_stride,
+                               cudaStream_t s);
 
 // math: 0 = TF32x3 (tcgen05), 1 = TF32 (tcgen05), 2 = fp32 SIMT
 cudaError_t gemm_tcgen05(const GemmArgs& a, int terms, cudaStream_t s);

@@ -18,6 +18,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstring>
+#include <tuple>
 
 #include "../core/json.hpp"
 #include "hetsim/errors.hpp"
@@ -301,6 +302,15 @@ void Engine::upload_resident() {
   }
   for (const auto& [key, pl] : planes_)
     hs_ok(hs_gemm_split_weights(s, resident_buf_.at(pl.gi), pl.nt ? 1 : 0, pl.n, pl.k, pl.ptr), "split weights");
+  for (const auto& fg : fuse_groups_) {
+    const int64_t members = int64_t(fg.kernels.size());
+    for (int64_t m = 0; m < members; ++m) {
+      const int gi = group_of_.at(nodes_.at(fg.kernels[size_t(m)]).inputs[1]);
+      hs_ok(hs_gemm_split_weights_strided(s, resident_buf_.at(gi), 0, fg.n, fg.k,
+                                          static_cast<float*>(fg.planes) + m * fg.n * fg.k, members * fg.n * fg.k),
+            "split grouped weights");
+    }
+  }
   hs_ok(hs_stream_sync(s), "resident upload sync");
   resident_uploaded_ = true;
 }
@@ -432,9 +442,50 @@ void Engine::issue(Slot& sl, const TaskComponent& t, const CommandQueueStructure
         }
         break;
       }
-      case CmdKind::ndrange:
-        launch_node(sl, s, c.kernel);
+      case CmdKind::ndrange: {
+        auto lead = graph ? fuse_leader_.find({t.id, ev}) : fuse_leader_.end();
+        auto member = graph ? fuse_member_.find({t.id, ev}) : fuse_member_.end();
+        if (lead != fuse_leader_.end()) {
+          // Grouped launch for every member: first make this stream wait for the
+          // other members' inter-edge inputs (their dependent writes come later
+          // in enqueue order), then one tcgen05 launch writes all outputs.
+          const FuseGroup& fg = fuse_groups_[size_t(lead->second)];
+          for (size_t m = 1; m < fg.kernels.size(); ++m)
+            for (const auto& qq : q.queues)
+              for (const Command& w : qq)
+                if (w.kernel == fg.kernels[m] && w.kind == CmdKind::write && w.dependent) {
+                  auto src = sl.edge_event.find(w.edge);
+                  if (src == sl.edge_event.end()) fail(Errc::deadlock, "grouped launch before its producer");
+                  hs_ok(hs_stream_wait(s, event(sl, src->second.first, src->second.second)), "inter-edge wait");
+                }
+          const Node& nd = nodes_.at(fg.kernels[0]);
+          hs_op_args a{};
+          a.n_in = 2;
+          a.in[0] = sl.buf.at(nd.inputs[0]);
+          a.in_stride[0] = bytes_.at(nd.inputs[0]) / 4;
+          a.in[1] = sl.buf.at(nd.inputs[1]);
+          a.in_stride[1] = 0;
+          a.out = sl.buf.at(nd.output);
+          a.out_stride = bytes_.at(nd.output) / 4;
+          for (int i = 0; i < 3; ++i) a.dims[i] = nd.dims[i];
+          a.aux = fg.planes;
+          a.n_out = int(fg.kernels.size());
+          for (size_t m = 0; m < fg.kernels.size(); ++m) {
+            const auto& okey = nodes_.at(fg.kernels[m]).output;
+            a.outs[m] = sl.buf.at(okey);
+            a.out_strides[m] = bytes_.at(okey) / 4;
+          }
+          hs_ok(hs_launch(s, nd.op, &a, cfg_.math, cfg_.batch), "hs_launch (grouped)");
+          record = true;
+        } else if (member != fuse_member_.end()) {
+          // computed by the group's leader launch: order this queue after it
+          const FuseGroup& fg = fuse_groups_[size_t(member->second)];
+          hs_ok(hs_stream_wait(s, event(sl, t.id, fg.events[0])), "grouped member wait");
+        } else {
+          launch_node(sl, s, c.kernel);
+        }
         break;
+      }
       case CmdKind::read:
         if (c.dependent) {
           sl.edge_event[c.edge] = {t.id, ev};
@@ -455,6 +506,62 @@ void Engine::issue(Slot& sl, const TaskComponent& t, const CommandQueueStructure
     if (record) hs_ok(hs_event_record(event(sl, t.id, ev), s), "event record");
     if (!graph && q.callbacks.count(ev))
       hs_ok(hs_host_callback(s, &CUDART_CB_trampoline, new CbData{this, {t.id, ev}}), "host callback");
+  }
+}
+
+void Engine::plan_fusion() {
+  auto producers = g_.producer_edge();
+  const auto& ec = sched_->edge_classes();
+  for (const auto& q : plan_.structures) {
+    std::set<int> dep_targets;
+    for (auto [a, b] : q.deps) dep_targets.insert(b);
+    // candidate key: (op, resolved A source, M, N, K) -> ndrange events
+    std::map<std::tuple<int, long long, int64_t, int64_t, int64_t>, std::vector<std::pair<int, int>>> cands;
+    for (int ev = 0; ev < q.event_count; ++ev) {
+      const Command& c = q.command_of(ev);
+      if (c.kind != CmdKind::ndrange || dep_targets.count(ev)) continue;
+      const Node& nd = nodes_.at(c.kernel);
+      if ((nd.op != HS_OP_GEMM && nd.op != HS_OP_GEMM_RELU) || !node_planes_.count(c.kernel)) continue;
+      if (nd.dims[1] != 64) continue;  // grouped tiles of 2 x 64 or 3 x 64 columns
+      // no producer inside the component: launching early cannot reorder a data dependency
+      bool intra = false;
+      for (const auto& in : nd.inputs) {
+        auto pe = producers.find(in);
+        if (pe != producers.end() && ec.edge_kind[size_t(pe->second)] == EdgeKind::intra) intra = true;
+      }
+      if (intra) continue;
+      const auto& a = nd.inputs[0];
+      long long src;
+      auto al = alias_.find(a);
+      if (al != alias_.end()) src = (static_cast<long long>(al->second.first) << 20) | al->second.second;
+      else if (group_of_.count(a)) src = -1 - group_of_.at(a);
+      else continue;
+      cands[{nd.op, src, nd.dims[0], nd.dims[1], nd.dims[2]}].push_back({ev, c.kernel});
+    }
+    for (auto& [key, list] : cands) {
+      size_t i = 0;
+      while (list.size() - i >= 2) {
+        const size_t take = (list.size() - i) >= 3 ? 3 : 2;
+        FuseGroup fg;
+        fg.component = q.component;
+        fg.n = std::get<3>(key);
+        fg.k = std::get<4>(key);
+        for (size_t j = 0; j < take; ++j) {
+          fg.events.push_back(list[i + j].first);
+          fg.kernels.push_back(list[i + j].second);
+        }
+        const size_t bytes = size_t(2 * int64_t(take) * fg.n * fg.k * 4);
+        hs_ok(hs_malloc(ctx_, bytes, &fg.planes), "hs_malloc");
+        allocations_.push_back(fg.planes);
+        device_bytes_ += int64_t(bytes);
+        const int gi = int(fuse_groups_.size());
+        fuse_leader_[{q.component, fg.events[0]}] = gi;
+        for (size_t j = 1; j < take; ++j) fuse_member_[{q.component, fg.events[j]}] = gi;
+        launches_per_batch_ -= int64_t(take) - 1;
+        fuse_groups_.push_back(std::move(fg));
+        i += take;
+      }
+    }
   }
 }
 
@@ -527,6 +634,7 @@ void Engine::run(int64_t first, int64_t n, int64_t* elapsed_ns) {
     if (cfg_.graph_mode) {
       PlanExecutor pe;
       plan_ = sched_->run(pe);
+      if (cfg_.fuse && cfg_.math != HS_MATH_FP32_SIMT) plan_fusion();
       for (auto& sl : slots_) capture(sl);
     }
     planned_ = true;
@@ -600,6 +708,8 @@ std::string Engine::info(const std::string& what) const {
     out.set("resident_groups", Value::of(static_cast<long long>(resident_buf_.size())));
     out.set("instance_groups", Value::of(static_cast<long long>(groups_.size() - resident_buf_.size())));
     out.set("aliased_inputs", Value::of(static_cast<long long>(alias_.size())));
+    out.set("grouped_launches", Value::of(static_cast<long long>(fuse_groups_.size())));
+    out.set("launches_per_batch", Value::of(static_cast<long long>(launches_per_batch_)));
   } else if (what == "stats") {
     out.set("launches_per_batch", Value::of(static_cast<long long>(launches_per_batch_)));
     out.set("runs", Value::of(static_cast<long long>(runs_)));
@@ -668,6 +778,7 @@ int hs_engine_create(const char* config_json, hs_engine_t* out) {
     }
     if (const json::Value* v = c.find("cpu_devices"))
       for (const json::Value* x : v->items()) cfg.cpu_devices.insert(x->as_int());
+    if (const json::Value* v = c.find("fuse")) cfg.fuse = v->as_int() != 0;
     *out = reinterpret_cast<hs_engine_t>(new Engine(std::move(cfg)));
   });
 }

@@ -41,6 +41,7 @@ struct EngineConfig {
   int slots = 2;
   int math = HS_MATH_TF32X3;
   std::set<int> cpu_devices;
+  bool fuse = true;  // grouped launch of sibling GEMMs (graph mode)
 };
 
 class Engine {
@@ -128,6 +129,21 @@ class Engine {
   };
   std::map<std::pair<int, bool>, Planes> planes_;
   std::map<int, void*> node_planes_;  // kernel -> planes
+
+  // Grouped launches (graph mode): sibling GEMM ndranges of one component that
+  // share their A input, have resident B and no intra-component producer run as
+  // one tcgen05 launch with their B planes side by side (N = members x 64).
+  struct FuseGroup {
+    int component = -1;
+    std::vector<int> kernels;  // members, ascending ndrange event
+    std::vector<int> events;
+    void* planes = nullptr;
+    int64_t n = 0, k = 0;  // per member
+  };
+  void plan_fusion();
+  std::vector<FuseGroup> fuse_groups_;
+  std::map<std::pair<int, int>, int> fuse_leader_;  // (component, ndrange event) -> group
+  std::map<std::pair<int, int>, int> fuse_member_;  // (component, ndrange event) -> group (non-leaders)
   hs_ctx_t ctx_ = nullptr;
   std::vector<Slot> slots_;
   bool planned_ = false;

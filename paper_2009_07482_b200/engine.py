@@ -28,9 +28,10 @@ def _ptr_and_nbytes(arr):
 
 class Engine:
     def __init__(self, spec_text: str, params: dict | None = None, *, gpu: int = 0, policy: str = "clustering",
-                 mode: str = "graph", batch: int = 1, slots: int = 2, math: str = "tf32x3", cpu_devices=()):
+                 mode: str = "graph", batch: int = 1, slots: int = 2, math: str = "tf32x3", cpu_devices=(),
+                 fuse: bool = True):
         cfg = {"spec": spec_text, "params": dict(params or {}), "gpu": gpu, "policy": policy, "mode": mode,
-               "batch": batch, "slots": slots, "math": math, "cpu_devices": list(cpu_devices)}
+               "batch": batch, "slots": slots, "math": math, "cpu_devices": list(cpu_devices), "fuse": int(fuse)}
         self._lib = lib()
         h = ctypes.c_void_p()
         check(self._lib.hs_engine_create(json.dumps(cfg).encode(), ctypes.byref(h)), "hs_engine_create")

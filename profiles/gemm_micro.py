@@ -50,7 +50,44 @@ def run(M, N, K, batch, op="gemm", math="tf32x3", presplit=True, shared=True, re
     return us
 
 
+def run_grouped(M, N, K, batch, members=3, reps=20):
+    """Grouped launch: `members` sibling GEMMs sharing A, N columns each, one launch."""
+    A = torch.randn(batch, M * K, device="cuda")
+    Bs = [torch.randn(N * K, device="cuda") for _ in range(members)]
+    planes = torch.empty(2 * members * N * K, device="cuda")
+    for m, B in enumerate(Bs):
+        _native.check(L.hs_gemm_split_weights_strided(st, B.data_ptr(), 0, N, K, planes.data_ptr() + 4 * m * N * K,
+                                                      members * N * K))
+    Cs = [torch.empty(batch, M * N, device="cuda") for _ in range(members)]
+    a = _native.OpArgs()
+    a.n_in = 2
+    a.in_[0], a.in_[1] = A.data_ptr(), Bs[0].data_ptr()
+    a.in_stride[0], a.in_stride[1] = M * K, 0
+    a.out, a.out_stride = Cs[0].data_ptr(), M * N
+    a.dims[0], a.dims[1], a.dims[2] = M, N, K
+    a.aux = planes.data_ptr()
+    a.n_out = members
+    for m in range(members):
+        a.outs[m], a.out_strides[m] = Cs[m].data_ptr(), M * N
+    for _ in range(3):
+        _native.check(L.hs_launch(st, 0, ctypes.byref(a), 0, batch))
+    _native.check(L.hs_event_record(e0, st))
+    for _ in range(reps):
+        _native.check(L.hs_launch(st, 0, ctypes.byref(a), 0, batch))
+    _native.check(L.hs_event_record(e1, st))
+    _native.check(L.hs_event_sync(e1))
+    ns = ctypes.c_int64()
+    _native.check(L.hs_event_elapsed_ns(e0, e1, ctypes.byref(ns)))
+    us = ns.value / 1e3 / reps
+    flops = 2.0 * M * N * K * batch * members
+    print(f"grouped   M={M:4d} N={members}x{N:3d} K={K:5d} batch={batch:4d}: {us:8.2f} us  {flops / us / 1e6:7.1f} TFLOP/s",
+          flush=True)
+
+
 if __name__ == "__main__":
+    for batch in (128, 148, 256):
+        run_grouped(128, 64, 512, batch)
+    run_grouped(128, 64, 512, 128, members=2)
     for batch in (64, 128, 148, 296, 592):
         run(128, 64, 512, batch)
     for K in (128, 512, 2048):

@@ -89,6 +89,23 @@ def test_two_layer_encoder_batched_graph(oracle_mod):
         assert _normwise(outs[key][i], ref[key][i]) <= TOL
 
 
+def test_grouped_sibling_gemms_match_unfused(oracle_mod):
+    """Graph mode groups each head's Q/K/V projections (3 x N=64, shared X) into one
+    N=192 tcgen05 launch; results equal the unfused launches and the oracle."""
+    text, params, meta = workloads.encoder(layers=2)
+    n = 3
+    arrays = _encoder_arrays(meta, params, n)
+    ref = oracle_mod.run_dag(text, params, arrays, n)
+    key = (meta["output"]["kernel"], meta["output"]["pos"])
+    fused, _, plan = _run_gpu(text, params, arrays, n, mode="graph", batch=3, fuse=True)
+    plain, _, plan0 = _run_gpu(text, params, arrays, n, mode="graph", batch=3, fuse=False)
+    assert plan["grouped_launches"] == 16 and plan0["grouped_launches"] == 0  # 8 heads x 2 layers
+    assert plan["launches_per_batch"] == plan0["launches_per_batch"] - 32
+    for i in range(n):
+        assert _normwise(fused[key][i], ref[key][i]) <= TOL
+        assert _normwise(fused[key][i], plain[key][i]) <= 1e-6
+
+
 def test_dynamic_completion_log_replays_identically(oracle_mod):
     """Bit-exact scheduling parity: the completion order observed on the GPU,
     fed back through the CPU scheduler (product and oracle restatement),
