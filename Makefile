@@ -13,7 +13,8 @@ SRC      := $(PKG)/csrc
 BUILD    := build
 ARCH     := -gencode arch=compute_100a,code=sm_100a
 CXXFLAGS := -std=c++20 -O2 -fPIC -Wall -Wextra -Iinclude -I$(SRC)
-NVFLAGS  := -std=c++20 -O3 $(ARCH) -lineinfo -Xcompiler -fPIC -Iinclude -I$(SRC) -Xptxas -v
+NVEXTRA  ?=
+NVFLAGS  := -std=c++20 -O3 $(ARCH) -lineinfo -Xcompiler -fPIC -Iinclude -I$(SRC) -Xptxas -v $(NVEXTRA)
 
 CPP_SRCS := $(wildcard $(SRC)/core/*.cpp) $(wildcard $(SRC)/sched/*.cpp) \
             $(wildcard $(SRC)/capi/*.cpp) $(wildcard $(SRC)/exec/*.cpp)

@@ -43,18 +43,35 @@ constexpr int BK = 32;  // fp32 elements per K-block = one 128-byte swizzle row
 #ifndef HS_SMEM_BUDGET_KB
 #define HS_SMEM_BUDGET_KB 200
 #endif
+#ifndef HS_NO_CAP
+#define HS_NO_CAP 4  // max TMEM A stages
+#endif
+// Timing experiments only (profiles/): skip data movement / A conversion.
+#ifndef HS_DBG_NOTMA
+#define HS_DBG_NOTMA 0
+#endif
+#ifndef HS_DBG_NOCONV
+#define HS_DBG_NOCONV 0
+#endif
+#ifndef HS_DBG_NOEPI
+#define HS_DBG_NOEPI 0
+#endif
 constexpr int kEpiWarps = 4;
+constexpr int kEpiTileBytes = 32 * 33 * 4;  // padded 32x32 fp32 transpose tile per epilogue warp
 // Converters work in groups of 4 warps (one per TMEM lane quarter); group g
 // handles the K-blocks with it % kConvGroups == g, so kConvGroups K-blocks are
 // split concurrently and the per-block latency chain (smem load -> split ->
 // tcgen05.st -> wait::st -> arrive) is overlapped instead of serialised.
 // Stage counts are multiples of kConvGroups so each group revisits only its
 // own slots, one phase at a time (a parity wait two phases ahead would alias).
-constexpr int kConvGroups = 2;
+#ifndef HS_CONV_GROUPS
+#define HS_CONV_GROUPS 2
+#endif
+constexpr int kConvGroups = HS_CONV_GROUPS;
 constexpr int kGroupWarps = 4;
 constexpr int kConvWarps = kConvGroups * kGroupWarps;
-constexpr int kThreads = 32 * (4 + kEpiWarps + kConvWarps);  // 4 control + 4 epilogue + 8 converter warps
-static_assert(kThreads == 512, "warp-role layout");
+constexpr int kThreads = 32 * (4 + kEpiWarps + kConvWarps);  // 4 control + 4 epilogue + converter warps
+static_assert(kThreads <= 1024, "warp-role layout");
 
 // ----------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -137,6 +154,9 @@ __device__ __forceinline__ float lds32(uint32_t addr) {
   asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
   return v;
 }
+__device__ __forceinline__ void sts32(uint32_t addr, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
 __device__ __forceinline__ void sts128(uint32_t addr, float4 v) {
   asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
                : "memory");
@@ -172,13 +192,14 @@ struct Cfg {
   static constexpr int kNOtm = (512 - kAccCols) / 64;
   static constexpr int kNOsm = (kBudget - 2 * kStaging) / kOperand;
   static constexpr int kNOmin = kNOtm < kNOsm ? kNOtm : kNOsm;
-  static constexpr int kNOcap = kNOmin < 4 ? kNOmin : 4;
+  static constexpr int kNOcap = kNOmin < HS_NO_CAP ? kNOmin : HS_NO_CAP;
   static constexpr int kNO = kNOcap - kNOcap % kConvGroups;
   static constexpr int kNSraw = (kBudget - kNO * kOperand) / kStaging;
   static constexpr int kNScap = kNSraw > 6 ? 6 : kNSraw;
   static constexpr int kNS = kNScap - kNScap % kConvGroups;
   static_assert(kNS % kConvGroups == 0 && kNO % kConvGroups == 0, "stage rings must divide among groups");
-  static constexpr int kTotal = kNS * kStaging + kNO * kOperand + 1024 /*barriers*/ + 1024 /*align*/;
+  static constexpr int kTotal =
+      kNS * kStaging + kNO * kOperand + 1024 /*barriers*/ + kEpiWarps * kEpiTileBytes + 1024 /*align*/;
   static_assert(kNS >= 2 && kNO >= 2, "pipeline too shallow");
   static_assert(kTotal <= 227 * 1024, "shared memory budget exceeded");
 };
@@ -236,6 +257,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto acc_full = [&](int a) { return bars + 8u * uint32_t(2 * NS + 2 * NO + a); };
   auto acc_empty = [&](int a) { return bars + 8u * uint32_t(2 * NS + 2 * NO + 2 + a); };
   const uint32_t tmem_slot = bars + 8u * uint32_t(2 * NS + 2 * NO + 4);
+  const uint32_t scratch = bars + 1024u;  // epilogue transpose tiles, one per epilogue warp
   const uint32_t* tmem_slot_ptr = reinterpret_cast<const uint32_t*>(smem_raw + (tmem_slot - smem_u32(smem_raw)));
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -289,18 +311,41 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int s = int(it % NS);
           mbar_wait(st_empty(s), ((it / NS) & 1u) ^ 1u);
           const uint32_t sa = staging + uint32_t(s) * L::kStaging;
+#if HS_DBG_NOTMA  // timing experiment only: no data movement
+          mbar_arrive(st_full(s));
+          (void)sa; (void)ia; (void)ib; (void)m0;
+#else
           mbar_expect_tx(st_full(s), L::kStaging);
           tma_load_3d(sa, &tmA, st_full(s), kb * BK, m0, ia);
           if constexpr (kBSrc == 0) tma_load_3d(sa + L::kStageA, &tmB, st_full(s), kb * BK, n0, ib);
           if constexpr (kBSrc == 1) tma_load_3d(sa + L::kStageA, &tmB, st_full(s), n0, kb * BK, ib);
-          if constexpr (L::kBPre) {
-            // pre-split weight planes (hi at plane 0, lo at plane 1) straight into the operand ring
+#endif
+        }
+      }
+    }
+  } else if (warp == 3) {
+    // ------------------------------------------------------------ weight producer
+    // Pre-split weight planes (hi at plane 0, lo at plane 1) straight into the
+    // operand ring. A separate thread from the A producer, so A prefetch runs
+    // kNS deep instead of stalling behind the operand ring.
+    if constexpr (L::kBPre) {
+      if (lane == 0) {
+        uint32_t it = 0;
+        for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
+          int m0, inst, n0;
+          decode(t, m0, inst, n0);
+          for (int kb = 0; kb < nk; ++kb, ++it) {
             const int o = int(it % NO);
             mbar_wait(op_empty(o), ((it / NO) & 1u) ^ 1u);
             const uint32_t b_hi = operand + uint32_t(o) * L::kOperand;
+#if HS_DBG_NOTMA
+            mbar_arrive(op_full(o));
+            (void)b_hi;
+#else
             mbar_expect_tx(op_full(o), (kTerms > 1 ? 2 : 1) * L::kPlaneB);
             tma_load_3d(b_hi, &tmB, op_full(o), kb * BK, n0, 0);
             if constexpr (kTerms > 1) tma_load_3d(b_hi + L::kPlaneB, &tmB, op_full(o), kb * BK, n0, 1);
+#endif
           }
         }
       }
@@ -371,35 +416,48 @@ __global__ void __launch_bounds__(kThreads, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(acc_empty(int(acc)));
         }
+        // Transpose the 32x32 chunk through this warp's padded smem tile: TMEM
+        // hands each thread one row, so storing straight from registers would
+        // make every store instruction touch 32 rows. After the transpose each
+        // group of 8 lanes writes one full 128-byte row (coalesced).
+        const uint32_t tile = scratch + uint32_t(q) * uint32_t(kEpiTileBytes);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float v = __uint_as_float(r[j]);
+          sts32(tile + uint32_t(lane * 33 + j) * 4u, p.relu ? fmaxf(v, 0.f) : v);
+        }
+        __syncwarp();
         // destination of this 32-column chunk: the single C, or member m's C
-        int c0 = n0 + cb * 32, ncols = p.N;
-        float* crow;
+        int c0 = n0 + cb * 32, ld = p.N;
+        float* cbase;
         if (p.n_out > 0) {
           const int m = c0 / p.Nm;
           c0 -= m * p.Nm;
-          ncols = p.Nm;
-          crow = p.Cs[m] + int64_t(inst) * p.sCs[m] + int64_t(row) * p.Nm;
+          ld = p.Nm;
+          cbase = p.Cs[m] + int64_t(inst) * p.sCs[m];
         } else {
-          crow = p.C + int64_t(inst) * p.sC + int64_t(row) * p.N;
+          cbase = p.C + int64_t(inst) * p.sC;
         }
-        if (row < p.M) {
-          if (c0 + 32 <= ncols && (ncols & 3) == 0) {
+        const int cq = (lane & 7) * 4, rsub = lane >> 3;
+        const bool vec = c0 + 32 <= ld && (ld & 3) == 0;
 #pragma unroll
-            for (int j = 0; j < 32; j += 4) {
-              float4 v = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
-                                     __uint_as_float(r[j + 3]));
-              if (p.relu) {
-                v.x = fmaxf(v.x, 0.f); v.y = fmaxf(v.y, 0.f); v.z = fmaxf(v.z, 0.f); v.w = fmaxf(v.w, 0.f);
-              }
-              *reinterpret_cast<float4*>(crow + c0 + j) = v;
-            }
-          } else {
-            for (int j = 0; j < 32 && c0 + j < ncols; ++j) {
-              float v = __uint_as_float(r[j]);
-              crow[c0 + j] = p.relu ? fmaxf(v, 0.f) : v;
+        for (int pass = 0; pass < 8; ++pass) {
+          const int rr = pass * 4 + rsub;
+          const int grow = m0 + q * 32 + rr;
+          const uint32_t src = tile + uint32_t(rr * 33 + cq) * 4u;
+          const float4 v = make_float4(lds32(src), lds32(src + 4), lds32(src + 8), lds32(src + 12));
+          if (grow < p.M && !HS_DBG_NOEPI) {
+            float* dst = cbase + int64_t(grow) * ld + c0 + cq;
+            if (vec) {
+              *reinterpret_cast<float4*>(dst) = v;
+            } else {
+              const float e[4] = {v.x, v.y, v.z, v.w};
+              for (int i = 0; i < 4; ++i)
+                if (c0 + cq + i < ld) dst[i] = e[i];
             }
           }
         }
+        __syncwarp();  // the next chunk reuses the tile
       }
     }
   } else if (warp >= 8) {
@@ -423,7 +481,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t sa = staging + uint32_t(s) * L::kStaging, sb = sa + L::kStageA;
         const uint32_t ta = tmem_a + (uint32_t(q * 32) << 16) + uint32_t(o) * 64u;
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
+        for (int hh = 0; hh < (HS_DBG_NOCONV ? 0 : 2); ++hh) {
           uint32_t hi[16], lo[16];
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
@@ -621,7 +679,7 @@ cudaError_t gemm_tcgen05(const GemmArgs& a, int terms, cudaStream_t s) {
     // grouped launch: one tile covers every member (a.N = total columns)
     if (!a.Bplanes || a.N % a.n_out || (a.N / a.n_out) % 32 || a.n_out > 4) return cudaErrorInvalidValue;
     if (a.N == 128) return launch_bn<128>(a, terms, s);
-    if (a.N == 192) return launch_bn<192>(a, terms, s);
+    if (a.N == 192) return terms > 1 ? launch<192, 2, 3>(a, s) : launch<192, 2, 1>(a, s);
     return cudaErrorInvalidValue;
   }
   if (a.N <= 64) return launch_bn<64>(a, terms, s);

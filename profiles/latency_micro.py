@@ -1,6 +1,7 @@
-"""Per-launch fixed cost of node kernels: back-to-back stream launches vs the
-same launches captured in a CUDA graph (hs_capture_*), for a 1-K-block GEMM,
-a small elementwise add and a softmax."""
+"""Per-launch fixed cost of node kernels inside CUDA graphs (hs_capture_*):
+GEMMs of 1 and 16 K-blocks with 1 and 148 CTAs, and small HBM-bound nodes.
+Back-to-back stream launches from Python are host-bound for small kernels, so
+graph replay is the number that matters for the engine."""
 import ctypes
 import sys
 
@@ -17,31 +18,24 @@ _native.check(L.hs_event_create(ctx, 1, ctypes.byref(e0)))
 _native.check(L.hs_event_create(ctx, 1, ctypes.byref(e1)))
 
 
-def timed(fn, reps=50, graph=False):
-    for _ in range(3):
-        fn()
+def graph_us(fn, reps=50):
+    fn()
     _native.check(L.hs_stream_sync(st))
-    g = None
-    if graph:
-        g = ctypes.c_void_p()
-        _native.check(L.hs_capture_begin(st))
-        for _ in range(reps):
-            fn()
-        _native.check(L.hs_capture_end(st, ctypes.byref(g)))
+    g = ctypes.c_void_p()
+    _native.check(L.hs_capture_begin(st))
+    for _ in range(reps):
+        fn()
+    _native.check(L.hs_capture_end(st, ctypes.byref(g)))
+    for _ in range(2):
         _native.check(L.hs_graph_launch(g, st))
-        _native.check(L.hs_stream_sync(st))
+    _native.check(L.hs_stream_sync(st))
     _native.check(L.hs_event_record(e0, st))
-    if graph:
-        _native.check(L.hs_graph_launch(g, st))
-    else:
-        for _ in range(reps):
-            fn()
+    _native.check(L.hs_graph_launch(g, st))
     _native.check(L.hs_event_record(e1, st))
     _native.check(L.hs_event_sync(e1))
     ns = ctypes.c_int64()
     _native.check(L.hs_event_elapsed_ns(e0, e1, ctypes.byref(ns)))
-    if g is not None:
-        L.hs_graph_destroy(g)
+    L.hs_graph_destroy(g)
     return ns.value / 1e3 / reps
 
 
@@ -78,16 +72,19 @@ def op_fn(op, n, batch, dims, fparam=(1.0, 1e-5)):
     return lambda: (keep, _native.check(L.hs_launch(st, op, ctypes.byref(a), 0, batch)))
 
 
-cases = {
-    "gemm 128x64x32 batch=1 (1 CTA, 1 K-block)": gemm_fn(128, 64, 32, 1),
-    "gemm 128x64x32 batch=148": gemm_fn(128, 64, 32, 148),
-    "gemm 128x64x512 batch=1": gemm_fn(128, 64, 512, 1),
-    "gemm 128x64x512 batch=128": gemm_fn(128, 64, 512, 128),
-    "add n=256 batch=1": op_fn(6, 256, 1, [256]),
-    "add n=65536 batch=128": op_fn(6, 65536, 128, [65536]),
-    "softmax 128x128 batch=128": op_fn(5, 16384, 128, [128, 128], (0.125, 1e-5)),
+CASES = {
+    "gemm 128x64x32 batch=1": lambda: gemm_fn(128, 64, 32, 1),
+    "gemm 128x64x32 batch=148": lambda: gemm_fn(128, 64, 32, 148),
+    "gemm 128x64x512 batch=1": lambda: gemm_fn(128, 64, 512, 1),
+    "gemm 128x64x512 batch=148": lambda: gemm_fn(128, 64, 512, 148),
+    "gemm 128x128x512 batch=148": lambda: gemm_fn(128, 128, 512, 148),
+    "add n=256 batch=1": lambda: op_fn(6, 256, 1, [256]),
+    "softmax 128x128 batch=128": lambda: op_fn(5, 16384, 128, [128, 128], (0.125, 1e-5)),
 }
-for name, fn in cases.items():
-    s = timed(fn)
-    g = timed(fn, graph=True)
-    print(f"{name:45s} stream {s:7.2f} us/launch   graph {g:7.2f} us/node", flush=True)
+
+if __name__ == "__main__":
+    only = sys.argv[1] if len(sys.argv) > 1 else ""
+    for name, make in CASES.items():
+        if only and only not in name:
+            continue
+        print(f"{name:32s} graph {graph_us(make()):7.2f} us/node", flush=True)
