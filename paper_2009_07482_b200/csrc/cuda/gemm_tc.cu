@@ -53,6 +53,9 @@ constexpr int BK = 32;  // fp32 elements per K-block = one 128-byte swizzle row
 #ifndef HS_DBG_NOCONV
 #define HS_DBG_NOCONV 0
 #endif
+#ifndef HS_SMALL_GEMM
+#define HS_SMALL_GEMM 1
+#endif
 #ifndef HS_DBG_NOEPI
 #define HS_DBG_NOEPI 0
 #endif
@@ -174,9 +177,15 @@ __device__ __forceinline__ void split_store(uint32_t hi, uint32_t lo, uint32_t o
 }
 
 // B source: 0 = activation [N,K] (nt), 1 = activation [K,N] (nn), 2 = pre-split planes
-template <int BN, int kBSrc>
+// kSmall: configuration for short-K GEMMs (<= 4 K-blocks: attention QK^T,
+// P·V, C·W_h). Two CTAs share an SM (256 TMEM columns, ~100 KB smem each), so
+// the fixed prologue/epilogue latency of one tile overlaps another tile's work
+// and kernels of concurrently running components can co-reside.
+template <int BN, int kBSrc, bool kSmall = false>
 struct Cfg {
   static constexpr bool kBPre = kBSrc == 2;
+  static constexpr int kCtasPerSm = kSmall ? 2 : 1;
+  static constexpr int kTmemCols = kSmall ? 256 : 512;
   static constexpr int kStageA = BM * BK * 4;              // 16 KB fp32 A tile (SW128 via TMA)
   static constexpr int kStageB = kBPre ? 0 : BN * BK * 4;  // fp32 B staging (activations only)
   static constexpr int kStaging = kStageA + kStageB;
@@ -186,22 +195,23 @@ struct Cfg {
   // columns (32 hi + 32 lo tf32 columns, one row per lane).
   // Double-buffer the accumulator only when that still leaves room for 4 A
   // stages (BN <= 128); wider tiles trade epilogue overlap for pipeline depth.
-  static constexpr int kAccBufs = (2 * BN + 4 * 64 <= 512) ? 2 : 1;
+  static constexpr int kAccBufs = (2 * BN + (kSmall ? 2 : 4) * 64 <= kTmemCols) ? 2 : 1;
   static constexpr int kAccCols = kAccBufs * BN;
   static constexpr int kBudget = HS_SMEM_BUDGET_KB * 1024;  // + barriers/alignment stays under the 227 KB opt-in limit
-  static constexpr int kNOtm = (512 - kAccCols) / 64;
+  static constexpr int kNOtm = (kTmemCols - kAccCols) / 64;
   static constexpr int kNOsm = (kBudget - 2 * kStaging) / kOperand;
   static constexpr int kNOmin = kNOtm < kNOsm ? kNOtm : kNOsm;
-  static constexpr int kNOcap = kNOmin < HS_NO_CAP ? kNOmin : HS_NO_CAP;
+  static constexpr int kNOcap = kSmall ? 2 : (kNOmin < HS_NO_CAP ? kNOmin : HS_NO_CAP);
   static constexpr int kNO = kNOcap - kNOcap % kConvGroups;
   static constexpr int kNSraw = (kBudget - kNO * kOperand) / kStaging;
-  static constexpr int kNScap = kNSraw > 6 ? 6 : kNSraw;
+  static constexpr int kNScap = kSmall ? 2 : (kNSraw > 6 ? 6 : kNSraw);
   static constexpr int kNS = kNScap - kNScap % kConvGroups;
+  static_assert(kAccCols + kNO * 64 <= kTmemCols, "TMEM budget exceeded");
   static_assert(kNS % kConvGroups == 0 && kNO % kConvGroups == 0, "stage rings must divide among groups");
   static constexpr int kTotal =
       kNS * kStaging + kNO * kOperand + 1024 /*barriers*/ + kEpiWarps * kEpiTileBytes + 1024 /*align*/;
   static_assert(kNS >= 2 && kNO >= 2, "pipeline too shallow");
-  static_assert(kTotal <= 227 * 1024, "shared memory budget exceeded");
+  static_assert(kTotal * kCtasPerSm <= 227 * 1024, "shared memory budget exceeded");
 };
 
 struct TileParams {
@@ -240,10 +250,10 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16
       : "memory");
 }
 
-template <int BN, int kBSrc, int kTerms>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int BN, int kBSrc, int kTerms, bool kSmall>
+__global__ void __launch_bounds__(kThreads, kSmall ? 2 : 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TileParams p) {
-  using L = Cfg<BN, kBSrc>;
+  using L = Cfg<BN, kBSrc, kSmall>;
   constexpr int NS = L::kNS, NO = L::kNO;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
@@ -281,7 +291,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tmem_slot), "r"(512));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tmem_slot),
+                 "r"(L::kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
@@ -532,7 +543,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(L::kTmemCols));
   }
 }
 
@@ -604,10 +615,10 @@ int num_sms() {
   return n;
 }
 
-template <int BN, int kBSrc, int kTerms>
+template <int BN, int kBSrc, int kTerms, bool kSmall = false>
 cudaError_t launch(const GemmArgs& a, cudaStream_t s) {
-  using L = Cfg<BN, kBSrc>;
-  auto kernel = gemm_tc_kernel<BN, kBSrc, kTerms>;
+  using L = Cfg<BN, kBSrc, kSmall>;
+  auto kernel = gemm_tc_kernel<BN, kBSrc, kTerms, kSmall>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [&] {
@@ -649,16 +660,17 @@ cudaError_t launch(const GemmArgs& a, cudaStream_t s) {
     p.sCs[i] = a.sCs[i];
   }
   p.total_tiles = p.m_tiles * p.n_tiles * a.batch;
-  const int grid = p.total_tiles < num_sms() ? p.total_tiles : num_sms();
+  const int slots = num_sms() * L::kCtasPerSm;
+  const int grid = p.total_tiles < slots ? p.total_tiles : slots;
   kernel<<<grid, kThreads, L::kTotal, s>>>(mA, mB, p);
   return cudaGetLastError();
 }
 
-template <int BN>
+template <int BN, bool kSmall = false>
 cudaError_t launch_bn(const GemmArgs& a, int terms, cudaStream_t s) {
-  if (a.Bplanes) return terms > 1 ? launch<BN, 2, 3>(a, s) : launch<BN, 2, 1>(a, s);
-  if (a.layout == GemmLayout::nt) return terms > 1 ? launch<BN, 0, 3>(a, s) : launch<BN, 0, 1>(a, s);
-  return terms > 1 ? launch<BN, 1, 3>(a, s) : launch<BN, 1, 1>(a, s);
+  if (a.Bplanes) return terms > 1 ? launch<BN, 2, 3, kSmall>(a, s) : launch<BN, 2, 1, kSmall>(a, s);
+  if (a.layout == GemmLayout::nt) return terms > 1 ? launch<BN, 0, 3, kSmall>(a, s) : launch<BN, 0, 1, kSmall>(a, s);
+  return terms > 1 ? launch<BN, 1, 3, kSmall>(a, s) : launch<BN, 1, 1, kSmall>(a, s);
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
@@ -682,6 +694,8 @@ cudaError_t gemm_tcgen05(const GemmArgs& a, int terms, cudaStream_t s) {
     if (a.N == 192) return terms > 1 ? launch<192, 2, 3>(a, s) : launch<192, 2, 1>(a, s);
     return cudaErrorInvalidValue;
   }
+  // short K (attention-sized GEMMs): 64-wide tiles, two CTAs per SM
+  if (a.K <= 4 * BK && a.N <= 128 && HS_SMALL_GEMM) return launch_bn<64, true>(a, terms, s);
   if (a.N <= 64) return launch_bn<64>(a, terms, s);
   return launch_bn<128>(a, terms, s);
 }

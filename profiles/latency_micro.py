@@ -39,19 +39,21 @@ def graph_us(fn, reps=50):
     return ns.value / 1e3 / reps
 
 
-def gemm_fn(M, N, K, batch):
+def gemm_fn(M, N, K, batch, shared=True):
     A = torch.randn(batch, M * K, device="cuda")
-    B = torch.randn(N * K, device="cuda")
+    B = torch.randn(N * K if shared else batch * N * K, device="cuda")
     C = torch.empty(batch, M * N, device="cuda")
-    planes = torch.empty(2 * N * K, device="cuda")
-    _native.check(L.hs_gemm_split_weights(st, B.data_ptr(), 0, N, K, planes.data_ptr()))
+    planes = None
+    if shared:
+        planes = torch.empty(2 * N * K, device="cuda")
+        _native.check(L.hs_gemm_split_weights(st, B.data_ptr(), 0, N, K, planes.data_ptr()))
     a = _native.OpArgs()
     a.n_in = 2
     a.in_[0], a.in_[1] = A.data_ptr(), B.data_ptr()
-    a.in_stride[0], a.in_stride[1] = M * K, 0
+    a.in_stride[0], a.in_stride[1] = M * K, 0 if shared else N * K
     a.out, a.out_stride = C.data_ptr(), M * N
     a.dims[0], a.dims[1], a.dims[2] = M, N, K
-    a.aux = planes.data_ptr()
+    a.aux = planes.data_ptr() if planes is not None else None
     keep = (A, B, C, planes)
     return lambda: (keep, _native.check(L.hs_launch(st, 0, ctypes.byref(a), 0, batch)))
 
@@ -78,6 +80,10 @@ CASES = {
     "gemm 128x64x512 batch=1": lambda: gemm_fn(128, 64, 512, 1),
     "gemm 128x64x512 batch=148": lambda: gemm_fn(128, 64, 512, 148),
     "gemm 128x128x512 batch=148": lambda: gemm_fn(128, 128, 512, 148),
+    "dag QK^T 128x128x64 act-B batch=256": lambda: gemm_fn(128, 128, 64, 256, shared=False),
+    "dag PV 128x64x128 act-B batch=256": lambda: gemm_fn(128, 64, 128, 256, shared=False),
+    "dag CW 128x64x64 weight batch=256": lambda: gemm_fn(128, 64, 64, 256),
+    "dag FFN2 128x512x2048 batch=256": lambda: gemm_fn(128, 512, 2048, 256),
     "add n=256 batch=1": lambda: op_fn(6, 256, 1, [256]),
     "softmax 128x128 batch=128": lambda: op_fn(5, 16384, 128, [128, 128], (0.125, 1e-5)),
 }
