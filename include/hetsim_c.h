@@ -108,7 +108,10 @@ typedef enum {
 typedef enum {
   HS_MATH_TF32X3 = 0,   /* tcgen05 kind::tf32, 3-term split: fp32-accurate (default) */
   HS_MATH_TF32 = 1,     /* tcgen05 kind::tf32, single term (fast, ~1e-3)            */
-  HS_MATH_FP32_SIMT = 2 /* CUDA-core fp32 FMA (diagnostic)                          */
+  HS_MATH_FP32_SIMT = 2, /* CUDA-core fp32 FMA (diagnostic)                         */
+  HS_MATH_BF16X3 = 3     /* GEMMs with resident (pre-split) B: kind::f16 with bf16 hi/lo
+                            3-term split (~1e-5, 2x the tf32 MMA rate); other GEMMs
+                            run TF32X3. B planes must be prepared with format 1. */
 } hs_math;
 
 #define HS_MAX_INPUTS 16
@@ -139,6 +142,9 @@ int hs_gemm_split_weights(hs_stream_t s, const void* B, int transposed, int64_t 
  * used to lay several weights side by side for a grouped launch. */
 int hs_gemm_split_weights_strided(hs_stream_t s, const void* B, int transposed, int64_t N, int64_t K, void* planes,
                                   int64_t plane_stride);
+/* format 0 = tf32 hi/lo in fp32 containers (TF32X3/TF32), 1 = bf16 hi/lo (BF16X3). */
+int hs_gemm_split_weights_ex(hs_stream_t s, const void* B, int transposed, int64_t N, int64_t K, void* planes,
+                             int64_t plane_stride, int format);
 
 int hs_host_callback(hs_stream_t s, void (*fn)(void*), void* user);
 int hs_capture_begin(hs_stream_t s);

@@ -90,6 +90,7 @@ _PROTOS = {
     "hs_launch_count": (c_int64, []),
     "hs_gemm_split_weights": (c_int, [c_void_p, c_void_p, c_int, c_int64, c_int64, c_void_p]),
     "hs_gemm_split_weights_strided": (c_int, [c_void_p, c_void_p, c_int, c_int64, c_int64, c_void_p, c_int64]),
+    "hs_gemm_split_weights_ex": (c_int, [c_void_p, c_void_p, c_int, c_int64, c_int64, c_void_p, c_int64, c_int]),
     "hs_engine_create": (c_int, [c_char_p, ctypes.POINTER(c_void_p)]),
     "hs_engine_destroy": (c_int, [c_void_p]),
     "hs_engine_bind": (c_int, [c_void_p, c_int, c_int, c_void_p, c_int64, c_int]),

@@ -127,9 +127,24 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
   return uint64_t((addr >> 4) & 0x3FFFu) | (uint64_t(1) << 16) | (uint64_t(1024 >> 4) << 32) | (uint64_t(1) << 46) |
          (uint64_t(2) << 61);
 }
+// Same for SWIZZLE_64B (bf16 B planes: 32 bf16 = 64-byte rows, 8-row groups 512 B apart).
+__device__ __forceinline__ uint64_t smem_desc_sw64(uint32_t addr) {
+  return uint64_t((addr >> 4) & 0x3FFFu) | (uint64_t(1) << 16) | (uint64_t(512 >> 4) << 32) | (uint64_t(1) << 46) |
+         (uint64_t(4) << 61);
+}
 // Instruction descriptor: D=f32, A=B=tf32, both K-major, M=128, N=n.
 __host__ __device__ constexpr uint32_t instr_desc_tf32(int n) {
   return (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(n >> 3) << 17) | (uint32_t(BM >> 4) << 24);
+}
+// Instruction descriptor: D=f32, A=B=bf16 (kind::f16), both K-major, M=128, N=n.
+__host__ __device__ constexpr uint32_t instr_desc_bf16(int n) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(n >> 3) << 17) | (uint32_t(BM >> 4) << 24);
+}
+// {bf16(hi_elem) : bf16(lo_elem)} with lo_elem in the low half (the lower k index).
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo_elem, float hi_elem) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi_elem), "f"(lo_elem));
+  return r;
 }
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
   asm volatile(
@@ -181,24 +196,29 @@ __device__ __forceinline__ void split_store(uint32_t hi, uint32_t lo, uint32_t o
 // P·V, C·W_h). Two CTAs share an SM (256 TMEM columns, ~100 KB smem each), so
 // the fixed prologue/epilogue latency of one tile overlaps another tile's work
 // and kernels of concurrently running components can co-reside.
-template <int BN, int kBSrc, bool kSmall = false>
+// kBf16: BF16x3 math (pre-split weights only): A and B split into bf16 hi/lo,
+// D += Alo·Bhi + Ahi·Blo + Ahi·Bhi with kind::f16 MMAs (K=16 per instruction,
+// twice the tf32 rate); B planes are 32 bf16 = 64-byte SW64 rows per K-block,
+// A stages are 16 + 16 TMEM columns (bf16 pairs packed per 32-bit column).
+template <int BN, int kBSrc, bool kSmall = false, bool kBf16 = false>
 struct Cfg {
+  static_assert(!kBf16 || kBSrc == 2, "bf16x3 is implemented for pre-split (resident) B only");
   static constexpr bool kBPre = kBSrc == 2;
   static constexpr int kCtasPerSm = kSmall ? 2 : 1;
   static constexpr int kTmemCols = kSmall ? 256 : 512;
   static constexpr int kStageA = BM * BK * 4;              // 16 KB fp32 A tile (SW128 via TMA)
   static constexpr int kStageB = kBPre ? 0 : BN * BK * 4;  // fp32 B staging (activations only)
   static constexpr int kStaging = kStageA + kStageB;
-  static constexpr int kPlaneB = BN * 128;                 // one SW128 tf32 plane of B
+  static constexpr int kPlaneB = BN * (kBf16 ? 64 : 128);  // one SW128 tf32 / SW64 bf16 plane of B
   static constexpr int kOperand = 2 * kPlaneB;             // B hi + lo (A lives in TMEM)
-  // TMEM (512 columns): two BN-wide fp32 accumulators + kNO A stages of 64
-  // columns (32 hi + 32 lo tf32 columns, one row per lane).
-  // Double-buffer the accumulator only when that still leaves room for 4 A
-  // stages (BN <= 128); wider tiles trade epilogue overlap for pipeline depth.
-  static constexpr int kAccBufs = (2 * BN + (kSmall ? 2 : 4) * 64 <= kTmemCols) ? 2 : 1;
+  static constexpr int kAStage = kBf16 ? 32 : 64;          // TMEM columns per A stage (hi + lo)
+  // TMEM: BN-wide fp32 accumulator(s) + kNO A stages of kAStage columns (one
+  // row per lane). Double-buffer the accumulator only when that still leaves
+  // room for 4 A stages; wider tiles trade epilogue overlap for pipeline depth.
+  static constexpr int kAccBufs = (2 * BN + (kSmall ? 2 : 4) * kAStage <= kTmemCols) ? 2 : 1;
   static constexpr int kAccCols = kAccBufs * BN;
   static constexpr int kBudget = HS_SMEM_BUDGET_KB * 1024;  // + barriers/alignment stays under the 227 KB opt-in limit
-  static constexpr int kNOtm = (kTmemCols - kAccCols) / 64;
+  static constexpr int kNOtm = (kTmemCols - kAccCols) / kAStage;
   static constexpr int kNOsm = (kBudget - 2 * kStaging) / kOperand;
   static constexpr int kNOmin = kNOtm < kNOsm ? kNOtm : kNOsm;
   static constexpr int kNOcap = kSmall ? 2 : (kNOmin < HS_NO_CAP ? kNOmin : HS_NO_CAP);
@@ -206,7 +226,7 @@ struct Cfg {
   static constexpr int kNSraw = (kBudget - kNO * kOperand) / kStaging;
   static constexpr int kNScap = kSmall ? 2 : (kNSraw > 6 ? 6 : kNSraw);
   static constexpr int kNS = kNScap - kNScap % kConvGroups;
-  static_assert(kAccCols + kNO * 64 <= kTmemCols, "TMEM budget exceeded");
+  static_assert(kAccCols + kNO * kAStage <= kTmemCols, "TMEM budget exceeded");
   static_assert(kNS % kConvGroups == 0 && kNO % kConvGroups == 0, "stage rings must divide among groups");
   static constexpr int kTotal =
       kNS * kStaging + kNO * kOperand + 1024 /*barriers*/ + kEpiWarps * kEpiTileBytes + 1024 /*align*/;
@@ -241,6 +261,17 @@ __device__ __forceinline__ void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, ui
       : "memory");
 }
 
+// D[tmem] (+)= A[tmem] · B[smem] with bf16 operands (kind::f16), fp32 accumulate.
+__device__ __forceinline__ void mma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc,
+                                           uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, {%5, %6, %7, %8}, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(b), "r"(idesc), "r"(acc), "r"(0u), "r"(0u), "r"(0u), "r"(0u)
+      : "memory");
+}
+
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
@@ -250,10 +281,10 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16
       : "memory");
 }
 
-template <int BN, int kBSrc, int kTerms, bool kSmall>
+template <int BN, int kBSrc, int kTerms, bool kSmall, bool kBf16>
 __global__ void __launch_bounds__(kThreads, kSmall ? 2 : 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TileParams p) {
-  using L = Cfg<BN, kBSrc, kSmall>;
+  using L = Cfg<BN, kBSrc, kSmall, kBf16>;
   constexpr int NS = L::kNS, NO = L::kNO;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
@@ -364,7 +395,7 @@ __global__ void __launch_bounds__(kThreads, kSmall ? 2 : 1)
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
-      constexpr uint32_t idesc = instr_desc_tf32(BN);
+      constexpr uint32_t idesc = kBf16 ? instr_desc_bf16(BN) : instr_desc_tf32(BN);
       uint32_t it = 0, lt = 0;
       for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x, ++lt) {
         const uint32_t acc = lt % uint32_t(L::kAccBufs);
@@ -375,10 +406,21 @@ __global__ void __launch_bounds__(kThreads, kSmall ? 2 : 1)
           const int o = int(it % NO);
           mbar_wait(op_full(o), (it / NO) & 1u);
           tc_fence_after();
-          const uint32_t a_hi = tmem_a + uint32_t(o) * 64u;
-          const uint32_t a_lo = a_hi + 32u;
+          const uint32_t a_hi = tmem_a + uint32_t(o) * uint32_t(L::kAStage);
+          const uint32_t a_lo = a_hi + uint32_t(L::kAStage / 2);
           const uint32_t b_hi = operand + uint32_t(o) * L::kOperand;
           const uint32_t b_lo = b_hi + L::kPlaneB;
+          if constexpr (kBf16) {
+            // K = 16 bf16 per instruction: 8 TMEM columns of packed pairs, 32 bytes of a SW64 row
+#pragma unroll
+            for (int kk = 0; kk < BK / 16; ++kk) {
+              const uint32_t kcol = uint32_t(kk) * 8u, koff = uint32_t(kk) * 32u;
+              const uint32_t first = (kb | kk) ? 1u : 0u;
+              mma_f16_ts(d, a_lo + kcol, smem_desc_sw64(b_hi + koff), idesc, first);
+              mma_f16_ts(d, a_hi + kcol, smem_desc_sw64(b_lo + koff), idesc, 1u);
+              mma_f16_ts(d, a_hi + kcol, smem_desc_sw64(b_hi + koff), idesc, 1u);
+            }
+          } else
 #pragma unroll
           for (int kk = 0; kk < BK / 8; ++kk) {  // K = 8 tf32 per instruction
             const uint32_t kcol = uint32_t(kk) * 8u, koff = uint32_t(kk) * 32u;
@@ -490,7 +532,25 @@ __global__ void __launch_bounds__(kThreads, kSmall ? 2 : 1)
         mbar_wait(op_empty(o), ((it / NO) & 1u) ^ 1u);
         tc_fence_after();
         const uint32_t sa = staging + uint32_t(s) * L::kStaging, sb = sa + L::kStageA;
-        const uint32_t ta = tmem_a + (uint32_t(q * 32) << 16) + uint32_t(o) * 64u;
+        const uint32_t ta = tmem_a + (uint32_t(q * 32) << 16) + uint32_t(o) * uint32_t(L::kAStage);
+        if constexpr (kBf16) {
+          // 32 fp32 of this row -> bf16 hi/lo, packed in pairs (lower k in the low half):
+          // hi -> columns [0,16), lo -> [16,32) of the stage.
+          uint32_t hi[16], lo[16];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            float4 x = lds128(sa + sw128(row, c));
+            const uint32_t h01 = pack_bf16x2(x.x, x.y), h23 = pack_bf16x2(x.z, x.w);
+            hi[2 * c] = h01;
+            hi[2 * c + 1] = h23;
+            lo[2 * c] = pack_bf16x2(x.x - __uint_as_float(h01 << 16), x.y - __uint_as_float(h01 & 0xFFFF0000u));
+            lo[2 * c + 1] = pack_bf16x2(x.z - __uint_as_float(h23 << 16), x.w - __uint_as_float(h23 & 0xFFFF0000u));
+          }
+          if (!HS_DBG_NOCONV) {
+            tmem_st16(ta, hi);
+            tmem_st16(ta + 16u, lo);
+          }
+        } else
 #pragma unroll
         for (int hh = 0; hh < (HS_DBG_NOCONV ? 0 : 2); ++hh) {
           uint32_t hi[16], lo[16];
@@ -547,7 +607,33 @@ __global__ void __launch_bounds__(kThreads, kSmall ? 2 : 1)
   }
 }
 
-// Weight preparation: B (resident) -> K-major tf32 hi/lo planes [2][N][K].
+// Weight preparation: B (resident) -> K-major hi/lo planes [2][N][K], tf32
+// (fp32 containers) or bf16 (hi = bf16_rn(x), lo = bf16_rn(x - hi)).
+template <bool kNT>
+__global__ void split_weights_bf16_kernel(const float* __restrict__ B, uint16_t* __restrict__ planes, int N, int K,
+                                          int64_t plane) {
+  __shared__ float tile[32][33];
+  const int n0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    int n = n0 + (kNT ? i : threadIdx.x), k = k0 + (kNT ? threadIdx.x : i);
+    float v = 0.f;
+    if (n < N && k < K) v = kNT ? B[int64_t(n) * K + k] : B[int64_t(k) * N + n];
+    if (kNT) tile[i][threadIdx.x] = v;
+    else tile[threadIdx.x][i] = v;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    int n = n0 + i, k = k0 + threadIdx.x;
+    if (n < N && k < K) {
+      const float x = tile[i][threadIdx.x];
+      const uint32_t h = pack_bf16x2(x, 0.f) & 0xFFFFu;
+      const uint32_t l = pack_bf16x2(x - __uint_as_float(h << 16), 0.f) & 0xFFFFu;
+      planes[int64_t(n) * K + k] = uint16_t(h);
+      planes[plane + int64_t(n) * K + k] = uint16_t(l);
+    }
+  }
+}
+
 template <bool kNT>
 __global__ void split_weights_kernel(const float* __restrict__ B, float* __restrict__ planes, int N, int K,
                                      int64_t plane) {
@@ -590,17 +676,20 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-// 3-D fp32 tensor map: dims {d0 (contiguous), d1, d2}, byte strides {s1, s2}.
-bool make_map(CUtensorMap* m, const float* ptr, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1, uint64_t s2,
-              uint32_t b0, uint32_t b1, bool swizzle128) {
+// 3-D tensor map (fp32, or bf16 with 64-byte swizzle): dims {d0 (contiguous), d1, d2},
+// byte strides {s1, s2}.
+bool make_map(CUtensorMap* m, const void* ptr, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1, uint64_t s2,
+              uint32_t b0, uint32_t b1, bool swizzle, bool bf16 = false) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[3] = {d0, d1, d2};
   cuuint64_t strides[2] = {s1, s2};
   cuuint32_t box[3] = {b0, b1, 1};
   cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(ptr), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+  const CUtensorMapSwizzle sw = !swizzle ? CU_TENSOR_MAP_SWIZZLE_NONE
+                                : (bf16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B);
+  CUresult r = fn(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+                  const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -615,10 +704,10 @@ int num_sms() {
   return n;
 }
 
-template <int BN, int kBSrc, int kTerms, bool kSmall = false>
+template <int BN, int kBSrc, int kTerms, bool kSmall = false, bool kBf16 = false>
 cudaError_t launch(const GemmArgs& a, cudaStream_t s) {
-  using L = Cfg<BN, kBSrc, kSmall>;
-  auto kernel = gemm_tc_kernel<BN, kBSrc, kTerms, kSmall>;
+  using L = Cfg<BN, kBSrc, kSmall, kBf16>;
+  auto kernel = gemm_tc_kernel<BN, kBSrc, kTerms, kSmall, kBf16>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [&] {
@@ -631,7 +720,9 @@ cudaError_t launch(const GemmArgs& a, cudaStream_t s) {
   CUtensorMap mA, mB;
   if (!make_map(&mA, a.A, K, M, nA, K * 4, sA, BK, BM, true)) return cudaErrorInvalidValue;
   bool ok = false;
-  if constexpr (kBSrc == 2) {
+  if constexpr (kBSrc == 2 && kBf16) {
+    ok = make_map(&mB, a.Bplanes, K, N, 2, K * 2, N * K * 2, BK, BN, true, true);
+  } else if constexpr (kBSrc == 2) {
     ok = make_map(&mB, a.Bplanes, K, N, 2, K * 4, N * K * 4, BK, BN, true);
   } else if constexpr (kBSrc == 0) {
     const uint64_t sB = (a.sB ? uint64_t(a.sB) : N * K) * 4;
@@ -668,6 +759,7 @@ cudaError_t launch(const GemmArgs& a, cudaStream_t s) {
 
 template <int BN, bool kSmall = false>
 cudaError_t launch_bn(const GemmArgs& a, int terms, cudaStream_t s) {
+  if (a.Bplanes && a.bf16) return launch<BN, 2, 3, kSmall, true>(a, s);
   if (a.Bplanes) return terms > 1 ? launch<BN, 2, 3, kSmall>(a, s) : launch<BN, 2, 1, kSmall>(a, s);
   if (a.layout == GemmLayout::nt) return terms > 1 ? launch<BN, 0, 3, kSmall>(a, s) : launch<BN, 0, 1, kSmall>(a, s);
   return terms > 1 ? launch<BN, 1, 3, kSmall>(a, s) : launch<BN, 1, 1, kSmall>(a, s);
@@ -691,7 +783,10 @@ cudaError_t gemm_tcgen05(const GemmArgs& a, int terms, cudaStream_t s) {
     // grouped launch: one tile covers every member (a.N = total columns)
     if (!a.Bplanes || a.N % a.n_out || (a.N / a.n_out) % 32 || a.n_out > 4) return cudaErrorInvalidValue;
     if (a.N == 128) return launch_bn<128>(a, terms, s);
-    if (a.N == 192) return terms > 1 ? launch<192, 2, 3>(a, s) : launch<192, 2, 1>(a, s);
+    if (a.N == 192) {
+      if (a.bf16) return launch<192, 2, 3, false, true>(a, s);
+      return terms > 1 ? launch<192, 2, 3>(a, s) : launch<192, 2, 1>(a, s);
+    }
     return cudaErrorInvalidValue;
   }
   // short K (attention-sized GEMMs): 64-wide tiles, two CTAs per SM
@@ -700,9 +795,17 @@ cudaError_t gemm_tcgen05(const GemmArgs& a, int terms, cudaStream_t s) {
   return launch_bn<128>(a, terms, s);
 }
 
-cudaError_t gemm_split_weights(const float* B, GemmLayout layout, int N, int K, float* planes, int64_t plane_stride,
-                               cudaStream_t s) {
+cudaError_t gemm_split_weights(const float* B, GemmLayout layout, int N, int K, void* planes_v, int64_t plane_stride,
+                               cudaStream_t s, bool bf16) {
   const int64_t plane = plane_stride > 0 ? plane_stride : int64_t(N) * K;
+  if (bf16) {
+    dim3 grid((N + 31) / 32, (K + 31) / 32), block(32, 8);
+    auto* planes = static_cast<uint16_t*>(planes_v);
+    if (layout == GemmLayout::nt) split_weights_bf16_kernel<true><<<grid, block, 0, s>>>(B, planes, N, K, plane);
+    else split_weights_bf16_kernel<false><<<grid, block, 0, s>>>(B, planes, N, K, plane);
+    return cudaGetLastError();
+  }
+  float* planes = static_cast<float*>(planes_v);
   dim3 grid((N + 31) / 32, (K + 31) / 32), block(32, 8);
   if (layout == GemmLayout::nt) split_weights_kernel<true><<<grid, block, 0, s>>>(B, planes, N, K, plane);
   else split_weights_kernel<false><<<grid, block, 0, s>>>(B, planes, N, K, plane);

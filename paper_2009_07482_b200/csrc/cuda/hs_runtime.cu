@@ -250,6 +250,13 @@ int hs_launch(hs_stream_t st, int op, const hs_op_args* a, int math, int batch) 
                      int(a->dims[0]), int(a->dims[1]), int(a->dims[2]), batch,
                      op == HS_OP_GEMM_NT ? hs::GemmLayout::nt : hs::GemmLayout::nn, op == HS_OP_GEMM_RELU,
                      math == HS_MATH_FP32_SIMT ? nullptr : static_cast<const float*>(a->aux)};
+      // BF16X3 applies to GEMMs whose B arrives pre-split (bf16 planes); the rest run TF32X3.
+      g.bf16 = (math == HS_MATH_BF16X3 && a->aux) ? 1 : 0;
+      if (g.bf16 && (g.K % 8) && a->n_out <= 1) {
+        // bf16 planes need 16-byte rows (K % 8 == 0) for TMA: split B in-kernel instead (TF32X3)
+        g.bf16 = 0;
+        g.Bplanes = nullptr;
+      }
       if (a->n_out > 1) {
         // grouped launch of sibling GEMMs (tcgen05 only; the caller checked eligibility)
         if (a->n_out > 4 || !a->aux || math == HS_MATH_FP32_SIMT) return invalid("bad grouped GEMM launch");
@@ -309,12 +316,18 @@ int hs_gemm_split_weights(hs_stream_t st, const void* B, int transposed, int64_t
 
 int hs_gemm_split_weights_strided(hs_stream_t st, const void* B, int transposed, int64_t N, int64_t K, void* planes,
                                   int64_t plane_stride) {
+  return hs_gemm_split_weights_ex(st, B, transposed, N, K, planes, plane_stride, 0);
+}
+
+int hs_gemm_split_weights_ex(hs_stream_t st, const void* B, int transposed, int64_t N, int64_t K, void* planes,
+                             int64_t plane_stride, int format) {
   if (!st || !B || !planes) return invalid("null argument");
+  if (format != 0 && format != 1) return invalid("format must be 0 (tf32) or 1 (bf16)");
   if (N < 1 || K < 1 || N > (1 << 30) || K > (1 << 30)) return invalid("bad weight shape");
   if (plane_stride < N * K) return invalid("plane stride smaller than one plane");
   if (int r = use_device(st->gpu)) return r;
   cudaError_t e = hs::gemm_split_weights(static_cast<const float*>(B), transposed ? hs::GemmLayout::nt : hs::GemmLayout::nn,
-                                         int(N), int(K), static_cast<float*>(planes), plane_stride, st->s);
+                                         int(N), int(K), planes, plane_stride, st->s, format == 1);
   if (e != cudaSuccess) return check(e, "split weights");
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return HS_OK;

@@ -29,11 +29,13 @@ struct GemmArgs {
   int n_out = 0;
   float* Cs[4] = {nullptr, nullptr, nullptr, nullptr};
   int64_t sCs[4] = {0, 0, 0, 0};
+  // Bplanes hold bf16 hi/lo (math BF16x3) instead of tf32 hi/lo.
+  int bf16 = 0;
 };
 
 // planes: hi at planes[n*K + k], lo at planes[plane_stride + n*K + k]
-cudaError_t gemm_split_weights(const float* B, GemmLayout layout, int N, int K, float* planes, int64_t plane_stride,
-                               cudaStream_t s);
+cudaError_t gemm_split_weights(const float* B, GemmLayout layout, int N, int K, void* planes, int64_t plane_stride,
+                               cudaStream_t s, bool bf16 = false);
 
 // math: 0 = TF32x3 (tcgen05), 1 = TF32 (tcgen05), 2 = fp32 SIMT
 cudaError_t gemm_tcgen05(const GemmArgs& a, int terms, cudaStream_t s);

@@ -255,9 +255,9 @@ void Engine::plan_buffers() {
         pl.nt = nt;
         pl.n = nd.dims[1];
         pl.k = nd.dims[2];
-        hs_ok(hs_malloc(ctx_, size_t(2 * pl.n * pl.k * 4), &pl.ptr), "hs_malloc");
+        hs_ok(hs_malloc(ctx_, size_t(2 * pl.n * pl.k * plane_elem_bytes()), &pl.ptr), "hs_malloc");
         allocations_.push_back(pl.ptr);
-        device_bytes_ += 2 * pl.n * pl.k * 4;
+        device_bytes_ += 2 * pl.n * pl.k * plane_elem_bytes();
         it = planes_.emplace(key, pl).first;
       }
       node_planes_[kid] = it->second.ptr;
@@ -301,13 +301,16 @@ void Engine::upload_resident() {
           "resident upload");
   }
   for (const auto& [key, pl] : planes_)
-    hs_ok(hs_gemm_split_weights(s, resident_buf_.at(pl.gi), pl.nt ? 1 : 0, pl.n, pl.k, pl.ptr), "split weights");
+    hs_ok(hs_gemm_split_weights_ex(s, resident_buf_.at(pl.gi), pl.nt ? 1 : 0, pl.n, pl.k, pl.ptr, pl.n * pl.k,
+                                   plane_format()),
+          "split weights");
   for (const auto& fg : fuse_groups_) {
     const int64_t members = int64_t(fg.kernels.size());
     for (int64_t m = 0; m < members; ++m) {
       const int gi = group_of_.at(nodes_.at(fg.kernels[size_t(m)]).inputs[1]);
-      hs_ok(hs_gemm_split_weights_strided(s, resident_buf_.at(gi), 0, fg.n, fg.k,
-                                          static_cast<float*>(fg.planes) + m * fg.n * fg.k, members * fg.n * fg.k),
+      hs_ok(hs_gemm_split_weights_ex(s, resident_buf_.at(gi), 0, fg.n, fg.k,
+                                     static_cast<char*>(fg.planes) + m * fg.n * fg.k * plane_elem_bytes(),
+                                     members * fg.n * fg.k, plane_format()),
             "split grouped weights");
     }
   }
@@ -550,7 +553,7 @@ void Engine::plan_fusion() {
           fg.events.push_back(list[i + j].first);
           fg.kernels.push_back(list[i + j].second);
         }
-        const size_t bytes = size_t(2 * int64_t(take) * fg.n * fg.k * 4);
+        const size_t bytes = size_t(2 * int64_t(take) * fg.n * fg.k * plane_elem_bytes());
         hs_ok(hs_malloc(ctx_, bytes, &fg.planes), "hs_malloc");
         allocations_.push_back(fg.planes);
         device_bytes_ += int64_t(bytes);
@@ -774,7 +777,8 @@ int hs_engine_create(const char* config_json, hs_engine_t* out) {
       if (m == "tf32x3") cfg.math = HS_MATH_TF32X3;
       else if (m == "tf32") cfg.math = HS_MATH_TF32;
       else if (m == "simt") cfg.math = HS_MATH_FP32_SIMT;
-      else fail(Errc::invalid_param, "math must be tf32x3|tf32|simt");
+      else if (m == "bf16x3") cfg.math = HS_MATH_BF16X3;
+      else fail(Errc::invalid_param, "math must be tf32x3|tf32|bf16x3|simt");
     }
     if (const json::Value* v = c.find("cpu_devices"))
       for (const json::Value* x : v->items()) cfg.cpu_devices.insert(x->as_int());

@@ -141,6 +141,9 @@ class Engine {
     int64_t n = 0, k = 0;  // per member
   };
   void plan_fusion();
+  // weight planes: bf16 hi/lo for BF16X3, tf32 hi/lo (fp32 containers) otherwise
+  int plane_format() const { return cfg_.math == HS_MATH_BF16X3 ? 1 : 0; }
+  int64_t plane_elem_bytes() const { return cfg_.math == HS_MATH_BF16X3 ? 2 : 4; }
   std::vector<FuseGroup> fuse_groups_;
   std::map<std::pair<int, int>, int> fuse_leader_;  // (component, ndrange event) -> group
   std::map<std::pair<int, int>, int> fuse_member_;  // (component, ndrange event) -> group (non-leaders)

@@ -10,7 +10,7 @@ from paper_2009_07482_b200 import _native
 
 OPS = {"gemm": 0, "gemm_nt": 1, "gemm_relu": 2, "transpose": 3, "scale": 4, "softmax": 5, "add": 6,
        "add_layernorm": 7, "concat": 8}
-MATH = {"tf32x3": 0, "tf32": 1, "simt": 2}
+MATH = {"tf32x3": 0, "tf32": 1, "simt": 2, "bf16x3": 3}
 
 _ctx = None
 _stream = None
@@ -28,12 +28,13 @@ def stream():
     return _stream
 
 
-def split_weights(B, transposed, N, K):
-    """Pre-split a shared GEMM B into tf32 hi/lo K-major planes (hs_gemm_split_weights)."""
+def split_weights(B, transposed, N, K, bf16=False):
+    """Pre-split a shared GEMM B into K-major hi/lo planes (tf32, or bf16 for math bf16x3)."""
     import torch
-    planes = torch.empty(2 * N * K, device="cuda")
+    planes = torch.empty(2 * N * K, device="cuda")  # fp32-sized: bf16 planes use half of it
     L = _native.lib()
-    _native.check(L.hs_gemm_split_weights(stream(), B.data_ptr(), int(transposed), N, K, planes.data_ptr()))
+    _native.check(L.hs_gemm_split_weights_ex(stream(), B.data_ptr(), int(transposed), N, K, planes.data_ptr(), N * K,
+                                             int(bf16)))
     _native.check(L.hs_stream_sync(stream()))
     return planes
 

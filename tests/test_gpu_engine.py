@@ -106,6 +106,21 @@ def test_grouped_sibling_gemms_match_unfused(oracle_mod):
         assert _normwise(fused[key][i], plain[key][i]) <= 1e-6
 
 
+@pytest.mark.parametrize("mode", ["graph", "dynamic"])
+def test_encoder_bf16x3_within_tolerance(mode, oracle_mod):
+    """BF16X3 math (resident-weight GEMMs as 3-term bf16 splits on kind::f16) stays
+    within the 1e-4 fp32 tolerance on a 2-layer encoder (profiles/split_precision.py
+    predicts ~5e-6 for 12 layers)."""
+    text, params, meta = workloads.encoder(layers=2)
+    n = 2
+    arrays = _encoder_arrays(meta, params, n)
+    ref = oracle_mod.run_dag(text, params, arrays, n)
+    key = (meta["output"]["kernel"], meta["output"]["pos"])
+    outs, _, _ = _run_gpu(text, params, arrays, n, mode=mode, batch=2, math="bf16x3")
+    for i in range(n):
+        assert _normwise(outs[key][i], ref[key][i]) <= TOL
+
+
 def test_dynamic_completion_log_replays_identically(oracle_mod):
     """Bit-exact scheduling parity: the completion order observed on the GPU,
     fed back through the CPU scheduler (product and oracle restatement),

@@ -63,9 +63,9 @@ def test_gemm_parity(M, N, K, op, batch, shared, math, oracle_mod):
 
 @pytest.mark.parametrize("M,N,K,op,batch,shared", [c for c in GEMM_CASES if c[5]] + [(128, 128, 64, "gemm_nt", 3, True),
                                                                               (72, 100, 36, "gemm", 2, True)])
-@pytest.mark.parametrize("math", ["tf32x3", "tf32"])
+@pytest.mark.parametrize("math", ["tf32x3", "tf32", "bf16x3"])
 def test_gemm_presplit_weights(M, N, K, op, batch, shared, math, oracle_mod):
-    """Resident-weight path: B pre-split once into K-major tf32 planes, fed by TMA."""
+    """Resident-weight path: B pre-split once into K-major tf32 (or bf16) planes, fed by TMA."""
     from tests.gpu_util import launch, normwise, split_weights
     import torch
     A = _rand(31, (batch, M * K))
@@ -73,11 +73,11 @@ def test_gemm_presplit_weights(M, N, K, op, batch, shared, math, oracle_mod):
     ref = np.empty((batch, M * N), np.float32)
     oracle_mod.run_node(op, [A, B], [M * K, 0], ref, M * N, [M, N, K], batch)
     Bt = _t(B)
-    planes = split_weights(Bt, op == "gemm_nt", N, K)
+    planes = split_weights(Bt, op == "gemm_nt", N, K, bf16=math == "bf16x3")
     out = torch.full((batch, M * N), float("nan"), device="cuda")
     launch(op, [_t(A), Bt], out, [M, N, K], math=math, batch=batch, aux=planes)
     y = out.cpu().numpy()
-    tol = TOL_TF32X3 if math == "tf32x3" else 5e-3
+    tol = {"tf32x3": TOL_TF32X3, "bf16x3": 5e-5, "tf32": 5e-3}[math]
     for b in range(batch):
         assert normwise(y[b], ref[b]) <= tol, b
 
