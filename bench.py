@@ -55,6 +55,7 @@ def parse_args():
     ap.add_argument("--math", default="tf32x3")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-alt", action="store_true", help="skip the alternate-math measurement")
     return ap.parse_args()
 
 
@@ -182,11 +183,11 @@ def run_reference(args, world, rank):
     layers = args.layers
     vals = []
     for i in range(args.warmup + args.steps):
-        v, threads, t = cpu_sample(layers, n_inst=1)
+        v, threads, t = cpu_sample(layers, n_inst=2)
         if i >= args.warmup:
             vals.append(v)
     v = statistics.mean(vals)
-    sample = f"1 instance of the {layers}-layer encoder DAG per step (CPU oracle port: clustering + fp32 kernels)"
+    sample = f"2 instances of the {layers}-layer encoder DAG per step (CPU oracle port: clustering + fp32 kernels)"
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1000.0 / v, "higher_is_better": True, "scaling": "strong",
@@ -201,36 +202,43 @@ def run_reference(args, world, rank):
 
 # --------------------------------------------------------------------------- GPU arm
 
-def gemm_roofline(batch, tflops_peak, reps=20):
-    """Time the dominant kernel (FFN1: gemm_relu 128x2048x512 per instance, batched like
-    the graph launches it) live on its own stream with CUDA events; returns achieved TFLOP/s."""
+def gemm_roofline(batch, math_mode, reps=20):
+    """Time the dominant kernel exactly as the DAG launches it — FFN1, gemm_relu
+    128x2048x512 per instance, batched, resident weight pre-split into planes —
+    on its own stream with CUDA events around `reps` launches (after warm-up).
+    Returns (achieved TFLOP/s, ms per launch, algorithmic FLOP per launch)."""
     import ctypes
 
     import torch
 
     from paper_2009_07482_b200 import _native
     L = _native.lib()
+    code = {"tf32x3": 0, "tf32": 1, "simt": 2, "bf16x3": 3}[math_mode]
     M, N, K = 128, 2048, 512
     A = torch.randn(batch, M * K, device="cuda")
     W = torch.randn(K * N, device="cuda")
     C = torch.empty(batch, M * N, device="cuda")
+    planes = torch.empty(2 * N * K, device="cuda")
     ctx, st, e0, e1 = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
     _native.check(L.hs_ctx_create(torch.cuda.current_device(), ctypes.byref(ctx)))
     _native.check(L.hs_stream_create(ctx, 0, ctypes.byref(st)))
     _native.check(L.hs_event_create(ctx, 1, ctypes.byref(e0)))
     _native.check(L.hs_event_create(ctx, 1, ctypes.byref(e1)))
+    _native.check(L.hs_gemm_split_weights_ex(st, W.data_ptr(), 0, N, K, planes.data_ptr(), N * K,
+                                             1 if math_mode == "bf16x3" else 0))
     a = _native.OpArgs()
     a.n_in = 2
     a.in_[0], a.in_[1] = A.data_ptr(), W.data_ptr()
     a.in_stride[0], a.in_stride[1] = M * K, 0
     a.out, a.out_stride = C.data_ptr(), M * N
     a.dims[0], a.dims[1], a.dims[2] = M, N, K
+    a.aux = planes.data_ptr()
     for _ in range(3):
-        _native.check(L.hs_launch(st, 2, ctypes.byref(a), 0, batch))
+        _native.check(L.hs_launch(st, 2, ctypes.byref(a), code, batch))
     _native.check(L.hs_stream_sync(st))
     _native.check(L.hs_event_record(e0, st))
     for _ in range(reps):
-        _native.check(L.hs_launch(st, 2, ctypes.byref(a), 0, batch))
+        _native.check(L.hs_launch(st, 2, ctypes.byref(a), code, batch))
     _native.check(L.hs_event_record(e1, st))
     _native.check(L.hs_event_sync(e1))
     ns = ctypes.c_int64()
@@ -244,13 +252,13 @@ def gemm_roofline(batch, tflops_peak, reps=20):
     return flops / t / 1e12, t * 1e3, flops
 
 
-def tf32_cublas_peak():
-    """cuBLAS TF32 dense throughput at 8192^3 (the tensor peak the 3xTF32 path is held to)."""
+def matmul_peak(dtype):
+    """cuBLAS dense throughput at 8192^3 in-run: torch.float32 with TF32 enabled, or bf16."""
     import torch
     torch.backends.cuda.matmul.allow_tf32 = True
     n = 8192
-    a = torch.randn(n, n, device="cuda")
-    b = torch.randn(n, n, device="cuda")
+    a = torch.randn(n, n, device="cuda", dtype=dtype)
+    b = torch.randn(n, n, device="cuda", dtype=dtype)
     for _ in range(3):
         torch.matmul(a, b)
     torch.cuda.synchronize()
@@ -265,6 +273,25 @@ def tf32_cublas_peak():
     torch.backends.cuda.matmul.allow_tf32 = False
     del a, b
     return 2.0 * n ** 3 / best / 1e12
+
+
+def oracle_reference(layers, first):
+    """CPU oracle output (fp32, sequential-k GEMMs) of instance `first`, for the in-run parity check."""
+    from oracle import oracle as O
+    from paper_2009_07482_b200 import workloads
+    text, params, meta = workloads.encoder(layers=layers)
+    x = workloads.encoder_inputs(meta, params, 1, first=first).reshape(1, -1)
+    arrays = {(i["kernel"], i["pos"]): x for i in meta["x_inputs"]}
+    for k, w in workloads.encoder_weights(meta).items():
+        arrays[k] = w.reshape(-1)
+    out = O.run_dag(text, params, arrays, 1)
+    return out[(meta["output"]["kernel"], meta["output"]["pos"])].reshape(-1)
+
+
+def normwise(y, ref):
+    import numpy as np
+    y, ref = np.asarray(y, np.float64), np.asarray(ref, np.float64)
+    return float(np.max(np.abs(y - ref)) / max(float(np.max(np.abs(ref))), 1e-30))
 
 
 def run_ours(args, world, rank, local):
@@ -283,8 +310,8 @@ def run_ours(args, world, rank, local):
     x_np = workloads.encoder_inputs(meta, params, n, first=first).reshape(n, S * D)
     out_key = (meta["output"]["kernel"], meta["output"]["pos"])
 
-    def make_engine(x, out):
-        eng = Engine(text, params, gpu=local, batch=args.batch, slots=args.slots, math=args.math, mode="graph")
+    def make_engine(x, out, math_mode):
+        eng = Engine(text, params, gpu=local, batch=args.batch, slots=args.slots, math=math_mode, mode="graph")
         for i in meta["x_inputs"]:
             eng.bind(i["kernel"], i["pos"], x)
         for key, w in weights.items():
@@ -292,41 +319,57 @@ def run_ours(args, world, rank, local):
         eng.bind(*out_key, out)
         return eng
 
-    # device-resident arm
-    x_dev = torch.from_numpy(x_np).cuda()
-    out_dev = torch.empty(n, S * D, device="cuda")
-    eng_d = make_engine(x_dev, out_dev)
-
     def timed(eng, steps):
         tot = 0
         for _ in range(steps):
             tot += eng.run(0, n)
         return tot / 1e9
 
-    for _ in range(args.warmup):
-        eng_d.run(0, n)
-    barrier(world)
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
-        dev_s = timed(eng_d, args.steps)
-    torch.cuda.synchronize()
-    barrier(world)
-    dev_s = reduce_max(world, dev_s, local)
-    ms_per_step = dev_s / args.steps * 1e3
+    def device_resident(math_mode, sample_clocks):
+        """Device-resident arm: X and outputs in HBM. Returns (ms/step max over ranks, plan, stats, out row 0, clocks)."""
+        x_dev = torch.from_numpy(x_np).cuda()
+        out_dev = torch.empty(n, S * D, device="cuda")
+        eng = make_engine(x_dev, out_dev, math_mode)
+        for _ in range(args.warmup):
+            eng.run(0, n)
+        barrier(world)
+        torch.cuda.synchronize()
+        clk = None
+        if sample_clocks:
+            with ClockSampler(local) as c:
+                s = timed(eng, args.steps)
+            clk = c.summary()
+        else:
+            s = timed(eng, args.steps)
+        torch.cuda.synchronize()
+        barrier(world)
+        s = reduce_max(world, s, local)
+        plan, stats = eng.info("plan"), eng.info("stats")
+        row0 = out_dev[0].cpu().numpy().copy()
+        finite = bool(torch.isfinite(out_dev).all())
+        eng.close()
+        del x_dev, out_dev
+        torch.cuda.empty_cache()
+        return s / args.steps * 1e3, plan, stats, row0, clk, finite
+
+    ms_per_step, plan, stats, row0, clocks, finite = device_resident(args.math, True)
+    assert finite, "non-finite outputs"
     value = args.instances / (ms_per_step / 1e3)
-    stats = eng_d.info("stats")
-    plan = eng_d.info("plan")
     launches = int(stats["launches_per_batch"]) * math.ceil(n / args.batch) * args.steps
+
+    alt = None
+    if not args.no_alt:
+        alt_math = "bf16x3" if args.math != "bf16x3" else "tf32x3"
+        alt_ms, _, _, alt_row0, alt_clk, alt_finite = device_resident(alt_math, True)
+        alt = {"math": alt_math, "value": args.instances / (alt_ms / 1e3), "ms_per_step": alt_ms, "clocks": alt_clk,
+               "_row0": alt_row0, "finite": alt_finite}
 
     # end-to-end arm through the public API with pinned host buffers
     e2e = None
     if not args.no_e2e:
-        eng_d.close()
-        del x_dev, out_dev
-        torch.cuda.empty_cache()
         x_host = torch.from_numpy(x_np).pin_memory()
         out_host = torch.empty(n, S * D).pin_memory()
-        eng_h = make_engine(x_host, out_host)
+        eng_h = make_engine(x_host, out_host, args.math)
         for _ in range(args.warmup):
             eng_h.run(0, n)
         barrier(world)
@@ -337,44 +380,69 @@ def run_ours(args, world, rank, local):
         e2e = {"value": args.instances / (e2e_s / args.steps), "unit": UNIT,
                "h2d_bytes_per_step": args.instances * inst_bytes, "d2h_bytes_per_step": args.instances * inst_bytes,
                "ms_per_step": e2e_s / args.steps * 1e3}
-        ref = workloads.encoder_inputs(meta, params, 1, first=first).reshape(-1)
-        assert np.array_equal(x_host[0].numpy(), ref)
-        assert torch.isfinite(out_host).all()
+        assert np.array_equal(out_host[0].numpy(), row0), "e2e output differs from the device-resident run"
         eng_h.close()
 
     line = None
     if rank == 0:
         pk, pk_kind = peaks()
-        tf32 = tf32_cublas_peak()
-        achieved, ms_launch, flops = gemm_roofline(args.batch, tf32)
-        peak3 = tf32 / 3.0
+        tf32 = matmul_peak(torch.float32)
+        achieved, ms_launch, flops = gemm_roofline(args.batch, args.math)
+        if args.math == "bf16x3":
+            bf16 = pk["bf16_tflops"]
+            peak, peak_note = bf16 / 3.0, (f"MEASURED_PEAKS.json ({pk_kind}) dense bf16 burst {bf16:.0f} TFLOP/s "
+                                           f"/ 3 MMAs per product")
+        else:
+            peak, peak_note = tf32 / 3.0, f"cuBLAS TF32 measured in-run {tf32:.0f} TFLOP/s / 3 MMAs per product"
+        traffic = None
+        tf = ROOT / "profiles" / "ffn1_traffic.json"
+        if tf.exists():
+            t = json.loads(tf.read_text())
+            traffic = t.get(args.math, {}).get("dram_bytes_per_launch_per_instance")
+            traffic = traffic * args.batch if traffic else None
+        # parity of this very run: instance `first` against the CPU oracle (fp32, sequential-k)
+        t0 = time.perf_counter()
+        ref = oracle_reference(args.layers, first)
+        t_cpu = time.perf_counter() - t0
+        parity = {"instance": first, "math": args.math, "normwise_err_vs_cpu_oracle": normwise(row0, ref), "tol": 1e-4}
+        if alt is not None:
+            alt["normwise_err_vs_cpu_oracle"] = normwise(alt.pop("_row0"), ref)
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
-            v, threads, t = cpu_sample(args.layers, n_inst=1)
+            v, threads, t = cpu_sample(args.layers, n_inst=12)
             cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
-                   "sample": f"1 instance of the {args.layers}-layer DAG ({t:.1f} s), oracle port, all host threads"}
+                   "sample": f"12 instances of the {args.layers}-layer DAG ({t:.1f} s; oracle port: clustering "
+                             f"scheduler + fp32 kernels on all host threads)"}
         flop_per_inst = 782.2e6 * args.layers
+        dtypes = {"tf32x3": "f32 (3xTF32 split on tcgen05, fp32-accurate)",
+                  "bf16x3": "f32 (bf16x3 split on tcgen05 for weight GEMMs, 3xTF32 elsewhere; <=1e-4)",
+                  "tf32": "tf32", "simt": "f32"}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f32 (3xTF32 tcgen05)" if args.math == "tf32x3" else args.math,
+            "vs_baseline": None, "dtype": dtypes.get(args.math, args.math),
             "data": "synthetic (splitmix64 uniform inputs, random-init weights)",
             "config": {"workload": f"C5: {args.layers}-layer encoder DAG (8 heads, d_model 512, seq 128, d_ff 2048), "
                                    f"stream of {args.instances} instances",
                        "kernels_per_dag": plan["kernels"], "edges": plan["edges"], "components": plan["components"],
-                       "policy": "clustering", "queues_per_device": args.queues, "logical_devices": args.devices, "batch": args.batch,
-                       "slots": args.slots, "mode": "graph", "parallelism": f"instance partition x{world}",
+                       "policy": "clustering", "queues_per_device": args.queues, "logical_devices": args.devices,
+                       "batch": args.batch, "slots": args.slots, "mode": "graph",
+                       "grouped_launches_per_batch": plan.get("grouped_launches"),
+                       "parallelism": f"instance partition x{world}", "math": args.math,
                        "l2": "inputs (1 GiB X + 1 GiB out per step) larger than L2"},
-            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak3, "unit": "TFLOP/s",
-                         "frac": achieved / peak3, "traffic": None,
-                         "kernel": f"gemm_relu tcgen05 3xTF32 128x2048x512 x{args.batch} ({ms_launch:.3f} ms/launch)",
-                         "peak_note": f"cuBLAS TF32 measured in-run {tf32:.0f} TFLOP/s / 3 MMAs per product"},
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": f"gemm_tc_kernel FFN1 gemm_relu 128x2048x512 x{args.batch}, resident pre-split "
+                                   f"weight, {args.math} ({ms_launch:.3f} ms/launch)",
+                         "peak_note": peak_note, "measured_peaks_file": pk_kind},
             "dag_roofline": {"flop_per_dag": flop_per_inst, "achieved_tflops": flop_per_inst * value / 1e12,
-                             "frac_of_3xtf32": flop_per_inst * value / 1e12 / (peak3 * world)},
+                             "frac_of_peak": flop_per_inst * value / 1e12 / (peak * world)},
+            "parity": parity,
+            "alt_math": alt,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
-            "clocks": clk.summary(),
+            "clocks": clocks,
             "device_bytes": plan["device_bytes"],
         }
     return line
