@@ -428,6 +428,8 @@ def run_ours(args, world, rank, local):
                        "policy": "clustering", "queues_per_device": args.queues, "logical_devices": args.devices,
                        "batch": args.batch, "slots": args.slots, "mode": "graph",
                        "grouped_launches_per_batch": plan.get("grouped_launches"),
+                       "chain_rewrites_per_batch": plan.get("chain_rewrites"),
+                       "launches_per_batch": plan.get("launches_per_batch"),
                        "parallelism": f"instance partition x{world}", "math": args.math,
                        "l2": "inputs (1 GiB X + 1 GiB out per step) larger than L2"},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",

@@ -130,7 +130,18 @@ typedef struct {
   int n_out;
   void* outs[4];
   int64_t out_strides[4];
+  /* GEMM output placement and epilogue (zero-initialised = plain C[M,N]):
+   * out_ld  row stride of C in elements (0 = N): a GEMM can write one column
+   *         block of a wider row-major matrix (e.g. its slot in a concat);
+   * epilogue HS_EPI_SOFTMAX: C = row softmax(A·B · fparam[0]) over all N
+   *         columns (N <= 128, tcgen05 math only) -- a GEMM fused with the
+   *         softmax node that consumes it. */
+  int64_t out_ld;
+  int epilogue;
 } hs_op_args;
+
+#define HS_EPI_NONE 0
+#define HS_EPI_SOFTMAX 1
 
 int hs_op_from_name(const char* name); /* -1 if unknown */
 int hs_launch(hs_stream_t s, int op, const hs_op_args* args, int math_mode, int batch);

@@ -46,7 +46,12 @@ class OpArgs(ctypes.Structure):
         ("n_out", c_int),
         ("outs", c_void_p * 4),
         ("out_strides", c_int64 * 4),
+        ("out_ld", c_int64),
+        ("epilogue", c_int),
     ]
+
+
+EPI_NONE, EPI_SOFTMAX = 0, 1
 
 
 _PROTOS = {

@@ -2,7 +2,8 @@
 // fp32 reference for the tcgen05 kernels and a fallback for shapes the
 // tensor-core path rejects (K or N not a multiple of 4). Same contract as
 // the tcgen05 kernel: C = A·B (B row-major [K,N] or [N,K]), optional ReLU,
-// batched over instances with per-operand strides.
+// batched over instances with per-operand strides and an optional output row
+// stride (ldc). The softmax epilogue is tcgen05-only.
 #include <cuda_runtime.h>
 
 #include "kernels.cuh"
@@ -63,7 +64,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs p) {
       if (gn >= p.N) continue;
       float v = acc[i][j];
       if (p.relu) v = fmaxf(v, 0.f);
-      C[int64_t(gm) * p.N + gn] = v;
+      C[int64_t(gm) * (p.ldc ? p.ldc : p.N) + gn] = v;
     }
   }
 }

@@ -248,6 +248,10 @@ struct TileParams {
   int n_out, Nm;
   float* Cs[4];
   int64_t sCs[4];
+  int64_t ldc;  // row stride of C (0 = N, or Nm for grouped launches)
+  // Softmax epilogue (one tile covers all N columns): C = softmax_row(acc * escale).
+  int softmax;
+  float escale;
 };
 
 // D[tmem] (+)= A[tmem] · B[smem]; A is K-major in TMEM (lane = row, column = k).
@@ -279,6 +283,25 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16
       "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
       "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
       : "memory");
+}
+
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// 32 consecutive accumulator columns of this warp's TMEM lane quarter -> registers.
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
 template <int BN, int kBSrc, int kTerms, bool kSmall, bool kBf16>
@@ -448,21 +471,40 @@ __global__ void __launch_bounds__(kThreads, kSmall ? 2 : 1)
       const uint32_t acc = lt % uint32_t(L::kAccBufs);
       mbar_wait(acc_full(int(acc)), (lt / uint32_t(L::kAccBufs)) & 1u);
       tc_fence_after();
-      const int row = m0 + q * 32 + lane;
+      const uint32_t tacc = tmem + (uint32_t(q * 32) << 16) + acc * uint32_t(BN);
+      // Softmax epilogue: this thread owns one full row of the tile (N <= BN).
+      // Two read passes over TMEM give the row max and the sequential sum of
+      // exp(s*x - max) in the oracle's order; the store pass scales by 1/sum.
+      // exp is ex2.approx on (s*x - max)*log2(e) (rel. error ~2^-21, far inside
+      // the 1e-4 tolerance): one MUFU op instead of the ~20-instruction expf,
+      // which matters because one warp per scheduler does all of this.
+      float smax = 0.f, ssum = 1.f, sl = 0.f, ml = 0.f;
+      if (p.softmax) {
+        uint32_t r[32];
+        smax = -INFINITY;
+#pragma unroll 1
+        for (int cb = 0; cb < BN / 32 && cb * 32 < p.N; ++cb) {
+          tmem_ld32(tacc + uint32_t(cb * 32), r);
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (cb * 32 + j < p.N) smax = fmaxf(smax, __uint_as_float(r[j]) * p.escale);
+        }
+        sl = p.escale * 1.4426950408889634f;
+        ml = smax * 1.4426950408889634f;
+        ssum = 0.f;
+#pragma unroll 1
+        for (int cb = 0; cb < BN / 32 && cb * 32 < p.N; ++cb) {
+          tmem_ld32(tacc + uint32_t(cb * 32), r);
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (cb * 32 + j < p.N) ssum = ssum + ex2_approx(fmaf(__uint_as_float(r[j]), sl, -ml));
+        }
+        ssum = 1.f / ssum;  // used as the reciprocal below
+      }
 #pragma unroll 1
       for (int cb = 0; cb < BN / 32; ++cb) {
         uint32_t r[32];
-        const uint32_t taddr = tmem + (uint32_t(q * 32) << 16) + acc * uint32_t(BN) + uint32_t(cb * 32);
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-              "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]),
-              "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]),
-              "=r"(r[30]), "=r"(r[31])
-            : "r"(taddr));
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        tmem_ld32(tacc + uint32_t(cb * 32), r);
         if (cb == BN / 32 - 1) {
           // accumulator drained into registers: hand it back to the MMA warp early
           tc_fence_before();
@@ -476,23 +518,26 @@ __global__ void __launch_bounds__(kThreads, kSmall ? 2 : 1)
         const uint32_t tile = scratch + uint32_t(q) * uint32_t(kEpiTileBytes);
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
-          const float v = __uint_as_float(r[j]);
+          float v = __uint_as_float(r[j]);
+          if (p.softmax) v = ex2_approx(fmaf(v, sl, -ml)) * ssum;
           sts32(tile + uint32_t(lane * 33 + j) * 4u, p.relu ? fmaxf(v, 0.f) : v);
         }
         __syncwarp();
-        // destination of this 32-column chunk: the single C, or member m's C
-        int c0 = n0 + cb * 32, ld = p.N;
+        // destination of this 32-column chunk: the single C, or member m's C;
+        // `ncols` valid columns, rows `ld` elements apart
+        int c0 = n0 + cb * 32, ncols = p.N;
         float* cbase;
         if (p.n_out > 0) {
           const int m = c0 / p.Nm;
           c0 -= m * p.Nm;
-          ld = p.Nm;
+          ncols = p.Nm;
           cbase = p.Cs[m] + int64_t(inst) * p.sCs[m];
         } else {
           cbase = p.C + int64_t(inst) * p.sC;
         }
+        const int64_t ld = p.ldc ? p.ldc : ncols;
         const int cq = (lane & 7) * 4, rsub = lane >> 3;
-        const bool vec = c0 + 32 <= ld && (ld & 3) == 0;
+        const bool vec = c0 + 32 <= ncols && (ld & 3) == 0;
 #pragma unroll
         for (int pass = 0; pass < 8; ++pass) {
           const int rr = pass * 4 + rsub;
@@ -506,7 +551,7 @@ __global__ void __launch_bounds__(kThreads, kSmall ? 2 : 1)
             } else {
               const float e[4] = {v.x, v.y, v.z, v.w};
               for (int i = 0; i < 4; ++i)
-                if (c0 + cq + i < ld) dst[i] = e[i];
+                if (c0 + cq + i < ncols) dst[i] = e[i];
             }
           }
         }
@@ -750,6 +795,10 @@ cudaError_t launch(const GemmArgs& a, cudaStream_t s) {
     p.Cs[i] = a.Cs[i];
     p.sCs[i] = a.sCs[i];
   }
+  p.ldc = a.ldc;
+  p.softmax = a.softmax;
+  p.escale = a.escale;
+  if (p.softmax && p.n_tiles != 1) return cudaErrorInvalidValue;
   p.total_tiles = p.m_tiles * p.n_tiles * a.batch;
   const int slots = num_sms() * L::kCtasPerSm;
   const int grid = p.total_tiles < slots ? p.total_tiles : slots;
@@ -789,6 +838,8 @@ cudaError_t gemm_tcgen05(const GemmArgs& a, int terms, cudaStream_t s) {
     }
     return cudaErrorInvalidValue;
   }
+  // softmax epilogue: one 128-wide tile holds whole rows
+  if (a.softmax) return a.N <= 128 ? launch_bn<128>(a, terms, s) : cudaErrorInvalidValue;
   // short K (attention-sized GEMMs): 64-wide tiles, two CTAs per SM
   if (a.K <= 4 * BK && a.N <= 128 && HS_SMALL_GEMM) return launch_bn<64, true>(a, terms, s);
   if (a.N <= 64) return launch_bn<64>(a, terms, s);

@@ -250,6 +250,15 @@ int hs_launch(hs_stream_t st, int op, const hs_op_args* a, int math, int batch) 
                      int(a->dims[0]), int(a->dims[1]), int(a->dims[2]), batch,
                      op == HS_OP_GEMM_NT ? hs::GemmLayout::nt : hs::GemmLayout::nn, op == HS_OP_GEMM_RELU,
                      math == HS_MATH_FP32_SIMT ? nullptr : static_cast<const float*>(a->aux)};
+      if (a->out_ld < 0 || (a->out_ld > 0 && a->out_ld < a->dims[1])) return invalid("gemm out_ld < N");
+      if (a->epilogue != HS_EPI_NONE && a->epilogue != HS_EPI_SOFTMAX) return invalid("unknown GEMM epilogue");
+      g.ldc = a->out_ld;
+      if (a->epilogue == HS_EPI_SOFTMAX) {
+        if (math == HS_MATH_FP32_SIMT || op == HS_OP_GEMM_RELU || a->n_out > 1 || a->dims[1] > 128)
+          return invalid("softmax epilogue needs tcgen05 math, a plain GEMM and N <= 128");
+        g.softmax = 1;
+        g.escale = a->fparam[0];
+      }
       // BF16X3 applies to GEMMs whose B arrives pre-split (bf16 planes); the rest run TF32X3.
       g.bf16 = (math == HS_MATH_BF16X3 && a->aux) ? 1 : 0;
       if (g.bf16 && (g.K % 8) && a->n_out <= 1) {
@@ -270,8 +279,12 @@ int hs_launch(hs_stream_t st, int op, const hs_op_args* a, int math, int batch) 
         g.sC = g.sCs[0];
         if (!hs::gemm_tcgen05_supported(g)) return invalid("grouped GEMM shape not supported");
         e = hs::gemm_tcgen05(g, math == HS_MATH_TF32 ? 1 : 3, s);
-      } else if (math == HS_MATH_FP32_SIMT || !hs::gemm_tcgen05_supported(g)) e = hs::gemm_simt(g, s);
-      else e = hs::gemm_tcgen05(g, math == HS_MATH_TF32 ? 1 : 3, s);
+      } else if (math == HS_MATH_FP32_SIMT || !hs::gemm_tcgen05_supported(g)) {
+        if (g.softmax) return invalid("softmax epilogue: GEMM shape not supported by the tcgen05 path");
+        e = hs::gemm_simt(g, s);
+      } else {
+        e = hs::gemm_tcgen05(g, math == HS_MATH_TF32 ? 1 : 3, s);
+      }
       break;
     }
     case HS_OP_TRANSPOSE:

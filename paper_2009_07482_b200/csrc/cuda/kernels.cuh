@@ -31,6 +31,11 @@ struct GemmArgs {
   int64_t sCs[4] = {0, 0, 0, 0};
   // Bplanes hold bf16 hi/lo (math BF16x3) instead of tf32 hi/lo.
   int bf16 = 0;
+  // Row stride of C in elements (0 = N, or the member width for grouped launches).
+  int64_t ldc = 0;
+  // 1 = row softmax of (A·B)·escale over the N columns (N <= 128, one tile row).
+  int softmax = 0;
+  float escale = 1.f;
 };
 
 // planes: hi at planes[n*K + k], lo at planes[plane_stride + n*K + k]

@@ -373,11 +373,14 @@ void Engine::launch_node(Slot& sl, hs_stream_t s, int kernel) {
     const bool shared = gi != group_of_.end() && groups_[size_t(gi->second)].resident;
     a.in_stride[i] = shared ? 0 : bytes_.at(key) / 4;
   }
-  a.out = sl.buf.at(nd.output);
+  a.out = static_cast<float*>(sl.buf.at(nd.output)) + nd.out_off;
   a.out_stride = bytes_.at(nd.output) / 4;
   for (int i = 0; i < 4; ++i) a.dims[i] = nd.dims[i];
   a.fparam[0] = nd.fparam[0];
   a.fparam[1] = nd.fparam[1];
+  a.out_ld = nd.out_ld;
+  a.epilogue = nd.epilogue;
+  if (nd.epilogue == HS_EPI_SOFTMAX) a.fparam[0] = nd.escale;
   auto pl = node_planes_.find(kernel);
   a.aux = pl == node_planes_.end() ? nullptr : pl->second;
   hs_ok(hs_launch(s, nd.op, &a, cfg_.math, cfg_.batch), "hs_launch");
@@ -484,9 +487,9 @@ void Engine::issue(Slot& sl, const TaskComponent& t, const CommandQueueStructure
           // computed by the group's leader launch: order this queue after it
           const FuseGroup& fg = fuse_groups_[size_t(member->second)];
           hs_ok(hs_stream_wait(s, event(sl, t.id, fg.events[0])), "grouped member wait");
-        } else {
+        } else if (!nodes_.at(c.kernel).elided) {
           launch_node(sl, s, c.kernel);
-        }
+        }  // elided: computed by the launch that absorbed it (plan_chain_rewrites)
         break;
       }
       case CmdKind::read:
@@ -568,6 +571,92 @@ void Engine::plan_fusion() {
   }
 }
 
+// Chain rewrites (graph mode). Each rule removes one node's launch by folding
+// it into its producer; it fires only when the intermediate buffer is
+// internal to the DAG (exactly one consumer edge, no isolated read), so no
+// observable buffer changes. The plan's commands, events and E_Q / inter-edge
+// waits are untouched: an elided ndrange still records its events, so every
+// consumer keeps waiting on the same chain.
+//   transpose_into_gemm_nt  T = transpose(X) consumed only as B of a gemm:
+//                           the gemm reads X as gemm_nt (B = [N,K]).
+//   softmax_epilogue        P = softmax(S·s) where S = gemm(..) feeds only the
+//                           softmax and N <= 128: the gemm computes P directly.
+//   concat_in_place         Y = concat(Z_0..Z_n-1), Z_i = gemm(..) feeding only
+//                           the concat: gemm i writes Y[:, i·c:(i+1)·c] (ld n·c).
+void Engine::plan_chain_rewrites() {
+  const auto consumers = g_.consumer_edges();
+  std::set<int> grouped;
+  for (const auto& fg : fuse_groups_) grouped.insert(fg.kernels.begin(), fg.kernels.end());
+  auto sole_consumer = [&](std::pair<int, int> out, int* dst_kernel, int* dst_pos) {
+    auto it = consumers.find(out);
+    if (it == consumers.end() || it->second.size() != 1) return false;
+    const DagEdge& e = g_.edges[size_t(it->second.front())];
+    if (io_copy_.count({e.dst_kernel, e.dst_pos})) return false;  // io inputs are copies, not aliases
+    *dst_kernel = e.dst_kernel;
+    *dst_pos = e.dst_pos;
+    return true;
+  };
+  auto is_gemm = [](int op) { return op == HS_OP_GEMM || op == HS_OP_GEMM_NT || op == HS_OP_GEMM_RELU; };
+  auto resident = [&](std::pair<int, int> key) {
+    auto gi = group_of_.find(key);
+    return gi != group_of_.end() && groups_[size_t(gi->second)].resident;
+  };
+  for (auto& [kid, nd] : nodes_) {
+    if (nd.op != HS_OP_TRANSPOSE || nd.elided) continue;
+    int ck, cp;
+    if (!sole_consumer(nd.output, &ck, &cp)) continue;
+    Node& g = nodes_.at(ck);
+    if (g.op != HS_OP_GEMM || cp != g.inputs[1].second || grouped.count(ck) || g.epilogue) continue;
+    if (resident(nd.inputs[0]) || node_planes_.count(ck)) continue;
+    // X is R x C; T = X^T is C x R = K x N, so gemm_nt reads X as [N = R, K = C]
+    if (g.dims[1] != nd.dims[0] || g.dims[2] != nd.dims[1]) continue;
+    g.op = HS_OP_GEMM_NT;
+    g.inputs[1] = nd.inputs[0];
+    nd.elided = true;
+    ++rewrites_["transpose_into_gemm_nt"];
+  }
+  for (auto& [kid, g] : nodes_) {
+    if ((g.op != HS_OP_GEMM && g.op != HS_OP_GEMM_NT) || g.elided || g.epilogue || grouped.count(kid)) continue;
+    int ck, cp;
+    if (!sole_consumer(g.output, &ck, &cp)) continue;
+    Node& sm = nodes_.at(ck);
+    if (sm.op != HS_OP_SOFTMAX || sm.elided) continue;
+    if (sm.dims[0] != g.dims[0] || sm.dims[1] != g.dims[1] || g.dims[1] > 128) continue;
+    g.epilogue = HS_EPI_SOFTMAX;
+    g.escale = sm.fparam[0];
+    g.output = sm.output;
+    sm.elided = true;
+    ++rewrites_["softmax_epilogue"];
+  }
+  for (auto& [kid, cat] : nodes_) {
+    if (cat.op != HS_OP_CONCAT || cat.elided) continue;
+    const int64_t n = int64_t(cat.inputs.size()), rows = cat.dims[0], cols = cat.dims[1];
+    std::vector<int> producers;
+    for (const auto& in : cat.inputs) {
+      auto al = alias_.find(in);
+      if (al == alias_.end()) break;
+      int ck, cp;
+      if (!sole_consumer(al->second, &ck, &cp) || ck != kid) break;
+      const int pk = al->second.first;
+      const Node& z = nodes_.at(pk);
+      if (!is_gemm(z.op) || z.elided || grouped.count(pk) || z.out_ld || z.output != al->second) break;
+      if (z.dims[0] != rows || z.dims[1] != cols) break;
+      producers.push_back(pk);
+    }
+    if (int64_t(producers.size()) != n || cols % 4) continue;
+    for (int64_t i = 0; i < n; ++i) {
+      Node& z = nodes_.at(producers[size_t(i)]);
+      z.output = cat.output;
+      z.out_off = i * cols;
+      z.out_ld = n * cols;
+    }
+    cat.elided = true;
+    ++rewrites_["concat_in_place"];
+  }
+  for (const auto& [kid, nd] : nodes_)
+    if (nd.elided) --launches_per_batch_;
+}
+
 void Engine::capture(Slot& sl) {
   // Every stream the plan touches joins the capture through a fork event.
   std::set<std::pair<int, int>> used;
@@ -637,7 +726,8 @@ void Engine::run(int64_t first, int64_t n, int64_t* elapsed_ns) {
     if (cfg_.graph_mode) {
       PlanExecutor pe;
       plan_ = sched_->run(pe);
-      if (cfg_.fuse && cfg_.math != HS_MATH_FP32_SIMT) plan_fusion();
+      if (cfg_.fuse >= 1 && cfg_.math != HS_MATH_FP32_SIMT) plan_fusion();
+      if (cfg_.fuse >= 2 && cfg_.math != HS_MATH_FP32_SIMT) plan_chain_rewrites();
       for (auto& sl : slots_) capture(sl);
     }
     planned_ = true;
@@ -712,6 +802,9 @@ std::string Engine::info(const std::string& what) const {
     out.set("instance_groups", Value::of(static_cast<long long>(groups_.size() - resident_buf_.size())));
     out.set("aliased_inputs", Value::of(static_cast<long long>(alias_.size())));
     out.set("grouped_launches", Value::of(static_cast<long long>(fuse_groups_.size())));
+    Value rw = Value::make_object();
+    for (const auto& [rule, n] : rewrites_) rw.set(rule, Value::of(static_cast<long long>(n)));
+    out.set("chain_rewrites", std::move(rw));
     out.set("launches_per_batch", Value::of(static_cast<long long>(launches_per_batch_)));
   } else if (what == "stats") {
     out.set("launches_per_batch", Value::of(static_cast<long long>(launches_per_batch_)));
@@ -782,7 +875,10 @@ int hs_engine_create(const char* config_json, hs_engine_t* out) {
     }
     if (const json::Value* v = c.find("cpu_devices"))
       for (const json::Value* x : v->items()) cfg.cpu_devices.insert(x->as_int());
-    if (const json::Value* v = c.find("fuse")) cfg.fuse = v->as_int() != 0;
+    if (const json::Value* v = c.find("fuse")) {
+      cfg.fuse = v->as_int();
+      if (cfg.fuse < 0 || cfg.fuse > 2) fail(Errc::invalid_param, "fuse must be 0, 1 or 2");
+    }
     *out = reinterpret_cast<hs_engine_t>(new Engine(std::move(cfg)));
   });
 }

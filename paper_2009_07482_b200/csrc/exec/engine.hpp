@@ -41,7 +41,10 @@ struct EngineConfig {
   int slots = 2;
   int math = HS_MATH_TF32X3;
   std::set<int> cpu_devices;
-  bool fuse = true;  // grouped launch of sibling GEMMs (graph mode)
+  // Graph-mode launch lowering: 0 = one launch per ndrange, 1 = + grouped
+  // sibling GEMMs, 2 = + chain rewrites (transpose folded into gemm_nt,
+  // softmax as a GEMM epilogue, concat inputs written in place).
+  int fuse = 2;
 };
 
 class Engine {
@@ -65,6 +68,13 @@ class Engine {
     std::pair<int, int> output{-1, -1};
     int64_t dims[4] = {0, 0, 0, 0};
     float fparam[2] = {1.f, 1e-5f};
+    // chain rewrites (graph mode, plan_fusion): the output lands at element
+    // `out_off` of `output` with rows `out_ld` apart; `epilogue` is an
+    // HS_EPI_* applied by the GEMM; an elided node has no launch of its own.
+    int64_t out_off = 0, out_ld = 0;
+    int epilogue = HS_EPI_NONE;
+    float escale = 1.f;
+    bool elided = false;
   };
   struct Binding {
     void* ptr = nullptr;
@@ -141,6 +151,8 @@ class Engine {
     int64_t n = 0, k = 0;  // per member
   };
   void plan_fusion();
+  void plan_chain_rewrites();
+  std::map<std::string, int64_t> rewrites_;  // rule -> times applied
   // weight planes: bf16 hi/lo for BF16X3, tf32 hi/lo (fp32 containers) otherwise
   int plane_format() const { return cfg_.math == HS_MATH_BF16X3 ? 1 : 0; }
   int64_t plane_elem_bytes() const { return cfg_.math == HS_MATH_BF16X3 ? 2 : 4; }

@@ -29,7 +29,11 @@ def _ptr_and_nbytes(arr):
 class Engine:
     def __init__(self, spec_text: str, params: dict | None = None, *, gpu: int = 0, policy: str = "clustering",
                  mode: str = "graph", batch: int = 1, slots: int = 2, math: str = "tf32x3", cpu_devices=(),
-                 fuse: bool = True):
+                 fuse: int | bool = 2):
+        """fuse (graph mode): 0 = one launch per ndrange; 1 = + grouped sibling GEMMs;
+        2 (default, also True) = + chain rewrites (transpose -> gemm_nt, softmax as a GEMM
+        epilogue, concat inputs written in place). Dynamic mode always launches per ndrange."""
+        fuse = 2 if fuse is True else int(fuse)
         cfg = {"spec": spec_text, "params": dict(params or {}), "gpu": gpu, "policy": policy, "mode": mode,
                "batch": batch, "slots": slots, "math": math, "cpu_devices": list(cpu_devices), "fuse": int(fuse)}
         self._lib = lib()

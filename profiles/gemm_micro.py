@@ -18,7 +18,7 @@ OPS = {"gemm": 0, "gemm_nt": 1, "gemm_relu": 2}
 MATH = {"tf32x3": 0, "tf32": 1, "simt": 2}
 
 
-def run(M, N, K, batch, op="gemm", math="tf32x3", presplit=True, shared=True, reps=20):
+def run(M, N, K, batch, op="gemm", math="tf32x3", presplit=True, shared=True, reps=20, epilogue=0):
     A = torch.randn(batch, M * K, device="cuda")
     B = torch.randn(N * K if shared else batch * N * K, device="cuda")
     C = torch.empty(batch, M * N, device="cuda")
@@ -33,6 +33,8 @@ def run(M, N, K, batch, op="gemm", math="tf32x3", presplit=True, shared=True, re
     a.out, a.out_stride = C.data_ptr(), M * N
     a.dims[0], a.dims[1], a.dims[2] = M, N, K
     a.aux = planes.data_ptr() if planes is not None else None
+    a.epilogue = epilogue
+    a.fparam[0] = 0.125
     for _ in range(3):
         _native.check(L.hs_launch(st, OPS[op], ctypes.byref(a), MATH[math], batch))
     _native.check(L.hs_stream_sync(st))
@@ -46,7 +48,7 @@ def run(M, N, K, batch, op="gemm", math="tf32x3", presplit=True, shared=True, re
     us = ns.value / 1e3 / reps
     flops = 2.0 * M * N * K * batch
     print(f"{op:9s} M={M:4d} N={N:5d} K={K:5d} batch={batch:4d} math={math:6s} presplit={int(presplit)} "
-          f"shared={int(shared)}: {us:8.2f} us  {flops / us / 1e6:7.1f} TFLOP/s", flush=True)
+          f"shared={int(shared)} epi={epilogue}: {us:8.2f} us  {flops / us / 1e6:7.1f} TFLOP/s", flush=True)
     return us
 
 

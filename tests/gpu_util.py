@@ -40,16 +40,19 @@ def split_weights(B, transposed, N, K, bf16=False):
 
 
 def launch(op, inputs, out, dims, fparam=(1.0, 1e-5), math="tf32x3", batch=1, strides=None, out_stride=None,
-           aux=None):
-    """inputs/out: torch CUDA float32 tensors shaped [batch, elems] or [elems] (shared)."""
+           aux=None, out_ld=0, epilogue=0, out_offset=0):
+    """inputs/out: torch CUDA float32 tensors shaped [batch, elems] or [elems] (shared).
+    out_offset (elements) / out_ld / epilogue: GEMM output placement and epilogue."""
     L = _native.lib()
     a = _native.OpArgs()
+    a.out_ld = out_ld
+    a.epilogue = epilogue
     a.aux = aux.data_ptr() if aux is not None else None
     a.n_in = len(inputs)
     for i, t in enumerate(inputs):
         a.in_[i] = t.data_ptr()
         a.in_stride[i] = (strides[i] if strides else (0 if t.dim() == 1 else t.shape[-1]))
-    a.out = out.data_ptr()
+    a.out = out.data_ptr() + 4 * out_offset
     a.out_stride = out_stride if out_stride is not None else out.shape[-1]
     for i, d in enumerate(dims):
         a.dims[i] = d

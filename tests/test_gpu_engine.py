@@ -97,13 +97,33 @@ def test_grouped_sibling_gemms_match_unfused(oracle_mod):
     arrays = _encoder_arrays(meta, params, n)
     ref = oracle_mod.run_dag(text, params, arrays, n)
     key = (meta["output"]["kernel"], meta["output"]["pos"])
-    fused, _, plan = _run_gpu(text, params, arrays, n, mode="graph", batch=3, fuse=True)
-    plain, _, plan0 = _run_gpu(text, params, arrays, n, mode="graph", batch=3, fuse=False)
+    fused, _, plan = _run_gpu(text, params, arrays, n, mode="graph", batch=3, fuse=1)
+    plain, _, plan0 = _run_gpu(text, params, arrays, n, mode="graph", batch=3, fuse=0)
     assert plan["grouped_launches"] == 16 and plan0["grouped_launches"] == 0  # 8 heads x 2 layers
     assert plan["launches_per_batch"] == plan0["launches_per_batch"] - 32
     for i in range(n):
         assert _normwise(fused[key][i], ref[key][i]) <= TOL
         assert _normwise(fused[key][i], plain[key][i]) <= 1e-6
+
+
+@pytest.mark.parametrize("math", ["tf32x3", "bf16x3"])
+def test_chain_rewrites_match_oracle(math, oracle_mod):
+    """fuse=2 (default): per head the transpose folds into a gemm_nt, the softmax
+    becomes the QK^T GEMM's epilogue and the 8 Z_h GEMMs write the concat in
+    place: 2 x 17 launches fewer per layer pair, same results within tolerance."""
+    text, params, meta = workloads.encoder(layers=2)
+    n = 3
+    arrays = _encoder_arrays(meta, params, n)
+    ref = oracle_mod.run_dag(text, params, arrays, n)
+    key = (meta["output"]["kernel"], meta["output"]["pos"])
+    chained, _, plan = _run_gpu(text, params, arrays, n, mode="graph", batch=2, fuse=2, math=math)
+    grouped, _, plan1 = _run_gpu(text, params, arrays, n, mode="graph", batch=2, fuse=1, math=math)
+    assert plan["chain_rewrites"] == {"concat_in_place": 2, "softmax_epilogue": 16, "transpose_into_gemm_nt": 16}
+    assert plan1["chain_rewrites"] == {}
+    assert plan["launches_per_batch"] == plan1["launches_per_batch"] - 34
+    for i in range(n):
+        assert _normwise(chained[key][i], ref[key][i]) <= TOL
+        assert _normwise(chained[key][i], grouped[key][i]) <= 1e-5
 
 
 @pytest.mark.parametrize("mode", ["graph", "dynamic"])

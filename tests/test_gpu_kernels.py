@@ -99,6 +99,66 @@ def test_gemm_tf32_single_term_is_coarser(oracle_mod):
     assert errs["tf32x3"] * 10 < errs["tf32"], errs
 
 
+@pytest.mark.parametrize("math,presplit", [("tf32x3", False), ("tf32x3", True), ("bf16x3", True), ("simt", False)])
+def test_gemm_writes_column_block(math, presplit, oracle_mod):
+    """out_ld: a GEMM writes its [M,N] result as columns [off, off+N) of a wider
+    row-major matrix (how a concat input is produced in place); the other
+    columns are untouched."""
+    from tests.gpu_util import launch, normwise, split_weights
+    import torch
+    M, N, K, batch, width, off = 128, 64, 64, 3, 512, 192
+    A = _rand(41, (batch, M * K))
+    B = (_rand(42, (N * K,)) * np.float32(1.0 / np.sqrt(K))).astype(np.float32)
+    ref = np.empty((batch, M * N), np.float32)
+    oracle_mod.run_node("gemm", [A, B], [M * K, 0], ref, M * N, [M, N, K], batch)
+    Bt = _t(B)
+    planes = split_weights(Bt, False, N, K, bf16=math == "bf16x3") if presplit else None
+    Y = torch.full((batch, M * width), -7.0, device="cuda")
+    launch("gemm", [_t(A), Bt], Y, [M, N, K], math=math, batch=batch, aux=planes, out_ld=width, out_offset=off)
+    y = Y.cpu().numpy().reshape(batch, M, width)
+    tol = {"tf32x3": TOL_TF32X3, "bf16x3": 5e-5, "simt": 1e-5}[math]
+    for b in range(batch):
+        assert normwise(y[b, :, off:off + N].reshape(-1), ref[b]) <= tol, b
+    mask = np.ones(width, bool)
+    mask[off:off + N] = False
+    assert (y[:, :, mask] == -7.0).all()
+
+
+@pytest.mark.parametrize("M,N,K,op,batch", [(128, 128, 64, "gemm_nt", 3), (128, 128, 64, "gemm", 2),
+                                             (100, 72, 36, "gemm_nt", 2), (200, 128, 64, "gemm", 1)])
+@pytest.mark.parametrize("math", ["tf32x3", "tf32"])
+def test_gemm_softmax_epilogue(M, N, K, op, batch, math, oracle_mod):
+    """HS_EPI_SOFTMAX: P = softmax_row((A·B)·s) from one launch, against the oracle's
+    gemm followed by its softmax (the GEMM's own error passes through exp)."""
+    from tests.gpu_util import launch, normwise
+    import torch
+    A = _rand(51, (batch, M * K)) * np.float32(2)
+    B = _rand(52, (batch, N * K))
+    S = np.empty((batch, M * N), np.float32)
+    oracle_mod.run_node(op, [A, B], [M * K, N * K], S, M * N, [M, N, K], batch)
+    ref = np.empty_like(S)
+    oracle_mod.run_node("softmax", [S], [M * N], ref, M * N, [M, N, 1, 8], batch)
+    out = torch.full((batch, M * N), float("nan"), device="cuda")
+    launch(op, [_t(A), _t(B)], out, [M, N, K], fparam=(0.125, 1e-5), math=math, batch=batch, epilogue=1)
+    y = out.cpu().numpy()
+    assert np.isfinite(y).all()
+    assert np.allclose(y.reshape(-1, N).sum(axis=1), 1.0, atol=1e-5)
+    tol = TOL_TF32X3 if math == "tf32x3" else 5e-3
+    for b in range(batch):
+        assert normwise(y[b], ref[b]) <= tol, b
+
+
+def test_softmax_epilogue_rejects_wide_rows():
+    from paper_2009_07482_b200._native import HetsimError
+    from tests.gpu_util import launch
+    import torch
+    A = torch.zeros(1, 128 * 64, device="cuda")
+    B = torch.zeros(1, 256 * 64, device="cuda")
+    out = torch.empty(1, 128 * 256, device="cuda")
+    with pytest.raises(HetsimError):
+        launch("gemm_nt", [A, B], out, [128, 256, 64], epilogue=1)
+
+
 @pytest.mark.parametrize("R,C,batch", [(128, 64, 3), (64, 128, 1), (37, 45, 2)])
 def test_transpose_bit_exact(R, C, batch, oracle_mod):
     from tests.gpu_util import launch
