@@ -304,6 +304,93 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// A converter step: this thread's row of a 128 x 32 fp32 staging tile (K-major,
+// SWIZZLE_128B) -> hi/lo split written to the TMEM A stage at `ta` (its lane
+// quarter): tf32 hi -> columns [0,32), lo -> [32,64); bf16 hi/lo packed in
+// pairs (lower k in the low half) -> [0,16) and [16,32).
+template <int kTerms, bool kBf16>
+__device__ __forceinline__ void split_a_to_tmem(uint32_t sa, uint32_t ta, int row) {
+  if constexpr (kBf16) {
+    // 32 fp32 of this row -> bf16 hi/lo, packed in pairs (lower k in the low half):
+    // hi -> columns [0,16), lo -> [16,32) of the stage.
+    uint32_t hi[16], lo[16];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      float4 x = lds128(sa + sw128(row, c));
+      const uint32_t h01 = pack_bf16x2(x.x, x.y), h23 = pack_bf16x2(x.z, x.w);
+      hi[2 * c] = h01;
+      hi[2 * c + 1] = h23;
+      lo[2 * c] = pack_bf16x2(x.x - __uint_as_float(h01 << 16), x.y - __uint_as_float(h01 & 0xFFFF0000u));
+      lo[2 * c + 1] = pack_bf16x2(x.z - __uint_as_float(h23 << 16), x.w - __uint_as_float(h23 & 0xFFFF0000u));
+    }
+    if (!HS_DBG_NOCONV) {
+      tmem_st16(ta, hi);
+      tmem_st16(ta + 16u, lo);
+    }
+  } else
+#pragma unroll
+  for (int hh = 0; hh < (HS_DBG_NOCONV ? 0 : 2); ++hh) {
+    uint32_t hi[16], lo[16];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      float4 x = lds128(sa + sw128(row, 4 * hh + c));
+      const float xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float hv = tf32_rna(xs[e]);
+        hi[4 * c + e] = __float_as_uint(hv);
+        lo[4 * c + e] = __float_as_uint(xs[e] - hv);
+      }
+    }
+    tmem_st16(ta + uint32_t(16 * hh), hi);
+    if constexpr (kTerms > 1) tmem_st16(ta + 32u + uint32_t(16 * hh), lo);
+  }
+}
+
+// Epilogue store of one 32-column chunk: v = this thread's row values for
+// columns [c0, c0+32) of the tile; transposed through the warp's padded smem
+// tile so each group of 8 lanes writes one full 128-byte row (coalesced).
+// Rows >= M (or the whole chunk when !rows_valid) are not stored.
+__device__ __forceinline__ void epi_store_chunk(const TileParams& p, uint32_t tile, const float (&v)[32], int lane,
+                                                int q, int m0, int inst, int c0, bool rows_valid) {
+#pragma unroll
+  for (int j = 0; j < 32; ++j) sts32(tile + uint32_t(lane * 33 + j) * 4u, v[j]);
+  __syncwarp();
+  // destination of this 32-column chunk: the single C, or member m's C;
+  // `ncols` valid columns, rows `ld` elements apart
+  int ncols = p.N;
+  float* cbase;
+  if (p.n_out > 0) {
+    const int m = c0 / p.Nm;
+    c0 -= m * p.Nm;
+    ncols = p.Nm;
+    cbase = p.Cs[m] + int64_t(inst) * p.sCs[m];
+  } else {
+    cbase = p.C + int64_t(inst) * p.sC;
+  }
+  const int64_t ld = p.ldc ? p.ldc : ncols;
+  const int cq = (lane & 7) * 4, rsub = lane >> 3;
+  const bool vec = c0 + 32 <= ncols && (ld & 3) == 0;
+#pragma unroll
+  for (int pass = 0; pass < 8; ++pass) {
+    const int rr = pass * 4 + rsub;
+    const int grow = m0 + q * 32 + rr;
+    const uint32_t src = tile + uint32_t(rr * 33 + cq) * 4u;
+    const float4 x = make_float4(lds32(src), lds32(src + 4), lds32(src + 8), lds32(src + 12));
+    if (rows_valid && grow < p.M && !HS_DBG_NOEPI) {
+      float* dst = cbase + int64_t(grow) * ld + c0 + cq;
+      if (vec) {
+        *reinterpret_cast<float4*>(dst) = x;
+      } else {
+        const float e[4] = {x.x, x.y, x.z, x.w};
+        for (int i = 0; i < 4; ++i)
+          if (c0 + cq + i < ncols) dst[i] = e[i];
+      }
+    }
+  }
+  __syncwarp();  // the next chunk reuses the tile
+}
+
 template <int BN, int kBSrc, int kTerms, bool kSmall, bool kBf16>
 __global__ void __launch_bounds__(kThreads, kSmall ? 2 : 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TileParams p) {
@@ -511,51 +598,14 @@ __global__ void __launch_bounds__(kThreads, kSmall ? 2 : 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(acc_empty(int(acc)));
         }
-        // Transpose the 32x32 chunk through this warp's padded smem tile: TMEM
-        // hands each thread one row, so storing straight from registers would
-        // make every store instruction touch 32 rows. After the transpose each
-        // group of 8 lanes writes one full 128-byte row (coalesced).
-        const uint32_t tile = scratch + uint32_t(q) * uint32_t(kEpiTileBytes);
+        float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
-          float v = __uint_as_float(r[j]);
-          if (p.softmax) v = ex2_approx(fmaf(v, sl, -ml)) * ssum;
-          sts32(tile + uint32_t(lane * 33 + j) * 4u, p.relu ? fmaxf(v, 0.f) : v);
+          float x = __uint_as_float(r[j]);
+          if (p.softmax) x = ex2_approx(fmaf(x, sl, -ml)) * ssum;
+          v[j] = p.relu ? fmaxf(x, 0.f) : x;
         }
-        __syncwarp();
-        // destination of this 32-column chunk: the single C, or member m's C;
-        // `ncols` valid columns, rows `ld` elements apart
-        int c0 = n0 + cb * 32, ncols = p.N;
-        float* cbase;
-        if (p.n_out > 0) {
-          const int m = c0 / p.Nm;
-          c0 -= m * p.Nm;
-          ncols = p.Nm;
-          cbase = p.Cs[m] + int64_t(inst) * p.sCs[m];
-        } else {
-          cbase = p.C + int64_t(inst) * p.sC;
-        }
-        const int64_t ld = p.ldc ? p.ldc : ncols;
-        const int cq = (lane & 7) * 4, rsub = lane >> 3;
-        const bool vec = c0 + 32 <= ncols && (ld & 3) == 0;
-#pragma unroll
-        for (int pass = 0; pass < 8; ++pass) {
-          const int rr = pass * 4 + rsub;
-          const int grow = m0 + q * 32 + rr;
-          const uint32_t src = tile + uint32_t(rr * 33 + cq) * 4u;
-          const float4 v = make_float4(lds32(src), lds32(src + 4), lds32(src + 8), lds32(src + 12));
-          if (grow < p.M && !HS_DBG_NOEPI) {
-            float* dst = cbase + int64_t(grow) * ld + c0 + cq;
-            if (vec) {
-              *reinterpret_cast<float4*>(dst) = v;
-            } else {
-              const float e[4] = {v.x, v.y, v.z, v.w};
-              for (int i = 0; i < 4; ++i)
-                if (c0 + cq + i < ncols) dst[i] = e[i];
-            }
-          }
-        }
-        __syncwarp();  // the next chunk reuses the tile
+        epi_store_chunk(p, scratch + uint32_t(q) * uint32_t(kEpiTileBytes), v, lane, q, m0, inst, n0 + cb * 32, true);
       }
     }
   } else if (warp >= 8) {
@@ -578,41 +628,7 @@ __global__ void __launch_bounds__(kThreads, kSmall ? 2 : 1)
         tc_fence_after();
         const uint32_t sa = staging + uint32_t(s) * L::kStaging, sb = sa + L::kStageA;
         const uint32_t ta = tmem_a + (uint32_t(q * 32) << 16) + uint32_t(o) * uint32_t(L::kAStage);
-        if constexpr (kBf16) {
-          // 32 fp32 of this row -> bf16 hi/lo, packed in pairs (lower k in the low half):
-          // hi -> columns [0,16), lo -> [16,32) of the stage.
-          uint32_t hi[16], lo[16];
-#pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            float4 x = lds128(sa + sw128(row, c));
-            const uint32_t h01 = pack_bf16x2(x.x, x.y), h23 = pack_bf16x2(x.z, x.w);
-            hi[2 * c] = h01;
-            hi[2 * c + 1] = h23;
-            lo[2 * c] = pack_bf16x2(x.x - __uint_as_float(h01 << 16), x.y - __uint_as_float(h01 & 0xFFFF0000u));
-            lo[2 * c + 1] = pack_bf16x2(x.z - __uint_as_float(h23 << 16), x.w - __uint_as_float(h23 & 0xFFFF0000u));
-          }
-          if (!HS_DBG_NOCONV) {
-            tmem_st16(ta, hi);
-            tmem_st16(ta + 16u, lo);
-          }
-        } else
-#pragma unroll
-        for (int hh = 0; hh < (HS_DBG_NOCONV ? 0 : 2); ++hh) {
-          uint32_t hi[16], lo[16];
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            float4 x = lds128(sa + sw128(row, 4 * hh + c));
-            const float xs[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float hv = tf32_rna(xs[e]);
-              hi[4 * c + e] = __float_as_uint(hv);
-              lo[4 * c + e] = __float_as_uint(xs[e] - hv);
-            }
-          }
-          tmem_st16(ta + uint32_t(16 * hh), hi);
-          if constexpr (kTerms > 1) tmem_st16(ta + 32u + uint32_t(16 * hh), lo);
-        }
+        split_a_to_tmem<kTerms, kBf16>(sa, ta, row);
         const uint32_t b_hi = operand + uint32_t(o) * L::kOperand;
         const uint32_t b_lo = b_hi + L::kPlaneB;
         if constexpr (kBSrc == 0) {  // [N,K] staging (SW128) -> same offsets
@@ -649,6 +665,390 @@ __global__ void __launch_bounds__(kThreads, kSmall ? 2 : 1)
   if (warp == 2) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(L::kTmemCols));
+  }
+}
+
+// ============================================================ CTA-pair kernel
+// cta_group::2 variant for resident (pre-split) B: a cluster of two CTAs on
+// one TPC computes a 256 x BN tile with M = 256 tcgen05.mma instructions
+// issued by the leader (rank 0). Each CTA brings its own 128 rows of A (its
+// "row block": one (instance, m-tile), so a pair covers two instances of the
+// batch) as a hi/lo split in its own TMEM, and BN/2 of the B columns in its
+// own shared memory; each CTA's TMEM receives its 128 rows x BN columns.
+// Why: N = 256 per instruction amortises the TMEM A-operand read (64 B/cycle)
+// over twice the columns of the single-CTA N = 128 tile, and splitting B
+// across the pair halves the per-SM shared-memory traffic for B (TMA write +
+// three MMA reads per K-block), which is what bounds a single CTA at N = 256.
+//
+// Synchronisation (all mbarriers live in each CTA's smem; "leader's X" is
+// reached through mapa + mbarrier.arrive.release.cluster):
+//   st_full/st_empty   local: A TMA <-> converters (as the 1-CTA kernel)
+//   op_full[o]         leader's only: both CTAs' converter warps arrive after
+//                      their A stage is in TMEM; the leader's B producer posts
+//                      expect_tx for both B halves; both halves' TMA (with
+//                      .cta_group::2) complete_tx on it.
+//   op_empty[o]        each CTA: tcgen05.commit multicast (mask 0b11)
+//   acc_full[a]        each CTA: commit multicast at the end of a tile
+//   acc_empty[a]       leader's only: both CTAs' epilogue warps arrive.
+#ifndef HS_PAIR_NO_CAP
+#define HS_PAIR_NO_CAP 4
+#endif
+#ifndef HS_PAIR_GEMM
+#define HS_PAIR_GEMM 1
+#endif
+#ifndef HS_PAIR_BN  // pair tile width for N >= 256
+#define HS_PAIR_BN 256
+#endif
+#ifndef HS_PAIR_MIN_ASTAGES  // double-buffer the accumulator if this many A stages still fit
+#define HS_PAIR_MIN_ASTAGES 4
+#endif
+
+template <int BN, bool kBf16>
+struct CfgPair {
+  static_assert(BN % 32 == 0 && BN <= 256, "pair tile N");
+  static constexpr int kTmemCols = 512;
+  static constexpr int kStaging = BM * BK * 4;                  // 16 KB fp32 A tile
+  static constexpr int kHalfN = BN / 2;                          // B rows held by each CTA
+  static constexpr int kPlaneB = kHalfN * (kBf16 ? 64 : 128);   // one SW128 tf32 / SW64 bf16 half plane
+  static constexpr int kOperand = 2 * kPlaneB;
+  static constexpr int kAStage = kBf16 ? 32 : 64;
+  static constexpr int kAccBufs = (2 * BN + HS_PAIR_MIN_ASTAGES * kAStage <= kTmemCols) ? 2 : 1;
+  static constexpr int kAccCols = kAccBufs * BN;
+  static constexpr int kBudget = HS_SMEM_BUDGET_KB * 1024;
+  static constexpr int kNOtm = (kTmemCols - kAccCols) / kAStage;
+  static constexpr int kNOsm = (kBudget - 2 * kStaging) / kOperand;
+  static constexpr int kNOmin = kNOtm < kNOsm ? kNOtm : kNOsm;
+  static constexpr int kNOcap = kNOmin < HS_PAIR_NO_CAP ? kNOmin : HS_PAIR_NO_CAP;
+  static constexpr int kNO = kNOcap - kNOcap % kConvGroups;
+  static constexpr int kNSraw = (kBudget - kNO * kOperand) / kStaging;
+  static constexpr int kNScap = kNSraw > 8 ? 8 : kNSraw;
+  static constexpr int kNS = kNScap - kNScap % kConvGroups;
+  static_assert(kAccCols + kNO * kAStage <= kTmemCols, "TMEM budget exceeded");
+  static_assert(kNS >= 2 && kNO >= 2, "pipeline too shallow");
+  // epilogue: per warp two 32 x 32 fp32 SW128 staging tiles for TMA stores
+  static constexpr int kEpiStage = 32 * 32 * 4;
+  static constexpr int kTotal = kNS * kStaging + kNO * kOperand + 1024 + kEpiWarps * 2 * kEpiStage + 1024;
+  static_assert(kTotal <= 227 * 1024, "shared memory budget exceeded");
+};
+
+// Output tensor maps for TMA stores: one per output (member) matrix.
+struct CMaps {
+  CUtensorMap m[4];
+};
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_id_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t nclusters_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cta address of this CTA -> shared::cluster address of the same object in CTA `rank`
+__device__ __forceinline__ uint32_t mapa_rank(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// TMA into this CTA's smem, completing bytes on an mbarrier that may be in the peer CTA.
+__device__ __forceinline__ void tma_load_3d_pair(uint32_t dst, const CUtensorMap* map, uint32_t cluster_bar, int c0,
+                                                 int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
+      "%5}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(cluster_bar), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void mma_pair_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc,
+                                                 uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], %2, %3, {%5, %5, %5, %5, %5, %5, %5, %5}, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(b), "r"(idesc), "r"(acc), "r"(0u)
+      : "memory");
+}
+__device__ __forceinline__ void mma_pair_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc,
+                                                uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, {%5, %5, %5, %5, %5, %5, %5, %5}, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(b), "r"(idesc), "r"(acc), "r"(0u)
+      : "memory");
+}
+// TMA store of one 32 x 32 fp32 box from shared memory (bulk-group completion).
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, uint32_t src, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(src), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void mma_commit_pair(uint32_t bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+      "h"(uint16_t(3))
+      : "memory");
+}
+
+template <int BN, int kTerms, bool kBf16>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const __grid_constant__ CMaps tmC, TileParams p) {
+  using L = CfgPair<BN, kBf16>;
+  constexpr int NS = L::kNS, NO = L::kNO;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  const uint32_t staging = base;
+  const uint32_t operand = staging + NS * L::kStaging;
+  const uint32_t bars = operand + NO * L::kOperand;
+  auto st_full = [&](int s) { return bars + 8u * uint32_t(s); };
+  auto st_empty = [&](int s) { return bars + 8u * uint32_t(NS + s); };
+  auto op_full = [&](int s) { return bars + 8u * uint32_t(2 * NS + s); };
+  auto op_empty = [&](int s) { return bars + 8u * uint32_t(2 * NS + NO + s); };
+  auto acc_full = [&](int a) { return bars + 8u * uint32_t(2 * NS + 2 * NO + a); };
+  auto acc_empty = [&](int a) { return bars + 8u * uint32_t(2 * NS + 2 * NO + 2 + a); };
+  const uint32_t tmem_slot = bars + 8u * uint32_t(2 * NS + 2 * NO + 4);
+  const uint32_t scratch = bars + 1024u;
+  const uint32_t* tmem_slot_ptr = reinterpret_cast<const uint32_t*>(smem_raw + (tmem_slot - smem_u32(smem_raw)));
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nk = (p.K + BK - 1) / BK;
+  const uint32_t rank = cluster_ctarank();
+  const int pair0 = int(cluster_id_x()), npairs = int(nclusters_x());
+  const int total_rb = p.batch * p.m_tiles;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(st_full(s), 1);
+      mbar_init(st_empty(s), kGroupWarps);
+    }
+    for (int s = 0; s < NO; ++s) {
+      mbar_init(op_full(s), 2 * kGroupWarps + 1);
+      mbar_init(op_empty(s), 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(acc_full(a), 1);
+      mbar_init(acc_empty(a), 2 * kEpiWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tmem_slot),
+                 "r"(L::kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync_all();  // barriers initialised and TMEM allocated in both CTAs
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot_ptr;
+  const uint32_t tmem_a = tmem + uint32_t(L::kAccCols);
+
+  // pair tile t -> (n0, this CTA's row block rb = (instance, m-tile)); n fastest,
+  // so the pairs running at once share A row blocks through L2.
+  auto decode = [&](int t, int& n0, int& inst, int& m0, bool& valid) {
+    const int nt = t % p.n_tiles, rp = t / p.n_tiles;
+    const int rb = 2 * rp + int(rank);
+    valid = rb < total_rb;
+    inst = rb / p.m_tiles;
+    m0 = (rb % p.m_tiles) * BM;
+    n0 = nt * BN;
+  };
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ A producer (local)
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (int t = pair0; t < p.total_tiles; t += npairs) {
+        int n0, inst, m0;
+        bool valid;
+        decode(t, n0, inst, m0, valid);
+        const int ia = p.a_batched ? inst : 0;  // inst >= batch (odd tail) -> zero-filled box
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = int(it % NS);
+          mbar_wait(st_empty(s), ((it / NS) & 1u) ^ 1u);
+          const uint32_t sa = staging + uint32_t(s) * L::kStaging;
+#if HS_DBG_NOTMA
+          mbar_arrive(st_full(s));
+          (void)sa; (void)ia; (void)m0;
+#else
+          mbar_expect_tx(st_full(s), L::kStaging);
+          tma_load_3d(sa, &tmA, st_full(s), kb * BK, m0, ia);
+#endif
+        }
+      }
+    }
+  } else if (warp == 3) {
+    // ------------------------------------------------------------ B producer: this CTA's half
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (int t = pair0; t < p.total_tiles; t += npairs) {
+        int n0, inst, m0;
+        bool valid;
+        decode(t, n0, inst, m0, valid);
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int o = int(it % NO);
+          mbar_wait(op_empty(o), ((it / NO) & 1u) ^ 1u);
+          const uint32_t b_hi = operand + uint32_t(o) * L::kOperand;
+          const uint32_t full = mapa_rank(op_full(o), 0);
+#if HS_DBG_NOTMA
+          if (rank == 0) mbar_arrive(op_full(o));
+          (void)b_hi; (void)full;
+#else
+          if (rank == 0) mbar_expect_tx(op_full(o), 2 * (kTerms > 1 ? 2 : 1) * L::kPlaneB);
+          const int nrow = n0 + int(rank) * L::kHalfN;
+          tma_load_3d_pair(b_hi, &tmB, full, kb * BK, nrow, 0);
+          if constexpr (kTerms > 1) tma_load_3d_pair(b_hi + L::kPlaneB, &tmB, full, kb * BK, nrow, 1);
+#endif
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (leader only)
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc = (kBf16 ? instr_desc_bf16(BN) : instr_desc_tf32(BN)) + (uint32_t(BM >> 4) << 24);
+      uint32_t it = 0, lt = 0;
+      for (int t = pair0; t < p.total_tiles; t += npairs, ++lt) {
+        const uint32_t acc = lt % uint32_t(L::kAccBufs);
+        mbar_wait(acc_empty(int(acc)), ((lt / uint32_t(L::kAccBufs)) & 1u) ^ 1u);
+        tc_fence_after();
+        const uint32_t d = tmem + acc * uint32_t(BN);
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int o = int(it % NO);
+          mbar_wait(op_full(o), (it / NO) & 1u);
+          tc_fence_after();
+          const uint32_t a_hi = tmem_a + uint32_t(o) * uint32_t(L::kAStage);
+          const uint32_t a_lo = a_hi + uint32_t(L::kAStage / 2);
+          const uint32_t b_hi = operand + uint32_t(o) * L::kOperand;
+          const uint32_t b_lo = b_hi + L::kPlaneB;
+          if constexpr (kBf16) {
+#pragma unroll
+            for (int kk = 0; kk < BK / 16; ++kk) {
+              const uint32_t kcol = uint32_t(kk) * 8u, koff = uint32_t(kk) * 32u;
+              const uint32_t first = (kb | kk) ? 1u : 0u;
+              mma_pair_f16_ts(d, a_lo + kcol, smem_desc_sw64(b_hi + koff), idesc, first);
+              mma_pair_f16_ts(d, a_hi + kcol, smem_desc_sw64(b_lo + koff), idesc, 1u);
+              mma_pair_f16_ts(d, a_hi + kcol, smem_desc_sw64(b_hi + koff), idesc, 1u);
+            }
+          } else {
+#pragma unroll
+            for (int kk = 0; kk < BK / 8; ++kk) {
+              const uint32_t kcol = uint32_t(kk) * 8u, koff = uint32_t(kk) * 32u;
+              const uint32_t first = (kb | kk) ? 1u : 0u;
+              if constexpr (kTerms > 1) {
+                mma_pair_tf32_ts(d, a_lo + kcol, smem_desc(b_hi + koff), idesc, first);
+                mma_pair_tf32_ts(d, a_hi + kcol, smem_desc(b_lo + koff), idesc, 1u);
+                mma_pair_tf32_ts(d, a_hi + kcol, smem_desc(b_hi + koff), idesc, 1u);
+              } else {
+                mma_pair_tf32_ts(d, a_hi + kcol, smem_desc(b_hi + koff), idesc, first);
+              }
+            }
+          }
+          mma_commit_pair(op_empty(o));
+        }
+        mma_commit_pair(acc_full(int(acc)));
+      }
+    }
+  } else if (warp >= 4 && warp < 4 + kEpiWarps) {
+    // ------------------------------------------------------------ epilogue (this CTA's rows)
+    // TMEM -> registers -> (ReLU) -> SW128 smem staging tile -> TMA store. The
+    // stores run asynchronously, so the accumulator is released as soon as its
+    // last columns are in registers and the warps never wait on global writes.
+    // Rows past M, columns past N and the odd row block of a ragged batch fall
+    // outside the output tensor map and are clipped by the TMA unit.
+    const int q = warp & 3;
+    const uint32_t stage0 = scratch + uint32_t(q) * uint32_t(2 * L::kEpiStage);
+    uint32_t lt = 0, cnt = 0;
+    for (int t = pair0; t < p.total_tiles; t += npairs, ++lt) {
+      int n0, inst, m0;
+      bool valid;
+      decode(t, n0, inst, m0, valid);
+      const uint32_t acc = lt % uint32_t(L::kAccBufs);
+      mbar_wait(acc_full(int(acc)), (lt / uint32_t(L::kAccBufs)) & 1u);
+      tc_fence_after();
+      const uint32_t tacc = tmem + (uint32_t(q * 32) << 16) + acc * uint32_t(BN);
+#pragma unroll 1
+      for (int cb = 0; cb < BN / 32; ++cb) {
+        uint32_t r[32];
+        tmem_ld32(tacc + uint32_t(cb * 32), r);
+        if (cb == BN / 32 - 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(mapa_rank(acc_empty(int(acc)), 0));
+        }
+        int c0 = n0 + cb * 32;
+        if (c0 >= p.N || !valid) continue;
+        int mi = 0;
+        if (p.n_out > 0) {
+          mi = c0 / p.Nm;
+          c0 -= mi * p.Nm;
+        }
+        const uint32_t buf = stage0 + (cnt & 1u) * uint32_t(L::kEpiStage);
+        if (cnt >= 2) {
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          __syncwarp();
+        }
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          float4 x = make_float4(__uint_as_float(r[4 * c]), __uint_as_float(r[4 * c + 1]),
+                                 __uint_as_float(r[4 * c + 2]), __uint_as_float(r[4 * c + 3]));
+          if (p.relu) x = make_float4(fmaxf(x.x, 0.f), fmaxf(x.y, 0.f), fmaxf(x.z, 0.f), fmaxf(x.w, 0.f));
+          sts128(buf + uint32_t(lane) * 128u + (uint32_t(c ^ (lane & 7)) << 4), x);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0 && !HS_DBG_NOEPI) tma_store_3d(&tmC.m[mi], buf, c0, m0 + q * 32, inst);
+        ++cnt;
+      }
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  } else if (warp >= 8) {
+    // ------------------------------------------------------------ converters (this CTA's A rows)
+    const int g = (warp - 8) / kGroupWarps;
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    uint32_t it = 0;
+    for (int tile = pair0; tile < p.total_tiles; tile += npairs) {
+      for (int kb = 0; kb < nk; ++kb, ++it) {
+        if (int(it % kConvGroups) != g) continue;
+        const int s = int(it % NS), o = int(it % NO);
+        mbar_wait(st_full(s), (it / NS) & 1u);
+        mbar_wait(op_empty(o), ((it / NO) & 1u) ^ 1u);
+        tc_fence_after();
+        const uint32_t sa = staging + uint32_t(s) * L::kStaging;
+        const uint32_t ta = tmem_a + (uint32_t(q * 32) << 16) + uint32_t(o) * uint32_t(L::kAStage);
+        split_a_to_tmem<kTerms, kBf16>(sa, ta, row);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(st_empty(s));
+          mbar_arrive_cluster(mapa_rank(op_full(o), 0));
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();  // both CTAs done with TMEM, smem barriers and remote arrivals
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(L::kTmemCols));
   }
 }
 
@@ -806,6 +1206,95 @@ cudaError_t launch(const GemmArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// CTA-pair launch (resident B planes): clusters of 2, one pair per TPC,
+// persistent over the 256 x BN pair tiles.
+template <int BN, int kTerms, bool kBf16>
+cudaError_t launch_pair(const GemmArgs& a, cudaStream_t s) {
+  using L = CfgPair<BN, kBf16>;
+  auto kernel = gemm_pair_kernel<BN, kTerms, kBf16>;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  static int max_pairs = 0;
+  std::call_once(once, [&] {
+    attr_err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal);
+    if (attr_err != cudaSuccess) return;
+    cudaLaunchConfig_t q{};
+    q.gridDim = dim3(2 * (num_sms() / 2));
+    q.blockDim = dim3(kThreads);
+    q.dynamicSmemBytes = L::kTotal;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    q.attrs = at;
+    q.numAttrs = 1;
+    int n = 0;
+    attr_err = cudaOccupancyMaxActiveClusters(&n, kernel, &q);
+    max_pairs = n > 0 ? n : num_sms() / 2;
+  });
+  if (attr_err != cudaSuccess) return attr_err;
+  const uint64_t M = uint64_t(a.M), N = uint64_t(a.N), K = uint64_t(a.K);
+  const uint64_t nA = a.sA ? uint64_t(a.batch) : 1;
+  const uint64_t sA = (a.sA ? uint64_t(a.sA) : M * K) * 4;
+  CUtensorMap mA, mB;
+  if (!make_map(&mA, a.A, K, M, nA, K * 4, sA, BK, BM, true)) return cudaErrorInvalidValue;
+  const uint64_t eb = kBf16 ? 2 : 4;
+  if (!make_map(&mB, a.Bplanes, K, N, 2, K * eb, N * K * eb, BK, BN / 2, true, kBf16)) return cudaErrorInvalidValue;
+  TileParams p{};
+  p.C = a.C;
+  p.sC = a.sC;
+  p.M = a.M;
+  p.N = a.N;
+  p.K = a.K;
+  p.batch = a.batch;
+  p.a_batched = a.sA != 0;
+  p.b_batched = 0;
+  p.relu = a.relu ? 1 : 0;
+  p.m_tiles = (a.M + BM - 1) / BM;
+  p.n_tiles = (a.N + BN - 1) / BN;
+  p.n_out = a.n_out > 1 ? a.n_out : 0;
+  p.Nm = p.n_out ? a.N / a.n_out : a.N;
+  for (int i = 0; i < p.n_out; ++i) {
+    p.Cs[i] = a.Cs[i];
+    p.sCs[i] = a.sCs[i];
+  }
+  p.ldc = a.ldc;
+  // output maps: {columns, rows, instances}, 32 x 32 boxes, SW128 (matches the staging layout)
+  CMaps mc{};
+  const int nmaps = p.n_out ? p.n_out : 1;
+  for (int i = 0; i < nmaps; ++i) {
+    float* c = p.n_out ? a.Cs[i] : a.C;
+    const uint64_t sc = uint64_t(p.n_out ? a.sCs[i] : a.sC);
+    const uint64_t ncols = uint64_t(p.Nm);
+    const uint64_t ld = a.ldc ? uint64_t(a.ldc) : ncols;
+    if (!make_map(&mc.m[i], c, ncols, M, uint64_t(a.batch), ld * 4, (sc ? sc : ld * M) * 4, 32, 32, true))
+      return cudaErrorInvalidValue;
+  }
+  const int row_pairs = (a.batch * p.m_tiles + 1) / 2;
+  p.total_tiles = p.n_tiles * row_pairs;
+  const int pairs = p.total_tiles < max_pairs ? p.total_tiles : max_pairs;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2 * pairs);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = L::kTotal;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, mA, mB, mc, p);
+}
+
+template <int BN>
+cudaError_t launch_pair_bn(const GemmArgs& a, int terms, cudaStream_t s) {
+  if (a.bf16) return launch_pair<BN, 3, true>(a, s);
+  return terms > 1 ? launch_pair<BN, 3, false>(a, s) : launch_pair<BN, 1, false>(a, s);
+}
+
 template <int BN, bool kSmall = false>
 cudaError_t launch_bn(const GemmArgs& a, int terms, cudaStream_t s) {
   if (a.Bplanes && a.bf16) return launch<BN, 2, 3, kSmall, true>(a, s);
@@ -828,6 +1317,22 @@ bool gemm_tcgen05_supported(const GemmArgs& a) {
 }
 
 cudaError_t gemm_tcgen05(const GemmArgs& a, int terms, cudaStream_t s) {
+  // Resident-weight GEMMs with wide N and at least two row blocks run on CTA
+  // pairs (M = 256 tcgen05.mma over two instances / m-tiles).
+  const int row_blocks = a.batch * ((a.M + BM - 1) / BM);
+  bool store_ok = true;  // TMA stores: 16-byte aligned bases, row and instance strides
+  const int nm = a.n_out > 1 ? a.n_out : 1;
+  for (int i = 0; i < nm; ++i) {
+    const void* c = a.n_out > 1 ? a.Cs[i] : a.C;
+    const int64_t sc = a.n_out > 1 ? a.sCs[i] : a.sC;
+    const int64_t ld = a.ldc ? a.ldc : (a.n_out > 1 ? a.N / a.n_out : a.N);
+    if ((reinterpret_cast<uintptr_t>(c) & 15u) || (ld & 3) || (sc & 3) || (a.batch > 1 && sc == 0)) store_ok = false;
+  }
+  if (HS_PAIR_GEMM && store_ok && a.Bplanes && !a.softmax && row_blocks >= 2 &&
+      !(a.n_out > 1 && a.N / a.n_out % 32)) {
+    if (a.N == 192) return launch_pair_bn<192>(a, terms, s);
+    if (a.N >= 256 && a.n_out <= 1) return launch_pair_bn<HS_PAIR_BN>(a, terms, s);
+  }
   if (a.n_out > 1) {
     // grouped launch: one tile covers every member (a.N = total columns)
     if (!a.Bplanes || a.N % a.n_out || (a.N / a.n_out) % 32 || a.n_out > 4) return cudaErrorInvalidValue;

@@ -26,6 +26,7 @@ def run(M, N, K, batch, op="gemm", math="tf32x3", presplit=True, shared=True, re
     if presplit and shared:
         planes = torch.empty(2 * N * K, device="cuda")
         _native.check(L.hs_gemm_split_weights(st, B.data_ptr(), int(op == "gemm_nt"), N, K, planes.data_ptr()))
+    torch.cuda.synchronize()
     a = _native.OpArgs()
     a.n_in = 2
     a.in_[0], a.in_[1] = A.data_ptr(), B.data_ptr()
@@ -61,6 +62,7 @@ def run_grouped(M, N, K, batch, members=3, reps=20):
         _native.check(L.hs_gemm_split_weights_strided(st, B.data_ptr(), 0, N, K, planes.data_ptr() + 4 * m * N * K,
                                                       members * N * K))
     Cs = [torch.empty(batch, M * N, device="cuda") for _ in range(members)]
+    torch.cuda.synchronize()
     a = _native.OpArgs()
     a.n_in = 2
     a.in_[0], a.in_[1] = A.data_ptr(), Bs[0].data_ptr()

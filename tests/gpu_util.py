@@ -32,6 +32,7 @@ def split_weights(B, transposed, N, K, bf16=False):
     """Pre-split a shared GEMM B into K-major hi/lo planes (tf32, or bf16 for math bf16x3)."""
     import torch
     planes = torch.empty(2 * N * K, device="cuda")  # fp32-sized: bf16 planes use half of it
+    torch.cuda.synchronize()  # B was produced on torch's stream
     L = _native.lib()
     _native.check(L.hs_gemm_split_weights_ex(stream(), B.data_ptr(), int(transposed), N, K, planes.data_ptr(), N * K,
                                              int(bf16)))
@@ -43,6 +44,10 @@ def launch(op, inputs, out, dims, fparam=(1.0, 1e-5), math="tf32x3", batch=1, st
            aux=None, out_ld=0, epilogue=0, out_offset=0):
     """inputs/out: torch CUDA float32 tensors shaped [batch, elems] or [elems] (shared).
     out_offset (elements) / out_ld / epilogue: GEMM output placement and epilogue."""
+    import torch
+    # Our stream is non-blocking: it does not order after torch's stream, so the
+    # tensors torch just filled/copied must be complete before we launch.
+    torch.cuda.synchronize()
     L = _native.lib()
     a = _native.OpArgs()
     a.out_ld = out_ld

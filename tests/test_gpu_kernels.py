@@ -61,8 +61,14 @@ def test_gemm_parity(M, N, K, op, batch, shared, math, oracle_mod):
         assert err <= (TOL_TF32X3 if math == "tf32x3" else 1e-5), (b, err)
 
 
+PAIR_CASES = [  # CTA-pair path (resident B, N >= 192, >= 2 row blocks): odd row-block tails, m-tiles, ragged N
+    (128, 2048, 512, "gemm_relu", 3, True), (200, 256, 96, "gemm", 3, True), (130, 512, 64, "gemm", 1, True),
+    (128, 300, 64, "gemm_nt", 2, True), (128, 192, 512, "gemm", 5, True)]
+
+
 @pytest.mark.parametrize("M,N,K,op,batch,shared", [c for c in GEMM_CASES if c[5]] + [(128, 128, 64, "gemm_nt", 3, True),
-                                                                              (72, 100, 36, "gemm", 2, True)])
+                                                                              (72, 100, 36, "gemm", 2, True)]
+                         + PAIR_CASES)
 @pytest.mark.parametrize("math", ["tf32x3", "tf32", "bf16x3"])
 def test_gemm_presplit_weights(M, N, K, op, batch, shared, math, oracle_mod):
     """Resident-weight path: B pre-split once into K-major tf32 (or bf16) planes, fed by TMA."""
