@@ -102,7 +102,8 @@ typedef enum {
   HS_OP_ADD = 6,       /* C = A + B                               */
   HS_OP_ADD_LN = 7,    /* Y = LayerNorm(A + B) * gamma + beta     */
   HS_OP_CONCAT = 8,    /* Y[:, i*c:(i+1)*c] = Z_i                 */
-  HS_OP_COUNT = 9
+  HS_OP_ATTN_HEAD = 9, /* Z = softmax(s Q K^T) V W  (fused head)  */
+  HS_OP_COUNT = 10
 } hs_op;
 
 typedef enum {
@@ -142,6 +143,11 @@ typedef struct {
 
 #define HS_EPI_NONE 0
 #define HS_EPI_SOFTMAX 1
+/* HS_OP_ATTN_HEAD ("attn_head"): in = {Q, K, V, W}, Q/K/V [S, dk] per instance,
+ * W [dk, dw] shared and pre-split (aux, hs_gemm_split_weights_ex format 0);
+ * dims = {S, dk, dw} with S <= 128, dk = dw = 64; fparam[0] = softmax scale;
+ * out = Z [S, dw] (rows out_ld apart, 0 = dw). tcgen05 math (TF32X3 / TF32)
+ * only. The transformer head of PAPER.md:323 as one node. */
 
 int hs_op_from_name(const char* name); /* -1 if unknown */
 int hs_launch(hs_stream_t s, int op, const hs_op_args* args, int math_mode, int batch);

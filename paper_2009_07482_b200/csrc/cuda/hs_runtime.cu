@@ -226,7 +226,8 @@ int hs_memset(hs_stream_t s, void* dst, int value, size_t bytes) {
 
 int hs_op_from_name(const char* name) {
   static const char* kNames[HS_OP_COUNT] = {"gemm",    "gemm_nt", "gemm_relu", "transpose",   "scale",
-                                             "softmax", "add",     "add_layernorm", "concat"};
+                                             "softmax", "add",     "add_layernorm", "concat",
+                                             "attn_head"};
   if (!name) return -1;
   for (int i = 0; i < HS_OP_COUNT; ++i)
     if (std::strcmp(name, kNames[i]) == 0) return i;
@@ -311,6 +312,16 @@ int hs_launch(hs_stream_t st, int op, const hs_op_args* a, int math, int batch) 
       const float* z[HS_MAX_INPUTS];
       for (int i = 0; i < a->n_in; ++i) z[i] = in(i);
       e = hs::concat(z, a->in_stride, a->n_in, out, a->out_stride, int(a->dims[0]), int(a->dims[1]), batch, s);
+      break;
+    }
+    case HS_OP_ATTN_HEAD: {
+      if (a->n_in < 4 || !a->aux) return invalid("attn_head needs {Q, K, V, W} and pre-split W planes (aux)");
+      if (math == HS_MATH_FP32_SIMT) return invalid("attn_head runs on the tensor cores only");
+      hs::AttnArgs t{in(0), a->in_stride[0], in(1), a->in_stride[1], in(2), a->in_stride[2], a->aux,
+                     out,   a->out_stride,   a->out_ld, int(a->dims[0]), int(a->dims[1]), int(a->dims[2]),
+                     batch, a->fparam[0]};
+      if (!hs::attn_head_supported(t)) return invalid("attn_head: needs S <= 128, dk = dw = 64, 16-byte alignment");
+      e = hs::attn_head(t, math == HS_MATH_TF32 ? 1 : 3, s);
       break;
     }
     default:

@@ -48,6 +48,27 @@ cudaError_t gemm_simt(const GemmArgs& a, cudaStream_t s);
 // true when the tcgen05 path supports this shape/alignment
 bool gemm_tcgen05_supported(const GemmArgs& a);
 
+// Fused attention head (HS_OP_ATTN_HEAD): Z = softmax_row(scale · Q Kᵀ) · V · W per
+// instance; Q, K, V are [S, dk] (S <= 128, dk = 64), W is [dk, dw] (dw = 64)
+// pre-split into tf32 hi/lo planes [2][dw][dk] (gemm_split_weights format 0).
+// Z rows are ldz elements apart (0 = dw) so Z can be a column block of a concat.
+struct AttnArgs {
+  const float* Q;
+  int64_t sQ;
+  const float* K;
+  int64_t sK;
+  const float* V;
+  int64_t sV;
+  const void* Wplanes;
+  float* Z;
+  int64_t sZ;
+  int64_t ldz;
+  int S, dk, dw, batch;
+  float scale;
+};
+bool attn_head_supported(const AttnArgs& a);
+cudaError_t attn_head(const AttnArgs& a, int terms, cudaStream_t s);
+
 cudaError_t transpose(const float* A, int64_t sA, float* B, int64_t sB, int R, int C, int batch, cudaStream_t s);
 cudaError_t scale(const float* A, int64_t sA, float* B, int64_t sB, int64_t n, float f, int batch, cudaStream_t s);
 cudaError_t add(const float* A, int64_t sA, const float* B, int64_t sB, float* C, int64_t sC, int64_t n, int batch,

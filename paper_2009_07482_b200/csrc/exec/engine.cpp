@@ -175,6 +175,14 @@ void Engine::build_nodes() {
         for (auto in : nd.inputs) need(elems(in) == v[0] * v[1], "input size != rows*cols_each");
         need(elems(nd.output) == v[0] * v[1] * int64_t(nin), "output size != rows*cols_each*count");
         break;
+      case HS_OP_ATTN_HEAD:
+        need(v.size() >= 3 && nin == 4, "expects (Q, K, V, W, Z, S, dk, dw[, num, den])");
+        for (int i = 0; i < 3; ++i) nd.dims[i] = v[size_t(i)];
+        nd.fparam[0] = v.size() >= 5 && v[4] != 0 ? float(double(v[3]) / double(v[4])) : 1.f;
+        for (size_t i = 0; i < 3; ++i) need(elems(nd.inputs[i]) == v[0] * v[1], "Q/K/V size != S*dk");
+        need(elems(nd.inputs[3]) == v[1] * v[2], "W size != dk*dw");
+        need(elems(nd.output) == v[0] * v[2], "Z size != S*dw");
+        break;
       default: break;
     }
     nodes_[k.id] = nd;
@@ -243,6 +251,24 @@ void Engine::plan_buffers() {
   // (tf32 hi/lo, K-major) so the tensor cores are fed by TMA with no conversion.
   if (cfg_.math != HS_MATH_FP32_SIMT) {
     for (const auto& [kid, nd] : nodes_) {
+      if (nd.op == HS_OP_ATTN_HEAD) {  // spec-level fused head: W must be resident, tf32 planes
+        auto gi = group_of_.find(nd.inputs[3]);
+        if (gi == group_of_.end() || !groups_[size_t(gi->second)].resident)
+          fail(Errc::invalid_param, "attn_head kernel " + std::to_string(kid) + ": W must be bound as shared (resident)");
+        auto it = attn_planes_.find(gi->second);
+        if (it == attn_planes_.end()) {
+          Planes pl;
+          pl.gi = gi->second;
+          pl.n = nd.dims[2];
+          pl.k = nd.dims[1];
+          hs_ok(hs_malloc(ctx_, size_t(2 * pl.n * pl.k * 4), &pl.ptr), "hs_malloc");
+          allocations_.push_back(pl.ptr);
+          device_bytes_ += 2 * pl.n * pl.k * 4;
+          it = attn_planes_.emplace(gi->second, pl).first;
+        }
+        node_planes_[kid] = it->second.ptr;
+        continue;
+      }
       if (nd.op != HS_OP_GEMM && nd.op != HS_OP_GEMM_NT && nd.op != HS_OP_GEMM_RELU) continue;
       auto gi = group_of_.find(nd.inputs[1]);
       if (gi == group_of_.end() || !groups_[size_t(gi->second)].resident) continue;
@@ -304,6 +330,9 @@ void Engine::upload_resident() {
     hs_ok(hs_gemm_split_weights_ex(s, resident_buf_.at(pl.gi), pl.nt ? 1 : 0, pl.n, pl.k, pl.ptr, pl.n * pl.k,
                                    plane_format()),
           "split weights");
+  for (const auto& [gi, pl] : attn_planes_)
+    hs_ok(hs_gemm_split_weights_ex(s, resident_buf_.at(gi), 0, pl.n, pl.k, pl.ptr, pl.n * pl.k, 0),
+          "split attention weights");
   for (const auto& fg : fuse_groups_) {
     const int64_t members = int64_t(fg.kernels.size());
     for (int64_t m = 0; m < members; ++m) {
@@ -652,6 +681,59 @@ void Engine::plan_chain_rewrites() {
     }
     cat.elided = true;
     ++rewrites_["concat_in_place"];
+  }
+  // attention_head: P = gemm_nt(Q, K) with the softmax epilogue (rules above),
+  // C = gemm(P, V), Z = gemm(C, W) with W resident, each intermediate feeding
+  // only the next: one HS_OP_ATTN_HEAD launch computes Z (keeping any concat
+  // placement of Z); the first two GEMMs are elided.
+  for (auto& [kid, z] : nodes_) {
+    if (z.op != HS_OP_GEMM || z.elided || z.epilogue || grouped.count(kid) || !resident(z.inputs[1])) continue;
+    auto pc = alias_.find(z.inputs[0]);
+    if (pc == alias_.end()) continue;
+    int ck, cp;
+    if (!sole_consumer(pc->second, &ck, &cp) || ck != kid) continue;
+    const int k2 = pc->second.first;
+    Node& g2 = nodes_.at(k2);
+    if (g2.op != HS_OP_GEMM || g2.elided || g2.epilogue || g2.out_ld || grouped.count(k2) || g2.output != pc->second)
+      continue;
+    if (resident(g2.inputs[1])) continue;  // V is an activation
+    auto pp = alias_.find(g2.inputs[0]);
+    if (pp == alias_.end() || !sole_consumer(pp->second, &ck, &cp) || ck != k2) continue;
+    // P is the softmax node's output, written by the GEMM that absorbed it
+    int k1 = -1;
+    for (const auto& [id, nd] : nodes_)
+      if (!nd.elided && nd.op == HS_OP_GEMM_NT && nd.epilogue == HS_EPI_SOFTMAX && nd.output == pp->second) k1 = id;
+    if (k1 < 0 || grouped.count(k1)) continue;
+    Node& g1 = nodes_.at(k1);
+    const int64_t S = g1.dims[0];
+    if (g1.dims[1] != S || g1.dims[2] != 64 || g1.out_ld || S > 128) continue;
+    if (g2.dims[0] != S || g2.dims[1] != 64 || g2.dims[2] != S) continue;
+    if (z.dims[0] != S || z.dims[1] != 64 || z.dims[2] != 64) continue;
+    const std::pair<int, int> wkey = z.inputs[1];
+    z.op = HS_OP_ATTN_HEAD;
+    z.inputs = {g1.inputs[0], g1.inputs[1], g2.inputs[1], wkey};
+    z.dims[0] = S;
+    z.dims[1] = 64;
+    z.dims[2] = 64;
+    z.fparam[0] = g1.escale;
+    g1.elided = true;
+    g2.elided = true;
+    if (plane_format() != 0) {  // the fused head consumes tf32 planes; BF16X3 keeps bf16 ones for GEMMs
+      const int gi = group_of_.at(wkey);
+      auto it = attn_planes_.find(gi);
+      if (it == attn_planes_.end()) {
+        Planes pl;
+        pl.gi = gi;
+        pl.n = 64;
+        pl.k = 64;
+        hs_ok(hs_malloc(ctx_, size_t(2 * 64 * 64 * 4), &pl.ptr), "hs_malloc");
+        allocations_.push_back(pl.ptr);
+        device_bytes_ += 2 * 64 * 64 * 4;
+        it = attn_planes_.emplace(gi, pl).first;
+      }
+      node_planes_[kid] = it->second.ptr;
+    }
+    ++rewrites_["attention_head"];
   }
   for (const auto& [kid, nd] : nodes_)
     if (nd.elided) --launches_per_batch_;

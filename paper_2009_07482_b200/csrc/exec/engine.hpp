@@ -139,6 +139,7 @@ class Engine {
   };
   std::map<std::pair<int, bool>, Planes> planes_;
   std::map<int, void*> node_planes_;  // kernel -> planes
+  std::map<int, Planes> attn_planes_;  // resident group -> tf32 planes for fused heads (BF16X3 engines)
 
   // Grouped launches (graph mode): sibling GEMM ndranges of one component that
   // share their A input, have resident B and no intra-component producer run as

@@ -109,8 +109,9 @@ def test_grouped_sibling_gemms_match_unfused(oracle_mod):
 @pytest.mark.parametrize("math", ["tf32x3", "bf16x3"])
 def test_chain_rewrites_match_oracle(math, oracle_mod):
     """fuse=2 (default): per head the transpose folds into a gemm_nt, the softmax
-    becomes the QK^T GEMM's epilogue and the 8 Z_h GEMMs write the concat in
-    place: 2 x 17 launches fewer per layer pair, same results within tolerance."""
+    becomes the QK^T GEMM's epilogue, the 8 Z_h GEMMs write the concat in place
+    and each head's QK^T -> P·V -> C·W_h chain runs as one fused attn_head launch:
+    33 launches fewer per layer, same results within tolerance."""
     text, params, meta = workloads.encoder(layers=2)
     n = 3
     arrays = _encoder_arrays(meta, params, n)
@@ -118,9 +119,10 @@ def test_chain_rewrites_match_oracle(math, oracle_mod):
     key = (meta["output"]["kernel"], meta["output"]["pos"])
     chained, _, plan = _run_gpu(text, params, arrays, n, mode="graph", batch=2, fuse=2, math=math)
     grouped, _, plan1 = _run_gpu(text, params, arrays, n, mode="graph", batch=2, fuse=1, math=math)
-    assert plan["chain_rewrites"] == {"concat_in_place": 2, "softmax_epilogue": 16, "transpose_into_gemm_nt": 16}
+    assert plan["chain_rewrites"] == {"attention_head": 16, "concat_in_place": 2, "softmax_epilogue": 16,
+                                      "transpose_into_gemm_nt": 16}
     assert plan1["chain_rewrites"] == {}
-    assert plan["launches_per_batch"] == plan1["launches_per_batch"] - 34
+    assert plan["launches_per_batch"] == plan1["launches_per_batch"] - 66
     for i in range(n):
         assert _normwise(chained[key][i], ref[key][i]) <= TOL
         assert _normwise(chained[key][i], grouped[key][i]) <= 1e-5

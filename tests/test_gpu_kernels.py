@@ -231,3 +231,64 @@ def test_concat_bit_exact(count, rows, cols, batch, oracle_mod):
     out = torch.empty((batch, rows * cols * count), device="cuda")
     launch("concat", [_t(z) for z in Z], out, [rows, cols], batch=batch)
     assert np.array_equal(out.cpu().numpy(), ref)
+
+
+def _attn_ref(oracle_mod, Q, K, V, W, S, batch, scale_den=8):
+    dk, dw = 64, 64
+    A = np.empty((batch, S * S), np.float32)
+    oracle_mod.run_node("gemm_nt", [Q, K], [S * dk, S * dk], A, S * S, [S, S, dk], batch)
+    P = np.empty_like(A)
+    oracle_mod.run_node("softmax", [A], [S * S], P, S * S, [S, S, 1, scale_den], batch)
+    C = np.empty((batch, S * dk), np.float32)
+    oracle_mod.run_node("gemm", [P, V], [S * S, S * dk], C, S * dk, [S, dk, S], batch)
+    Z = np.empty((batch, S * dw), np.float32)
+    oracle_mod.run_node("gemm", [C, W], [S * dk, 0], Z, S * dw, [S, dw, dk], batch)
+    return Z
+
+
+@pytest.mark.parametrize("S,batch,math,ld", [(128, 3, "tf32x3", 0), (100, 2, "tf32x3", 0), (128, 5, "tf32", 0),
+                                              (128, 3, "tf32x3", 512), (128, 300, "tf32x3", 0)])
+def test_attn_head_matches_oracle(S, batch, math, ld, oracle_mod):
+    """HS_OP_ATTN_HEAD: Z = softmax(Q Kᵀ/8) V W in one launch, against the oracle's
+    four-node chain (gemm_nt, softmax, gemm, gemm)."""
+    from tests.gpu_util import launch, normwise, split_weights
+    import torch
+    dk = 64
+    Q, K, V = (_rand(60 + i, (batch, S * dk)) for i in range(3))
+    W = (_rand(63, (dk * dk,)) * np.float32(1 / 8)).astype(np.float32)
+    ref = _attn_ref(oracle_mod, Q, K, V, W, S, batch)
+    Wt = _t(W)
+    planes = split_weights(Wt, False, dk, dk)
+    width, off = (ld, 128) if ld else (dk, 0)
+    Y = torch.full((batch, S * width), -3.0, device="cuda")
+    launch("attn_head", [_t(Q), _t(K), _t(V), Wt], Y, [S, dk, dk], fparam=(0.125, 1e-5), math=math, batch=batch,
+           aux=planes, out_ld=ld, out_offset=off)
+    y = Y.cpu().numpy().reshape(batch, S, width)
+    tol = TOL_TF32X3 if math == "tf32x3" else 5e-3
+    for b in range(batch):
+        assert normwise(y[b, :, off:off + dk].reshape(-1), ref[b]) <= tol, b
+    if ld:
+        mask = np.ones(width, bool)
+        mask[off:off + dk] = False
+        assert (y[:, :, mask] == -3.0).all()
+
+
+def test_attn_head_bit_identical_to_unfused_chain():
+    """The fused head keeps every intermediate in TMEM / smem but computes it
+    exactly as the unfused tcgen05 chain does (same splits, same MMA order):
+    Z is bit-identical to gemm_nt+softmax epilogue -> gemm -> gemm (pre-split W)."""
+    from tests.gpu_util import launch, split_weights
+    import torch
+    S, dk, batch = 128, 64, 4
+    Q, K, V = (_t(_rand(70 + i, (batch, S * dk))) for i in range(3))
+    W = _t((_rand(73, (dk * dk,)) * np.float32(1 / 8)).astype(np.float32))
+    planes = split_weights(W, False, dk, dk)
+    P = torch.empty(batch, S * S, device="cuda")
+    launch("gemm_nt", [Q, K], P, [S, S, dk], fparam=(0.125, 1e-5), batch=batch, epilogue=1)
+    C = torch.empty(batch, S * dk, device="cuda")
+    launch("gemm", [P, V], C, [S, dk, S], batch=batch)
+    Z0 = torch.empty(batch, S * dk, device="cuda")
+    launch("gemm", [C, W], Z0, [S, dk, dk], batch=batch, aux=planes)
+    Z1 = torch.empty(batch, S * dk, device="cuda")
+    launch("attn_head", [Q, K, V, W], Z1, [S, dk, dk], fparam=(0.125, 1e-5), batch=batch, aux=planes)
+    assert torch.equal(Z0, Z1)
