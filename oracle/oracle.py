@@ -478,6 +478,18 @@ def run_node(name, ins, strides, out, out_stride, vals, batch):
         ptrs = (ctypes.c_void_p * n)(*[a.ctypes.data for a in ins])
         st = (ctypes.c_int64 * n)(*strides)
         L.or_concat(ptrs, st, n, _p(out), out_stride, vals[0], vals[1], batch)
+    elif name == "attn_head":
+        # the fused head node is, by definition, the paper's head chain:
+        # A = gemm_nt(Q, K); P = softmax(A * num/den); C = gemm(P, V); Z = gemm(C, W)
+        S, dk, dw = vals[:3]
+        sm = [S, S] + (list(vals[3:5]) if len(vals) >= 5 else [])
+        A = np.empty((batch, S * S), np.float32)
+        run_node("gemm_nt", ins[:2], strides[:2], A, S * S, [S, S, dk], batch)
+        P = np.empty_like(A)
+        run_node("softmax", [A], [S * S], P, S * S, sm, batch)
+        C = np.empty((batch, S * dk), np.float32)
+        run_node("gemm", [P, ins[2]], [S * S, strides[2]], C, S * dk, [S, dk, S], batch)
+        run_node("gemm", [C, ins[3]], [S * dk, strides[3]], out, out_stride, [S, dw, dk], batch)
     else:
         raise ValueError(name)
 

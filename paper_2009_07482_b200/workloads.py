@@ -91,7 +91,7 @@ def attention(seq=128, dk=64, queues=3):
 ENCODER_PARAMS = {"S": 128, "D": 512, "DK": 64, "DFF": 2048}
 
 
-def encoder(layers=1, heads=8, tc_mode="per_head", queues=3, devices=1, params=None):
+def encoder(layers=1, heads=8, tc_mode="per_head", queues=3, devices=1, params=None, fused_heads=False):
     """C3/C4/C5 — transformer encoder layers as a fine-grained kernel DAG.
 
     Per head (PAPER.md:323): Q,K,V = gemm(X, W*); Kt = transpose(K); A = gemm(Q, Kt);
@@ -99,6 +99,8 @@ def encoder(layers=1, heads=8, tc_mode="per_head", queues=3, devices=1, params=N
     add_layernorm(X, concat) -> gemm_relu(., W1) -> gemm(., W2) -> add_layernorm.
     tc_mode: per_head (8 head components + 1 tail per layer),
     per_kernel (every kernel its own component, the eager/HEFT setting), single.
+    fused_heads: each head's Kt/A/P/C/Z chain is one `attn_head` node
+    (Z = softmax(Q Kᵀ · 1/8) V W_h; 4 kernels per head instead of 8).
     Returns (spec_text, params, meta) where meta locates inputs/outputs.
     """
     p = dict(ENCODER_PARAMS if params is None else params)
@@ -119,6 +121,23 @@ def encoder(layers=1, heads=8, tc_mode="per_head", queues=3, devices=1, params=N
                 meta["weights"].append({"kernel": kid, "pos": 1, "shape": [p["D"], p["DK"]], "fan_in": p["D"],
                                         "key": f"L{layer}.H{h}.W{role}"})
             q, k, v = proj
+            if fused_heads:
+                z = b.kernel("attn_head", [(0, "S*DK"), (1, "S*DK"), (2, "S*DK"), (3, "DK*DK")], [(4, "S*DK")],
+                             [(5, "S"), (6, "DK"), (7, "DK"), (8, 1), (9, 8)])
+                meta["weights"].append({"kernel": z, "pos": 3, "shape": [p["DK"], p["DK"]], "fan_in": p["DK"],
+                                        "key": f"L{layer}.H{h}.Wh"})
+                ks.append(z)
+                b.edge(q, 2, z, 0)
+                b.edge(k, 2, z, 1)
+                b.edge(v, 2, z, 2)
+                for kid in proj:
+                    if prev_out is None:
+                        meta["x_inputs"].append({"kernel": kid, "pos": 0})
+                    else:
+                        b.edge(prev_out[0], prev_out[1], kid, 0)
+                head_ids.append(ks)
+                z_ids.append(z)
+                continue
             kt = b.kernel("transpose", [(0, "S*DK")], [(1, "DK*S")], [(2, "S"), (3, "DK")])
             a = b.gemm("S", "S", "DK")
             sm = b.kernel("softmax", [(0, "S*S")], [(1, "S*S")], [(2, "S"), (3, "S"), (4, 1), (5, 8)])
@@ -144,7 +163,7 @@ def encoder(layers=1, heads=8, tc_mode="per_head", queues=3, devices=1, params=N
         cat = b.kernel("concat", [(i, "S*DK") for i in range(heads)], [(heads, f"S*DK*{heads}")],
                        [(heads + 1, "S"), (heads + 2, "DK")])
         for i, z in enumerate(z_ids):
-            b.edge(z, 2, cat, i)
+            b.edge(z, 4 if fused_heads else 2, cat, i)
         ln1 = b.kernel("add_layernorm", [(0, "S*D"), (1, "S*D"), (2, "D"), (3, "D")], [(4, "S*D")], [(5, "S"), (6, "D")])
         if prev_out is None:
             meta["x_inputs"].append({"kernel": ln1, "pos": 0})

@@ -157,3 +157,18 @@ def test_dynamic_completion_log_replays_identically(oracle_mod):
     o = oracle_mod.schedule(oracle_mod.Spec(text, params), replay=log)
     assert o["dispatches"] == info["dispatches"]
     assert o["kernel_finish_order"] == replay["kernel_finish_order"]
+
+
+@pytest.mark.parametrize("mode", ["graph", "dynamic"])
+def test_spec_level_attn_head_nodes(mode, oracle_mod):
+    """A DAG written with `attn_head` nodes (one per head: 4 kernels per head
+    instead of 8) runs in both modes and matches the oracle."""
+    text, params, meta = workloads.encoder(layers=2, fused_heads=True)
+    n = 3
+    arrays = _encoder_arrays(meta, params, n)
+    ref = oracle_mod.run_dag(text, params, arrays, n)
+    key = (meta["output"]["kernel"], meta["output"]["pos"])
+    outs, _, plan = _run_gpu(text, params, arrays, n, mode=mode, batch=2)
+    assert plan["kernels"] == 74
+    for i in range(n):
+        assert _normwise(outs[key][i], ref[key][i]) <= TOL

@@ -88,3 +88,24 @@ def test_dag_executor_matches_layer_math(oracle_mod):
     f = np.maximum(h1 @ w1, 0) @ w2
     ref = ln(h1 + f, g2, b2)
     assert np.max(np.abs(y - ref)) / np.max(np.abs(ref)) < 1e-5
+
+
+def test_attn_head_node_is_the_head_chain():
+    """The oracle's attn_head node is defined as the paper's head chain: a layer
+    written with fused heads gives bit-identical outputs to the 8-kernel heads
+    (same inputs and the same weights, matched by role)."""
+    from oracle import oracle as O
+    from paper_2009_07482_b200 import workloads
+    text0, params, meta0 = workloads.encoder(layers=1)
+    w0 = workloads.encoder_weights(meta0)
+    by_role = {m["key"]: w0[(m["kernel"], m["pos"])] for m in meta0["weights"]}
+    outs = []
+    for fused in (False, True):
+        text, params, meta = workloads.encoder(layers=1, fused_heads=fused)
+        x = workloads.encoder_inputs(meta, params, 2).reshape(2, -1)
+        arrays = {(i["kernel"], i["pos"]): x for i in meta["x_inputs"]}
+        for m in meta["weights"]:
+            arrays[(m["kernel"], m["pos"])] = by_role[m["key"]].reshape(-1)
+        out = O.run_dag(text, params, arrays, 2)
+        outs.append(out[(meta["output"]["kernel"], meta["output"]["pos"])])
+    assert np.array_equal(outs[0], outs[1])
