@@ -48,7 +48,7 @@ def parse_args():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--instances", type=int, default=TOTAL_INSTANCES)
     ap.add_argument("--layers", type=int, default=LAYERS)
-    ap.add_argument("--batch", type=int, default=256, help="instances per batched node launch")
+    ap.add_argument("--batch", type=int, default=512, help="instances per batched node launch")
     ap.add_argument("--slots", type=int, default=2)
     ap.add_argument("--queues", type=int, default=3)
     ap.add_argument("--devices", type=int, default=1, help="logical devices in the cq map (all on this GPU)")
