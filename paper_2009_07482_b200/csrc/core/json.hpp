@@ -40,6 +40,7 @@ class Value {
   static Value make_object() { Value v; v.kind_ = Kind::object; return v; }
   static Value of(long long i) { Value v; v.kind_ = Kind::integer; v.i_ = i; return v; }
   static Value of(const std::string& s) { Value v; v.kind_ = Kind::string; v.s_ = s; return v; }
+  static Value real(double d) { Value v; v.kind_ = Kind::floating; v.f_ = d; return v; }
   static Value boolean(bool b) { Value v; v.kind_ = Kind::boolean; v.b_ = b; return v; }
 
   Kind kind() const { return kind_; }

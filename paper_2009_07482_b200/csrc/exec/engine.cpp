@@ -89,6 +89,7 @@ Engine::Engine(EngineConfig cfg) : cfg_(std::move(cfg)) {
 Engine::~Engine() {
   if (!ctx_) return;
   hs_ctx_sync(ctx_);
+  clear_trace();
   for (auto& sl : slots_) {
     hs_graph_destroy(sl.graph);
     for (auto& [k, e] : sl.events) hs_event_destroy(e);
@@ -443,6 +444,19 @@ void Engine::issue(Slot& sl, const TaskComponent& t, const CommandQueueStructure
     if (pit != preds.end())
       for (int p : pit->second) hs_ok(hs_stream_wait(s, event(sl, t.id, p)), "E_Q wait");
     bool record = dep_sources.count(ev) || q.callbacks.count(ev);
+    TraceRec tr;
+    if (tracing_) {
+      tr.component = t.id;
+      tr.event = ev;
+      tr.kind = int(c.kind);
+      tr.kernel = c.kernel;
+      tr.device = d;
+      tr.queue = qi;
+      tr.label = c.label;
+      hs_ok(hs_event_create(ctx_, 1, &tr.t0), "hs_event_create");
+      hs_ok(hs_event_create(ctx_, 1, &tr.t1), "hs_event_create");
+      hs_ok(hs_event_record(tr.t0, s), "trace record");
+    }
     switch (c.kind) {
       case CmdKind::write: {
         const std::pair<int, int> key{c.buffer->kernel, c.buffer->pos};
@@ -537,6 +551,10 @@ void Engine::issue(Slot& sl, const TaskComponent& t, const CommandQueueStructure
           }
         }
         break;
+    }
+    if (tracing_) {
+      hs_ok(hs_event_record(tr.t1, s), "trace record");
+      trace_.push_back(tr);
     }
     if (record) hs_ok(hs_event_record(event(sl, t.id, ev), s), "event record");
     if (!graph && q.callbacks.count(ev))
@@ -739,15 +757,14 @@ void Engine::plan_chain_rewrites() {
     if (nd.elided) --launches_per_batch_;
 }
 
-void Engine::capture(Slot& sl) {
-  // Every stream the plan touches joins the capture through a fork event.
+void Engine::emit_plan(Slot& sl) {
+  // Every stream the plan touches joins through a fork event on the origin
+  // stream and is joined back at the end (the capture boundary in graph mode).
   std::set<std::pair<int, int>> used;
   for (size_t i = 0; i < plan_.dispatches.size(); ++i) {
     const auto& q = plan_.structures[i];
     for (size_t qi = 0; qi < q.queues.size(); ++qi) used.insert({q.device, int(qi)});
   }
-  for (auto [d, qi] : used) stream(sl, d, qi);  // create before capture
-  hs_ok(hs_capture_begin(sl.origin), "capture begin");
   hs_event_t fork = event(sl, -1, 0);
   hs_ok(hs_event_record(fork, sl.origin), "fork record");
   for (auto [d, qi] : used) hs_ok(hs_stream_wait(stream(sl, d, qi), fork), "fork wait");
@@ -767,7 +784,25 @@ void Engine::capture(Slot& sl) {
     hs_ok(hs_event_record(e, stream(sl, d, qi)), "join record");
     hs_ok(hs_stream_wait(sl.origin, e), "join wait");
   }
+}
+
+void Engine::capture(Slot& sl) {
+  for (size_t i = 0; i < plan_.dispatches.size(); ++i) {
+    const auto& q = plan_.structures[i];
+    for (size_t qi = 0; qi < q.queues.size(); ++qi) stream(sl, q.device, int(qi));  // create before capture
+  }
+  hs_ok(hs_capture_begin(sl.origin), "capture begin");
+  emit_plan(sl);
   hs_ok(hs_capture_end(sl.origin, &sl.graph), "capture end");
+}
+
+void Engine::clear_trace() {
+  for (auto& r : trace_) {
+    hs_event_destroy(r.t0);
+    hs_event_destroy(r.t1);
+  }
+  trace_.clear();
+  trace_dispatch_.clear();
 }
 
 void Engine::push_completion(const Completion& c) {
@@ -799,6 +834,8 @@ void Engine::run_dynamic(Slot& sl, int64_t first, int64_t n) {
   CudaDispatch ex(*this, sl, first, n);
   ScheduleResult r = sched_->run(ex);
   last_dispatches_ = r.dispatches;
+  if (tracing_)
+    for (const auto& rec : r.dispatches) trace_dispatch_.push_back({rec.component, rec.device});
 }
 
 void Engine::run(int64_t first, int64_t n, int64_t* elapsed_ns) {
@@ -821,20 +858,32 @@ void Engine::run(int64_t first, int64_t n, int64_t* elapsed_ns) {
   // Every stream that can carry work starts after t_start.
   hs_ok(hs_event_record(s0.t_start, s0.origin), "start record");
   for (size_t i = 1; i < slots_.size(); ++i) hs_ok(hs_stream_wait(slots_[i].origin, s0.t_start), "start wait");
+  if (cfg_.trace) clear_trace();
   if (cfg_.graph_mode) {
     for (int64_t b = 0; b < nb; ++b) {
       Slot& sl = slots_[size_t(b % int64_t(slots_.size()))];
       const int64_t f = first + b * B, cnt = std::min(B, n - b * B);
       for (size_t gi = 0; gi < groups_.size(); ++gi)
         if (!groups_[gi].resident) copy_in(sl, sl.origin, int(gi), f, cnt);
-      hs_ok(hs_graph_launch(sl.graph, sl.origin), "graph launch");
+      if (cfg_.trace && b == 0) {
+        // traced batch: the same plan issued directly (not replayed) with a
+        // timing event pair around every command
+        tracing_ = true;
+        for (const auto& rec : plan_.dispatches) trace_dispatch_.push_back({rec.component, rec.device});
+        emit_plan(sl);
+        tracing_ = false;
+      } else {
+        hs_ok(hs_graph_launch(sl.graph, sl.origin), "graph launch");
+      }
       copy_out(sl, sl.origin, f, cnt);
     }
   } else {
     for (auto& [k, s] : s0.streams) hs_ok(hs_stream_wait(s, s0.t_start), "start wait");
     for (int64_t b = 0; b < nb; ++b) {
       const int64_t f = first + b * B, cnt = std::min(B, n - b * B);
+      tracing_ = cfg_.trace && b == 0;
       run_dynamic(s0, f, cnt);
+      tracing_ = false;
     }
     // join every queue stream back into the origin
     int j = 0;
@@ -892,6 +941,33 @@ std::string Engine::info(const std::string& what) const {
     out.set("launches_per_batch", Value::of(static_cast<long long>(launches_per_batch_)));
     out.set("runs", Value::of(static_cast<long long>(runs_)));
     out.set("batches", Value::of(static_cast<long long>(batches_run_)));
+  } else if (what == "trace") {
+    // SPEC.md:435 trace records of the first batch of the last run (times in ms
+    // from the run's start event): event id = position in issue order.
+    static const char* kinds[3] = {"write", "ndrange", "read"};
+    Value arr = Value::make_array();
+    long long id = 0;
+    for (const auto& r : trace_) {
+      int64_t a = 0, b = 0;
+      hs_ok(hs_event_elapsed_ns(slots_.front().t_start, r.t0, &a), "trace elapsed");
+      hs_ok(hs_event_elapsed_ns(slots_.front().t_start, r.t1, &b), "trace elapsed");
+      Value rec = Value::make_object();
+      rec.set("event", Value::of(id++));
+      rec.set("kind", Value::of(std::string(kinds[r.kind])));
+      rec.set("label", Value::of(r.label));
+      rec.set("kernel", Value::of(static_cast<long long>(r.kernel)));
+      rec.set("component", Value::of(static_cast<long long>(r.component)));
+      rec.set("device", Value::of(static_cast<long long>(r.device)));
+      rec.set("queue", Value::of(static_cast<long long>(r.queue)));
+      rec.set("channel", Value::of(-1LL));
+      rec.set("start", Value::real(double(a) / 1e6));
+      rec.set("finish", Value::real(double(b) / 1e6));
+      arr.push_back(std::move(rec));
+    }
+    out.set("trace", std::move(arr));
+    out.set("dispatches", pairs(trace_dispatch_, &DispatchRecord::component, &DispatchRecord::device));
+    out.set("mode", Value::of(std::string(cfg_.graph_mode ? "graph" : "dynamic")));
+    out.set("batch", Value::of(static_cast<long long>(cfg_.batch)));
   } else if (what == "completions") {
     out.set("completions", pairs(last_log_, &Completion::component, &Completion::event));
     out.set("dispatches", pairs(last_dispatches_, &DispatchRecord::component, &DispatchRecord::device));
@@ -955,6 +1031,7 @@ int hs_engine_create(const char* config_json, hs_engine_t* out) {
       else if (m == "bf16x3") cfg.math = HS_MATH_BF16X3;
       else fail(Errc::invalid_param, "math must be tf32x3|tf32|bf16x3|simt");
     }
+    if (const json::Value* v = c.find("trace")) cfg.trace = v->as_int() != 0;
     if (const json::Value* v = c.find("cpu_devices"))
       for (const json::Value* x : v->items()) cfg.cpu_devices.insert(x->as_int());
     if (const json::Value* v = c.find("fuse")) {

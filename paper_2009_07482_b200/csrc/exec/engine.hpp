@@ -45,6 +45,9 @@ struct EngineConfig {
   // sibling GEMMs, 2 = + chain rewrites (transpose folded into gemm_nt,
   // softmax as a GEMM epilogue, concat inputs written in place).
   int fuse = 2;
+  // Record a timing-event pair around every command of the first batch of each
+  // run (dynamic mode: as dispatched; graph mode: the plan issued directly).
+  bool trace = false;
 };
 
 class Engine {
@@ -104,6 +107,8 @@ class Engine {
   void plan_buffers();
   void upload_resident();
   void capture(Slot& sl);
+  void emit_plan(Slot& sl);
+  void clear_trace();
   hs_stream_t stream(Slot& sl, int device, int queue);
   hs_event_t event(Slot& sl, int comp, int ev);
   void issue(Slot& sl, const TaskComponent& t, const CommandQueueStructure& q, int prev_comp,
@@ -174,6 +179,14 @@ class Engine {
   std::condition_variable cv_;
   std::deque<Completion> done_q_;
   std::vector<Completion> last_log_;
+  struct TraceRec {
+    int component = -1, event = -1, kind = 0, kernel = -1, device = -1, queue = -1;
+    std::string label;
+    hs_event_t t0 = nullptr, t1 = nullptr;
+  };
+  bool tracing_ = false;
+  std::vector<TraceRec> trace_;
+  std::vector<DispatchRecord> trace_dispatch_;
   std::vector<DispatchRecord> last_dispatches_;
 };
 

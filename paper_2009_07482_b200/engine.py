@@ -29,13 +29,17 @@ def _ptr_and_nbytes(arr):
 class Engine:
     def __init__(self, spec_text: str, params: dict | None = None, *, gpu: int = 0, policy: str = "clustering",
                  mode: str = "graph", batch: int = 1, slots: int = 2, math: str = "tf32x3", cpu_devices=(),
-                 fuse: int | bool = 2):
+                 fuse: int | bool = 2, trace: bool = False):
         """fuse (graph mode): 0 = one launch per ndrange; 1 = + grouped sibling GEMMs;
         2 (default, also True) = + chain rewrites (transpose -> gemm_nt, softmax as a GEMM
-        epilogue, concat inputs written in place). Dynamic mode always launches per ndrange."""
+        epilogue, concat inputs written in place, fused attention heads). Dynamic mode always
+        launches per ndrange.
+        trace: time every command of the first batch of each run with CUDA events
+        (see trace(); graph mode issues that batch's plan directly instead of replaying it)."""
         fuse = 2 if fuse is True else int(fuse)
         cfg = {"spec": spec_text, "params": dict(params or {}), "gpu": gpu, "policy": policy, "mode": mode,
-               "batch": batch, "slots": slots, "math": math, "cpu_devices": list(cpu_devices), "fuse": int(fuse)}
+               "batch": batch, "slots": slots, "math": math, "cpu_devices": list(cpu_devices), "fuse": int(fuse),
+               "trace": int(bool(trace))}
         self._lib = lib()
         h = ctypes.c_void_p()
         check(self._lib.hs_engine_create(json.dumps(cfg).encode(), ctypes.byref(h)), "hs_engine_create")
@@ -68,6 +72,12 @@ class Engine:
             return json.loads(ctypes.string_at(p).decode())
         finally:
             self._lib.hs_free_string(p)
+
+    def trace(self) -> list[dict]:
+        """SPEC.md:435 trace records of the last run's first batch: dicts with event, kind
+        (write|ndrange|read), label (w1/e2/r1), kernel, component, device, queue, channel,
+        start, finish (ms from the run's start event). Requires trace=True."""
+        return self.info("trace")["trace"]
 
     def close(self):
         if getattr(self, "_h", None) and self._h.value:

@@ -172,3 +172,38 @@ def test_spec_level_attn_head_nodes(mode, oracle_mod):
     assert plan["kernels"] == 74
     for i in range(n):
         assert _normwise(outs[key][i], ref[key][i]) <= TOL
+
+
+def test_trace_records_every_command_in_both_modes(oracle_mod):
+    """trace=True: a CUDA-event pair around every command of the first batch.
+    Same command count in both modes, queue order respected, outputs unchanged,
+    and the device gaps between components are larger in dynamic mode (host
+    callback round trip) than in graph mode (event join)."""
+    from paper_2009_07482_b200 import reporting as R
+    import statistics
+    text, params, meta = workloads.encoder(layers=1)
+    n = 2
+    arrays = _encoder_arrays(meta, params, n)
+    ref = oracle_mod.run_dag(text, params, arrays, n)
+    key = (meta["output"]["kernel"], meta["output"]["pos"])
+    med = {}
+    counts = {}
+    for mode in ("dynamic", "graph"):
+        outs = {(k, p): np.zeros((n, e), np.float32) for k, p, e in workloads.isolated_outputs(text, params)}
+        with Engine(text, params, mode=mode, batch=n, trace=True) as eng:
+            for k, arr in arrays.items():
+                eng.bind(*k, arr, shared=arr.ndim == 1)
+            for k, arr in outs.items():
+                eng.bind(*k, arr)
+            eng.run(0, n)
+            tr = eng.trace()
+            disp = [c for c, _ in eng.info("trace")["dispatches"]]
+        for i in range(n):
+            assert _normwise(outs[key][i], ref[key][i]) <= TOL
+        assert sum(r["kind"] == "ndrange" for r in tr) == 69
+        assert all(0 <= r["start"] <= r["finish"] for r in tr)
+        assert R.audit_queue_order(tr) == []
+        counts[mode] = len(tr)
+        med[mode] = statistics.median(g["gap"] for g in R.component_gaps(tr, disp))
+    assert counts["dynamic"] == counts["graph"]
+    assert med["dynamic"] > med["graph"], med
