@@ -325,6 +325,8 @@ def setup_cq(spec: Spec, comp_id: int, device: int, device_type: str, r: int) ->
         "end_marks": [lab(e) for e in sorted(end_marks)],
         "commands": cmds,
         "_terminal": [q[-1] for q in queues if q],
+        "_queues": [list(q) for q in queues],
+        "_deps": sorted(deps),
         "_callbacks": sorted(callbacks),
         "_end_marks": sorted(end_marks),
     }
@@ -332,7 +334,11 @@ def setup_cq(spec: Spec, comp_id: int, device: int, device_type: str, r: int) ->
 
 # ============================================================================ scheduler
 
-def schedule(spec: Spec, policy="clustering", times=None, cpu_devices=(), replay=None) -> dict:
+def schedule(spec: Spec, policy="clustering", times=None, cpu_devices=(), replay=None, executor=None) -> dict:
+    """Alg. 1. Completions come from `replay` (a recorded log), from `executor`
+    (an object with dispatch(component, device, q) and wait_next() -> (c, ev),
+    e.g. oracle/platform_sim.py), or else from the plan model: components
+    complete in dispatch order, callback events in event order."""
     comps = components(spec)
     devices = sorted(spec.cq)
     dtype = {d: ("cpu" if d in cpu_devices else "gpu") for d in devices}
@@ -396,6 +402,8 @@ def schedule(spec: Spec, policy="clustering", times=None, cpu_devices=(), replay
             state[c] = "dispatched"
             live[c] = {"device": d, "q": q, "done": set()}
             dispatches.append([c, d])
+            if executor is not None:
+                executor.dispatch(c, d, q)
             for ev in q["_callbacks"]:
                 pending.append((c, ev))
         if len(finished) >= len(spec.kernels):
@@ -404,6 +412,8 @@ def schedule(spec: Spec, policy="clustering", times=None, cpu_devices=(), replay
             raise OracleError("Deadlock")
         if log is not None:
             c, ev = log.popleft()
+        elif executor is not None:
+            c, ev = executor.wait_next()
         else:
             c, ev = pending.popleft()
         L = live[c]

@@ -14,6 +14,7 @@
 #include "hetsim/expr.hpp"
 #include "hetsim/graph_analysis.hpp"
 #include "hetsim/rational.hpp"
+#include "hetsim/platform_sim.hpp"
 #include "hetsim/scheduler.hpp"
 #include "hetsim/spec_model.hpp"
 #include "hetsim_c.h"
@@ -154,6 +155,65 @@ Value schedule(const DagSpec& g, const Value& req) {
   return out;
 }
 
+Ratio ratio_of(const Value& v) { return v.is_string() ? Ratio::parse(v.as_string()) : Ratio(v.as_int64()); }
+
+// {"op":"simulate", spec, params, policy, cpu_devices, callback_delay,
+//  "device_profiles": [{"device", "type", "kernel_times": {id: ms}, "kernel_share": {id: s},
+//                       "copy_channels", "bandwidth" (bytes/ms), "transfer_latency" (ms)}]}
+Value simulate_req(const DagSpec& g, const Value& req) {
+  std::set<int> cpu_ids;
+  if (const Value* c = req.find("cpu_devices"))
+    for (const Value* v : c->items()) cpu_ids.insert(v->as_int());
+  Platform p = Platform::from_spec(g, cpu_ids);
+  Policy pol = policy_from_name(req.find("policy") ? req.at("policy").as_string() : "clustering");
+  std::vector<DeviceProfile> profs;
+  for (const Value* d : req.at("device_profiles").items()) {
+    DeviceProfile dp;
+    dp.device_id = d->at("device").as_int();
+    dp.device_type = d->at("type").as_string() == "cpu" ? DeviceType::cpu : DeviceType::gpu;
+    if (const Value* t = d->find("kernel_times"))
+      for (const auto& [k, v] : t->object_items()) dp.kernel_times[std::stoi(k)] = ratio_of(v);
+    if (const Value* t = d->find("kernel_share"))
+      for (const auto& [k, v] : t->object_items()) dp.kernel_share[std::stoi(k)] = ratio_of(v);
+    if (const Value* v = d->find("copy_channels")) dp.copy_channels = v->as_int();
+    if (const Value* v = d->find("bandwidth")) dp.bandwidth = ratio_of(*v);
+    if (const Value* v = d->find("transfer_latency")) dp.transfer_latency = ratio_of(*v);
+    profs.push_back(std::move(dp));
+  }
+  const Value* cd = req.find("callback_delay");
+  SimResult r = simulate(g, p, profs, pol, cd ? ratio_of(*cd) : Ratio(0));
+  Value out = Value::make_object();
+  out.set("makespan", S(r.makespan.str()));
+  out.set("makespan_ms", Value::real(r.makespan.to_double()));
+  Value tr = Value::make_array();
+  for (const auto& e : r.trace) {
+    Value x = Value::make_object();
+    x.set("event", V(e.event_id));
+    x.set("kind", S(cmd_kind_name(e.kind)));
+    x.set("label", S(e.label));
+    x.set("kernel", V(e.kernel));
+    x.set("component", V(e.component));
+    x.set("cmd_event", V(e.cmd_event));
+    x.set("device", V(e.device));
+    x.set("queue", V(e.queue));
+    x.set("channel", V(e.channel));
+    x.set("start", S(e.start.str()));
+    x.set("finish", S(e.finish.str()));
+    tr.push_back(std::move(x));
+  }
+  out.set("trace", std::move(tr));
+  Value d = Value::make_array();
+  for (const auto& rec : r.schedule.dispatches) {
+    Value x = Value::make_array();
+    x.push_back(V(rec.component));
+    x.push_back(V(rec.device));
+    d.push_back(std::move(x));
+  }
+  out.set("dispatches", std::move(d));
+  out.set("kernel_finish_order", ints(r.schedule.kernel_finish_order));
+  return out;
+}
+
 Value run(const Value& req) {
   const std::string op = req.at("op").as_string();
   Value out = Value::make_object();
@@ -228,6 +288,8 @@ Value run(const Value& req) {
     out.set("cq", json::parse(to_debug_json(q)));
   } else if (op == "schedule") {
     out.set("schedule", schedule(g, req));
+  } else if (op == "simulate") {
+    out.set("simulate", simulate_req(g, req));
   } else {
     fail(Errc::invalid_param, "unknown op " + op);
   }
