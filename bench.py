@@ -56,6 +56,7 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-alt", action="store_true", help="skip the alternate-math measurement")
+    ap.add_argument("--no-makespans", action="store_true", help="skip the C1-C4 makespan block")
     return ap.parse_args()
 
 
@@ -289,6 +290,99 @@ def oracle_reference(layers, first):
     return out[(meta["output"]["kernel"], meta["output"]["pos"])].reshape(-1)
 
 
+def config_spec(cfg, queues=3, devices=1):
+    """(spec_text, params, per-instance inputs {key: [n, e] or shared [e]}, output keys, n_instances, shared keys,
+    io bytes per instance) for BASELINE.json configs C1-C4 (workloads.py)."""
+    from paper_2009_07482_b200 import workloads
+    if cfg in ("C1", "C2"):
+        text, params = workloads.fork_join(queues=queues) if cfg == "C1" else workloads.attention(queues=queues)
+        arrays = workloads.generic_inputs(text, params, 1)
+        outs = [(k, p, e) for k, p, e in workloads.isolated_outputs(text, params)]
+        io = 4 * (sum(a.shape[1] for a in arrays.values()) + sum(e for _, _, e in outs))
+        return text, params, arrays, outs, 1, [], io
+    layers, n = (1, 1) if cfg == "C3" else (6, 64)
+    text, params, meta = workloads.encoder(layers=layers, queues=queues, devices=devices)
+    x = workloads.encoder_inputs(meta, params, n).reshape(n, -1)
+    arrays = {(i["kernel"], i["pos"]): x for i in meta["x_inputs"]}
+    shared = []
+    for key, w in workloads.encoder_weights(meta).items():
+        arrays[key] = w.reshape(-1)
+        shared.append(key)
+    outs = [(meta["output"]["kernel"], meta["output"]["pos"], params["S"] * params["D"])]
+    return text, params, arrays, outs, n, shared, 2 * x.shape[1] * 4
+
+
+def config_makespan(cfg, fuse=2, queues=3, devices=1, reps=20, warmup=3, math_mode="tf32x3", check=True, batch=None,
+                    slots=1):
+    """Makespan of one whole run of config `cfg` (all its instances in one batch) in graph
+    mode with device-resident inputs/outputs: median over `reps` runs of the engine's own
+    CUDA-event timing (start event -> end event on the origin stream, which joins every
+    queue stream). Returns the makespan, T* (roofline.dag_bound) and T*/makespan; with
+    `check`, instance 0's outputs are compared with the CPU oracle (normwise, 1e-4)."""
+    import numpy as np
+    import torch
+
+    from paper_2009_07482_b200 import roofline
+    from paper_2009_07482_b200.engine import Engine
+    text, params, arrays, outs, n, shared, io = config_spec(cfg, queues, devices)
+    dev = {}
+    x_cache = {}
+    for key, a in arrays.items():
+        if id(a) not in x_cache:
+            x_cache[id(a)] = torch.from_numpy(np.ascontiguousarray(a)).cuda()
+        dev[key] = x_cache[id(a)]
+    out_dev = {(k, p): torch.zeros(n, e, device="cuda") for k, p, e in outs}
+    torch.cuda.synchronize()
+    batch = batch or n
+    with Engine(text, params, batch=batch, slots=slots, mode="graph", fuse=fuse, math=math_mode) as eng:
+        for key, t in dev.items():
+            eng.bind(*key, t, shared=key in shared or t.dim() == 1)
+        for key, t in out_dev.items():
+            eng.bind(*key, t)
+        for _ in range(warmup):
+            eng.run(0, n)
+        ns = [eng.run(0, n) for _ in range(reps)]
+        launches = eng.info("plan").get("launches_per_batch")
+    ms = statistics.median(ns) / 1e6
+    pk, _ = peaks()
+    P = pk["bf16_tflops"] / 2.0 / 3.0 if math_mode != "bf16x3" else pk["bf16_tflops"] / 3.0
+    bound = roofline.dag_bound(text, params, n, P, pk["hbm_gbs"], shared_inputs=shared, io_bytes=io)
+    r = {"config": cfg, "instances": n, "batch": batch, "slots": slots, "fuse": fuse, "queues": queues, "logical_devices": devices, "math": math_mode,
+         "launches": launches, "makespan_ms": ms, "makespan_min_ms": min(ns) / 1e6, "t_star_ms": bound["t_star_ms"],
+         "bound": bound["bound"], "frac": bound["t_star_ms"] / ms}
+    if check:
+        from oracle import oracle as O
+        ref = O.run_dag(text, params, {k: (a[:1] if a.ndim == 2 else a) for k, a in arrays.items()}, 1)
+        r["normwise_err_vs_cpu_oracle"] = max(normwise(out_dev[k][0].cpu().numpy(), ref[k][0]) for k in out_dev)
+    return r
+
+
+def config_makespans():
+    """BASELINE.json configs C1-C4 on this GPU: makespan of one run (all instances, one
+    batch, graph mode, device-resident), T* and T*/makespan, parity of instance 0 vs the
+    CPU oracle; plus the paper's fine- vs coarse-grained comparison:
+    3 queues per device vs 1, with one launch per ndrange (fuse 0, the paper's execution)
+    and with the launch rewrites (fuse 2)."""
+    out = {}
+    best = {"C1": {}, "C2": {}, "C3": {"devices": 9}, "C4": {"devices": 9}}
+    for cfg, kw in best.items():
+        r = config_makespan(cfg, **kw)
+        out[cfg] = {k: r[k] for k in ("instances", "logical_devices", "queues", "fuse", "launches", "makespan_ms",
+                                      "t_star_ms", "bound", "frac", "normwise_err_vs_cpu_oracle")}
+    out["C4"]["target_1p5x_t_star_ms"] = 1.5 * out["C4"]["t_star_ms"]
+    grain = []
+    for cfg in ("C3", "C4"):
+        for fuse in (0, 2):
+            for queues in (1, 3):
+                r = config_makespan(cfg, fuse=fuse, queues=queues, devices=1, reps=10, check=False)
+                grain.append({"config": cfg, "fuse": fuse, "queues": queues, "makespan_ms": r["makespan_ms"]})
+    out["fine_vs_coarse"] = {"logical_devices": 1, "rows": grain,
+                             "note": "queues=1 is the coarse-grained default mc=(1,0,0); queues=3 fine-grained"}
+    out["note"] = ("median of 20 runs of the engine's CUDA-event makespan (start -> end event on the origin stream); "
+                   "C3/C4 use one logical device per component of a layer (9) so that heads run concurrently")
+    return out
+
+
 def normwise(y, ref):
     import numpy as np
     y, ref = np.asarray(y, np.float64), np.asarray(ref, np.float64)
@@ -420,6 +514,7 @@ def run_ours(args, world, rank, local):
             cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
                    "sample": f"12 instances of the {args.layers}-layer DAG ({t:.1f} s; oracle port: clustering "
                              f"scheduler + fp32 kernels on all host threads)"}
+        makespans = None if args.no_makespans else config_makespans()
         flop_per_inst = 782.2e6 * args.layers
         dtypes = {"tf32x3": "f32 (3xTF32 split on tcgen05, fp32-accurate)",
                   "bf16x3": "f32 (bf16x3 split on tcgen05 for weight GEMMs, 3xTF32 elsewhere; <=1e-4)",
@@ -445,7 +540,10 @@ def run_ours(args, world, rank, local):
                                    f"weight, {args.math} ({ms_launch:.3f} ms/launch)",
                          "peak_note": peak_note, "measured_peaks_file": pk_kind},
             "dag_roofline": {"flop_per_dag": flop_per_inst, "achieved_tflops": flop_per_inst * value / 1e12,
-                             "frac_of_peak": flop_per_inst * value / 1e12 / (peak * world)},
+                             "frac_of_peak": flop_per_inst * value / 1e12 / (peak * world),
+                             "t_star_ms": args.instances * flop_per_inst / (peak * world * 1e12) * 1e3,
+                             "note": "T* = instances x flop/DAG / P (compute-bound, SURVEY.md 8d); frac_of_peak = T*/ms_per_step"},
+            "makespans": makespans,
             "parity": parity,
             "alt_math": alt,
             "cpu_baseline": cpu,

@@ -13,13 +13,21 @@
 // unfused GEMM kernel, so each intermediate is bit-identical to what the
 // unfused chain writes to HBM).
 //
-// Warp roles (384 threads):
+// Warp roles (512 threads):
 //   warp 0      TMA: W planes once; per instance Q + K, then V into Q's buffer
 //   warp 1      MMA issuer (one lane)
 //   warp 2      TMEM allocator (512 columns)
-//   warps 4-7   row warps (thread = row): Q split -> TMEM; softmax over the S
-//               accumulator -> P split -> TMEM; C (= P·V) split -> TMEM; Z -> TMA store
-//   warps 8-11  operand warps: K -> tf32 hi (in place) / lo; V -> K-major hi / lo
+//   warps 4-11  row warps: warp 4+q+4g owns TMEM lane quarter q (rows 32q..32q+31)
+//               and column half g of every per-row pass: Q split -> TMEM; softmax
+//               over the S accumulator (64 columns per thread held in registers,
+//               row max / sum exchanged with the partner warp through smem) -> P
+//               split -> TMEM; C (= P·V) split -> TMEM; Z -> TMA store. Two warps
+//               per scheduler on the latency-bound row passes.
+//   warps 12-15 operand warps: K -> tf32 hi (in place) / lo; V -> K-major hi / lo
+//
+// Softmax summation order: sequential over columns [0,64) and over [64,128), then
+// s0 + s1 — the same order as the GEMM softmax epilogue (gemm_tc.cu), so the fused
+// head stays bit-identical to the unfused chain.
 //
 // TMEM columns: [0,128) S accumulator | [128,384) A operand region: Q hi/lo,
 // then P hi/lo, then C hi/lo | [384,448) C accumulator | [448,512) Z accumulator.
@@ -37,7 +45,7 @@ using namespace tc;
 constexpr int kS = 128;  // max rows = keys per head (one M tile; softmax width <= 128)
 constexpr int kDK = 64;  // head width: K of QKᵀ, N of P·V, K of C·W
 constexpr int kDW = 64;  // output width: N of C·W
-constexpr int kAttnThreads = 384;
+constexpr int kAttnThreads = 512;
 
 // shared memory regions (bytes from the 1024-aligned base)
 constexpr uint32_t kQV = 0;                  // Q staging: 2 SW128 tiles [128 rows][32 k] (32 KB); then V staging
@@ -45,7 +53,8 @@ constexpr uint32_t kKhi = kQV + 32768;       // K staging [128 n][32 k] x 2, con
 constexpr uint32_t kKlo = kKhi + 32768;      // K lo
 constexpr uint32_t kVop = kKlo + 32768;      // V operand: hi 4 x [64 n][32 k] SW128 (32 KB), lo (32 KB)
 constexpr uint32_t kW = kVop + 65536;        // W planes: hi 2 x [64 n][32 k] (16 KB), lo (16 KB)
-constexpr uint32_t kEpi = kW + 32768;        // Z staging: 4 warps x 2 x [32 rows][32 cols] (32 KB)
+constexpr uint32_t kEpi = kW + 32768;        // Z staging: 8 warps x [32 rows][32 cols] (32 KB); its first
+                                             // 256 B per warp also carry the softmax row max / sum exchange
 constexpr uint32_t kBar = kEpi + 32768;      // mbarriers + TMEM slot
 constexpr int kAttnSmem = int(kBar) + 256 + 1024;
 
@@ -98,7 +107,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     mbar_init(bar(QK_FULL), 1);
     mbar_init(bar(V_FULL), 1);
     mbar_init(bar(W_FULL), 1);
-    for (uint32_t b : {Q_FREE, K_READY, A_READY, P_READY, VB_READY, V_FREE, C_READY}) mbar_init(bar(b), 4);
+    for (uint32_t b : {Q_FREE, A_READY, P_READY, C_READY}) mbar_init(bar(b), 8);  // row warps
+    for (uint32_t b : {K_READY, VB_READY, V_FREE}) mbar_init(bar(b), 4);           // operand warps
     for (uint32_t b : {S_FULL, O_FULL, Z_FULL}) mbar_init(bar(b), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (const CUtensorMap* m : {&tmQ, &tmK, &tmV, &tmW, &tmZ})
@@ -180,33 +190,35 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         mma_commit(bar(Z_FULL));
       }
     }
-  } else if (warp >= 4 && warp < 8) {
+  } else if (warp >= 4 && warp < 12) {
     // -------------------------------------------------------------- row warps
-    const int q = warp & 3, row = q * 32 + lane;
+    const int q = warp & 3, g = (warp - 4) >> 2, row = q * 32 + lane;
     const uint32_t lane_base = tmem + (uint32_t(q * 32) << 16);
-    const uint32_t stage0 = base + kEpi + uint32_t(q) * 8192u;
+    const uint32_t stage = base + kEpi + uint32_t(q * 2 + g) * 4096u;
+    // softmax exchange with the partner warp (same lane quarter, other column half):
+    // max at stage[lane], sum at stage[32 + lane] of each warp's own staging tile
+    const uint32_t mine = stage + uint32_t(lane) * 4u;
+    const uint32_t other = base + kEpi + uint32_t(q * 2 + (g ^ 1)) * 4096u + uint32_t(lane) * 4u;
     const float sl = p.scale * 1.4426950408889634f;
-    uint32_t i = 0, stores = 0;
+    uint32_t i = 0;
     for (int inst = blockIdx.x; inst < p.batch; inst += gridDim.x, ++i) {
       const uint32_t ph = i & 1u;
-      // (A) Q row -> tf32 hi [kTA, kTA+64) / lo [kTA+64, kTA+128)
+      // (A) Q row, columns [32g, 32g+32) -> tf32 hi [kTA, kTA+64) / lo [kTA+64, kTA+128)
       mbar_wait(bar(QK_FULL), ph);
 #pragma unroll
-      for (int kb = 0; kb < 2; ++kb)
+      for (int hh = 0; hh < 2; ++hh) {
+        float x[16];
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          float x[16];
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            const float4 v = lds128(base + kQV + uint32_t(kb) * 16384u + sw128(row, 4 * hh + c));
-            x[4 * c] = v.x; x[4 * c + 1] = v.y; x[4 * c + 2] = v.z; x[4 * c + 3] = v.w;
-          }
-          uint32_t hi[16], lo[16];
-          split16(x, hi, lo);
-          const uint32_t col = kTA + uint32_t(kb * 32 + hh * 16);
-          tmem_st16(lane_base + col, hi);
-          tmem_st16(lane_base + col + 64u, lo);
+        for (int c = 0; c < 4; ++c) {
+          const float4 v = lds128(base + kQV + uint32_t(g) * 16384u + sw128(row, 4 * hh + c));
+          x[4 * c] = v.x; x[4 * c + 1] = v.y; x[4 * c + 2] = v.z; x[4 * c + 3] = v.w;
         }
+        uint32_t hi[16], lo[16];
+        split16(x, hi, lo);
+        const uint32_t col = kTA + uint32_t(g * 32 + hh * 16);
+        tmem_st16(lane_base + col, hi);
+        tmem_st16(lane_base + col + 64u, lo);
+      }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
       __syncwarp();
@@ -214,56 +226,71 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         mbar_arrive(bar(A_READY));
         mbar_arrive(bar(Q_FREE));
       }
-      // (B) softmax over the S accumulator row -> P hi [kTA, kTA+128) / lo [kTA+128, kTA+256)
+      // (B) softmax over S columns [64g, 64g+64) held in registers -> P hi [kTA, kTA+128) / lo [+128)
       mbar_wait(bar(S_FULL), ph);
       tc_fence_after();
-      uint32_t r[32];
+      uint32_t r0[32], r1[32];
+      tmem_ld32_nowait(lane_base + kTS + uint32_t(g * 64), r0);
+      tmem_ld32_nowait(lane_base + kTS + uint32_t(g * 64 + 32), r1);
+      tmem_ld_wait(r0);
+      tmem_ld_dep(r1);
+      // S is consumed (registers): nothing else of this instance reads it
       float mx = -INFINITY;
-#pragma unroll 1
-      for (int cb = 0; cb < kS / 32; ++cb) {
-        tmem_ld32(lane_base + kTS + uint32_t(cb * 32), r);
 #pragma unroll
-        for (int j = 0; j < 32; ++j)
-          if (cb * 32 + j < p.S) mx = fmaxf(mx, __uint_as_float(r[j]) * p.scale);
+      for (int j = 0; j < 32; ++j) {
+        if (g * 64 + j < p.S) mx = fmaxf(mx, __uint_as_float(r0[j]) * p.scale);
+        if (g * 64 + 32 + j < p.S) mx = fmaxf(mx, __uint_as_float(r1[j]) * p.scale);
       }
+      if (i > 0) {  // the previous Z store has finished reading this warp's staging tile
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncwarp();
+      }
+      sts32(mine, mx);
+      named_bar(1u + uint32_t(q), 64u);  // the two warps of lane quarter q
+      mx = fmaxf(mx, lds32(other));
       const float ml = mx * 1.4426950408889634f;
       float sum = 0.f;
-#pragma unroll 1
-      for (int cb = 0; cb < kS / 32; ++cb) {
-        tmem_ld32(lane_base + kTS + uint32_t(cb * 32), r);
 #pragma unroll
-        for (int j = 0; j < 32; ++j)
-          if (cb * 32 + j < p.S) sum = sum + ex2_approx(fmaf(__uint_as_float(r[j]), sl, -ml));
+      for (int j = 0; j < 32; ++j) {
+        const float e = g * 64 + j < p.S ? ex2_approx(fmaf(__uint_as_float(r0[j]), sl, -ml)) : 0.f;
+        sum = sum + e;
+        r0[j] = __float_as_uint(e);
       }
-      const float inv = 1.f / sum;
-#pragma unroll 1
-      for (int cb = 0; cb < kS / 32; ++cb) {
-        tmem_ld32(lane_base + kTS + uint32_t(cb * 32), r);
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          float x[16];
+      for (int j = 0; j < 32; ++j) {
+        const float e = g * 64 + 32 + j < p.S ? ex2_approx(fmaf(__uint_as_float(r1[j]), sl, -ml)) : 0.f;
+        sum = sum + e;
+        r1[j] = __float_as_uint(e);
+      }
+      sts32(mine + 128u, sum);
+      named_bar(1u + uint32_t(q), 64u);
+      const float s_other = lds32(other + 128u);
+      const float inv = 1.f / (g == 0 ? sum + s_other : s_other + sum);  // s0 + s1
+      // P = e * inv split in place: r -> hi (tmem_st16 reads it), lo computed alongside
 #pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const int c = cb * 32 + hh * 16 + e;
-            x[e] = c < p.S ? ex2_approx(fmaf(__uint_as_float(r[hh * 16 + e]), sl, -ml)) * inv : 0.f;
-          }
-          uint32_t hi[16], lo[16];
-          split16(x, hi, lo);
-          const uint32_t col = kTA + uint32_t(cb * 32 + hh * 16);
-          tmem_st16(lane_base + col, hi);
-          tmem_st16(lane_base + col + 128u, lo);
+      for (int hh = 0; hh < 4; ++hh) {
+        uint32_t hi[16], lo[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const float x = __uint_as_float(hh < 2 ? r0[(hh & 1) * 16 + e] : r1[(hh & 1) * 16 + e]) * inv;
+          const float h = tf32_rna(x);
+          hi[e] = __float_as_uint(h);
+          lo[e] = __float_as_uint(x - h);
         }
+        const uint32_t col = kTA + uint32_t(g * 64 + hh * 16);
+        tmem_st16(lane_base + col, hi);
+        tmem_st16(lane_base + col + 128u, lo);
       }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(bar(P_READY));
-      // (C) C = P·V accumulator -> tf32 hi [kTA, kTA+64) / lo [kTA+64, kTA+128)
+      // (C) C = P·V accumulator columns [32g, 32g+32) -> tf32 hi [kTA, kTA+64) / lo [kTA+64, kTA+128)
       mbar_wait(bar(O_FULL), ph);
       tc_fence_after();
-#pragma unroll 1
-      for (int cb = 0; cb < kDK / 32; ++cb) {
-        tmem_ld32(lane_base + kTC + uint32_t(cb * 32), r);
+      {
+        uint32_t r[32];
+        tmem_ld32(lane_base + kTC + uint32_t(g * 32), r);
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
           float x[16];
@@ -271,7 +298,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           for (int e = 0; e < 16; ++e) x[e] = __uint_as_float(r[hh * 16 + e]);
           uint32_t hi[16], lo[16];
           split16(x, hi, lo);
-          const uint32_t col = kTA + uint32_t(cb * 32 + hh * 16);
+          const uint32_t col = kTA + uint32_t(g * 32 + hh * 16);
           tmem_st16(lane_base + col, hi);
           tmem_st16(lane_base + col + 64u, lo);
         }
@@ -280,32 +307,27 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(bar(C_READY));
-      // (D) Z accumulator -> SW128 staging -> TMA store (rows >= S clipped by the map)
+      // (D) Z accumulator columns [32g, 32g+32) -> SW128 staging -> TMA store (rows >= S clipped by the map)
       mbar_wait(bar(Z_FULL), ph);
       tc_fence_after();
-#pragma unroll 1
-      for (int cb = 0; cb < kDW / 32; ++cb) {
-        tmem_ld32(lane_base + kTZ + uint32_t(cb * 32), r);
-        const uint32_t buf = stage0 + uint32_t(cb) * 4096u;
-        if (stores >= 2) {
-          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-          __syncwarp();
-        }
+      {
+        uint32_t r[32];
+        tmem_ld32(lane_base + kTZ + uint32_t(g * 32), r);  // the partner read this tile's exchange
+                                                              // words before arriving on P_READY
 #pragma unroll
         for (int c = 0; c < 8; ++c)
-          sts128(buf + uint32_t(lane) * 128u + (uint32_t(c ^ (lane & 7)) << 4),
+          sts128(stage + uint32_t(lane) * 128u + (uint32_t(c ^ (lane & 7)) << 4),
                  make_float4(__uint_as_float(r[4 * c]), __uint_as_float(r[4 * c + 1]), __uint_as_float(r[4 * c + 2]),
                              __uint_as_float(r[4 * c + 3])));
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
-        if (lane == 0) tma_store_3d(&tmZ, buf, cb * 32, q * 32, inst);
-        ++stores;
+        if (lane == 0) tma_store_3d(&tmZ, stage, g * 32, q * 32, inst);
       }
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-  } else if (warp >= 8) {
+  } else if (warp >= 12) {
     // -------------------------------------------------------------- operand warps
-    const int t = threadIdx.x - 256;  // 0..127
+    const int t = threadIdx.x - 384;  // 0..127
     uint32_t i = 0;
     for (int inst = blockIdx.x; inst < p.batch; inst += gridDim.x, ++i) {
       const uint32_t ph = i & 1u;

@@ -401,8 +401,8 @@ __global__ void __launch_bounds__(kThreads, kSmall ? 2 : 1)
       tc_fence_after();
       const uint32_t tacc = tmem + (uint32_t(q * 32) << 16) + acc * uint32_t(BN);
       // Softmax epilogue: this thread owns one full row of the tile (N <= BN).
-      // Two read passes over TMEM give the row max and the sequential sum of
-      // exp(s*x - max) in the oracle's order; the store pass scales by 1/sum.
+      // Two read passes over TMEM give the row max and the sum of exp(s*x - max);
+      // the store pass scales by 1/sum.
       // exp is ex2.approx on (s*x - max)*log2(e) (rel. error ~2^-21, far inside
       // the 1e-4 tolerance): one MUFU op instead of the ~20-instruction expf,
       // which matters because one warp per scheduler does all of this.
@@ -419,15 +419,19 @@ __global__ void __launch_bounds__(kThreads, kSmall ? 2 : 1)
         }
         sl = p.escale * 1.4426950408889634f;
         ml = smax * 1.4426950408889634f;
-        ssum = 0.f;
+        // summation order: sequential over columns [0,64) and [64,128), then s0 + s1
+        // (the fused attention head's order, attn_head.cu)
+        float s2[2] = {0.f, 0.f};
 #pragma unroll 1
         for (int cb = 0; cb < BN / 32 && cb * 32 < p.N; ++cb) {
           tmem_ld32(tacc + uint32_t(cb * 32), r);
+          float acc_s = s2[cb >= 2];
 #pragma unroll
           for (int j = 0; j < 32; ++j)
-            if (cb * 32 + j < p.N) ssum = ssum + ex2_approx(fmaf(__uint_as_float(r[j]), sl, -ml));
+            if (cb * 32 + j < p.N) acc_s = acc_s + ex2_approx(fmaf(__uint_as_float(r[j]), sl, -ml));
+          s2[cb >= 2] = acc_s;
         }
-        ssum = 1.f / ssum;  // used as the reciprocal below
+        ssum = 1.f / (s2[0] + s2[1]);  // used as the reciprocal below
       }
 #pragma unroll 1
       for (int cb = 0; cb < BN / 32; ++cb) {
