@@ -312,7 +312,7 @@ def config_spec(cfg, queues=3, devices=1):
     return text, params, arrays, outs, n, shared, 2 * x.shape[1] * 4
 
 
-def config_makespan(cfg, fuse=2, queues=3, devices=1, reps=20, warmup=3, math_mode="tf32x3", check=True, batch=None,
+def config_makespan(cfg, fuse=3, queues=3, devices=1, reps=20, warmup=3, math_mode="tf32x3", check=True, batch=None,
                     slots=1):
     """Makespan of one whole run of config `cfg` (all its instances in one batch) in graph
     mode with device-resident inputs/outputs: median over `reps` runs of the engine's own
@@ -362,7 +362,7 @@ def config_makespans():
     batch, graph mode, device-resident), T* and T*/makespan, parity of instance 0 vs the
     CPU oracle; plus the paper's fine- vs coarse-grained comparison:
     3 queues per device vs 1, with one launch per ndrange (fuse 0, the paper's execution)
-    and with the launch rewrites (fuse 2)."""
+    and with all launch rewrites (fuse 3)."""
     out = {}
     best = {"C1": {}, "C2": {}, "C3": {"devices": 9}, "C4": {"devices": 9}}
     for cfg, kw in best.items():
@@ -372,7 +372,7 @@ def config_makespans():
     out["C4"]["target_1p5x_t_star_ms"] = 1.5 * out["C4"]["t_star_ms"]
     grain = []
     for cfg in ("C3", "C4"):
-        for fuse in (0, 2):
+        for fuse in (0, 3):
             for queues in (1, 3):
                 r = config_makespan(cfg, fuse=fuse, queues=queues, devices=1, reps=10, check=False)
                 grain.append({"config": cfg, "fuse": fuse, "queues": queues, "makespan_ms": r["makespan_ms"]})

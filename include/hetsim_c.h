@@ -103,7 +103,8 @@ typedef enum {
   HS_OP_ADD_LN = 7,    /* Y = LayerNorm(A + B) * gamma + beta     */
   HS_OP_CONCAT = 8,    /* Y[:, i*c:(i+1)*c] = Z_i                 */
   HS_OP_ATTN_HEAD = 9, /* Z = softmax(s Q K^T) V W  (fused head)  */
-  HS_OP_COUNT = 10
+  HS_OP_HEAD = 10,     /* [Q|K|V] = X Wqkv; Z = softmax(s Q K^T) V Wh (whole head) */
+  HS_OP_COUNT = 11
 } hs_op;
 
 typedef enum {
@@ -148,6 +149,12 @@ typedef struct {
  * dims = {S, dk, dw} with S <= 128, dk = dw = 64; fparam[0] = softmax scale;
  * out = Z [S, dw] (rows out_ld apart, 0 = dw). tcgen05 math (TF32X3 / TF32)
  * only. The transformer head of PAPER.md:323 as one node. */
+/* HS_OP_HEAD (engine launch rewrite, no spec name): the head component of the
+ * encoder DAG including its Q/K/V projections. in = {X, Wh planes}: X [S, D] per
+ * instance, Wh [dk, dk] pre-split (format 0, stride 0); aux = Wq|Wk|Wv pre-split
+ * side by side (hs_gemm_split_weights_strided, N = 3 dk, plane stride 3 dk D);
+ * dims = {S, D, dk} with S <= 128, D % 32 == 0, dk = 64; fparam[0] = softmax
+ * scale; out = Z [S, dk] (rows out_ld apart). TF32X3 / TF32 only. */
 
 int hs_op_from_name(const char* name); /* -1 if unknown */
 int hs_launch(hs_stream_t s, int op, const hs_op_args* args, int math_mode, int batch);
@@ -177,7 +184,9 @@ typedef struct hs_engine* hs_engine_t;
 /* config_json: {"spec": "<spec document>", "params": {..}, "gpu": 0,
  *   "policy": "clustering"|"eager"|"heft", "mode": "graph"|"dynamic",
  *   "batch": B, "slots": 2, "math": "tf32x3"|"tf32"|"simt",
- *   "cpu_devices": [..], "trace": false} */
+ *   "cpu_devices": [..], "trace": false, "fuse": 3}
+ * fuse (graph mode launch lowering): 0 one launch per ndrange,
+ * 1 + grouped sibling GEMMs, 2 + chain rewrites, 3 (default) + whole-head launches. */
 int hs_engine_create(const char* config_json, hs_engine_t* out);
 int hs_engine_destroy(hs_engine_t e);
 

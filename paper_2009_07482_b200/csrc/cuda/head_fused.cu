@@ -1,0 +1,514 @@
+// Whole transformer head as one sm_100a launch (HS_OP_HEAD):
+//
+//   Q | K | V = X · [Wq | Wk | Wv]         X: [S, D]   W*: [D, 64]   (resident, pre-split)
+//   Z         = softmax_row(s · Q Kᵀ) · V · Wh              Wh: [64, 64] (resident, pre-split)
+//
+// which is the head component of the encoder DAG (SURVEY.md §8 C3:
+// three projection GEMMs, transpose, QKᵀ, softmax, P·V, C·W_h) after the engine's
+// launch rewrites: the grouped Q/K/V projection (gemm_tc.cu, gemm_pair_kernel<192>)
+// and the fused attention chain (attn_head.cu) in one kernel, so Q, K, V never
+// leave the SM. Each product is 3xTF32 with the operand split and the MMA order of
+// those two kernels.
+//
+// CTA pair (cluster of 2 on one TPC) per pair of instances, persistent over pairs.
+// Phase 1 (projection): the pair GEMM main loop with M = 256 (each CTA its own
+// instance's 128 rows), N = 192, K = D: X tiles by TMA into staging, split hi/lo
+// into TMEM by the converter warps, W planes by TMA (each CTA half of N).
+// Phase 2 (attention), all MMAs still cta_group::2 with M = 256:
+//   S  = [Q0;Q1] [K0;K1]ᵀ   N = 256: B rows 0-127 are CTA 0's keys, 128-255 CTA 1's;
+//                           CTA r keeps its own block, columns [128r, 128r+128)
+//   C  = [P0;P1] [V0 V1]    N = 128: B = Vᵀ, rows 0-63 CTA 0's, 64-127 CTA 1's;
+//                           CTA r keeps columns [64r, 64r+64)
+//   Z  = [C0;C1] Wh         N = 64: each CTA holds half of Whᵀ's rows
+// The off-diagonal blocks of S and C are computed and discarded (2x the QKᵀ and
+// P·V flops, 14 % of the head's): the price of one cta_group for the whole kernel.
+//
+// Warp roles (512 threads):
+//   warp 0      TMA: X tiles (phase 1)
+//   warp 1      MMA issuer (leader CTA, one lane)
+//   warp 2      TMEM allocator (512 columns, cta_group::2)
+//   warp 3      TMA: W planes (phase 1, this CTA's half of N), Wh half once
+//   warps 4-11  phase 1: converters, group g = (w-4)/4 takes every other K-block
+//               phase 2: row warps, TMEM lane quarter q = w%4, column half g:
+//               Q split -> TMEM; softmax (S in registers, row max / sum exchanged
+//               with the partner warp); C split -> TMEM; Z -> TMA store
+//   warps 12-15 phase 2: K -> K-major smem hi/lo; V -> Vᵀ K-major smem hi/lo
+//
+// TMEM columns: phase 1: QKV accumulator [0,192) | A stages [192,448).
+// phase 2: S [0,256) -> C acc [0,128) + Z acc [128,192); A operand [256,512):
+// Q hi/lo [256,384) -> P hi/lo [256,512) -> C hi/lo [256,384).
+#include <mutex>
+
+#include "kernels.cuh"
+#include "tc_common.cuh"
+
+namespace hs {
+
+namespace {
+
+using namespace tc;
+
+constexpr int kS = 128, kDK = 64, kN = 3 * kDK;  // rows, head width, projection width
+constexpr int kThreads = 512;
+constexpr int kNS = 4;  // X staging stages
+constexpr int kNO = 4;  // W operand stages = TMEM A stages
+constexpr uint32_t kStaging = BM * BK * 4;            // 16 KB X tile
+constexpr uint32_t kPlaneB = (kN / 2) * 128;          // 96 rows x 128 B: this CTA's half of N
+constexpr uint32_t kOperand = 2 * kPlaneB;            // hi + lo
+// shared memory (bytes from the 1024-aligned base)
+constexpr uint32_t kU = 0;                            // union: phase 1 stages | phase 2 operands
+constexpr uint32_t kOpB = kU + kNS * kStaging;        // phase 1 W operand ring
+constexpr uint32_t kKop = kU;                         // phase 2: K hi/lo, 2 planes x 2 k-blocks x [128][128 B]
+constexpr uint32_t kVop = kU + 65536;                 // phase 2: Vᵀ hi/lo, 2 planes x 4 k-blocks x [64][128 B]
+constexpr uint32_t kUEnd = kOpB + kNO * kOperand;     // 160 KB
+constexpr uint32_t kWh = kUEnd;                       // Whᵀ half: 2 planes x 2 k-blocks x [32][128 B] (16 KB)
+constexpr uint32_t kEpi = kWh + 16384;                // Z staging: 8 warps x [32][32] fp32 (32 KB)
+constexpr uint32_t kBar = kEpi + 32768;
+constexpr int kSmem = int(kBar) + 512 + 1024;
+static_assert(kVop + 65536 <= kUEnd, "phase 2 operands exceed the union");
+static_assert(kSmem <= 227 * 1024, "shared memory budget exceeded");
+
+constexpr uint32_t kTQ = 256;  // TMEM A-operand region (phase 2)
+constexpr uint32_t kTStage = 192;
+
+enum Bar : uint32_t {
+  ST_FULL = 0,             // [kNS] local
+  ST_EMPTY = ST_FULL + kNS,  // [kNS] local, 4 converter warps
+  OP_FULL = ST_EMPTY + kNS,  // [kNO] leader: 2 x 4 converter warps + expect_tx
+  OP_EMPTY = OP_FULL + kNO,  // [kNO] each CTA (commit multicast)
+  ACC_FULL = OP_EMPTY + kNO,
+  A_READY,   // leader: 2 x (8 row + 4 operand) warps
+  S_FULL,    // each CTA
+  P_READY,   // leader: 2 x 8
+  O_FULL,    // each CTA
+  C_READY,   // leader: 2 x 8
+  Z_FULL,    // each CTA
+  Z_DONE,    // leader: 2 x 8 (Z accumulator drained)
+  WH_FULL,   // leader: expect_tx
+  TMEM_SLOT,
+  kNumBars
+};
+static_assert(kNumBars * 8 <= 512, "barrier area");
+
+struct HeadParams {
+  int S, D, batch, pairs;
+  float scale;
+};
+
+template <int kTerms>
+__device__ __forceinline__ void mma3(uint32_t d, uint32_t a_hi, uint32_t a_lo, uint32_t b_hi, uint32_t b_lo,
+                                     uint32_t idesc, uint32_t first) {
+  if constexpr (kTerms > 1) {
+    mma_pair_tf32_ts(d, a_lo, smem_desc(b_hi), idesc, first);
+    mma_pair_tf32_ts(d, a_hi, smem_desc(b_lo), idesc, 1u);
+    mma_pair_tf32_ts(d, a_hi, smem_desc(b_hi), idesc, 1u);
+  } else {
+    mma_pair_tf32_ts(d, a_hi, smem_desc(b_hi), idesc, first);
+  }
+}
+
+template <int kTerms>
+__device__ __forceinline__ void split_row16(const uint32_t* r, uint32_t (&hi)[16], uint32_t (&lo)[16]) {
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    const float x = __uint_as_float(r[e]);
+    const float h = tf32_rna(x);
+    hi[e] = __float_as_uint(h);
+    lo[e] = __float_as_uint(x - h);
+  }
+}
+
+template <int kTerms>
+__global__ void __launch_bounds__(kThreads, 1)
+    head_pair_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
+                     const __grid_constant__ CUtensorMap tmWh, const __grid_constant__ CUtensorMap tmZ, HeadParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  auto bar = [&](uint32_t b) { return base + kBar + 8u * b; };
+  const uint32_t* tmem_slot_ptr =
+      reinterpret_cast<const uint32_t*>(smem_raw + (bar(TMEM_SLOT) - smem_u32(smem_raw)));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int pair0 = int(cluster_id_x()), npairs = int(nclusters_x());
+  const int nk = p.D / BK;
+  auto leader = [&](uint32_t b) { return mapa_rank(bar(b), 0); };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kNS; ++s) {
+      mbar_init(bar(ST_FULL + s), 1);
+      mbar_init(bar(ST_EMPTY + s), 4);
+    }
+    for (int o = 0; o < kNO; ++o) {
+      mbar_init(bar(OP_FULL + o), 2 * 4 + 1);
+      mbar_init(bar(OP_EMPTY + o), 1);
+    }
+    for (uint32_t b : {ACC_FULL, S_FULL, O_FULL, Z_FULL, WH_FULL}) mbar_init(bar(b), 1);
+    mbar_init(bar(A_READY), 2 * 12);
+    for (uint32_t b : {P_READY, C_READY, Z_DONE}) mbar_init(bar(b), 2 * 8);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (const CUtensorMap* m : {&tmX, &tmW, &tmWh, &tmZ})
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(bar(TMEM_SLOT)), "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot_ptr;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ X producer
+    if (lane == 0) {
+      uint32_t it = 0, lt = 0;
+      for (int t = pair0; t < p.pairs; t += npairs, ++lt) {
+        if (lt > 0) mbar_wait(bar(O_FULL), (lt - 1) & 1u);  // phase 2 operands of the last pair consumed
+        const int inst = 2 * t + int(rank);                  // >= batch: zero-filled box
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = int(it % kNS);
+          mbar_wait(bar(ST_EMPTY + s), ((it / kNS) & 1u) ^ 1u);
+          mbar_expect_tx(bar(ST_FULL + s), kStaging);
+          tma_load_3d(base + kU + uint32_t(s) * kStaging, &tmX, bar(ST_FULL + s), kb * BK, 0, inst);
+        }
+      }
+    }
+  } else if (warp == 3) {
+    // ------------------------------------------------------------ W producer (this CTA's half of N)
+    if (lane == 0) {
+      if (rank == 0) mbar_expect_tx(bar(WH_FULL), 2u * 16384u);
+      for (int pl = 0; pl < 2; ++pl)
+        for (int kb = 0; kb < 2; ++kb)
+          tma_load_3d_pair(base + kWh + uint32_t(pl) * 8192u + uint32_t(kb) * 4096u, &tmWh, leader(WH_FULL), kb * BK,
+                           int(rank) * 32, pl);
+      uint32_t it = 0, lt = 0;
+      for (int t = pair0; t < p.pairs; t += npairs, ++lt) {
+        if (lt > 0) mbar_wait(bar(O_FULL), (lt - 1) & 1u);
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int o = int(it % kNO);
+          mbar_wait(bar(OP_EMPTY + o), ((it / kNO) & 1u) ^ 1u);
+          const uint32_t b_hi = base + kOpB + uint32_t(o) * kOperand;
+          if (rank == 0) mbar_expect_tx(bar(OP_FULL + o), 2 * (kTerms > 1 ? 2 : 1) * kPlaneB);
+          const int nrow = int(rank) * (kN / 2);
+          tma_load_3d_pair(b_hi, &tmW, leader(OP_FULL + o), kb * BK, nrow, 0);
+          if constexpr (kTerms > 1) tma_load_3d_pair(b_hi + kPlaneB, &tmW, leader(OP_FULL + o), kb * BK, nrow, 1);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (leader)
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t m256 = uint32_t(BM >> 4) << 24;
+      constexpr uint32_t idQKV = instr_desc_tf32(kN) + m256, idS = instr_desc_tf32(256) + m256,
+                         idC = instr_desc_tf32(128) + m256, idZ = instr_desc_tf32(kDK) + m256;
+      uint32_t it = 0, lt = 0;
+      bool wh = false;
+      for (int t = pair0; t < p.pairs; t += npairs, ++lt) {
+        const uint32_t ph = lt & 1u;
+        if (lt > 0) mbar_wait(bar(Z_DONE), (lt - 1) & 1u);  // C / Z accumulators of the last pair drained
+        tc_fence_after();
+        // phase 1: [Q|K|V] = X · W
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int o = int(it % kNO);
+          mbar_wait(bar(OP_FULL + o), (it / kNO) & 1u);
+          tc_fence_after();
+          const uint32_t a_hi = tmem + kTStage + uint32_t(o) * 64u, a_lo = a_hi + 32u;
+          const uint32_t b_hi = base + kOpB + uint32_t(o) * kOperand, b_lo = b_hi + kPlaneB;
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk)
+            mma3<kTerms>(tmem, a_hi + uint32_t(kk) * 8u, a_lo + uint32_t(kk) * 8u, b_hi + uint32_t(kk) * 32u,
+                         b_lo + uint32_t(kk) * 32u, idQKV, (kb | kk) ? 1u : 0u);
+          mma_commit_pair(bar(OP_EMPTY + o));
+        }
+        mma_commit_pair(bar(ACC_FULL));
+        // S = Q Kᵀ (K = 64)
+        mbar_wait(bar(A_READY), ph);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < kDK / 8; ++kk) {
+          const uint32_t kbo = uint32_t(kk >> 2) * 16384u + uint32_t(kk & 3) * 32u;
+          mma3<kTerms>(tmem, tmem + kTQ + uint32_t(kk) * 8u, tmem + kTQ + 64u + uint32_t(kk) * 8u, base + kKop + kbo,
+                       base + kKop + 32768u + kbo, idS, kk ? 1u : 0u);
+        }
+        mma_commit_pair(bar(S_FULL));
+        // C = P V (K = 128 keys)
+        mbar_wait(bar(P_READY), ph);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < kS / 8; ++kk) {
+          const uint32_t kbo = uint32_t(kk >> 2) * 8192u + uint32_t(kk & 3) * 32u;
+          mma3<kTerms>(tmem, tmem + kTQ + uint32_t(kk) * 8u, tmem + kTQ + 128u + uint32_t(kk) * 8u, base + kVop + kbo,
+                       base + kVop + 32768u + kbo, idC, kk ? 1u : 0u);
+        }
+        mma_commit_pair(bar(O_FULL));
+        // Z = C Wh (K = 64)
+        if (!wh) {
+          mbar_wait(bar(WH_FULL), 0);
+          wh = true;
+        }
+        mbar_wait(bar(C_READY), ph);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < kDK / 8; ++kk) {
+          const uint32_t kbo = uint32_t(kk >> 2) * 4096u + uint32_t(kk & 3) * 32u;
+          mma3<kTerms>(tmem + 128u, tmem + kTQ + uint32_t(kk) * 8u, tmem + kTQ + 64u + uint32_t(kk) * 8u,
+                       base + kWh + kbo, base + kWh + 8192u + kbo, idZ, kk ? 1u : 0u);
+        }
+        mma_commit_pair(bar(Z_FULL));
+      }
+    }
+  } else if (warp >= 4 && warp < 12) {
+    // ------------------------------------------------------------ converters (phase 1) / row warps (phase 2)
+    const int q = warp & 3, g = (warp - 4) >> 2, row = q * 32 + lane;
+    const uint32_t lane_base = tmem + (uint32_t(q * 32) << 16);
+    const uint32_t stage = base + kEpi + uint32_t(q * 2 + g) * 4096u;
+    const uint32_t mine = stage + uint32_t(lane) * 4u;
+    const uint32_t other = base + kEpi + uint32_t(q * 2 + (g ^ 1)) * 4096u + uint32_t(lane) * 4u;
+    const float sl = p.scale * 1.4426950408889634f;
+    const int col0 = int(rank) * kS;  // this CTA's block of S (its own keys)
+    uint32_t it = 0, lt = 0;
+    for (int t = pair0; t < p.pairs; t += npairs, ++lt) {
+      const uint32_t ph = lt & 1u;
+      const int inst = 2 * t + int(rank);
+      // ---- phase 1: split this CTA's X rows into the TMEM A stages (every other K-block)
+      for (int kb = 0; kb < nk; ++kb, ++it) {
+        if (int(it & 1u) != g) continue;
+        const int s = int(it % kNS), o = int(it % kNO);
+        mbar_wait(bar(ST_FULL + s), (it / kNS) & 1u);
+        mbar_wait(bar(OP_EMPTY + o), ((it / kNO) & 1u) ^ 1u);
+        tc_fence_after();
+        const uint32_t sa = base + kU + uint32_t(s) * kStaging;
+        const uint32_t ta = lane_base + kTStage + uint32_t(o) * 64u;
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          uint32_t x[16], hi[16], lo[16];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const float4 v = lds128(sa + sw128(row, 4 * hh + c));
+            x[4 * c] = __float_as_uint(v.x); x[4 * c + 1] = __float_as_uint(v.y);
+            x[4 * c + 2] = __float_as_uint(v.z); x[4 * c + 3] = __float_as_uint(v.w);
+          }
+          split_row16<kTerms>(x, hi, lo);
+          tmem_st16(ta + uint32_t(16 * hh), hi);
+          if constexpr (kTerms > 1) tmem_st16(ta + 32u + uint32_t(16 * hh), lo);
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(bar(ST_EMPTY + s));
+          mbar_arrive_cluster(leader(OP_FULL + o));
+        }
+      }
+      // ---- phase 2 (A): Q columns [32g, 32g+32) -> tf32 hi [256, 320) / lo [320, 384)
+      mbar_wait(bar(ACC_FULL), ph);
+      tc_fence_after();
+      {
+        uint32_t r[32], hi[16], lo[16];
+        tmem_ld32(lane_base + uint32_t(g * 32), r);
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          split_row16<kTerms>(r + 16 * hh, hi, lo);
+          const uint32_t col = kTQ + uint32_t(g * 32 + hh * 16);
+          tmem_st16(lane_base + col, hi);
+          tmem_st16(lane_base + col + 64u, lo);
+        }
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(leader(A_READY));
+      // ---- (B) softmax over this CTA's S block, columns [col0 + 64g, +64) in registers
+      mbar_wait(bar(S_FULL), ph);
+      tc_fence_after();
+      uint32_t r0[32], r1[32];
+      tmem_ld32_nowait(lane_base + uint32_t(col0 + g * 64), r0);
+      tmem_ld32_nowait(lane_base + uint32_t(col0 + g * 64 + 32), r1);
+      tmem_ld_wait(r0);
+      tmem_ld_dep(r1);
+      float mx = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        if (g * 64 + j < p.S) mx = fmaxf(mx, __uint_as_float(r0[j]) * p.scale);
+        if (g * 64 + 32 + j < p.S) mx = fmaxf(mx, __uint_as_float(r1[j]) * p.scale);
+      }
+      if (lt > 0) {  // the previous Z store has finished reading this warp's staging tile
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncwarp();
+      }
+      sts32(mine, mx);
+      named_bar(1u + uint32_t(q), 64u);
+      mx = fmaxf(mx, lds32(other));
+      const float ml = mx * 1.4426950408889634f;
+      float sum = 0.f;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float e = g * 64 + j < p.S ? ex2_approx(fmaf(__uint_as_float(r0[j]), sl, -ml)) : 0.f;
+        sum = sum + e;
+        r0[j] = __float_as_uint(e);
+      }
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float e = g * 64 + 32 + j < p.S ? ex2_approx(fmaf(__uint_as_float(r1[j]), sl, -ml)) : 0.f;
+        sum = sum + e;
+        r1[j] = __float_as_uint(e);
+      }
+      sts32(mine + 128u, sum);
+      named_bar(1u + uint32_t(q), 64u);
+      const float s_other = lds32(other + 128u);
+      const float inv = 1.f / (g == 0 ? sum + s_other : s_other + sum);
+#pragma unroll
+      for (int hh = 0; hh < 4; ++hh) {
+        uint32_t hi[16], lo[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const float x = __uint_as_float(hh < 2 ? r0[(hh & 1) * 16 + e] : r1[(hh & 1) * 16 + e]) * inv;
+          const float h = tf32_rna(x);
+          hi[e] = __float_as_uint(h);
+          lo[e] = __float_as_uint(x - h);
+        }
+        const uint32_t col = kTQ + uint32_t(g * 64 + hh * 16);
+        tmem_st16(lane_base + col, hi);
+        tmem_st16(lane_base + col + 128u, lo);
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(leader(P_READY));
+      // ---- (C) C columns [64r + 32g, +32) -> tf32 hi [256, 320) / lo [320, 384)
+      mbar_wait(bar(O_FULL), ph);
+      tc_fence_after();
+      {
+        uint32_t r[32], hi[16], lo[16];
+        tmem_ld32(lane_base + uint32_t(int(rank) * kDK + g * 32), r);
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          split_row16<kTerms>(r + 16 * hh, hi, lo);
+          const uint32_t col = kTQ + uint32_t(g * 32 + hh * 16);
+          tmem_st16(lane_base + col, hi);
+          tmem_st16(lane_base + col + 64u, lo);
+        }
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(leader(C_READY));
+      // ---- (D) Z columns [32g, 32g+32) -> SW128 staging -> TMA store
+      mbar_wait(bar(Z_FULL), ph);
+      tc_fence_after();
+      {
+        uint32_t r[32];
+        tmem_ld32(lane_base + 128u + uint32_t(g * 32), r);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(leader(Z_DONE));
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          sts128(stage + uint32_t(lane) * 128u + (uint32_t(c ^ (lane & 7)) << 4),
+                 make_float4(__uint_as_float(r[4 * c]), __uint_as_float(r[4 * c + 1]), __uint_as_float(r[4 * c + 2]),
+                             __uint_as_float(r[4 * c + 3])));
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0 && inst < p.batch) tma_store_3d(&tmZ, stage, g * 32, q * 32, inst);
+      }
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  } else if (warp >= 12) {
+    // ------------------------------------------------------------ K / V operand warps (phase 2)
+    const int q = warp & 3, key = q * 32 + lane;
+    const uint32_t lane_base = tmem + (uint32_t(q * 32) << 16);
+    uint32_t lt = 0;
+    for (int t = pair0; t < p.pairs; t += npairs, ++lt) {
+      mbar_wait(bar(ACC_FULL), lt & 1u);
+      tc_fence_after();
+      // K row (this key) -> K-major SW128 tiles [128 keys][32 d] x 2, hi at +0, lo at +32 KB
+#pragma unroll 1
+      for (int kb = 0; kb < 2; ++kb) {
+        uint32_t r[32];
+        tmem_ld32(lane_base + uint32_t(kDK + kb * 32), r);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const float4 x = make_float4(__uint_as_float(r[4 * c]), __uint_as_float(r[4 * c + 1]),
+                                       __uint_as_float(r[4 * c + 2]), __uint_as_float(r[4 * c + 3]));
+          const float4 h = make_float4(tf32_rna(x.x), tf32_rna(x.y), tf32_rna(x.z), tf32_rna(x.w));
+          const uint32_t dst = base + kKop + uint32_t(kb) * 16384u + sw128(key, c);
+          sts128(dst, h);
+          sts128(dst + 32768u, make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w));
+        }
+      }
+      // V row (this key) -> Vᵀ K-major SW128 tiles [64 d][32 keys] x 4 (k-block = key / 32 = q)
+#pragma unroll 1
+      for (int hb = 0; hb < 2; ++hb) {
+        uint32_t r[32];
+        tmem_ld32(lane_base + uint32_t(2 * kDK + hb * 32), r);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int n = hb * 32 + j;
+          const float x = __uint_as_float(r[j]);
+          const float h = tf32_rna(x);
+          const uint32_t dst = base + kVop + uint32_t(q) * 8192u + sw128(n, lane >> 2) + uint32_t(lane & 3) * 4u;
+          sts32(dst, h);
+          sts32(dst + 32768u, x - h);
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(leader(A_READY));
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
+}  // namespace
+
+bool head_fused_supported(const HeadArgs& a) {
+  if (a.S < 1 || a.S > kS || a.dk != kDK || a.D < BK || a.D % BK || a.batch < 1 || !a.Wqkv || !a.Wh) return false;
+  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
+  if (!al16(a.X) || !al16(a.Z) || !al16(a.Wqkv) || !al16(a.Wh)) return false;
+  const int64_t ld = a.ldz ? a.ldz : kDK;
+  if ((a.sX | a.sZ | ld) & 3) return false;
+  return encode_fn() != nullptr;
+}
+
+cudaError_t head_fused(const HeadArgs& a, int terms, cudaStream_t s) {
+  if (!head_fused_supported(a)) return cudaErrorInvalidValue;
+  auto kernel = terms > 1 ? head_pair_kernel<3> : head_pair_kernel<1>;
+  static std::once_flag once3, once1;
+  static cudaError_t err3 = cudaSuccess, err1 = cudaSuccess;
+  std::call_once(terms > 1 ? once3 : once1, [&] {
+    (terms > 1 ? err3 : err1) = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+  });
+  if (cudaError_t e = terms > 1 ? err3 : err1) return e;
+  const uint64_t S = uint64_t(a.S), D = uint64_t(a.D), B = uint64_t(a.batch);
+  const uint64_t ldz = uint64_t(a.ldz ? a.ldz : kDK);
+  CUtensorMap mX, mW, mWh, mZ;
+  bool ok = make_map(&mX, a.X, D, S, B, D * 4, uint64_t(a.sX ? a.sX : S * D) * 4, BK, BM, true) &&
+            make_map(&mW, a.Wqkv, D, kN, 2, D * 4, uint64_t(kN) * D * 4, BK, kN / 2, true) &&
+            make_map(&mWh, a.Wh, kDK, kDK, 2, kDK * 4, uint64_t(kDK * kDK) * 4, BK, kDK / 2, true) &&
+            make_map(&mZ, a.Z, kDK, S, B, ldz * 4, uint64_t(a.sZ ? a.sZ : S * ldz) * 4, 32, 32, true);
+  if (!ok) return cudaErrorInvalidValue;
+  HeadParams p{a.S, a.D, a.batch, (a.batch + 1) / 2, a.scale};
+  const int max_pairs = num_sms() / 2;
+  const int pairs = p.pairs < max_pairs ? p.pairs : max_pairs;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2 * pairs);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, mX, mW, mWh, mZ, p);
+}
+
+}  // namespace hs

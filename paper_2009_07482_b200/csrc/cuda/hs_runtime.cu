@@ -227,10 +227,10 @@ int hs_memset(hs_stream_t s, void* dst, int value, size_t bytes) {
 int hs_op_from_name(const char* name) {
   static const char* kNames[HS_OP_COUNT] = {"gemm",    "gemm_nt", "gemm_relu", "transpose",   "scale",
                                              "softmax", "add",     "add_layernorm", "concat",
-                                             "attn_head"};
+                                             "attn_head", nullptr /* HS_OP_HEAD: engine rewrite only */};
   if (!name) return -1;
   for (int i = 0; i < HS_OP_COUNT; ++i)
-    if (std::strcmp(name, kNames[i]) == 0) return i;
+    if (kNames[i] && std::strcmp(name, kNames[i]) == 0) return i;
   return -1;
 }
 
@@ -322,6 +322,15 @@ int hs_launch(hs_stream_t st, int op, const hs_op_args* a, int math, int batch) 
                      batch, a->fparam[0]};
       if (!hs::attn_head_supported(t)) return invalid("attn_head: needs S <= 128, dk = dw = 64, 16-byte alignment");
       e = hs::attn_head(t, math == HS_MATH_TF32 ? 1 : 3, s);
+      break;
+    }
+    case HS_OP_HEAD: {
+      if (a->n_in < 2 || !a->aux || !a->in[1]) return invalid("head needs {X, Wh planes} and Wqkv planes (aux)");
+      if (math != HS_MATH_TF32X3 && math != HS_MATH_TF32) return invalid("head runs in TF32X3 / TF32 only");
+      hs::HeadArgs h{in(0), a->in_stride[0], a->aux, a->in[1], out, a->out_stride, a->out_ld,
+                     int(a->dims[0]), int(a->dims[1]), int(a->dims[2]), batch, a->fparam[0]};
+      if (!hs::head_fused_supported(h)) return invalid("head: needs S <= 128, D % 32 == 0, dk = 64, 16-byte alignment");
+      e = hs::head_fused(h, math == HS_MATH_TF32 ? 1 : 3, s);
       break;
     }
     default:

@@ -69,6 +69,24 @@ struct AttnArgs {
 bool attn_head_supported(const AttnArgs& a);
 cudaError_t attn_head(const AttnArgs& a, int terms, cudaStream_t s);
 
+// Whole transformer head (HS_OP_HEAD): [Q|K|V] = X · Wqkv, Z = softmax_row(scale · Q Kᵀ)
+// · V · Wh per instance. X is [S, D] (S <= 128, D % 32 == 0); Wqkv is pre-split into
+// tf32 hi/lo planes [2][3 dk][D] (q | k | v rows, gemm_split_weights format 0, plane
+// stride 3 dk D); Wh planes [2][dk][dk]; dk = 64. Z rows are ldz apart (0 = dk).
+struct HeadArgs {
+  const float* X;
+  int64_t sX;
+  const void* Wqkv;
+  const void* Wh;
+  float* Z;
+  int64_t sZ;
+  int64_t ldz;
+  int S, D, dk, batch;
+  float scale;
+};
+bool head_fused_supported(const HeadArgs& a);
+cudaError_t head_fused(const HeadArgs& a, int terms, cudaStream_t s);
+
 cudaError_t transpose(const float* A, int64_t sA, float* B, int64_t sB, int R, int C, int batch, cudaStream_t s);
 cudaError_t scale(const float* A, int64_t sA, float* B, int64_t sB, int64_t n, float f, int batch, cudaStream_t s);
 cudaError_t add(const float* A, int64_t sA, const float* B, int64_t sB, float* C, int64_t sC, int64_t n, int batch,

@@ -413,6 +413,11 @@ void Engine::launch_node(Slot& sl, hs_stream_t s, int kernel) {
   if (nd.epilogue == HS_EPI_SOFTMAX) a.fparam[0] = nd.escale;
   auto pl = node_planes_.find(kernel);
   a.aux = pl == node_planes_.end() ? nullptr : pl->second;
+  if (nd.op == HS_OP_HEAD) {  // in = {X, Wh planes}, aux = Wq|Wk|Wv planes
+    a.in[1] = a.aux;
+    a.in_stride[1] = 0;
+    a.aux = head_qkv_planes_.at(kernel);
+  }
   hs_ok(hs_launch(s, nd.op, &a, cfg_.math, cfg_.batch), "hs_launch");
 }
 
@@ -507,6 +512,10 @@ void Engine::issue(Slot& sl, const TaskComponent& t, const CommandQueueStructure
                   if (src == sl.edge_event.end()) fail(Errc::deadlock, "grouped launch before its producer");
                   hs_ok(hs_stream_wait(s, event(sl, src->second.first, src->second.second)), "inter-edge wait");
                 }
+          if (fg.absorbed) {  // computed by the whole-head launch of this component
+            record = true;
+            break;
+          }
           const Node& nd = nodes_.at(fg.kernels[0]);
           hs_op_args a{};
           a.n_in = 2;
@@ -752,6 +761,51 @@ void Engine::plan_chain_rewrites() {
       node_planes_[kid] = it->second.ptr;
     }
     ++rewrites_["attention_head"];
+  }
+  // head_fused: an attn_head whose Q, K, V are the three outputs of one grouped
+  // projection launch (shared X, resident tf32 planes), each feeding only this
+  // node: one HS_OP_HEAD launch computes Z from X and the grouped launch is
+  // absorbed (its commands and events stay; only its kernel is not launched).
+  if (cfg_.fuse >= 3 && plane_format() == 0) {
+    for (auto& [kid, z] : nodes_) {
+      if (z.op != HS_OP_ATTN_HEAD || z.elided) continue;
+      int prod[3] = {-1, -1, -1};
+      bool ok = true;
+      for (int i = 0; i < 3 && ok; ++i) {
+        auto al = alias_.find(z.inputs[size_t(i)]);
+        int ck, cp;
+        // the producer's single consumer edge goes to z or to a node absorbed into z
+        // (the elided gemm_nt / transpose / P·V GEMM of the attention_head rule)
+        if (al == alias_.end() || !sole_consumer(al->second, &ck, &cp) || (ck != kid && !nodes_.at(ck).elided)) {
+          ok = false;
+          break;
+        }
+        const Node& pn = nodes_.at(al->second.first);
+        if (pn.op != HS_OP_GEMM || pn.elided || pn.epilogue || pn.out_ld || pn.output != al->second ||
+            pn.dims[0] != z.dims[0] || pn.dims[1] != 64 || pn.dims[2] % 32)
+          ok = false;
+        prod[i] = al->second.first;
+      }
+      if (!ok) continue;
+      FuseGroup* fg = nullptr;
+      for (auto& g : fuse_groups_) {
+        if (g.absorbed || g.kernels.size() != 3) continue;
+        std::set<int> members(g.kernels.begin(), g.kernels.end());
+        if (members == std::set<int>{prod[0], prod[1], prod[2]}) fg = &g;
+      }
+      // the members read one X (plan_fusion grouped them by resolved A source)
+      if (!fg || fg->n != 64) continue;
+      fg->kernels = {prod[0], prod[1], prod[2]};  // plane order q | k | v (the leader event is unchanged)
+      fg->absorbed = true;
+      const std::pair<int, int> wkey = z.inputs[3];
+      z.op = HS_OP_HEAD;
+      z.inputs = {nodes_.at(prod[0]).inputs[0], wkey};
+      z.dims[1] = fg->k;
+      z.dims[2] = 64;
+      head_qkv_planes_[kid] = fg->planes;
+      --launches_per_batch_;
+      ++rewrites_["head_fused"];
+    }
   }
   for (const auto& [kid, nd] : nodes_)
     if (nd.elided) --launches_per_batch_;
@@ -1036,7 +1090,7 @@ int hs_engine_create(const char* config_json, hs_engine_t* out) {
       for (const json::Value* x : v->items()) cfg.cpu_devices.insert(x->as_int());
     if (const json::Value* v = c.find("fuse")) {
       cfg.fuse = v->as_int();
-      if (cfg.fuse < 0 || cfg.fuse > 2) fail(Errc::invalid_param, "fuse must be 0, 1 or 2");
+      if (cfg.fuse < 0 || cfg.fuse > 3) fail(Errc::invalid_param, "fuse must be 0, 1, 2 or 3");
     }
     *out = reinterpret_cast<hs_engine_t>(new Engine(std::move(cfg)));
   });

@@ -44,7 +44,7 @@ struct EngineConfig {
   // Graph-mode launch lowering: 0 = one launch per ndrange, 1 = + grouped
   // sibling GEMMs, 2 = + chain rewrites (transpose folded into gemm_nt,
   // softmax as a GEMM epilogue, concat inputs written in place).
-  int fuse = 2;
+  int fuse = 3;
   // Record a timing-event pair around every command of the first batch of each
   // run (dynamic mode: as dispatched; graph mode: the plan issued directly).
   bool trace = false;
@@ -144,6 +144,7 @@ class Engine {
   };
   std::map<std::pair<int, bool>, Planes> planes_;
   std::map<int, void*> node_planes_;  // kernel -> planes
+  std::map<int, void*> head_qkv_planes_;  // HS_OP_HEAD kernel -> its absorbed group's Wq|Wk|Wv planes
   std::map<int, Planes> attn_planes_;  // resident group -> tf32 planes for fused heads (BF16X3 engines)
 
   // Grouped launches (graph mode): sibling GEMM ndranges of one component that
@@ -155,6 +156,7 @@ class Engine {
     std::vector<int> events;
     void* planes = nullptr;
     int64_t n = 0, k = 0;  // per member
+    bool absorbed = false;  // computed inside a whole-head launch (head_fused rule): no launch of its own
   };
   void plan_fusion();
   void plan_chain_rewrites();

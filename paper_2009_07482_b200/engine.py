@@ -29,14 +29,15 @@ def _ptr_and_nbytes(arr):
 class Engine:
     def __init__(self, spec_text: str, params: dict | None = None, *, gpu: int = 0, policy: str = "clustering",
                  mode: str = "graph", batch: int = 1, slots: int = 2, math: str = "tf32x3", cpu_devices=(),
-                 fuse: int | bool = 2, trace: bool = False):
+                 fuse: int | bool = 3, trace: bool = False):
         """fuse (graph mode): 0 = one launch per ndrange; 1 = + grouped sibling GEMMs;
-        2 (default, also True) = + chain rewrites (transpose -> gemm_nt, softmax as a GEMM
-        epilogue, concat inputs written in place, fused attention heads). Dynamic mode always
-        launches per ndrange.
+        2 = + chain rewrites (transpose -> gemm_nt, softmax as a GEMM epilogue, concat
+        inputs written in place, fused attention heads); 3 (default, also True) = + each
+        head's grouped Q/K/V projection absorbed into its attention launch (one
+        HS_OP_HEAD launch per head component). Dynamic mode always launches per ndrange.
         trace: time every command of the first batch of each run with CUDA events
         (see trace(); graph mode issues that batch's plan directly instead of replaying it)."""
-        fuse = 2 if fuse is True else int(fuse)
+        fuse = 3 if fuse is True else int(fuse)
         cfg = {"spec": spec_text, "params": dict(params or {}), "gpu": gpu, "policy": policy, "mode": mode,
                "batch": batch, "slots": slots, "math": math, "cpu_devices": list(cpu_devices), "fuse": int(fuse),
                "trace": int(bool(trace))}

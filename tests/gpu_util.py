@@ -9,7 +9,7 @@ import numpy as np
 from paper_2009_07482_b200 import _native
 
 OPS = {"gemm": 0, "gemm_nt": 1, "gemm_relu": 2, "transpose": 3, "scale": 4, "softmax": 5, "add": 6,
-       "add_layernorm": 7, "concat": 8, "attn_head": 9}
+       "add_layernorm": 7, "concat": 8, "attn_head": 9, "head": 10}
 MATH = {"tf32x3": 0, "tf32": 1, "simt": 2, "bf16x3": 3}
 
 _ctx = None

@@ -292,3 +292,112 @@ def test_attn_head_bit_identical_to_unfused_chain():
     Z1 = torch.empty(batch, S * dk, device="cuda")
     launch("attn_head", [Q, K, V, W], Z1, [S, dk, dk], fparam=(0.125, 1e-5), batch=batch, aux=planes)
     assert torch.equal(Z0, Z1)
+
+
+def _head_launch(X, planes_qkv, planes_h, Z, S, D, batch, math="tf32x3", ld=0, off=0):
+    """HS_OP_HEAD through the C ABI: in = {X, Wh planes}, aux = Wq|Wk|Wv planes."""
+    import ctypes
+    import torch
+    from paper_2009_07482_b200 import _native
+    from tests.gpu_util import MATH, stream
+    torch.cuda.synchronize()
+    L = _native.lib()
+    a = _native.OpArgs()
+    a.n_in = 2
+    a.in_[0], a.in_stride[0] = X.data_ptr(), S * D
+    a.in_[1], a.in_stride[1] = planes_h.data_ptr(), 0
+    a.aux = planes_qkv.data_ptr()
+    a.out, a.out_stride, a.out_ld = Z.data_ptr() + 4 * off, Z.shape[-1], ld
+    a.dims[0], a.dims[1], a.dims[2] = S, D, 64
+    a.fparam[0] = 0.125
+    _native.check(L.hs_launch(stream(), 10, ctypes.byref(a), MATH[math], batch), "hs_launch(head)")
+    _native.check(L.hs_stream_sync(stream()), "sync")
+
+
+def _qkv_planes(Ws, D):
+    import torch
+    from paper_2009_07482_b200 import _native
+    from tests.gpu_util import stream
+    planes = torch.empty(2 * 3 * 64 * D, device="cuda")
+    torch.cuda.synchronize()
+    L = _native.lib()
+    for m, W in enumerate(Ws):
+        _native.check(L.hs_gemm_split_weights_strided(stream(), W.data_ptr(), 0, 64, D,
+                                                      planes.data_ptr() + 4 * m * 64 * D, 3 * 64 * D))
+    _native.check(L.hs_stream_sync(stream()))
+    return planes
+
+
+def _grouped_qkv(X, Ws, planes, outs, S, D, batch):
+    import ctypes
+    import torch
+    from paper_2009_07482_b200 import _native
+    from tests.gpu_util import stream
+    torch.cuda.synchronize()
+    L = _native.lib()
+    a = _native.OpArgs()
+    a.n_in = 2
+    a.in_[0], a.in_stride[0] = X.data_ptr(), S * D
+    a.in_[1], a.in_stride[1] = Ws[0].data_ptr(), 0
+    a.out, a.out_stride = outs[0].data_ptr(), S * 64
+    a.dims[0], a.dims[1], a.dims[2] = S, 64, D
+    a.aux = planes.data_ptr()
+    a.n_out = 3
+    for m in range(3):
+        a.outs[m], a.out_strides[m] = outs[m].data_ptr(), S * 64
+    _native.check(L.hs_launch(stream(), 0, ctypes.byref(a), 0, batch), "hs_launch(grouped qkv)")
+    _native.check(L.hs_stream_sync(stream()), "sync")
+
+
+@pytest.mark.parametrize("S,batch", [(128, 1), (128, 4), (128, 7), (100, 3), (128, 300)])
+def test_head_fused_bit_identical_to_grouped_qkv_and_attn_head(S, batch):
+    """HS_OP_HEAD (projection + attention in one CTA-pair kernel, Q/K/V never leave
+    the SM) equals the two launches it replaces: the grouped Q/K/V pair GEMM writing
+    Q, K, V to HBM, then the fused attention head."""
+    from tests.gpu_util import launch, split_weights
+    import torch
+    D = 512
+    X = _t(_rand(80, (batch, S * D)))
+    Ws = [_t((_rand(81 + m, (D * 64,)) * np.float32(1 / np.sqrt(D))).astype(np.float32)) for m in range(3)]
+    Wh = _t((_rand(84, (64 * 64,)) * np.float32(1 / 8)).astype(np.float32))
+    pq = _qkv_planes(Ws, D)
+    ph = split_weights(Wh, False, 64, 64)
+    Q, K, V = (torch.empty(batch, S * 64, device="cuda") for _ in range(3))
+    _grouped_qkv(X, Ws, pq, (Q, K, V), S, D, batch)
+    Z0 = torch.empty(batch, S * 64, device="cuda")
+    launch("attn_head", [Q, K, V, Wh], Z0, [S, 64, 64], fparam=(0.125, 1e-5), batch=batch, aux=ph)
+    Z1 = torch.full((batch, S * 64), -7.0, device="cuda")
+    _head_launch(X, pq, ph, Z1, S, D, batch)
+    diff = (Z0 - Z1).abs().max().item()
+    assert torch.equal(Z0, Z1), f"max |diff| {diff:.3e}"
+
+
+@pytest.mark.parametrize("math,ld", [("tf32x3", 0), ("tf32x3", 512), ("tf32", 0)])
+def test_head_fused_matches_oracle(math, ld, oracle_mod):
+    """HS_OP_HEAD against the oracle's head chain: three projection GEMMs, then
+    gemm_nt -> softmax(1/8) -> gemm -> gemm (PAPER.md:323)."""
+    from tests.gpu_util import normwise, split_weights
+    import torch
+    S, D, dk, batch = 128, 512, 64, 5
+    X = _rand(90, (batch, S * D))
+    Ws = [(_rand(91 + m, (D * dk,)) * np.float32(1 / np.sqrt(D))).astype(np.float32) for m in range(3)]
+    Wh = (_rand(94, (dk * dk,)) * np.float32(1 / 8)).astype(np.float32)
+    proj = []
+    for W in Ws:
+        out = np.empty((batch, S * dk), np.float32)
+        oracle_mod.run_node("gemm", [X, W], [S * D, 0], out, S * dk, [S, dk, D], batch)
+        proj.append(out)
+    ref = _attn_ref(oracle_mod, proj[0], proj[1], proj[2], Wh, S, batch)
+    pq = _qkv_planes([_t(W) for W in Ws], D)
+    ph = split_weights(_t(Wh), False, dk, dk)
+    width, off = (ld, 128) if ld else (dk, 0)
+    Z = torch.full((batch, S * width), -3.0, device="cuda")
+    _head_launch(_t(X), pq, ph, Z, S, D, batch, math=math, ld=ld, off=off)
+    z = Z.cpu().numpy().reshape(batch, S, width)
+    tol = TOL_TF32X3 if math == "tf32x3" else 5e-3
+    for b in range(batch):
+        assert normwise(z[b, :, off:off + dk].reshape(-1), ref[b]) <= tol, b
+    if ld:
+        mask = np.ones(width, bool)
+        mask[off:off + dk] = False
+        assert (z[:, :, mask] == -3.0).all()
