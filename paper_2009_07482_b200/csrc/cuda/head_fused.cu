@@ -42,7 +42,25 @@
 #include "kernels.cuh"
 #include "tc_common.cuh"
 
+#ifndef HS_DBG_TIMELINE
+#define HS_DBG_TIMELINE 0
+#endif
+
 namespace hs {
+
+#if HS_DBG_TIMELINE
+// timing experiment only (profiles/head_timeline.py): clock64 stamps of cluster 0,
+// CTA 0, first 8 pairs x 16 points
+__device__ long long g_head_timeline[8 * 16];
+#define TL(t, k)                                                             \
+  do {                                                                       \
+    if (pair0 == 0 && rank == 0 && (t) < 8) g_head_timeline[(t) * 16 + (k)] = clock64(); \
+  } while (0)
+#else
+#define TL(t, k) \
+  do {           \
+  } while (0)
+#endif
 
 namespace {
 
@@ -62,13 +80,15 @@ constexpr uint32_t kKop = kU;                         // phase 2: K hi/lo, 2 pla
 constexpr uint32_t kVop = kU + 65536;                 // phase 2: Vᵀ hi/lo, 2 planes x 4 k-blocks x [64][128 B]
 constexpr uint32_t kUEnd = kOpB + kNO * kOperand;     // 160 KB
 constexpr uint32_t kWh = kUEnd;                       // Whᵀ half: 2 planes x 2 k-blocks x [32][128 B] (16 KB)
-constexpr uint32_t kEpi = kWh + 16384;                // Z staging: 8 warps x [32][32] fp32 (32 KB)
-constexpr uint32_t kBar = kEpi + 32768;
+constexpr uint32_t kEpi = kWh + 16384;                // Z staging: 4 warps x 2 x [32][32] fp32 (32 KB)
+constexpr uint32_t kExch = kEpi + 32768;              // softmax row max / sum exchange: 8 warps x 2 x 32 fp32
+constexpr uint32_t kBar = kExch + 2048;
 constexpr int kSmem = int(kBar) + 512 + 1024;
 static_assert(kVop + 65536 <= kUEnd, "phase 2 operands exceed the union");
 static_assert(kSmem <= 227 * 1024, "shared memory budget exceeded");
 
 constexpr uint32_t kTQ = 256;  // TMEM A-operand region (phase 2)
+constexpr uint32_t kTZ = 448;  // Z accumulator: P lo's columns, free after P·V; outside the projection's TMEM
 constexpr uint32_t kTStage = 192;
 
 enum Bar : uint32_t {
@@ -77,13 +97,13 @@ enum Bar : uint32_t {
   OP_FULL = ST_EMPTY + kNS,  // [kNO] leader: 2 x 4 converter warps + expect_tx
   OP_EMPTY = OP_FULL + kNO,  // [kNO] each CTA (commit multicast)
   ACC_FULL = OP_EMPTY + kNO,
-  A_READY,   // leader: 2 x (8 row + 4 operand) warps
+  A_READY,   // leader: Q split + K operand, 2 x 8 warps (S = Q Kᵀ may start)
+  V_READY,   // leader: Vᵀ operand, 2 x 8 warps (P·V may start)
   S_FULL,    // each CTA
   P_READY,   // leader: 2 x 8
   O_FULL,    // each CTA
   C_READY,   // leader: 2 x 8
   Z_FULL,    // each CTA
-  Z_DONE,    // leader: 2 x 8 (Z accumulator drained)
   WH_FULL,   // leader: expect_tx
   TMEM_SLOT,
   kNumBars
@@ -118,6 +138,72 @@ __device__ __forceinline__ void split_row16(const uint32_t* r, uint32_t (&hi)[16
   }
 }
 
+// Softmax passes over this thread's 64 S values (columns c0.. of its row): the
+// max of x·scale over valid keys, then e = 2^(x·scale·log2e - max·log2e) in place
+// with their sequential sum (columns >= S give e = 0 when kMask).
+template <bool kMask>
+__device__ __forceinline__ float row_max(const uint32_t (&r0)[32], const uint32_t (&r1)[32], int c0, int S,
+                                         float scale) {
+  float mx = -INFINITY;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    if (!kMask || c0 + j < S) mx = fmaxf(mx, __uint_as_float(r0[j]) * scale);
+    if (!kMask || c0 + 32 + j < S) mx = fmaxf(mx, __uint_as_float(r1[j]) * scale);
+  }
+  return mx;
+}
+template <bool kMask>
+__device__ __forceinline__ float row_exp(uint32_t (&r0)[32], uint32_t (&r1)[32], int c0, int S, float sl, float ml) {
+  float sum = 0.f;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const float e = (!kMask || c0 + j < S) ? ex2_approx(fmaf(__uint_as_float(r0[j]), sl, -ml)) : 0.f;
+    sum = sum + e;
+    r0[j] = __float_as_uint(e);
+  }
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const float e = (!kMask || c0 + 32 + j < S) ? ex2_approx(fmaf(__uint_as_float(r1[j]), sl, -ml)) : 0.f;
+    sum = sum + e;
+    r1[j] = __float_as_uint(e);
+  }
+  return sum;
+}
+
+// K row (this key = TMEM lane) -> K-major SW128 tiles [128 keys][32 d] x 2 (hi at +0, lo at +32 KB)
+__device__ __forceinline__ void store_k_operand(uint32_t base, uint32_t lane_base, int key) {
+#pragma unroll 1
+  for (int kb = 0; kb < 2; ++kb) {
+    uint32_t r[32];
+    tmem_ld32(lane_base + uint32_t(kDK + kb * 32), r);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const float4 x = make_float4(__uint_as_float(r[4 * c]), __uint_as_float(r[4 * c + 1]),
+                                   __uint_as_float(r[4 * c + 2]), __uint_as_float(r[4 * c + 3]));
+      const float4 h = make_float4(tf32_rna(x.x), tf32_rna(x.y), tf32_rna(x.z), tf32_rna(x.w));
+      const uint32_t dst = base + kKop + uint32_t(kb) * 16384u + sw128(key, c);
+      sts128(dst, h);
+      sts128(dst + 32768u, make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w));
+    }
+  }
+}
+
+// V row (this key = TMEM lane q*32 + lane), d in [32 half, 32 half + 32) -> Vᵀ K-major
+// SW128 tiles [64 d][32 keys] (k-block = key / 32 = q; hi at +0, lo at +32 KB)
+__device__ __forceinline__ void store_vt_operand(uint32_t base, uint32_t lane_base, int q, int lane, int half) {
+  uint32_t r[32];
+  tmem_ld32(lane_base + uint32_t(2 * kDK + half * 32), r);
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const int n = half * 32 + j;
+    const float x = __uint_as_float(r[j]);
+    const float h = tf32_rna(x);
+    const uint32_t dst = base + kVop + uint32_t(q) * 8192u + sw128(n, lane >> 2) + uint32_t(lane & 3) * 4u;
+    sts32(dst, h);
+    sts32(dst + 32768u, x - h);
+  }
+}
+
 template <int kTerms>
 __global__ void __launch_bounds__(kThreads, 1)
     head_pair_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
@@ -143,8 +229,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(bar(OP_EMPTY + o), 1);
     }
     for (uint32_t b : {ACC_FULL, S_FULL, O_FULL, Z_FULL, WH_FULL}) mbar_init(bar(b), 1);
-    mbar_init(bar(A_READY), 2 * 12);
-    for (uint32_t b : {P_READY, C_READY, Z_DONE}) mbar_init(bar(b), 2 * 8);
+    mbar_init(bar(A_READY), 2 * 8);
+    mbar_init(bar(V_READY), 2 * 8);
+    for (uint32_t b : {P_READY, C_READY}) mbar_init(bar(b), 2 * 8);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (const CUtensorMap* m : {&tmX, &tmW, &tmWh, &tmZ})
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
@@ -163,14 +250,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       uint32_t it = 0, lt = 0;
       for (int t = pair0; t < p.pairs; t += npairs, ++lt) {
-        if (lt > 0) mbar_wait(bar(O_FULL), (lt - 1) & 1u);  // phase 2 operands of the last pair consumed
-        const int inst = 2 * t + int(rank);                  // >= batch: zero-filled box
+        // X stages share the K operand's smem: free once the last pair's S = Q Kᵀ is done
+        if (lt > 0) mbar_wait(bar(S_FULL), (lt - 1) & 1u);
+        const int inst = 2 * t + int(rank);  // >= batch: zero-filled box
         for (int kb = 0; kb < nk; ++kb, ++it) {
           const int s = int(it % kNS);
           mbar_wait(bar(ST_EMPTY + s), ((it / kNS) & 1u) ^ 1u);
           mbar_expect_tx(bar(ST_FULL + s), kStaging);
           tma_load_3d(base + kU + uint32_t(s) * kStaging, &tmX, bar(ST_FULL + s), kb * BK, 0, inst);
         }
+        // warm L2 with this CTA's rows of the next pair: its loads start only after
+        // phase 2, and would otherwise pay the HBM latency at the head of the pipeline
+        if (t + npairs < p.pairs)
+          for (int kb = 0; kb < nk; ++kb) tma_prefetch_3d(&tmX, kb * BK, 0, 2 * (t + npairs) + int(rank));
       }
     }
   } else if (warp == 3) {
@@ -197,7 +289,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (leader)
-    if (lane == 0 && rank == 0) {
+    // The whole warp runs the loop (warp-uniform state and descriptors); one
+    // elected lane issues each batch of tcgen05.mma and its commit.
+    if (rank == 0) {
       constexpr uint32_t m256 = uint32_t(BM >> 4) << 24;
       constexpr uint32_t idQKV = instr_desc_tf32(kN) + m256, idS = instr_desc_tf32(256) + m256,
                          idC = instr_desc_tf32(128) + m256, idZ = instr_desc_tf32(kDK) + m256;
@@ -205,154 +299,180 @@ __global__ void __launch_bounds__(kThreads, 1)
       bool wh = false;
       for (int t = pair0; t < p.pairs; t += npairs, ++lt) {
         const uint32_t ph = lt & 1u;
-        if (lt > 0) mbar_wait(bar(Z_DONE), (lt - 1) & 1u);  // C / Z accumulators of the last pair drained
-        tc_fence_after();
+        // The last pair's C accumulator [0,128) was drained before C_READY and its Z
+        // accumulator lives at [448,512): the projection may overwrite [0,192) at once
+        // (tcgen05.mma executes in issue order, after the last pair's Z MMA).
+        if (lane == 0) TL(lt, 0);
         // phase 1: [Q|K|V] = X · W
         for (int kb = 0; kb < nk; ++kb, ++it) {
           const int o = int(it % kNO);
           mbar_wait(bar(OP_FULL + o), (it / kNO) & 1u);
+          if (lane == 0 && kb == 0) TL(lt, 2);
           tc_fence_after();
           const uint32_t a_hi = tmem + kTStage + uint32_t(o) * 64u, a_lo = a_hi + 32u;
           const uint32_t b_hi = base + kOpB + uint32_t(o) * kOperand, b_lo = b_hi + kPlaneB;
+          if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < BK / 8; ++kk)
-            mma3<kTerms>(tmem, a_hi + uint32_t(kk) * 8u, a_lo + uint32_t(kk) * 8u, b_hi + uint32_t(kk) * 32u,
-                         b_lo + uint32_t(kk) * 32u, idQKV, (kb | kk) ? 1u : 0u);
-          mma_commit_pair(bar(OP_EMPTY + o));
+            for (int kk = 0; kk < BK / 8; ++kk)
+              mma3<kTerms>(tmem, a_hi + uint32_t(kk) * 8u, a_lo + uint32_t(kk) * 8u, b_hi + uint32_t(kk) * 32u,
+                           b_lo + uint32_t(kk) * 32u, idQKV, (kb | kk) ? 1u : 0u);
+            mma_commit_pair(bar(OP_EMPTY + o));
+          }
+          __syncwarp();
         }
-        mma_commit_pair(bar(ACC_FULL));
+        if (lane == 0) TL(lt, 3);
+        if (elect_one()) mma_commit_pair(bar(ACC_FULL));
+        __syncwarp();
         // S = Q Kᵀ (K = 64)
         mbar_wait(bar(A_READY), ph);
+        if (lane == 0) TL(lt, 4);
         tc_fence_after();
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < kDK / 8; ++kk) {
-          const uint32_t kbo = uint32_t(kk >> 2) * 16384u + uint32_t(kk & 3) * 32u;
-          mma3<kTerms>(tmem, tmem + kTQ + uint32_t(kk) * 8u, tmem + kTQ + 64u + uint32_t(kk) * 8u, base + kKop + kbo,
-                       base + kKop + 32768u + kbo, idS, kk ? 1u : 0u);
+          for (int kk = 0; kk < kDK / 8; ++kk) {
+            const uint32_t kbo = uint32_t(kk >> 2) * 16384u + uint32_t(kk & 3) * 32u;
+            mma3<kTerms>(tmem, tmem + kTQ + uint32_t(kk) * 8u, tmem + kTQ + 64u + uint32_t(kk) * 8u,
+                         base + kKop + kbo, base + kKop + 32768u + kbo, idS, kk ? 1u : 0u);
+          }
+          mma_commit_pair(bar(S_FULL));
         }
-        mma_commit_pair(bar(S_FULL));
+        __syncwarp();
         // C = P V (K = 128 keys)
+        mbar_wait(bar(V_READY), ph);
         mbar_wait(bar(P_READY), ph);
+        if (lane == 0) TL(lt, 5);
         tc_fence_after();
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < kS / 8; ++kk) {
-          const uint32_t kbo = uint32_t(kk >> 2) * 8192u + uint32_t(kk & 3) * 32u;
-          mma3<kTerms>(tmem, tmem + kTQ + uint32_t(kk) * 8u, tmem + kTQ + 128u + uint32_t(kk) * 8u, base + kVop + kbo,
-                       base + kVop + 32768u + kbo, idC, kk ? 1u : 0u);
+          for (int kk = 0; kk < kS / 8; ++kk) {
+            const uint32_t kbo = uint32_t(kk >> 2) * 8192u + uint32_t(kk & 3) * 32u;
+            mma3<kTerms>(tmem, tmem + kTQ + uint32_t(kk) * 8u, tmem + kTQ + 128u + uint32_t(kk) * 8u,
+                         base + kVop + kbo, base + kVop + 32768u + kbo, idC, kk ? 1u : 0u);
+          }
+          mma_commit_pair(bar(O_FULL));
         }
-        mma_commit_pair(bar(O_FULL));
+        __syncwarp();
         // Z = C Wh (K = 64)
         if (!wh) {
           mbar_wait(bar(WH_FULL), 0);
           wh = true;
         }
         mbar_wait(bar(C_READY), ph);
+        if (lane == 0) TL(lt, 6);
         tc_fence_after();
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < kDK / 8; ++kk) {
-          const uint32_t kbo = uint32_t(kk >> 2) * 4096u + uint32_t(kk & 3) * 32u;
-          mma3<kTerms>(tmem + 128u, tmem + kTQ + uint32_t(kk) * 8u, tmem + kTQ + 64u + uint32_t(kk) * 8u,
-                       base + kWh + kbo, base + kWh + 8192u + kbo, idZ, kk ? 1u : 0u);
+          for (int kk = 0; kk < kDK / 8; ++kk) {
+            const uint32_t kbo = uint32_t(kk >> 2) * 4096u + uint32_t(kk & 3) * 32u;
+            mma3<kTerms>(tmem + kTZ, tmem + kTQ + uint32_t(kk) * 8u, tmem + kTQ + 64u + uint32_t(kk) * 8u,
+                         base + kWh + kbo, base + kWh + 8192u + kbo, idZ, kk ? 1u : 0u);
+          }
+          mma_commit_pair(bar(Z_FULL));
         }
-        mma_commit_pair(bar(Z_FULL));
+        __syncwarp();
       }
     }
   } else if (warp >= 4 && warp < 12) {
     // ------------------------------------------------------------ converters (phase 1) / row warps (phase 2)
     const int q = warp & 3, g = (warp - 4) >> 2, row = q * 32 + lane;
     const uint32_t lane_base = tmem + (uint32_t(q * 32) << 16);
-    const uint32_t stage = base + kEpi + uint32_t(q * 2 + g) * 4096u;
-    const uint32_t mine = stage + uint32_t(lane) * 4u;
-    const uint32_t other = base + kEpi + uint32_t(q * 2 + (g ^ 1)) * 4096u + uint32_t(lane) * 4u;
+    const uint32_t mine = base + kExch + uint32_t(q * 2 + g) * 256u + uint32_t(lane) * 4u;
+    const uint32_t other = base + kExch + uint32_t(q * 2 + (g ^ 1)) * 256u + uint32_t(lane) * 4u;
     const float sl = p.scale * 1.4426950408889634f;
     const int col0 = int(rank) * kS;  // this CTA's block of S (its own keys)
-    uint32_t it = 0, lt = 0;
-    for (int t = pair0; t < p.pairs; t += npairs, ++lt) {
-      const uint32_t ph = lt & 1u;
-      const int inst = 2 * t + int(rank);
-      // ---- phase 1: split this CTA's X rows into the TMEM A stages (every other K-block)
-      for (int kb = 0; kb < nk; ++kb, ++it) {
-        if (int(it & 1u) != g) continue;
-        const int s = int(it % kNS), o = int(it % kNO);
-        mbar_wait(bar(ST_FULL + s), (it / kNS) & 1u);
-        mbar_wait(bar(OP_EMPTY + o), ((it / kNO) & 1u) ^ 1u);
-        tc_fence_after();
-        const uint32_t sa = base + kU + uint32_t(s) * kStaging;
-        const uint32_t ta = lane_base + kTStage + uint32_t(o) * 64u;
-#pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          uint32_t x[16], hi[16], lo[16];
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            const float4 v = lds128(sa + sw128(row, 4 * hh + c));
-            x[4 * c] = __float_as_uint(v.x); x[4 * c + 1] = __float_as_uint(v.y);
-            x[4 * c + 2] = __float_as_uint(v.z); x[4 * c + 3] = __float_as_uint(v.w);
-          }
-          split_row16<kTerms>(x, hi, lo);
-          tmem_st16(ta + uint32_t(16 * hh), hi);
-          if constexpr (kTerms > 1) tmem_st16(ta + 32u + uint32_t(16 * hh), lo);
-        }
-        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(bar(ST_EMPTY + s));
-          mbar_arrive_cluster(leader(OP_FULL + o));
-        }
-      }
-      // ---- phase 2 (A): Q columns [32g, 32g+32) -> tf32 hi [256, 320) / lo [320, 384)
-      mbar_wait(bar(ACC_FULL), ph);
+    // one K-block of X rows -> TMEM A stage (iteration `i` of the stage rings)
+    auto convert = [&](uint32_t i, int kb) {
+      const int s = int(i % kNS), o = int(i % kNO);
+      mbar_wait(bar(ST_FULL + s), (i / kNS) & 1u);
+      mbar_wait(bar(OP_EMPTY + o), ((i / kNO) & 1u) ^ 1u);
       tc_fence_after();
-      {
-        uint32_t r[32], hi[16], lo[16];
-        tmem_ld32(lane_base + uint32_t(g * 32), r);
+      const uint32_t sa = base + kU + uint32_t(s) * kStaging;
+      const uint32_t ta = lane_base + kTStage + uint32_t(o) * 64u;
+      (void)kb;
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          split_row16<kTerms>(r + 16 * hh, hi, lo);
-          const uint32_t col = kTQ + uint32_t(g * 32 + hh * 16);
-          tmem_st16(lane_base + col, hi);
-          tmem_st16(lane_base + col + 64u, lo);
+      for (int hh = 0; hh < 2; ++hh) {
+        uint32_t x[16], hi[16], lo[16];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const float4 v = lds128(sa + sw128(row, 4 * hh + c));
+          x[4 * c] = __float_as_uint(v.x); x[4 * c + 1] = __float_as_uint(v.y);
+          x[4 * c + 2] = __float_as_uint(v.z); x[4 * c + 3] = __float_as_uint(v.w);
         }
+        split_row16<kTerms>(x, hi, lo);
+        tmem_st16(ta + uint32_t(16 * hh), hi);
+        if constexpr (kTerms > 1) tmem_st16(ta + 32u + uint32_t(16 * hh), lo);
       }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(leader(A_READY));
+      if (lane == 0) {
+        mbar_arrive(bar(ST_EMPTY + s));
+        mbar_arrive_cluster(leader(OP_FULL + o));
+      }
+    };
+    uint32_t it = 0, lt = 0;
+    bool pre = false;  // this group converted the current pair's first K-block during the last pair's P·V
+    for (int t = pair0; t < p.pairs; t += npairs, ++lt) {
+      const uint32_t ph = lt & 1u;
+      // ---- phase 1: split this CTA's X rows into the TMEM A stages (every other K-block)
+      for (int kb = 0; kb < nk; ++kb, ++it) {
+        if (int(it & 1u) != g || (kb == 0 && pre)) continue;
+        convert(it, kb);
+      }
+      pre = false;
+      // ---- phase 2 (A): operands of S = Q Kᵀ and C = P V, split across 12 warps:
+      //      g = 0: Q (64 columns) -> tf32 hi [256, 320) / lo [320, 384) in TMEM
+      //      g = 1: K -> K-major smem hi/lo, and Vᵀ for d in [0, 32)
+      //      (warps 12-15: Vᵀ for d in [32, 64))
+      if (warp == 4 && lane == 0) TL(lt, 7);
+      mbar_wait(bar(ACC_FULL), ph);
+      if (warp == 4 && lane == 0) TL(lt, 8);
+      tc_fence_after();
+      if (g == 0) {  // Q -> TMEM A operand
+#pragma unroll 1
+        for (int cb = 0; cb < 2; ++cb) {
+          uint32_t r[32], hi[16], lo[16];
+          tmem_ld32(lane_base + uint32_t(cb * 32), r);
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            split_row16<kTerms>(r + 16 * hh, hi, lo);
+            const uint32_t col = kTQ + uint32_t(cb * 32 + hh * 16);
+            tmem_st16(lane_base + col, hi);
+            tmem_st16(lane_base + col + 64u, lo);
+          }
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(leader(A_READY));
+      } else {  // K, then half of Vᵀ
+        store_k_operand(base, lane_base, row);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(leader(A_READY));
+        store_vt_operand(base, lane_base, q, lane, 0);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(leader(V_READY));
+      }
       // ---- (B) softmax over this CTA's S block, columns [col0 + 64g, +64) in registers
       mbar_wait(bar(S_FULL), ph);
+      if (warp == 4 && lane == 0) TL(lt, 9);
       tc_fence_after();
       uint32_t r0[32], r1[32];
       tmem_ld32_nowait(lane_base + uint32_t(col0 + g * 64), r0);
       tmem_ld32_nowait(lane_base + uint32_t(col0 + g * 64 + 32), r1);
       tmem_ld_wait(r0);
       tmem_ld_dep(r1);
-      float mx = -INFINITY;
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        if (g * 64 + j < p.S) mx = fmaxf(mx, __uint_as_float(r0[j]) * p.scale);
-        if (g * 64 + 32 + j < p.S) mx = fmaxf(mx, __uint_as_float(r1[j]) * p.scale);
-      }
-      if (lt > 0) {  // the previous Z store has finished reading this warp's staging tile
-        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-        __syncwarp();
-      }
+      const bool full = p.S >= kS;  // warp-uniform: no key masking
+      float mx = full ? row_max<false>(r0, r1, 0, p.S, p.scale) : row_max<true>(r0, r1, g * 64, p.S, p.scale);
       sts32(mine, mx);
       named_bar(1u + uint32_t(q), 64u);
       mx = fmaxf(mx, lds32(other));
       const float ml = mx * 1.4426950408889634f;
-      float sum = 0.f;
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const float e = g * 64 + j < p.S ? ex2_approx(fmaf(__uint_as_float(r0[j]), sl, -ml)) : 0.f;
-        sum = sum + e;
-        r0[j] = __float_as_uint(e);
-      }
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const float e = g * 64 + 32 + j < p.S ? ex2_approx(fmaf(__uint_as_float(r1[j]), sl, -ml)) : 0.f;
-        sum = sum + e;
-        r1[j] = __float_as_uint(e);
-      }
+      const float sum = full ? row_exp<false>(r0, r1, 0, p.S, sl, ml) : row_exp<true>(r0, r1, g * 64, p.S, sl, ml);
       sts32(mine + 128u, sum);
       named_bar(1u + uint32_t(q), 64u);
       const float s_other = lds32(other + 128u);
@@ -375,8 +495,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(leader(P_READY));
+      // The next pair's first K-block goes to A stage 0 = TMEM [192, 256), part of S:
+      // free once every warp of this lane quarter has read S (both passed the
+      // exchange barriers above). Convert it while P·V runs (its X tile was loaded
+      // after S_FULL into the K operand's smem).
+      if (t + npairs < p.pairs && int(it & 1u) == g && it % kNO == 0) {
+        convert(it, 0);
+        pre = true;
+      }
       // ---- (C) C columns [64r + 32g, +32) -> tf32 hi [256, 320) / lo [320, 384)
       mbar_wait(bar(O_FULL), ph);
+      if (warp == 4 && lane == 0) TL(lt, 10);
       tc_fence_after();
       {
         uint32_t r[32], hi[16], lo[16];
@@ -393,69 +522,56 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(leader(C_READY));
-      // ---- (D) Z columns [32g, 32g+32) -> SW128 staging -> TMA store
+      // The next pair's A stages 1-2 overlap C hi/lo [256, 384): convert only after
+      // the Z MMA has read them. The Z accumulator is drained by warps 12-15.
+      mbar_wait(bar(Z_FULL), ph);
+      if (warp == 4 && lane == 0) TL(lt, 11);
+    }
+  } else if (warp >= 12) {
+    // ------------------------------------------------------------ operand / Z warps (phase 2)
+    const int q = warp & 3;
+    const uint32_t lane_base = tmem + (uint32_t(q * 32) << 16);
+    const uint32_t stage = base + kEpi + uint32_t(q) * 8192u;
+    uint32_t lt = 0;
+    for (int t = pair0; t < p.pairs; t += npairs, ++lt) {
+      const uint32_t ph = lt & 1u;
+      const int inst = 2 * t + int(rank);
+      mbar_wait(bar(ACC_FULL), ph);
+      tc_fence_after();
+      if (warp == 12 && lane == 0) TL(lt, 12);
+      store_vt_operand(base, lane_base, q, lane, 1);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (warp == 12 && lane == 0) TL(lt, 13);
+      if (lane == 0) mbar_arrive_cluster(leader(V_READY));
+      // Z accumulator [448, 512) -> SW128 staging (2 x [32 rows][32 cols]) -> TMA store
       mbar_wait(bar(Z_FULL), ph);
       tc_fence_after();
-      {
+#pragma unroll 1
+      for (int cb = 0; cb < 2; ++cb) {
         uint32_t r[32];
-        tmem_ld32(lane_base + 128u + uint32_t(g * 32), r);
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(leader(Z_DONE));
+        tmem_ld32(lane_base + kTZ + uint32_t(cb * 32), r);
+        const uint32_t buf = stage + uint32_t(cb) * 4096u;
+        if (lt > 0) {  // the last pair's store of this buffer has read it
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          __syncwarp();
+        }
 #pragma unroll
         for (int c = 0; c < 8; ++c)
-          sts128(stage + uint32_t(lane) * 128u + (uint32_t(c ^ (lane & 7)) << 4),
+          sts128(buf + uint32_t(lane) * 128u + (uint32_t(c ^ (lane & 7)) << 4),
                  make_float4(__uint_as_float(r[4 * c]), __uint_as_float(r[4 * c + 1]), __uint_as_float(r[4 * c + 2]),
                              __uint_as_float(r[4 * c + 3])));
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
-        if (lane == 0 && inst < p.batch) tma_store_3d(&tmZ, stage, g * 32, q * 32, inst);
+        if (lane == 0) {
+          if (inst < p.batch) tma_store_3d(&tmZ, buf, cb * 32, q * 32, inst);
+          else asm volatile("cp.async.bulk.commit_group;" ::: "memory");  // keep the group count per buffer
+        }
       }
+      tc_fence_before();
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-  } else if (warp >= 12) {
-    // ------------------------------------------------------------ K / V operand warps (phase 2)
-    const int q = warp & 3, key = q * 32 + lane;
-    const uint32_t lane_base = tmem + (uint32_t(q * 32) << 16);
-    uint32_t lt = 0;
-    for (int t = pair0; t < p.pairs; t += npairs, ++lt) {
-      mbar_wait(bar(ACC_FULL), lt & 1u);
-      tc_fence_after();
-      // K row (this key) -> K-major SW128 tiles [128 keys][32 d] x 2, hi at +0, lo at +32 KB
-#pragma unroll 1
-      for (int kb = 0; kb < 2; ++kb) {
-        uint32_t r[32];
-        tmem_ld32(lane_base + uint32_t(kDK + kb * 32), r);
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const float4 x = make_float4(__uint_as_float(r[4 * c]), __uint_as_float(r[4 * c + 1]),
-                                       __uint_as_float(r[4 * c + 2]), __uint_as_float(r[4 * c + 3]));
-          const float4 h = make_float4(tf32_rna(x.x), tf32_rna(x.y), tf32_rna(x.z), tf32_rna(x.w));
-          const uint32_t dst = base + kKop + uint32_t(kb) * 16384u + sw128(key, c);
-          sts128(dst, h);
-          sts128(dst + 32768u, make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w));
-        }
-      }
-      // V row (this key) -> Vᵀ K-major SW128 tiles [64 d][32 keys] x 4 (k-block = key / 32 = q)
-#pragma unroll 1
-      for (int hb = 0; hb < 2; ++hb) {
-        uint32_t r[32];
-        tmem_ld32(lane_base + uint32_t(2 * kDK + hb * 32), r);
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int n = hb * 32 + j;
-          const float x = __uint_as_float(r[j]);
-          const float h = tf32_rna(x);
-          const uint32_t dst = base + kVop + uint32_t(q) * 8192u + sw128(n, lane >> 2) + uint32_t(lane & 3) * 4u;
-          sts32(dst, h);
-          sts32(dst + 32768u, x - h);
-        }
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(leader(A_READY));
-    }
   }
   tc_fence_before();
   cluster_sync_all();
@@ -466,6 +582,20 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 }  // namespace
+
+}  // namespace hs
+
+// timing experiment only: copy the debug timeline (8 x 16 clock64 stamps) to host
+extern "C" int hs_debug_head_timeline(long long* out) {
+#if HS_DBG_TIMELINE
+  return cudaMemcpyFromSymbol(out, hs::g_head_timeline, sizeof(long long) * 128) == cudaSuccess ? 0 : 1;
+#else
+  (void)out;
+  return 1;
+#endif
+}
+
+namespace hs {
 
 bool head_fused_supported(const HeadArgs& a) {
   if (a.S < 1 || a.S > kS || a.dk != kDK || a.D < BK || a.D % BK || a.batch < 1 || !a.Wqkv || !a.Wh) return false;

@@ -1,0 +1,45 @@
+"""Per-pair phase timeline of the whole-head kernel (needs a library built with
+-DHS_DBG_TIMELINE=1, e.g. variants/build.sh timeline "-DHS_DBG_TIMELINE=1" and
+HETSIM_LIB=variants/lib_timeline.so). clock64 cycles relative to pair 0's start.
+usage: python profiles/head_timeline.py [batch=296]"""
+import ctypes
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+from paper_2009_07482_b200 import _native  # noqa: E402
+from tests.gpu_util import split_weights, stream  # noqa: E402
+from tests.test_gpu_kernels import _qkv_planes  # noqa: E402
+
+L = _native.lib()
+S, D = 128, 512
+batch = int(sys.argv[1]) if len(sys.argv) > 1 else 296
+X = torch.randn(batch, S * D, device="cuda")
+Ws = [torch.randn(D * 64, device="cuda") / np.sqrt(D) for _ in range(3)]
+Wh = torch.randn(64 * 64, device="cuda") / 8
+pq, ph = _qkv_planes(Ws, D), split_weights(Wh, False, 64, 64)
+Z = torch.empty(batch, S * 64, device="cuda")
+h = _native.OpArgs()
+h.n_in = 2
+h.in_[0], h.in_stride[0] = X.data_ptr(), S * D
+h.in_[1], h.in_stride[1] = ph.data_ptr(), 0
+h.aux = pq.data_ptr()
+h.out, h.out_stride = Z.data_ptr(), S * 64
+h.dims[0], h.dims[1], h.dims[2] = S, D, 64
+h.fparam[0] = 0.125
+torch.cuda.synchronize()
+for _ in range(3):
+    _native.check(L.hs_launch(stream(), 10, ctypes.byref(h), 0, batch))
+_native.check(L.hs_stream_sync(stream()))
+buf = (ctypes.c_longlong * 128)()
+L.hs_debug_head_timeline.argtypes = [ctypes.c_void_p]
+assert L.hs_debug_head_timeline(ctypes.cast(buf, ctypes.c_void_p)) == 0, "library built without HS_DBG_TIMELINE"
+tl = np.array(buf[:], dtype=np.int64).reshape(8, 16)
+names = ["mma:start", "mma:z_done", "mma:op_full0", "mma:qkv_issued", "mma:a_ready", "mma:p_ready", "mma:c_ready",
+         "row:tile_start", "row:acc_full", "row:s_full", "row:o_full", "row:z_full", "kv:acc_full", "kv:done"]
+t0 = tl[0, 0]
+tiles = (batch + 1) // 2 // 74 + (1 if ((batch + 1) // 2) % 74 else 0)
+for t in range(min(tiles, 8)):
+    print(f"pair-tile {t}: " + "  ".join(f"{n}={tl[t, k] - t0}" for k, n in enumerate(names)))
