@@ -254,6 +254,91 @@ def gemm_roofline(batch, math_mode, reps=20):
     return flops / t / 1e12, t * 1e3, flops
 
 
+def _time_launches(L, st, launch, reps):
+    """CUDA events on the launching stream around `reps` launches (after 3 warm-up)."""
+    import ctypes
+
+    from paper_2009_07482_b200 import _native
+    ctx, e0, e1 = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+    _native.check(L.hs_ctx_create(0, ctypes.byref(ctx)))
+    _native.check(L.hs_event_create(ctx, 1, ctypes.byref(e0)))
+    _native.check(L.hs_event_create(ctx, 1, ctypes.byref(e1)))
+    for _ in range(3):
+        launch()
+    _native.check(L.hs_stream_sync(st))
+    _native.check(L.hs_event_record(e0, st))
+    for _ in range(reps):
+        launch()
+    _native.check(L.hs_event_record(e1, st))
+    _native.check(L.hs_event_sync(e1))
+    ns = ctypes.c_int64()
+    _native.check(L.hs_event_elapsed_ns(e0, e1, ctypes.byref(ns)))
+    for h in (e0, e1):
+        L.hs_event_destroy(h)
+    L.hs_ctx_destroy(ctx)
+    return ns.value / 1e9 / reps
+
+
+def kernel_rooflines(batch, peak_tflops, hbm_gbs, reps=20):
+    """The other two kernels of the C5 plan, launched as the DAG launches them:
+    the whole-head kernel (HS_OP_HEAD, tensor-bound; algorithmic flops of the head
+    chain, 2*S*192*D + 2*2*S*S*64 + 2*S*64*64 per instance) and add_layernorm
+    (HBM-bound; 3*R*C*4 + 8*C bytes per instance)."""
+    import ctypes
+
+    import torch
+
+    from paper_2009_07482_b200 import _native
+    L = _native.lib()
+    S, D, dk = 128, 512, 64
+    ctx, st = ctypes.c_void_p(), ctypes.c_void_p()
+    _native.check(L.hs_ctx_create(0, ctypes.byref(ctx)))
+    _native.check(L.hs_stream_create(ctx, 0, ctypes.byref(st)))
+    X = torch.randn(batch, S * D, device="cuda")
+    Wqkv = torch.randn(3, D * dk, device="cuda") / 22.6
+    Wh = torch.randn(dk * dk, device="cuda") / 8
+    pq = torch.empty(2 * 3 * dk * D, device="cuda")
+    ph = torch.empty(2 * dk * dk, device="cuda")
+    Z = torch.empty(batch, S * dk, device="cuda")
+    torch.cuda.synchronize()
+    for m in range(3):
+        _native.check(L.hs_gemm_split_weights_strided(st, Wqkv[m].data_ptr(), 0, dk, D, pq.data_ptr() + 4 * m * dk * D,
+                                                      3 * dk * D))
+    _native.check(L.hs_gemm_split_weights(st, Wh.data_ptr(), 0, dk, dk, ph.data_ptr()))
+    h = _native.OpArgs()
+    h.n_in = 2
+    h.in_[0], h.in_stride[0] = X.data_ptr(), S * D
+    h.in_[1], h.in_stride[1] = ph.data_ptr(), 0
+    h.aux = pq.data_ptr()
+    h.out, h.out_stride = Z.data_ptr(), S * dk
+    h.dims[0], h.dims[1], h.dims[2] = S, D, dk
+    h.fparam[0] = 0.125
+    t_head = _time_launches(L, st, lambda: _native.check(L.hs_launch(st, 10, ctypes.byref(h), 0, batch)), reps)
+    f_head = batch * (2.0 * S * 3 * dk * D + 2.0 * 2 * S * S * dk + 2.0 * S * dk * dk)
+    A, B2, Y = (torch.randn(batch, S * D, device="cuda") for _ in range(3))
+    g, be = torch.ones(D, device="cuda"), torch.zeros(D, device="cuda")
+    torch.cuda.synchronize()
+    a = _native.OpArgs()
+    a.n_in = 4
+    for i, t in enumerate((A, B2, g, be)):
+        a.in_[i], a.in_stride[i] = t.data_ptr(), (0 if t.dim() == 1 else S * D)
+    a.out, a.out_stride = Y.data_ptr(), S * D
+    a.dims[0], a.dims[1] = S, D
+    a.fparam[0], a.fparam[1] = 1.0, 1e-5
+    t_ln = _time_launches(L, st, lambda: _native.check(L.hs_launch(st, 7, ctypes.byref(a), 0, batch)), reps)
+    b_ln = batch * (3.0 * S * D * 4) + 8.0 * D
+    L.hs_stream_destroy(st)
+    L.hs_ctx_destroy(ctx)
+    return [
+        {"kernel": f"head_pair_kernel (HS_OP_HEAD: Q/K/V projection + attention) x{batch}", "bound": "tensor",
+         "achieved": f_head / t_head / 1e12, "peak": peak_tflops, "unit": "TFLOP/s",
+         "frac": f_head / t_head / 1e12 / peak_tflops, "ms_per_launch": t_head * 1e3,
+         "note": "algorithmic flops; the kernel also computes 2x the QK^T and P.V flops (off-diagonal pair blocks)"},
+        {"kernel": f"add_ln_kernel x{batch}", "bound": "hbm", "achieved": b_ln / t_ln / 1e9, "peak": hbm_gbs,
+         "unit": "GB/s", "frac": b_ln / t_ln / 1e9 / hbm_gbs, "ms_per_launch": t_ln * 1e3},
+    ]
+
+
 def matmul_peak(dtype):
     """cuBLAS dense throughput at 8192^3 in-run: torch.float32 with TF32 enabled, or bf16."""
     import torch
@@ -515,6 +600,7 @@ def run_ours(args, world, rank, local):
                    "sample": f"12 instances of the {args.layers}-layer DAG ({t:.1f} s; oracle port: clustering "
                              f"scheduler + fp32 kernels on all host threads)"}
         makespans = None if args.no_makespans else config_makespans()
+        others = kernel_rooflines(args.batch, peak, pk["hbm_gbs"]) if args.math in ("tf32x3", "tf32") else None
         flop_per_inst = 782.2e6 * args.layers
         dtypes = {"tf32x3": "f32 (3xTF32 split on tcgen05, fp32-accurate)",
                   "bf16x3": "f32 (bf16x3 split on tcgen05 for weight GEMMs, 3xTF32 elsewhere; <=1e-4)",
@@ -543,6 +629,7 @@ def run_ours(args, world, rank, local):
                              "frac_of_peak": flop_per_inst * value / 1e12 / (peak * world),
                              "t_star_ms": args.instances * flop_per_inst / (peak * world * 1e12) * 1e3,
                              "note": "T* = instances x flop/DAG / P (compute-bound, SURVEY.md 8d); frac_of_peak = T*/ms_per_step"},
+            "roofline_other_kernels": others,
             "makespans": makespans,
             "parity": parity,
             "alt_math": alt,
