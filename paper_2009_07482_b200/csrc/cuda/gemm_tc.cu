@@ -1085,6 +1085,11 @@ cudaError_t gemm_tcgen05(const GemmArgs& a, int terms, cudaStream_t s) {
   // short K (attention-sized GEMMs): 64-wide tiles, two CTAs per SM
   if (a.K <= 4 * BK && a.N <= 128 && HS_SMALL_GEMM) return launch_bn<64, true>(a, terms, s);
   if (a.N <= 64) return launch_bn<64>(a, terms, s);
+  // Latency-bound launches (a single instance's FFN, a 256^2 GEMM): when 128-wide
+  // tiles would leave most SMs idle, 64-wide tiles halve each CTA's serial K loop
+  // and double the CTAs working on it.
+  const int tiles128 = row_blocks * ((a.N + 127) / 128);
+  if (2 * tiles128 <= num_sms() / 2) return launch_bn<64>(a, terms, s);
   return launch_bn<128>(a, terms, s);
 }
 
