@@ -122,14 +122,22 @@ class ClockSampler:
 
 
 def dist_setup():
+    """One process per GPU (torchrun env). HS_BENCH_SHARED_GPU=1 is a test hook for
+    1-GPU boxes: every rank drives cuda:0 and the timing collectives use gloo, so the
+    multi-rank logic (partition, barrier, max over ranks) runs end to end."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if os.environ.get("HS_BENCH_SHARED_GPU") == "1":
+            local = 0
+            torch.cuda.set_device(0)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return world, rank, local
 
 
@@ -144,7 +152,8 @@ def reduce_max(world, x, local):
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+    dev = "cpu" if dist.get_backend() == "gloo" else f"cuda:{local}"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 

@@ -1,0 +1,44 @@
+"""bench.py end to end on the GPU at a small size: one rank, and two ranks under
+torchrun sharing the box's GPU (HS_BENCH_SHARED_GPU=1: gloo for the timing
+collectives), so the multi-rank partition / barrier / max-over-ranks path runs."""
+import json
+import os
+import pathlib
+import subprocess
+import sys
+
+import pytest
+
+ROOT = pathlib.Path(__file__).resolve().parents[1]
+ARGS = ["--instances", "128", "--batch", "64", "--layers", "2", "--steps", "1", "--warmup", "3", "--no-alt",
+        "--no-cpu-baseline", "--no-makespans"]
+
+
+def _line(out):
+    lines = [ln for ln in out.splitlines() if ln.startswith("{")]
+    assert lines, out[-2000:]
+    return json.loads(lines[-1])
+
+
+@pytest.mark.gpu
+def test_bench_single_rank():
+    p = subprocess.run([sys.executable, "bench.py", *ARGS], cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-2000:]
+    line = _line(p.stdout)
+    assert line["n_gpus"] == 1 and line["value"] > 0 and line["gpu_launches"] > 0
+    assert line["parity"]["normwise_err_vs_cpu_oracle"] <= 1e-4
+    assert line["e2e"]["h2d_bytes_per_step"] == 128 * 128 * 512 * 4
+
+
+@pytest.mark.gpu
+def test_bench_two_ranks_partition_the_stream():
+    env = dict(os.environ, HS_BENCH_SHARED_GPU="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", "29561", "bench.py", "--gpus", "2", *ARGS]
+    p = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
+    assert p.returncode == 0, p.stderr[-3000:]
+    line = _line(p.stdout)
+    assert line["n_gpus"] == 2 and line["value"] > 0
+    assert line["config"]["parallelism"] == "instance partition x2"
+    # rank 0 checks its own first instance (instance 0) against the oracle
+    assert line["parity"]["instance"] == 0 and line["parity"]["normwise_err_vs_cpu_oracle"] <= 1e-4
