@@ -85,6 +85,10 @@ int hs_memcpy_h2d(hs_stream_t s, void* dst, const void* src, size_t bytes);
 int hs_memcpy_d2h(hs_stream_t s, void* dst, const void* src, size_t bytes);
 int hs_memcpy_d2d(hs_stream_t s, void* dst, const void* src, size_t bytes);
 int hs_memcpy_peer(hs_stream_t s, void* dst, int dst_gpu, const void* src, int src_gpu, size_t bytes);
+/* Let kernels and copies of ctx `a`'s GPU reach ctx `b`'s memory directly over
+ * NVLink (cudaDeviceEnablePeerAccess); a no-op for the same GPU or when the
+ * pair has no peer path (peer copies then stage through the host). */
+int hs_ctx_enable_peer(hs_ctx_t a, hs_ctx_t b);
 int hs_memset(hs_stream_t s, void* dst, int value, size_t bytes);
 /* Strided copy of `height` rows of `width` bytes; kind 0=H2D 1=D2H 2=D2D 3=default. */
 int hs_memcpy_2d(hs_stream_t s, void* dst, size_t dpitch, const void* src, size_t spitch, size_t width,

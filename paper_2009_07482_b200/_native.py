@@ -83,6 +83,7 @@ _PROTOS = {
     "hs_memcpy_d2h": (c_int, [c_void_p, c_void_p, c_void_p, c_size_t]),
     "hs_memcpy_d2d": (c_int, [c_void_p, c_void_p, c_void_p, c_size_t]),
     "hs_memcpy_peer": (c_int, [c_void_p, c_void_p, c_int, c_void_p, c_int, c_size_t]),
+    "hs_ctx_enable_peer": (c_int, [c_void_p, c_void_p]),
     "hs_memset": (c_int, [c_void_p, c_void_p, c_int, c_size_t]),
     "hs_memcpy_2d": (c_int, [c_void_p, c_void_p, c_size_t, c_void_p, c_size_t, c_size_t, c_size_t, c_int]),
     "hs_op_from_name": (c_int, [c_char_p]),

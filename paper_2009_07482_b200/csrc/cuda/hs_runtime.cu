@@ -217,7 +217,25 @@ int hs_memcpy_d2d(hs_stream_t s, void* dst, const void* src, size_t bytes) {
 }
 int hs_memcpy_peer(hs_stream_t s, void* dst, int dst_gpu, const void* src, int src_gpu, size_t bytes) {
   if (!s) return invalid("null stream");
+  if (int r = use_device(s->gpu)) return r;
+  if (dst_gpu == src_gpu)  // one GPU (e.g. two memory domains of a 1-GPU engine): a device copy
+    return check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, s->s), "cudaMemcpyAsync");
   return check(cudaMemcpyPeerAsync(dst, dst_gpu, src, src_gpu, bytes, s->s), "cudaMemcpyPeerAsync");
+}
+
+int hs_ctx_enable_peer(hs_ctx_t a, hs_ctx_t b) {
+  if (!a || !b) return invalid("null context");
+  if (a->gpu == b->gpu) return HS_OK;
+  int can = 0;
+  if (int r = check(cudaDeviceCanAccessPeer(&can, a->gpu, b->gpu), "cudaDeviceCanAccessPeer")) return r;
+  if (!can) return HS_OK;
+  if (int r = use_device(a->gpu)) return r;
+  cudaError_t e = cudaDeviceEnablePeerAccess(b->gpu, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    return HS_OK;
+  }
+  return check(e, "cudaDeviceEnablePeerAccess");
 }
 int hs_memset(hs_stream_t s, void* dst, int value, size_t bytes) {
   if (!s) return invalid("null stream");

@@ -83,24 +83,91 @@ Engine::Engine(EngineConfig cfg) : cfg_(std::move(cfg)) {
       fail(Errc::invalid_param, "device " + std::to_string(d.id) + " is a CPU device; the B200 executor has no CPU path");
   sched_ = std::make_unique<Scheduler>(g_, platform_, Profiles{}, cfg_.policy);
   build_nodes();
-  hs_ok(hs_ctx_create(cfg_.gpu, &ctx_), "hs_ctx_create");
+  // Memory domains: one per physical GPU the logical devices map to (or per
+  // logical device with domain_per_device). Domain 0 hosts the origin streams.
+  std::map<long long, int> dom_of_key;
+  for (const auto& d : platform_.devices) {
+    auto it = cfg_.device_gpus.find(d.id);
+    const int gpu = it == cfg_.device_gpus.end() ? cfg_.gpu : it->second;
+    const long long key = cfg_.domain_per_device ? (1LL << 40) + d.id : gpu;
+    auto [pos, fresh] = dom_of_key.emplace(key, int(dom_gpu_.size()));
+    if (fresh) dom_gpu_.push_back(gpu);
+    dev_dom_[d.id] = pos->second;
+  }
+  if (dom_gpu_.empty()) dom_gpu_.push_back(cfg_.gpu);
+  if (dom_gpu_.size() > 1 && !cfg_.graph_mode)
+    fail(Errc::invalid_param, "components mapped to several GPUs need graph mode (the plan fixes their placement)");
+  for (int gpu : dom_gpu_) {
+    hs_ctx_t c = nullptr;
+    hs_ok(hs_ctx_create(gpu, &c), "hs_ctx_create");
+    dctx_.push_back(c);
+  }
+  ctx_ = dctx_.front();
+  for (size_t a = 0; a < dctx_.size(); ++a)
+    for (size_t b = 0; b < dctx_.size(); ++b)
+      if (dom_gpu_[a] != dom_gpu_[b]) {
+        hs_ok(hs_ctx_enable_peer(dctx_[a], dctx_[b]), "hs_ctx_enable_peer");
+        capture_ok_ = false;  // the plan is issued directly on several GPUs
+      }
+}
+
+int Engine::kdom(int kernel) const {
+  auto it = kernel_dom_.find(kernel);
+  return it == kernel_dom_.end() ? 0 : it->second;
+}
+
+void* Engine::dalloc(int dom, int64_t bytes) {
+  void* p = nullptr;
+  hs_ok(hs_malloc(dctx_[size_t(dom)], size_t(bytes), &p), "hs_malloc");
+  allocations_.push_back({dom, p});
+  device_bytes_ += bytes;
+  return p;
+}
+
+hs_stream_t Engine::dstream(Slot& sl, int dom) {
+  if (dom == 0) return sl.origin;
+  auto it = sl.dorigin.find(dom);
+  if (it != sl.dorigin.end()) return it->second;
+  hs_stream_t s = nullptr;
+  hs_ok(hs_stream_create(dctx_[size_t(dom)], 0, &s), "hs_stream_create");
+  stream_dom_[s] = dom;
+  hs_event_t a = nullptr, b = nullptr;
+  hs_ok(hs_event_create(dctx_[size_t(dom)], 0, &a), "hs_event_create");
+  hs_ok(hs_event_create(dctx_[size_t(dom)], 0, &b), "hs_event_create");
+  sl.din[dom] = a;
+  sl.dout[dom] = b;
+  sl.dorigin[dom] = s;
+  return s;
+}
+
+// Graph mode: the plan's component -> logical device choice fixes every
+// kernel's memory domain before buffers are placed.
+void Engine::place_components() {
+  for (const auto& rec : plan_.dispatches) comp_dom_[rec.component] = dev_dom_.at(rec.device);
+  for (const auto& t : sched_->components())
+    for (int k : t.kernel_ids) kernel_dom_[k] = comp_dom_.count(t.id) ? comp_dom_.at(t.id) : 0;
 }
 
 Engine::~Engine() {
   if (!ctx_) return;
-  hs_ctx_sync(ctx_);
+  for (hs_ctx_t c : dctx_) hs_ctx_sync(c);
   clear_trace();
   for (auto& sl : slots_) {
     hs_graph_destroy(sl.graph);
     for (auto& [k, e] : sl.events) hs_event_destroy(e);
     for (auto& [k, e] : sl.group_event) hs_event_destroy(e);
+    for (auto& [k, e] : sl.din) hs_event_destroy(e);
+    for (auto& [k, e] : sl.dout) hs_event_destroy(e);
+    hs_event_destroy(sl.copy_fork);
+    hs_event_destroy(sl.copy_join);
     hs_event_destroy(sl.t_start);
     hs_event_destroy(sl.t_end);
     for (auto& [k, s] : sl.streams) hs_stream_destroy(s);
+    for (auto& [k, s] : sl.dorigin) hs_stream_destroy(s);
     hs_stream_destroy(sl.origin);
   }
-  for (void* p : allocations_) hs_free(ctx_, p);
-  hs_ctx_destroy(ctx_);
+  for (auto [dom, p] : allocations_) hs_free(dctx_[size_t(dom)], p);
+  for (hs_ctx_t c : dctx_) hs_ctx_destroy(c);
 }
 
 void Engine::build_nodes() {
@@ -209,8 +276,10 @@ void Engine::plan_buffers() {
       auto pe = producers.find(key);
       if (pe != producers.end()) {
         const DagEdge& e = g_.edges[size_t(pe->second)];
-        if (b->kind == BufferKind::io) io_copy_[key] = {e.src_kernel, e.src_pos};
-        else alias_[key] = {e.src_kernel, e.src_pos};
+        const std::pair<int, int> src{e.src_kernel, e.src_pos};
+        if (kdom(k.id) != kdom(e.src_kernel)) peer_in_[key] = src;  // one peer copy per batch
+        else if (b->kind == BufferKind::io) io_copy_[key] = src;
+        else alias_[key] = src;
         continue;
       }
       auto bi = bindings_.find(key);
@@ -239,33 +308,28 @@ void Engine::plan_buffers() {
       if (ec.read_class.at(key) == CopyClass::isolated && bindings_.count(key)) outputs_.push_back(key);
     }
   }
-  // resident groups: one allocation per engine
-  for (size_t gi = 0; gi < groups_.size(); ++gi) {
-    if (!groups_[gi].resident) continue;
-    void* p = nullptr;
-    hs_ok(hs_malloc(ctx_, size_t(groups_[gi].bytes), &p), "hs_malloc");
-    allocations_.push_back(p);
-    device_bytes_ += groups_[gi].bytes;
-    resident_buf_[int(gi)] = p;
-  }
+  // resident groups: one copy per domain that reads them
+  for (const auto& [key, gi] : group_of_)
+    if (groups_[size_t(gi)].resident && !resident_.count({gi, kdom(key.first)}))
+      resident_[{gi, kdom(key.first)}] = dalloc(kdom(key.first), groups_[size_t(gi)].bytes);
   // GEMM nodes whose B operand is a resident weight get it pre-split once
   // (tf32 hi/lo, K-major) so the tensor cores are fed by TMA with no conversion.
   if (cfg_.math != HS_MATH_FP32_SIMT) {
     for (const auto& [kid, nd] : nodes_) {
+      const int dom = kdom(kid);
       if (nd.op == HS_OP_ATTN_HEAD) {  // spec-level fused head: W must be resident, tf32 planes
         auto gi = group_of_.find(nd.inputs[3]);
         if (gi == group_of_.end() || !groups_[size_t(gi->second)].resident)
           fail(Errc::invalid_param, "attn_head kernel " + std::to_string(kid) + ": W must be bound as shared (resident)");
-        auto it = attn_planes_.find(gi->second);
+        auto it = attn_planes_.find({gi->second, dom});
         if (it == attn_planes_.end()) {
           Planes pl;
           pl.gi = gi->second;
           pl.n = nd.dims[2];
           pl.k = nd.dims[1];
-          hs_ok(hs_malloc(ctx_, size_t(2 * pl.n * pl.k * 4), &pl.ptr), "hs_malloc");
-          allocations_.push_back(pl.ptr);
-          device_bytes_ += 2 * pl.n * pl.k * 4;
-          it = attn_planes_.emplace(gi->second, pl).first;
+          pl.dom = dom;
+          pl.ptr = dalloc(dom, 2 * pl.n * pl.k * 4);
+          it = attn_planes_.emplace(std::make_pair(gi->second, dom), pl).first;
         }
         node_planes_[kid] = it->second.ptr;
         continue;
@@ -274,7 +338,7 @@ void Engine::plan_buffers() {
       auto gi = group_of_.find(nd.inputs[1]);
       if (gi == group_of_.end() || !groups_[size_t(gi->second)].resident) continue;
       const bool nt = nd.op == HS_OP_GEMM_NT;
-      auto key = std::make_pair(gi->second, nt);
+      auto key = std::make_tuple(gi->second, nt, dom);
       auto it = planes_.find(key);
       if (it == planes_.end()) {
         Planes pl;
@@ -282,9 +346,8 @@ void Engine::plan_buffers() {
         pl.nt = nt;
         pl.n = nd.dims[1];
         pl.k = nd.dims[2];
-        hs_ok(hs_malloc(ctx_, size_t(2 * pl.n * pl.k * plane_elem_bytes()), &pl.ptr), "hs_malloc");
-        allocations_.push_back(pl.ptr);
-        device_bytes_ += 2 * pl.n * pl.k * plane_elem_bytes();
+        pl.dom = dom;
+        pl.ptr = dalloc(dom, 2 * pl.n * pl.k * plane_elem_bytes());
         it = planes_.emplace(key, pl).first;
       }
       node_planes_[kid] = it->second.ptr;
@@ -293,58 +356,65 @@ void Engine::plan_buffers() {
   const int64_t B = cfg_.batch;
   slots_.resize(size_t(cfg_.slots));
   for (auto& sl : slots_) {
-    auto alloc = [&](int64_t bytes) {
-      void* p = nullptr;
-      hs_ok(hs_malloc(ctx_, size_t(bytes * B), &p), "hs_malloc");
-      allocations_.push_back(p);
-      device_bytes_ += bytes * B;
-      return p;
-    };
     for (const auto& k : g_.kernels)
-      for (const auto* b : k.output_side()) sl.buf[{k.id, b->pos}] = alloc(bytes_.at({k.id, b->pos}));
-    for (size_t gi = 0; gi < groups_.size(); ++gi) {
-      if (groups_[gi].resident) continue;
-      if (groups_[gi].io) continue;  // io group lives in the (kernel,pos) output allocation
-      sl.group_buf[int(gi)] = alloc(groups_[gi].bytes);
-    }
+      for (const auto* b : k.output_side()) sl.buf[{k.id, b->pos}] = dalloc(kdom(k.id), bytes_.at({k.id, b->pos}) * B);
     for (const auto& [key, gi] : group_of_) {
-      if (groups_[size_t(gi)].io) sl.group_buf[gi] = sl.buf.at(key);
-      sl.buf[key] = groups_[size_t(gi)].resident ? resident_buf_.at(gi) : sl.group_buf.at(gi);
+      const Group& gr = groups_[size_t(gi)];
+      const int dom = kdom(key.first);
+      if (gr.resident) {
+        sl.buf[key] = resident_.at({gi, dom});
+        continue;
+      }
+      if (gr.io) sl.group_buf[{gi, dom}] = sl.buf.at(key);  // io group lives in the (kernel,pos) allocation
+      else if (!sl.group_buf.count({gi, dom})) sl.group_buf[{gi, dom}] = dalloc(dom, gr.bytes * B);
+      sl.buf[key] = sl.group_buf.at({gi, dom});
     }
     for (const auto& [key, src] : alias_) sl.buf[key] = sl.buf.at(src);
+    for (const auto& [key, src] : peer_in_)
+      if (!sl.buf.count(key)) sl.buf[key] = dalloc(kdom(key.first), bytes_.at(key) * B);  // io inputs reuse their output
     hs_ok(hs_stream_create(ctx_, 0, &sl.origin), "hs_stream_create");
+    stream_dom_[sl.origin] = 0;
     hs_ok(hs_event_create(ctx_, 1, &sl.t_start), "hs_event_create");
     hs_ok(hs_event_create(ctx_, 1, &sl.t_end), "hs_event_create");
+    if (dctx_.size() > 1) {
+      hs_ok(hs_event_create(ctx_, 0, &sl.copy_fork), "hs_event_create");
+      hs_ok(hs_event_create(ctx_, 0, &sl.copy_join), "hs_event_create");
+      for (size_t d = 1; d < dctx_.size(); ++d) dstream(sl, int(d));
+    }
   }
   launches_per_batch_ = int64_t(g_.kernels.size());
 }
 
 void Engine::upload_resident() {
   if (resident_uploaded_) return;
-  hs_stream_t s = slots_.front().origin;
-  for (const auto& [gi, dst] : resident_buf_) {
-    const Group& gr = groups_[size_t(gi)];
-    hs_ok(hs_memcpy_2d(s, dst, size_t(gr.bytes), gr.b.ptr, size_t(gr.bytes), size_t(gr.bytes), 1, gr.b.on_device ? 2 : 0),
+  Slot& s0 = slots_.front();
+  for (const auto& [gd, dst] : resident_) {
+    const Group& gr = groups_[size_t(gd.first)];
+    hs_ok(hs_memcpy_2d(dstream(s0, gd.second), dst, size_t(gr.bytes), gr.b.ptr, size_t(gr.bytes), size_t(gr.bytes), 1,
+                       gr.b.on_device ? 2 : 0),
           "resident upload");
   }
   for (const auto& [key, pl] : planes_)
-    hs_ok(hs_gemm_split_weights_ex(s, resident_buf_.at(pl.gi), pl.nt ? 1 : 0, pl.n, pl.k, pl.ptr, pl.n * pl.k,
-                                   plane_format()),
+    hs_ok(hs_gemm_split_weights_ex(dstream(s0, pl.dom), resident_.at({pl.gi, pl.dom}), pl.nt ? 1 : 0, pl.n, pl.k,
+                                   pl.ptr, pl.n * pl.k, plane_format()),
           "split weights");
-  for (const auto& [gi, pl] : attn_planes_)
-    hs_ok(hs_gemm_split_weights_ex(s, resident_buf_.at(gi), 0, pl.n, pl.k, pl.ptr, pl.n * pl.k, 0),
+  for (const auto& [key, pl] : attn_planes_)
+    hs_ok(hs_gemm_split_weights_ex(dstream(s0, pl.dom), resident_.at({pl.gi, pl.dom}), 0, pl.n, pl.k, pl.ptr,
+                                   pl.n * pl.k, 0),
           "split attention weights");
   for (const auto& fg : fuse_groups_) {
     const int64_t members = int64_t(fg.kernels.size());
+    const int dom = comp_dom_.count(fg.component) ? comp_dom_.at(fg.component) : 0;
     for (int64_t m = 0; m < members; ++m) {
       const int gi = group_of_.at(nodes_.at(fg.kernels[size_t(m)]).inputs[1]);
-      hs_ok(hs_gemm_split_weights_ex(s, resident_buf_.at(gi), 0, fg.n, fg.k,
+      hs_ok(hs_gemm_split_weights_ex(dstream(s0, dom), resident_.at({gi, dom}), 0, fg.n, fg.k,
                                      static_cast<char*>(fg.planes) + m * fg.n * fg.k * plane_elem_bytes(),
                                      members * fg.n * fg.k, plane_format()),
             "split grouped weights");
     }
   }
-  hs_ok(hs_stream_sync(s), "resident upload sync");
+  hs_ok(hs_stream_sync(s0.origin), "resident upload sync");
+  for (auto& [d, st] : s0.dorigin) hs_ok(hs_stream_sync(st), "resident upload sync");
   resident_uploaded_ = true;
 }
 
@@ -353,31 +423,71 @@ hs_stream_t Engine::stream(Slot& sl, int device, int queue) {
   auto it = sl.streams.find(key);
   if (it != sl.streams.end()) return it->second;
   hs_stream_t s = nullptr;
-  hs_ok(hs_stream_create(ctx_, 0, &s), "hs_stream_create");
+  const int dom = dev_dom_.count(device) ? dev_dom_.at(device) : 0;
+  hs_ok(hs_stream_create(dctx_[size_t(dom)], 0, &s), "hs_stream_create");
+  stream_dom_[s] = dom;
   sl.streams[key] = s;
   return s;
 }
 
-hs_event_t Engine::event(Slot& sl, int comp, int ev) {
+// Events are created in the domain of the stream they are recorded on: a
+// component's events in its domain, the plan's fork (-1) on the origin, joins
+// (-2, -3) with an explicit domain.
+hs_event_t Engine::event(Slot& sl, int comp, int ev, int dom) {
   auto key = std::make_pair(comp, ev);
   auto it = sl.events.find(key);
   if (it != sl.events.end()) return it->second;
+  if (dom < 0) dom = comp >= 0 && comp_dom_.count(comp) ? comp_dom_.at(comp) : 0;
   hs_event_t e = nullptr;
-  hs_ok(hs_event_create(ctx_, 0, &e), "hs_event_create");
+  hs_ok(hs_event_create(dctx_[size_t(dom)], 0, &e), "hs_event_create");
   sl.events[key] = e;
   return e;
 }
 
-void Engine::copy_in(Slot& sl, hs_stream_t s, int gi, int64_t first, int64_t n) {
+void Engine::copy_in(Slot& sl, hs_stream_t s, int gi, int64_t first, int64_t n, int dom) {
   const Group& gr = groups_[size_t(gi)];
+  auto dst = sl.group_buf.find({gi, dom});
+  if (dst == sl.group_buf.end()) return;  // no kernel of this domain reads the group
   const char* src = static_cast<const char*>(gr.b.ptr) + first * gr.b.stride;
-  hs_ok(hs_memcpy_2d(s, sl.group_buf.at(gi), size_t(gr.bytes), src, size_t(gr.b.stride), size_t(gr.bytes), size_t(n),
+  hs_ok(hs_memcpy_2d(s, dst->second, size_t(gr.bytes), src, size_t(gr.b.stride), size_t(gr.bytes), size_t(n),
                      gr.b.on_device ? 2 : 0),
         "copy-in");
 }
 
-void Engine::copy_out(Slot& sl, hs_stream_t s, int64_t first, int64_t n) {
+// Copy-in (in = true) or copy-out of one batch on the slot. With several memory
+// domains each domain's copies run on its own copy stream, forked from and
+// joined back into the origin stream.
+void Engine::copies(Slot& sl, int64_t first, int64_t n, bool in) {
+  if (dctx_.size() == 1) {
+    if (in) {
+      for (size_t gi = 0; gi < groups_.size(); ++gi)
+        if (!groups_[gi].resident) copy_in(sl, sl.origin, int(gi), first, n, 0);
+    } else {
+      copy_out(sl, sl.origin, first, n, 0);
+    }
+    return;
+  }
+  hs_ok(hs_event_record(sl.copy_fork, sl.origin), "copy fork");
+  for (size_t d = 0; d < dctx_.size(); ++d) {
+    hs_stream_t s = dstream(sl, int(d));
+    if (d > 0) hs_ok(hs_stream_wait(s, sl.copy_fork), "copy fork wait");
+    if (in) {
+      for (size_t gi = 0; gi < groups_.size(); ++gi)
+        if (!groups_[gi].resident) copy_in(sl, s, int(gi), first, n, int(d));
+    } else {
+      copy_out(sl, s, first, n, int(d));
+    }
+    if (d > 0) {
+      hs_event_t e = in ? sl.din.at(int(d)) : sl.dout.at(int(d));
+      hs_ok(hs_event_record(e, s), "copy join");
+      hs_ok(hs_stream_wait(sl.origin, e), "copy join wait");
+    }
+  }
+}
+
+void Engine::copy_out(Slot& sl, hs_stream_t s, int64_t first, int64_t n, int dom) {
   for (const auto& key : outputs_) {
+    if (kdom(key.first) != dom) continue;
     const Binding& b = bindings_.at(key);
     const int64_t bytes = bytes_.at(key);
     char* dst = static_cast<char*>(b.ptr) + first * b.stride;
@@ -458,8 +568,9 @@ void Engine::issue(Slot& sl, const TaskComponent& t, const CommandQueueStructure
       tr.device = d;
       tr.queue = qi;
       tr.label = c.label;
-      hs_ok(hs_event_create(ctx_, 1, &tr.t0), "hs_event_create");
-      hs_ok(hs_event_create(ctx_, 1, &tr.t1), "hs_event_create");
+      hs_ctx_t tctx = dctx_[size_t(stream_dom_.count(s) ? stream_dom_.at(s) : 0)];
+      hs_ok(hs_event_create(tctx, 1, &tr.t0), "hs_event_create");
+      hs_ok(hs_event_create(tctx, 1, &tr.t1), "hs_event_create");
       hs_ok(hs_event_record(tr.t0, s), "trace record");
     }
     switch (c.kind) {
@@ -471,14 +582,19 @@ void Engine::issue(Slot& sl, const TaskComponent& t, const CommandQueueStructure
             fail(Errc::deadlock, "dependent write for edge " + std::to_string(c.edge) + " issued before its producer");
           hs_ok(hs_stream_wait(s, event(sl, src->second.first, src->second.second)), "inter-edge wait");
           auto io = io_copy_.find(key);
+          auto pr = peer_in_.find(key);
           if (io != io_copy_.end())
             hs_ok(hs_memcpy_d2d(s, sl.buf.at(key), sl.buf.at(io->second), size_t(bytes_.at(key) * cfg_.batch)),
                   "dependent write");
+          else if (pr != peer_in_.end())  // producer in another memory domain: one peer copy (NVLink)
+            hs_ok(hs_memcpy_peer(s, sl.buf.at(key), dom_gpu_[size_t(kdom(key.first))], sl.buf.at(pr->second),
+                                 dom_gpu_[size_t(kdom(pr->second.first))], size_t(bytes_.at(key) * cfg_.batch)),
+                  "dependent write (peer)");
         } else if (!graph) {
           const int gi = group_of_.at(key);
           if (!groups_[size_t(gi)].resident) {
             if (!sl.group_done.count(gi)) {
-              copy_in(sl, s, gi, first, n);
+              copy_in(sl, s, gi, first, n, 0);
               auto ge = sl.group_event.find(gi);
               hs_event_t e = nullptr;
               if (ge == sl.group_event.end()) {
@@ -612,10 +728,8 @@ void Engine::plan_fusion() {
           fg.events.push_back(list[i + j].first);
           fg.kernels.push_back(list[i + j].second);
         }
-        const size_t bytes = size_t(2 * int64_t(take) * fg.n * fg.k * plane_elem_bytes());
-        hs_ok(hs_malloc(ctx_, bytes, &fg.planes), "hs_malloc");
-        allocations_.push_back(fg.planes);
-        device_bytes_ += int64_t(bytes);
+        fg.planes = dalloc(comp_dom_.count(q.component) ? comp_dom_.at(q.component) : 0,
+                           2 * int64_t(take) * fg.n * fg.k * plane_elem_bytes());
         const int gi = int(fuse_groups_.size());
         fuse_leader_[{q.component, fg.events[0]}] = gi;
         for (size_t j = 1; j < take; ++j) fuse_member_[{q.component, fg.events[j]}] = gi;
@@ -747,16 +861,16 @@ void Engine::plan_chain_rewrites() {
     g2.elided = true;
     if (plane_format() != 0) {  // the fused head consumes tf32 planes; BF16X3 keeps bf16 ones for GEMMs
       const int gi = group_of_.at(wkey);
-      auto it = attn_planes_.find(gi);
+      const int dom = kdom(kid);
+      auto it = attn_planes_.find({gi, dom});
       if (it == attn_planes_.end()) {
         Planes pl;
         pl.gi = gi;
         pl.n = 64;
         pl.k = 64;
-        hs_ok(hs_malloc(ctx_, size_t(2 * 64 * 64 * 4), &pl.ptr), "hs_malloc");
-        allocations_.push_back(pl.ptr);
-        device_bytes_ += 2 * 64 * 64 * 4;
-        it = attn_planes_.emplace(gi, pl).first;
+        pl.dom = dom;
+        pl.ptr = dalloc(dom, 2 * 64 * 64 * 4);
+        it = attn_planes_.emplace(std::make_pair(gi, dom), pl).first;
       }
       node_planes_[kid] = it->second.ptr;
     }
@@ -834,7 +948,7 @@ void Engine::emit_plan(Slot& sl) {
   }
   int j = 0;
   for (auto [d, qi] : used) {
-    hs_event_t e = event(sl, -2, j++);
+    hs_event_t e = event(sl, -2, j++, dev_dom_.count(d) ? dev_dom_.at(d) : 0);
     hs_ok(hs_event_record(e, stream(sl, d, qi)), "join record");
     hs_ok(hs_stream_wait(sl.origin, e), "join wait");
   }
@@ -895,13 +1009,17 @@ void Engine::run_dynamic(Slot& sl, int64_t first, int64_t n) {
 void Engine::run(int64_t first, int64_t n, int64_t* elapsed_ns) {
   if (n < 1) fail(Errc::invalid_param, "n_instances must be >= 1");
   if (!planned_) {
-    plan_buffers();
     if (cfg_.graph_mode) {
       PlanExecutor pe;
       plan_ = sched_->run(pe);
+      place_components();
+    }
+    plan_buffers();
+    if (cfg_.graph_mode) {
       if (cfg_.fuse >= 1 && cfg_.math != HS_MATH_FP32_SIMT) plan_fusion();
       if (cfg_.fuse >= 2 && cfg_.math != HS_MATH_FP32_SIMT) plan_chain_rewrites();
-      for (auto& sl : slots_) capture(sl);
+      if (capture_ok_)
+        for (auto& sl : slots_) capture(sl);
     }
     planned_ = true;
   }
@@ -917,19 +1035,20 @@ void Engine::run(int64_t first, int64_t n, int64_t* elapsed_ns) {
     for (int64_t b = 0; b < nb; ++b) {
       Slot& sl = slots_[size_t(b % int64_t(slots_.size()))];
       const int64_t f = first + b * B, cnt = std::min(B, n - b * B);
-      for (size_t gi = 0; gi < groups_.size(); ++gi)
-        if (!groups_[gi].resident) copy_in(sl, sl.origin, int(gi), f, cnt);
-      if (cfg_.trace && b == 0) {
+      copies(sl, f, cnt, true);
+      if ((cfg_.trace && b == 0) || !capture_ok_) {
         // traced batch: the same plan issued directly (not replayed) with a
         // timing event pair around every command
-        tracing_ = true;
-        for (const auto& rec : plan_.dispatches) trace_dispatch_.push_back({rec.component, rec.device});
+        // (or: several GPUs, where the plan is issued directly every batch)
+        tracing_ = cfg_.trace && b == 0;
+        if (tracing_)
+          for (const auto& rec : plan_.dispatches) trace_dispatch_.push_back({rec.component, rec.device});
         emit_plan(sl);
         tracing_ = false;
       } else {
         hs_ok(hs_graph_launch(sl.graph, sl.origin), "graph launch");
       }
-      copy_out(sl, sl.origin, f, cnt);
+      copies(sl, f, cnt, false);
     }
   } else {
     for (auto& [k, s] : s0.streams) hs_ok(hs_stream_wait(s, s0.t_start), "start wait");
@@ -983,8 +1102,16 @@ std::string Engine::info(const std::string& what) const {
     for (const auto& sl : slots_) streams += static_cast<long long>(sl.streams.size());
     out.set("streams", Value::of(streams));
     out.set("device_bytes", Value::of(static_cast<long long>(device_bytes_)));
-    out.set("resident_groups", Value::of(static_cast<long long>(resident_buf_.size())));
-    out.set("instance_groups", Value::of(static_cast<long long>(groups_.size() - resident_buf_.size())));
+    long long resident_groups = 0;
+    for (const auto& gr : groups_) resident_groups += gr.resident ? 1 : 0;
+    out.set("resident_groups", Value::of(resident_groups));
+    out.set("instance_groups", Value::of(static_cast<long long>(groups_.size()) - resident_groups));
+    out.set("memory_domains", Value::of(static_cast<long long>(dctx_.size())));
+    Value gpus = Value::make_array();
+    for (int gpu : dom_gpu_) gpus.push_back(Value::of(static_cast<long long>(gpu)));
+    out.set("domain_gpus", std::move(gpus));
+    out.set("peer_copies_per_batch", Value::of(static_cast<long long>(peer_in_.size())));
+    out.set("captured", Value::of(static_cast<long long>(capture_ok_ && cfg_.graph_mode ? 1 : 0)));
     out.set("aliased_inputs", Value::of(static_cast<long long>(alias_.size())));
     out.set("grouped_launches", Value::of(static_cast<long long>(fuse_groups_.size())));
     Value rw = Value::make_object();
@@ -1088,6 +1215,9 @@ int hs_engine_create(const char* config_json, hs_engine_t* out) {
     if (const json::Value* v = c.find("trace")) cfg.trace = v->as_int() != 0;
     if (const json::Value* v = c.find("cpu_devices"))
       for (const json::Value* x : v->items()) cfg.cpu_devices.insert(x->as_int());
+    if (const json::Value* v = c.find("device_gpus"))
+      for (const auto& [k, g] : v->object_items()) cfg.device_gpus[std::stoi(k)] = g.as_int();
+    if (const json::Value* v = c.find("domain_per_device")) cfg.domain_per_device = v->as_int() != 0;
     if (const json::Value* v = c.find("fuse")) {
       cfg.fuse = v->as_int();
       if (cfg.fuse < 0 || cfg.fuse > 3) fail(Errc::invalid_param, "fuse must be 0, 1, 2 or 3");

@@ -22,6 +22,7 @@
 #include <mutex>
 #include <set>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "hetsim/cq_builder.hpp"
@@ -48,6 +49,13 @@ struct EngineConfig {
   // Record a timing-event pair around every command of the first batch of each
   // run (dynamic mode: as dispatched; graph mode: the plan issued directly).
   bool trace = false;
+  // Components across GPUs: logical device -> physical GPU
+  // ordinal (default: every logical device on `gpu`). Each distinct GPU is a
+  // memory domain; an inter edge between domains is one peer copy on the
+  // consumer's dependent write. domain_per_device makes every logical device its
+  // own domain even on one GPU (exercises the peer path on a 1-GPU machine).
+  std::map<int, int> device_gpus;
+  bool domain_per_device = false;
 };
 
 class Engine {
@@ -92,7 +100,7 @@ class Engine {
   };
   struct Slot {
     std::map<std::pair<int, int>, void*> buf;  // (kernel,pos) -> device base for this slot
-    std::map<int, void*> group_buf;            // per-instance groups
+    std::map<std::pair<int, int>, void*> group_buf;  // per-instance groups: (group, domain) -> base
     hs_stream_t origin = nullptr;
     std::map<std::pair<int, int>, hs_stream_t> streams;  // (device, queue)
     std::map<std::pair<int, int>, hs_event_t> events;    // (component, event)
@@ -101,6 +109,10 @@ class Engine {
     std::set<int> group_done;
     hs_graph_t graph = nullptr;
     hs_event_t t_start = nullptr, t_end = nullptr;
+    // several memory domains: per-domain copy streams joined to `origin`
+    std::map<int, hs_stream_t> dorigin;
+    std::map<int, hs_event_t> din, dout;
+    hs_event_t copy_fork = nullptr, copy_join = nullptr;
   };
 
   void build_nodes();
@@ -110,12 +122,17 @@ class Engine {
   void emit_plan(Slot& sl);
   void clear_trace();
   hs_stream_t stream(Slot& sl, int device, int queue);
-  hs_event_t event(Slot& sl, int comp, int ev);
+  hs_event_t event(Slot& sl, int comp, int ev, int dom = -1);
   void issue(Slot& sl, const TaskComponent& t, const CommandQueueStructure& q, int prev_comp,
              const CommandQueueStructure* prev_q, bool graph, int64_t first, int64_t n);
   void launch_node(Slot& sl, hs_stream_t s, int kernel);
-  void copy_in(Slot& sl, hs_stream_t s, int group, int64_t first, int64_t n);
-  void copy_out(Slot& sl, hs_stream_t s, int64_t first, int64_t n);
+  void copy_in(Slot& sl, hs_stream_t s, int group, int64_t first, int64_t n, int dom);
+  void copy_out(Slot& sl, hs_stream_t s, int64_t first, int64_t n, int dom);
+  void copies(Slot& sl, int64_t first, int64_t n, bool in);
+  void place_components();
+  int kdom(int kernel) const;
+  void* dalloc(int dom, int64_t bytes);
+  hs_stream_t dstream(Slot& sl, int dom);
   void run_dynamic(Slot& sl, int64_t first, int64_t n);
   Completion wait_completion();
 
@@ -134,18 +151,19 @@ class Engine {
   std::map<std::pair<int, int>, std::pair<int, int>> io_copy_;  // io input fed by an edge -> producer
   std::map<std::pair<int, int>, int64_t> bytes_;                // (kernel,pos) -> bytes per instance
   std::vector<std::pair<int, int>> outputs_;                    // isolated outputs with a binding
-  std::map<int, void*> resident_buf_;
+  std::map<std::pair<int, int>, void*> resident_;  // (resident group, domain) -> device copy
   // resident GEMM weights pre-split into tf32 hi/lo planes: (group, transposed) -> planes
   struct Planes {
     void* ptr = nullptr;
     int gi = -1;
     bool nt = false;
     int64_t n = 0, k = 0;
+    int dom = 0;
   };
-  std::map<std::pair<int, bool>, Planes> planes_;
+  std::map<std::tuple<int, bool, int>, Planes> planes_;  // (group, transposed, domain)
   std::map<int, void*> node_planes_;  // kernel -> planes
   std::map<int, void*> head_qkv_planes_;  // HS_OP_HEAD kernel -> its absorbed group's Wq|Wk|Wv planes
-  std::map<int, Planes> attn_planes_;  // resident group -> tf32 planes for fused heads (BF16X3 engines)
+  std::map<std::pair<int, int>, Planes> attn_planes_;  // (resident group, domain) -> tf32 planes for fused heads
 
   // Grouped launches (graph mode): sibling GEMM ndranges of one component that
   // share their A input, have resident B and no intra-component producer run as
@@ -167,14 +185,22 @@ class Engine {
   std::vector<FuseGroup> fuse_groups_;
   std::map<std::pair<int, int>, int> fuse_leader_;  // (component, ndrange event) -> group
   std::map<std::pair<int, int>, int> fuse_member_;  // (component, ndrange event) -> group (non-leaders)
-  hs_ctx_t ctx_ = nullptr;
+  hs_ctx_t ctx_ = nullptr;  // domain 0
+  std::vector<hs_ctx_t> dctx_;       // memory domain -> context
+  std::vector<int> dom_gpu_;         // memory domain -> GPU ordinal
+  std::map<int, int> dev_dom_;       // logical device -> domain
+  std::map<int, int> comp_dom_;      // component -> domain (graph mode plan)
+  std::map<int, int> kernel_dom_;    // kernel -> domain
+  std::map<hs_stream_t, int> stream_dom_;
+  std::map<std::pair<int, int>, std::pair<int, int>> peer_in_;  // input fed across domains -> producer
+  bool capture_ok_ = true;           // one physical GPU: the plan is captured into graphs
   std::vector<Slot> slots_;
   bool planned_ = false;
   bool resident_uploaded_ = false;
   int64_t device_bytes_ = 0;
   int64_t launches_per_batch_ = 0;
   int64_t runs_ = 0, batches_run_ = 0;
-  std::vector<void*> allocations_;
+  std::vector<std::pair<int, void*>> allocations_;  // (domain, pointer)
 
   // dynamic-mode completion queue (MPSC: CUDA callback threads -> scheduler thread)
   std::mutex mu_;

@@ -29,18 +29,25 @@ def _ptr_and_nbytes(arr):
 class Engine:
     def __init__(self, spec_text: str, params: dict | None = None, *, gpu: int = 0, policy: str = "clustering",
                  mode: str = "graph", batch: int = 1, slots: int = 2, math: str = "tf32x3", cpu_devices=(),
-                 fuse: int | bool = 3, trace: bool = False):
+                 fuse: int | bool = 3, trace: bool = False, device_gpus: dict | None = None,
+                 domain_per_device: bool = False):
         """fuse (graph mode): 0 = one launch per ndrange; 1 = + grouped sibling GEMMs;
         2 = + chain rewrites (transpose -> gemm_nt, softmax as a GEMM epilogue, concat
         inputs written in place, fused attention heads); 3 (default, also True) = + each
         head's grouped Q/K/V projection absorbed into its attention launch (one
         HS_OP_HEAD launch per head component). Dynamic mode always launches per ndrange.
         trace: time every command of the first batch of each run with CUDA events
-        (see trace(); graph mode issues that batch's plan directly instead of replaying it)."""
+        (see trace(); graph mode issues that batch's plan directly instead of replaying it).
+        device_gpus: {logical device id: GPU ordinal} places components on several GPUs
+        (graph mode); an inter edge between GPUs becomes one peer copy over NVLink.
+        domain_per_device: every logical device gets its own memory (test hook: the peer
+        path on one GPU)."""
         fuse = 3 if fuse is True else int(fuse)
         cfg = {"spec": spec_text, "params": dict(params or {}), "gpu": gpu, "policy": policy, "mode": mode,
                "batch": batch, "slots": slots, "math": math, "cpu_devices": list(cpu_devices), "fuse": int(fuse),
-               "trace": int(bool(trace))}
+               "trace": int(bool(trace)), "domain_per_device": int(bool(domain_per_device))}
+        if device_gpus:
+            cfg["device_gpus"] = {str(k): int(v) for k, v in device_gpus.items()}
         self._lib = lib()
         h = ctypes.c_void_p()
         check(self._lib.hs_engine_create(json.dumps(cfg).encode(), ctypes.byref(h)), "hs_engine_create")

@@ -214,3 +214,31 @@ def test_trace_records_every_command_in_both_modes(oracle_mod):
         med[mode] = statistics.median(g["gap"] for g in R.component_gaps(tr, disp))
     assert counts["dynamic"] == counts["graph"]
     assert med["dynamic"] > med["graph"], med
+
+
+@pytest.mark.parametrize("fuse", [0, 3])
+def test_components_across_memory_domains(fuse, oracle_mod):
+    """components mapped to different GPUs. Every logical device gets its
+    own memory domain (domain_per_device: the multi-GPU placement on this 1-GPU box),
+    so each inter edge between components is one peer copy issued on the consumer's
+    dependent write. Outputs equal the single-domain engine bit for bit (same
+    kernels; a copy is exact) and match the oracle."""
+    text, params, meta = workloads.encoder(layers=2, devices=9)
+    n = 3
+    arrays = _encoder_arrays(meta, params, n)
+    ref = oracle_mod.run_dag(text, params, arrays, n)
+    key = (meta["output"]["kernel"], meta["output"]["pos"])
+    one, _, plan1 = _run_gpu(text, params, arrays, n, mode="graph", batch=2, fuse=fuse)
+    many, _, plan = _run_gpu(text, params, arrays, n, mode="graph", batch=2, fuse=fuse,
+                             device_gpus={d: 0 for d in range(9)}, domain_per_device=True)
+    assert plan1["memory_domains"] == 1 and plan1["peer_copies_per_batch"] == 0
+    assert plan["memory_domains"] == 9 and plan["peer_copies_per_batch"] > 0 and plan["captured"] == 1
+    assert np.array_equal(many[key], one[key])
+    for i in range(n):
+        assert _normwise(many[key][i], ref[key][i]) <= TOL
+
+
+def test_memory_domains_need_graph_mode():
+    text, params, meta = workloads.encoder(layers=1, devices=2)
+    with pytest.raises(Exception, match="graph mode"):
+        Engine(text, params, mode="dynamic", device_gpus={0: 0, 1: 0}, domain_per_device=True)
