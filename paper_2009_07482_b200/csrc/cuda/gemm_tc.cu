@@ -60,6 +60,9 @@ using namespace tc;
 #ifndef HS_DBG_NOEPI
 #define HS_DBG_NOEPI 0
 #endif
+#ifndef HS_SPLIT_K  // split-K with red.global.add for latency-bound single-CTA launches
+#define HS_SPLIT_K 1
+#endif
 #ifndef HS_DBG_EARLYREL
 #define HS_DBG_EARLYREL 0
 #endif
@@ -142,6 +145,10 @@ struct TileParams {
   // Softmax epilogue (one tile covers all N columns): C = softmax_row(acc * escale).
   int softmax;
   float escale;
+  // Split-K (single-CTA kernel, latency-bound launches): tile t computes output
+  // tile t % base_tiles over K-block range split t / base_tiles and adds it into
+  // C (zeroed before the launch) with red.global.add; total_tiles = base * split.
+  int split_k, base_tiles;
 };
 
 
@@ -220,7 +227,17 @@ __device__ __forceinline__ void epi_store_chunk(const TileParams& p, uint32_t ti
     const float4 x = make_float4(lds32(src), lds32(src + 4), lds32(src + 8), lds32(src + 12));
     if (rows_valid && grow < p.M && !HS_DBG_NOEPI) {
       float* dst = cbase + int64_t(grow) * ld + c0 + cq;
-      if (vec) {
+      if (p.split_k > 1) {  // partial sum of a K split: accumulate into C
+        if (vec) {
+          asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(x.x), "f"(x.y), "f"(x.z),
+                       "f"(x.w)
+                       : "memory");
+        } else {
+          const float e[4] = {x.x, x.y, x.z, x.w};
+          for (int i = 0; i < 4; ++i)
+            if (c0 + cq + i < ncols) atomicAdd(dst + i, e[i]);
+        }
+      } else if (vec) {
         *reinterpret_cast<float4*>(dst) = x;
       } else {
         const float e[4] = {x.x, x.y, x.z, x.w};
@@ -254,6 +271,9 @@ __global__ void __launch_bounds__(kThreads, kSmall ? 2 : 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nk = (p.K + BK - 1) / BK;
+  // K-block range of tile t (the whole K unless split-K)
+  auto kb_begin = [&](int t) { return (t / p.base_tiles) * nk / p.split_k; };
+  auto kb_end = [&](int t) { return (t / p.base_tiles + 1) * nk / p.split_k; };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
@@ -285,6 +305,7 @@ __global__ void __launch_bounds__(kThreads, kSmall ? 2 : 1)
 
   // tile index -> (m_tile, instance, n_tile); instance fastest after m.
   auto decode = [&](int t, int& m0, int& inst, int& n0) {
+    t %= p.base_tiles;
     const int mt = t % p.m_tiles;
     const int rest = t / p.m_tiles;
     inst = rest % p.batch;
@@ -300,7 +321,7 @@ __global__ void __launch_bounds__(kThreads, kSmall ? 2 : 1)
         int m0, inst, n0;
         decode(t, m0, inst, n0);
         const int ia = p.a_batched ? inst : 0, ib = p.b_batched ? inst : 0;
-        for (int kb = 0; kb < nk; ++kb, ++it) {
+        for (int kb = kb_begin(t); kb < kb_end(t); ++kb, ++it) {
           const int s = int(it % NS);
           mbar_wait(st_empty(s), ((it / NS) & 1u) ^ 1u);
           const uint32_t sa = staging + uint32_t(s) * L::kStaging;
@@ -327,7 +348,7 @@ __global__ void __launch_bounds__(kThreads, kSmall ? 2 : 1)
         for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
           int m0, inst, n0;
           decode(t, m0, inst, n0);
-          for (int kb = 0; kb < nk; ++kb, ++it) {
+          for (int kb = kb_begin(t); kb < kb_end(t); ++kb, ++it) {
             const int o = int(it % NO);
             mbar_wait(op_empty(o), ((it / NO) & 1u) ^ 1u);
             const uint32_t b_hi = operand + uint32_t(o) * L::kOperand;
@@ -353,7 +374,8 @@ __global__ void __launch_bounds__(kThreads, kSmall ? 2 : 1)
         mbar_wait(acc_empty(int(acc)), ((lt / uint32_t(L::kAccBufs)) & 1u) ^ 1u);
         tc_fence_after();
         const uint32_t d = tmem + acc * uint32_t(BN);
-        for (int kb = 0; kb < nk; ++kb, ++it) {
+        const int kb0 = kb_begin(t);
+        for (int kb = kb0; kb < kb_end(t); ++kb, ++it) {
           const int o = int(it % NO);
           mbar_wait(op_full(o), (it / NO) & 1u);
           tc_fence_after();
@@ -366,7 +388,7 @@ __global__ void __launch_bounds__(kThreads, kSmall ? 2 : 1)
 #pragma unroll
             for (int kk = 0; kk < BK / 16; ++kk) {
               const uint32_t kcol = uint32_t(kk) * 8u, koff = uint32_t(kk) * 32u;
-              const uint32_t first = (kb | kk) ? 1u : 0u;
+              const uint32_t first = ((kb - kb0) | kk) ? 1u : 0u;
               mma_f16_ts(d, a_lo + kcol, smem_desc_sw64(b_hi + koff), idesc, first);
               mma_f16_ts(d, a_hi + kcol, smem_desc_sw64(b_lo + koff), idesc, 1u);
               mma_f16_ts(d, a_hi + kcol, smem_desc_sw64(b_hi + koff), idesc, 1u);
@@ -375,7 +397,7 @@ __global__ void __launch_bounds__(kThreads, kSmall ? 2 : 1)
 #pragma unroll
           for (int kk = 0; kk < BK / 8; ++kk) {  // K = 8 tf32 per instruction
             const uint32_t kcol = uint32_t(kk) * 8u, koff = uint32_t(kk) * 32u;
-            const uint32_t first = (kb | kk) ? 1u : 0u;
+            const uint32_t first = ((kb - kb0) | kk) ? 1u : 0u;
             if constexpr (kTerms > 1) {
               mma_tf32_ts(d, a_lo + kcol, smem_desc(b_hi + koff), idesc, first);
               mma_tf32_ts(d, a_hi + kcol, smem_desc(b_lo + koff), idesc, 1u);
@@ -465,7 +487,7 @@ __global__ void __launch_bounds__(kThreads, kSmall ? 2 : 1)
     const int row = q * 32 + lane;
     uint32_t it = 0;
     for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
-      for (int kb = 0; kb < nk; ++kb, ++it) {
+      for (int kb = kb_begin(tile); kb < kb_end(tile); ++kb, ++it) {
         if (int(it % kConvGroups) != g) continue;
         const int s = int(it % NS), o = int(it % NO);
         mbar_wait(st_full(s), (it / NS) & 1u);
@@ -936,8 +958,29 @@ cudaError_t launch(const GemmArgs& a, cudaStream_t s) {
   p.softmax = a.softmax;
   p.escale = a.escale;
   if (p.softmax && p.n_tiles != 1) return cudaErrorInvalidValue;
-  p.total_tiles = p.m_tiles * p.n_tiles * a.batch;
+  const int base = p.m_tiles * p.n_tiles * a.batch;
   const int slots = num_sms() * L::kCtasPerSm;
+  // Split-K for latency-bound single-instance launches (few output tiles, long K
+  // loop: one instance's FFN2 runs 8 CTAs over 64 K-blocks): each split adds its
+  // partial sum into C with red.global.add, so C is zeroed first and the result
+  // is not bit-reproducible (fp32 addition order across splits). Batched
+  // launches never split.
+  const int nk = (a.K + BK - 1) / BK;
+  int split = 1;
+  if (HS_SPLIT_K && a.batch == 1 && !a.relu && !a.softmax && p.n_out == 0 && !a.ldc && nk >= 8 &&
+      4 * base <= slots) {
+    split = slots / base;
+    if (split > nk / 4) split = nk / 4;
+    if (split > 16) split = 16;
+    if (split < 2) split = 1;
+  }
+  p.split_k = split;
+  p.base_tiles = base;
+  p.total_tiles = base * split;
+  if (split > 1) {
+    const cudaError_t e = cudaMemsetAsync(a.C, 0, size_t(a.batch) * size_t(a.M) * size_t(a.N) * 4, s);
+    if (e != cudaSuccess) return e;
+  }
   const int grid = p.total_tiles < slots ? p.total_tiles : slots;
   kernel<<<grid, kThreads, L::kTotal, s>>>(mA, mB, p);
   return cudaGetLastError();

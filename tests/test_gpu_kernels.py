@@ -39,6 +39,10 @@ GEMM_CASES = [
     (100, 72, 36, "gemm", 2, False),        # ragged M/N/K tails
     (130, 200, 44, "gemm_nt", 1, False),
     (64, 8, 4, "gemm", 1, False),
+    # single-instance launches with a long K loop run split-K (red.global.add into a zeroed C)
+    (128, 512, 2048, "gemm", 1, True),
+    (256, 256, 256, "gemm", 1, False),
+    (100, 64, 1000, "gemm_nt", 1, False),
 ]
 
 
