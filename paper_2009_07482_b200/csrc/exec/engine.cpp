@@ -785,10 +785,28 @@ void Engine::plan_chain_rewrites() {
     nd.elided = true;
     ++rewrites_["transpose_into_gemm_nt"];
   }
+  // scale_into_softmax: B = scale(A, s) consumed only by P = softmax(B, t): the
+  // softmax reads A with scale s·t (one rounding instead of two; within
+  // tolerance, not bit-identical to the two launches).
+  std::map<int, int> folded_scale;  // elided scale -> the softmax that absorbed it
+  for (auto& [kid, sc] : nodes_) {
+    if (sc.op != HS_OP_SCALE || sc.elided) continue;
+    int ck, cp;
+    if (!sole_consumer(sc.output, &ck, &cp)) continue;
+    Node& sm = nodes_.at(ck);
+    if (sm.op != HS_OP_SOFTMAX || sm.elided || sc.dims[0] != sm.dims[0] * sm.dims[1] || resident(sc.inputs[0]))
+      continue;
+    sm.inputs[0] = sc.inputs[0];
+    sm.fparam[0] *= sc.fparam[0];
+    sc.elided = true;
+    folded_scale[kid] = ck;
+    ++rewrites_["scale_into_softmax"];
+  }
   for (auto& [kid, g] : nodes_) {
     if ((g.op != HS_OP_GEMM && g.op != HS_OP_GEMM_NT) || g.elided || g.epilogue || grouped.count(kid)) continue;
     int ck, cp;
     if (!sole_consumer(g.output, &ck, &cp)) continue;
+    if (folded_scale.count(ck)) ck = folded_scale.at(ck);  // gemm -> (scale folded into) softmax
     Node& sm = nodes_.at(ck);
     if (sm.op != HS_OP_SOFTMAX || sm.elided) continue;
     if (sm.dims[0] != g.dims[0] || sm.dims[1] != g.dims[1] || g.dims[1] > 128) continue;
