@@ -45,6 +45,9 @@
 #ifndef HS_DBG_TIMELINE
 #define HS_DBG_TIMELINE 0
 #endif
+#ifndef HS_DBG_HEAD_NOCONV  // timing experiment only (wrong results): skip the X split in phase 1
+#define HS_DBG_HEAD_NOCONV 0
+#endif
 
 namespace hs {
 
@@ -390,7 +393,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t ta = lane_base + kTStage + uint32_t(o) * 64u;
       (void)kb;
 #pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
+      for (int hh = 0; hh < (HS_DBG_HEAD_NOCONV ? 0 : 2); ++hh) {
         uint32_t x[16], hi[16], lo[16];
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
