@@ -63,7 +63,10 @@ class CudaDispatch : public Executor {
  public:
   CudaDispatch(Engine& e, Engine::Slot& sl, int64_t first, int64_t n) : e_(e), sl_(sl), first_(first), n_(n) {}
   void dispatch(const TaskComponent& t, const CommandQueueStructure& q) override {
+    const auto t0 = std::chrono::steady_clock::now();
     e_.issue(sl_, t, q, -1, nullptr, false, first_, n_);
+    e_.host_dispatch_ns_ += std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count();
+    ++e_.host_dispatches_;
   }
   Completion wait_next() override { return e_.wait_completion(); }
 
@@ -995,17 +998,27 @@ void Engine::push_completion(const Completion& c) {
   {
     std::lock_guard<std::mutex> lk(mu_);
     done_q_.push_back(c);
+    pending_.fetch_add(1, std::memory_order_release);
   }
   cv_.notify_one();
 }
 
+// The scheduler thread spins on the completion count for a short while before
+// sleeping on the condition variable: a host callback usually arrives within
+// tens of microseconds, and a condition-variable wake-up would add about as much.
 Completion Engine::wait_completion() {
+  const auto t0 = std::chrono::steady_clock::now();
+  while (pending_.load(std::memory_order_acquire) == 0 &&
+         std::chrono::steady_clock::now() - t0 < std::chrono::microseconds(kSpinUs)) {
+  }
   std::unique_lock<std::mutex> lk(mu_);
   if (!cv_.wait_for(lk, std::chrono::seconds(120), [&] { return !done_q_.empty(); }))
     fail(Errc::deadlock, "no completion callback within 120 s");
   Completion c = done_q_.front();
   done_q_.pop_front();
+  pending_.fetch_sub(1, std::memory_order_relaxed);
   last_log_.push_back(c);
+  host_wait_ns_ += std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count();
   return c;
 }
 
@@ -1016,6 +1029,7 @@ void Engine::run_dynamic(Slot& sl, int64_t first, int64_t n) {
   {
     std::lock_guard<std::mutex> lk(mu_);
     done_q_.clear();
+    pending_.store(0, std::memory_order_relaxed);
   }
   CudaDispatch ex(*this, sl, first, n);
   ScheduleResult r = sched_->run(ex);
@@ -1138,6 +1152,11 @@ std::string Engine::info(const std::string& what) const {
     out.set("launches_per_batch", Value::of(static_cast<long long>(launches_per_batch_)));
   } else if (what == "stats") {
     out.set("launches_per_batch", Value::of(static_cast<long long>(launches_per_batch_)));
+    // dynamic mode host cost: time in dispatch (setup of streams/events + launches)
+    // and waiting for completion callbacks, summed over all runs
+    out.set("host_dispatches", Value::of(static_cast<long long>(host_dispatches_)));
+    out.set("host_dispatch_us", Value::real(double(host_dispatch_ns_) / 1e3));
+    out.set("host_wait_us", Value::real(double(host_wait_ns_) / 1e3));
     out.set("runs", Value::of(static_cast<long long>(runs_)));
     out.set("batches", Value::of(static_cast<long long>(batches_run_)));
   } else if (what == "trace") {

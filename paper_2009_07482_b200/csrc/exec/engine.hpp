@@ -15,6 +15,7 @@
 //   isolated write/read                          -> H2D/D2H on the copy engines
 #pragma once
 
+#include <atomic>
 #include <condition_variable>
 #include <deque>
 #include <map>
@@ -206,6 +207,9 @@ class Engine {
   std::mutex mu_;
   std::condition_variable cv_;
   std::deque<Completion> done_q_;
+  std::atomic<int> pending_{0};
+  static constexpr int kSpinUs = 2000;
+  int64_t host_dispatch_ns_ = 0, host_wait_ns_ = 0, host_dispatches_ = 0;
   std::vector<Completion> last_log_;
   struct TraceRec {
     int component = -1, event = -1, kind = 0, kernel = -1, device = -1, queue = -1;
