@@ -42,3 +42,27 @@ def test_bench_two_ranks_partition_the_stream():
     assert line["config"]["parallelism"] == "instance partition x2"
     # rank 0 checks its own first instance (instance 0) against the oracle
     assert line["parity"]["instance"] == 0 and line["parity"]["normwise_err_vs_cpu_oracle"] <= 1e-4
+
+
+@pytest.mark.gpu
+def test_cli_run_and_measured_sweep(tmp_path):
+    """The CLI's B200 subcommands: `run` executes a spec through the engine and writes
+    its trace and outputs; `sweep --measure` profiles the head DAG's nodes on the GPU
+    (and the host) and simulates the mc grid."""
+    from paper_2009_07482_b200 import workloads
+    text, params = workloads.fork_join(n=256)
+    spec = tmp_path / "fj.json"
+    spec.write_text(text)
+    out = tmp_path / "out"
+    p = subprocess.run([sys.executable, "-m", "paper_2009_07482_b200", "run", "--spec", str(spec), "--params",
+                        "N=256", "--instances", "2", "--out", str(out)], cwd=ROOT, capture_output=True, text=True,
+                       timeout=300)
+    assert p.returncode == 0, p.stderr[-2000:]
+    assert p.stdout.startswith("makespan_ms")
+    assert (out / "trace.json").exists() and list(out.glob("out_k3_p2.npy"))
+    p = subprocess.run([sys.executable, "-m", "paper_2009_07482_b200", "sweep", "--heads", "2", "--beta", "128",
+                        "--qgpu", "1-2", "--qcpu", "1", "--measure"], cwd=ROOT, capture_output=True, text=True,
+                       timeout=300)
+    assert p.returncode == 0, p.stderr[-2000:]
+    lines = p.stdout.strip().splitlines()
+    assert lines[0].startswith("heads,beta") and lines[-1].startswith("best <")
