@@ -353,14 +353,14 @@ def _grouped_qkv(X, Ws, planes, outs, S, D, batch):
     _native.check(L.hs_stream_sync(stream()), "sync")
 
 
-@pytest.mark.parametrize("S,batch", [(128, 1), (128, 4), (128, 7), (100, 3), (128, 300)])
-def test_head_fused_bit_identical_to_grouped_qkv_and_attn_head(S, batch):
+@pytest.mark.parametrize("S,batch,D", [(128, 1, 512), (128, 4, 512), (128, 7, 512), (100, 3, 512), (128, 300, 512),
+                                       (128, 5, 256), (128, 3, 96), (64, 9, 1024)])
+def test_head_fused_bit_identical_to_grouped_qkv_and_attn_head(S, batch, D):
     """HS_OP_HEAD (projection + attention in one CTA-pair kernel, Q/K/V never leave
     the SM) equals the two launches it replaces: the grouped Q/K/V pair GEMM writing
     Q, K, V to HBM, then the fused attention head."""
     from tests.gpu_util import launch, split_weights
     import torch
-    D = 512
     X = _t(_rand(80, (batch, S * D)))
     Ws = [_t((_rand(81 + m, (D * 64,)) * np.float32(1 / np.sqrt(D))).astype(np.float32)) for m in range(3)]
     Wh = _t((_rand(84, (64 * 64,)) * np.float32(1 / 8)).astype(np.float32))
