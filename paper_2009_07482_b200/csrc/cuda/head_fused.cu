@@ -414,15 +414,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     };
     uint32_t it = 0, lt = 0;
-    bool pre = false;  // this group converted the current pair's first K-block during the last pair's P·V
+    // K-blocks of the current pair this group converted during the last pair's phase 2
+    bool pre0 = false, pre3 = false;
     for (int t = pair0; t < p.pairs; t += npairs, ++lt) {
       const uint32_t ph = lt & 1u;
       // ---- phase 1: split this CTA's X rows into the TMEM A stages (every other K-block)
       for (int kb = 0; kb < nk; ++kb, ++it) {
-        if (int(it & 1u) != g || (kb == 0 && pre)) continue;
+        if (int(it & 1u) != g || (kb == 0 && pre0) || (kb == 3 && pre3)) continue;
         convert(it, kb);
       }
-      pre = false;
+      pre0 = pre3 = false;
       // ---- phase 2 (A): operands of S = Q Kᵀ and C = P V, split across 12 warps:
       //      g = 0: Q (64 columns) -> tf32 hi [256, 320) / lo [320, 384) in TMEM
       //      g = 1: K -> K-major smem hi/lo, and Vᵀ for d in [0, 32)
@@ -504,7 +505,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // after S_FULL into the K operand's smem).
       if (t + npairs < p.pairs && int(it & 1u) == g && it % kNO == 0) {
         convert(it, 0);
-        pre = true;
+        pre0 = true;
       }
       // ---- (C) C columns [64r + 32g, +32) -> tf32 hi [256, 320) / lo [320, 384)
       mbar_wait(bar(O_FULL), ph);
@@ -525,6 +526,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(leader(C_READY));
+      // The next pair's K-block 3 goes to A stage 3 = TMEM [384, 448), P lo's
+      // columns: free once P·V has run (O_FULL, waited above). Its X tile was
+      // loaded after S_FULL like the first ones.
+      if (t + npairs < p.pairs && nk > 3 && int((it + 3u) & 1u) == g && it % kNO == 0) {
+        convert(it + 3u, 3);
+        pre3 = true;
+      }
       // The next pair's A stages 1-2 overlap C hi/lo [256, 384): convert only after
       // the Z MMA has read them. The Z accumulator is drained by warps 12-15.
       mbar_wait(bar(Z_FULL), ph);
