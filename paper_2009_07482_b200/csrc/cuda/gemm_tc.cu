@@ -785,17 +785,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #if HS_DBG_EARLYREL  // timing experiment only (wrong results): release the accumulator at once
       if (lane == 0) mbar_arrive_cluster(mapa_rank(acc_empty(int(acc)), 0));
 #endif
-#pragma unroll 1
-      for (int cb = 0; cb < BN / 32; ++cb) {
-        uint32_t r[32];
-        tmem_ld32(tacc + uint32_t(cb * 32), r);
-        if (cb == BN / 32 - 1 && !HS_DBG_EARLYREL) {
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive_cluster(mapa_rank(acc_empty(int(acc)), 0));
-        }
+      // one 32-column chunk: registers -> (ReLU) -> SW128 staging -> TMA store
+      auto store_chunk = [&](const uint32_t (&r)[32], int cb) {
         int c0 = n0 + cb * 32;
-        if (c0 >= p.N || !valid) continue;
+        if (c0 >= p.N || !valid) return;
         int mi = 0;
         if (p.n_out > 0) {
           mi = c0 / p.Nm;
@@ -817,6 +810,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (lane == 0 && !HS_DBG_NOEPI) tma_store_3d(&tmC.m[mi], buf, c0, m0 + q * 32, inst);
         ++cnt;
+      };
+      // Two chunks per TMEM round trip (two tcgen05.ld in flight, one wait); the
+      // accumulator is released as soon as the last pair is in registers.
+      static_assert((BN / 32) % 2 == 0, "pair epilogue drains chunks in pairs");
+#pragma unroll 1
+      for (int cb = 0; cb < BN / 32; cb += 2) {
+        uint32_t r0[32], r1[32];
+        tmem_ld32_nowait(tacc + uint32_t(cb * 32), r0);
+        tmem_ld32_nowait(tacc + uint32_t(cb * 32 + 32), r1);
+        tmem_ld_wait(r0);
+        tmem_ld_dep(r1);
+        if (cb + 2 == BN / 32 && !HS_DBG_EARLYREL) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(mapa_rank(acc_empty(int(acc)), 0));
+        }
+        store_chunk(r0, cb);
+        store_chunk(r1, cb + 1);
       }
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
