@@ -8,8 +8,8 @@ mc = (1, 0, 0) is the paper's default coarse-grained scheme. Two columns:
 
   simulated  platform_sim (hs_query "simulate") fed with kernel times
              measured on this machine: GPU times of each node on the B200 (engine
-             trace, one launch per ndrange), CPU times of the oracle's C kernels on
-             the host. Covers the whole grid, CPU heads included.
+             trace, one launch per ndrange), CPU times of numpy's fp32 kernels on the
+             host. Covers the whole grid, CPU heads included.
   measured   the same DAG on the B200 through the engine (graph mode, one launch per
              ndrange = the paper's execution model; all heads on the GPU, so only
              configurations with h_cpu = 0). The CPU never executes a node on the
@@ -157,25 +157,27 @@ def gpu_node_times(beta: int = 256, reps: int = 3) -> tuple[dict, dict]:
     return best, share
 
 
-def cpu_node_times(beta: int = 256, reps: int = 3) -> dict:
-    """Time of each node role with the oracle's C kernels on this host (the CPU
-    device of the simulated platform; test infrastructure, never the product)."""
+def cpu_node_times(beta: int = 256, reps: int = 5) -> dict:
+    """Time of each node role on this host's CPU (the CPU device of the simulated
+    platform), with numpy's fp32 kernels: BLAS sgemm, a strided transpose copy and a
+    row softmax. Best of `reps`."""
     import time
 
     import numpy as np
+    a = np.random.default_rng(0).standard_normal((beta, beta)).astype(np.float32)
 
-    from oracle import oracle as O
-    a = np.random.default_rng(0).standard_normal((1, beta * beta)).astype(np.float32)
-    out = np.empty_like(a)
-    cases = {"gemm": ("gemm", [a, a], [beta * beta] * 2, [beta, beta, beta]),
-             "transpose": ("transpose", [a], [beta * beta], [beta, beta]),
-             "softmax": ("softmax", [a], [beta * beta], [beta, beta, 1, 1])}
+    def softmax(x):
+        e = np.exp(x - x.max(axis=1, keepdims=True))
+        return e / e.sum(axis=1, keepdims=True)
+
+    cases = {"gemm": lambda: a @ a, "transpose": lambda: np.ascontiguousarray(a.T), "softmax": lambda: softmax(a)}
     res = {}
-    for ro, (name, ins, strides, vals) in cases.items():
+    for ro, fn in cases.items():
+        fn()
         t = []
         for _ in range(reps):
             t0 = time.perf_counter()
-            O.run_node(name, ins, strides, out, beta * beta, vals, 1)
+            fn()
             t.append((time.perf_counter() - t0) * 1e3)
         res[ro] = min(t)
     return res

@@ -1,4 +1,4 @@
-"""Offline precision study: emulate split-precision GEMMs (tf32x3, bf16x3,
+"""TEST INFRASTRUCTURE (offline study, uses the CPU oracle as the checker): precision study: emulate split-precision GEMMs (tf32x3, bf16x3,
 bf16x2+, tf32x1) inside the full 12-layer encoder DAG with numpy and report the
 normwise error of the final output against the fp32 CPU oracle.
 

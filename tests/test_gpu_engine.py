@@ -138,7 +138,7 @@ def test_chain_rewrites_match_oracle(math, oracle_mod):
 @pytest.mark.parametrize("mode", ["graph", "dynamic"])
 def test_encoder_bf16x3_within_tolerance(mode, oracle_mod):
     """BF16X3 math (resident-weight GEMMs as 3-term bf16 splits on kind::f16) stays
-    within the 1e-4 fp32 tolerance on a 2-layer encoder (profiles/split_precision.py
+    within the 1e-4 fp32 tolerance on a 2-layer encoder (tests/split_precision_study.py
     predicts ~5e-6 for 12 layers)."""
     text, params, meta = workloads.encoder(layers=2)
     n = 2
