@@ -242,3 +242,20 @@ def test_memory_domains_need_graph_mode():
     text, params, meta = workloads.encoder(layers=1, devices=2)
     with pytest.raises(Exception, match="graph mode"):
         Engine(text, params, mode="dynamic", device_gpus={0: 0, 1: 0}, domain_per_device=True)
+
+
+@pytest.mark.parametrize("S,D,DFF", [(100, 256, 512), (64, 128, 256)])
+def test_ragged_encoder_through_all_rewrites(S, D, DFF, oracle_mod):
+    """Encoder shapes other than the C3 ones (S < 128 rows, narrower d_model / d_ff)
+    through the default plan (whole-head kernels, concat in place, split-K for the
+    single-instance batch) against the oracle, in one- and two-instance batches."""
+    params = {"S": S, "D": D, "DK": 64, "DFF": DFF}
+    text, params, meta = workloads.encoder(layers=2, heads=D // 64, params=params)
+    key = (meta["output"]["kernel"], meta["output"]["pos"])
+    for n, batch in ((1, 1), (3, 2)):
+        arrays = _encoder_arrays(meta, params, n)
+        ref = oracle_mod.run_dag(text, params, arrays, n)
+        outs, _, plan = _run_gpu(text, params, arrays, n, mode="graph", batch=batch)
+        assert plan["chain_rewrites"].get("head_fused", 0) == 2 * (D // 64)
+        for i in range(n):
+            assert _normwise(outs[key][i], ref[key][i]) <= TOL, (n, i)
