@@ -288,6 +288,16 @@ def _time_launches(L, st, launch, reps):
     return ns.value / 1e9 / reps
 
 
+def _traffic(name, batch, math_mode="tf32x3"):
+    """DRAM bytes per launch from a committed ncu --set full capture (profiles/<name>),
+    scaled to `batch` instances; None when absent."""
+    f = ROOT / "profiles" / name
+    if not f.exists():
+        return None
+    per = json.loads(f.read_text()).get(math_mode, {}).get("dram_bytes_per_launch_per_instance")
+    return per * batch if per else None
+
+
 def kernel_rooflines(batch, peak_tflops, hbm_gbs, reps=20):
     """The other two kernels of the C5 plan, launched as the DAG launches them:
     the whole-head kernel (HS_OP_HEAD, tensor-bound; algorithmic flops of the head
@@ -342,6 +352,7 @@ def kernel_rooflines(batch, peak_tflops, hbm_gbs, reps=20):
         {"kernel": f"head_pair_kernel (HS_OP_HEAD: Q/K/V projection + attention) x{batch}", "bound": "tensor",
          "achieved": f_head / t_head / 1e12, "peak": peak_tflops, "unit": "TFLOP/s",
          "frac": f_head / t_head / 1e12 / peak_tflops, "ms_per_launch": t_head * 1e3,
+         "traffic": _traffic("head_traffic.json", batch),
          "note": "algorithmic flops; the kernel also computes 2x the QK^T and P.V flops (off-diagonal pair blocks)"},
         {"kernel": f"add_ln_kernel x{batch}", "bound": "hbm", "achieved": b_ln / t_ln / 1e9, "peak": hbm_gbs,
          "unit": "GB/s", "frac": b_ln / t_ln / 1e9 / hbm_gbs, "ms_per_launch": t_ln * 1e3},
