@@ -48,7 +48,9 @@ def parse_args():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--instances", type=int, default=TOTAL_INSTANCES)
     ap.add_argument("--layers", type=int, default=LAYERS)
-    ap.add_argument("--batch", type=int, default=512, help="instances per batched node launch")
+    ap.add_argument("--batch", type=int, default=0,
+                    help="instances per batched node launch (0: min(512, half of this rank's instances), so every "
+                         "rank pipelines at least two batches through its two slots)")
     ap.add_argument("--slots", type=int, default=2)
     ap.add_argument("--queues", type=int, default=3)
     ap.add_argument("--devices", type=int, default=1, help="logical devices in the cq map (all on this GPU)")
@@ -504,6 +506,9 @@ def run_ours(args, world, rank, local):
     torch.cuda.set_device(local)
     text, params, meta = workloads.encoder(layers=args.layers, queues=args.queues, devices=args.devices)
     first, n = partition(args.instances, world, rank)
+    if args.batch <= 0:  # same on every rank: derived from the largest partition
+        per = math.ceil(args.instances / world)
+        args.batch = max(1, min(512, math.ceil(per / 2)))
     S, D = params["S"], params["D"]
     inst_bytes = S * D * 4
     weights = workloads.encoder_weights(meta)
