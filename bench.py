@@ -50,8 +50,8 @@ def parse_args():
     ap.add_argument("--layers", type=int, default=LAYERS)
     ap.add_argument("--batch", type=int, default=0,
                     help="instances per batched node launch (0: min(512, half of this rank's instances), so every "
-                         "rank pipelines at least two batches through its two slots)")
-    ap.add_argument("--slots", type=int, default=2)
+                         "rank pipelines at least two batches through its slots)")
+    ap.add_argument("--slots", type=int, default=3, help="instance slots (graphs) in flight: copies of one batch overlap the others")
     ap.add_argument("--queues", type=int, default=3)
     ap.add_argument("--devices", type=int, default=1, help="logical devices in the cq map (all on this GPU)")
     ap.add_argument("--math", default="tf32x3")
