@@ -59,6 +59,35 @@ __global__ void transpose_kernel(const float* __restrict__ A, int64_t sA, float*
   }
 }
 
+// Wide tile: 32 rows x 128 columns per block, 16-byte loads along C (each thread
+// four float4, more bytes in flight than the 32 x 32 scalar tile), coalesced
+// 128-byte scalar stores along R. Needs C % 4 == 0 and 16-byte aligned rows.
+__global__ void transpose_wide_kernel(const float* __restrict__ A, int64_t sA, float* __restrict__ B, int64_t sB,
+                                      int R, int C) {
+  __shared__ float tile[32][129];
+  const int64_t inst = blockIdx.z;
+  A += inst * sA;
+  B += inst * sB;
+  const int c0 = blockIdx.x * 128, r0 = blockIdx.y * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = r0 + ty + 8 * i, c = c0 + 4 * tx;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (r < R && c < C) v = __ldg(reinterpret_cast<const float4*>(A + int64_t(r) * C + c));
+    tile[ty + 8 * i][4 * tx] = v.x;
+    tile[ty + 8 * i][4 * tx + 1] = v.y;
+    tile[ty + 8 * i][4 * tx + 2] = v.z;
+    tile[ty + 8 * i][4 * tx + 3] = v.w;
+  }
+  __syncthreads();
+#pragma unroll 4
+  for (int i = 0; i < 16; ++i) {
+    const int c = c0 + ty + 8 * i, r = r0 + tx;
+    if (r < R && c < C) B[int64_t(c) * R + r] = tile[tx][ty + 8 * i];
+  }
+}
+
 // ---------------------------------------------------------------- elementwise
 template <bool kVec>
 __global__ void scale_kernel(const float* __restrict__ A, int64_t sA, float* __restrict__ B, int64_t sB, int64_t n,
@@ -102,15 +131,18 @@ __global__ void add_kernel(const float* __restrict__ A, int64_t sA, const float*
 // ---------------------------------------------------------------- softmax
 // One warp per row. kV > 0: cols == 128*kV, each lane holds kV float4 in
 // registers. kV == 0: generic cols (<= 1024), scalar loads.
+// One warp per row; the instance is blockIdx.y (no 64-bit division per row).
+// kV > 0: cols == 128*kV, each lane holds kV float4 in registers. kV == 0:
+// generic cols (<= 1024), scalar loads.
 template <int kV>
 __global__ void softmax_kernel(const float* __restrict__ A, int64_t sA, float* __restrict__ B, int64_t sB, int rows,
-                               int cols, float f, int64_t total_rows) {
+                               int cols, float f) {
   const int lane = threadIdx.x & 31;
-  const int64_t row = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (row >= total_rows) return;
-  const int64_t inst = row / rows, r = row % rows;
-  const float* a = A + inst * sA + r * cols;
-  float* b = B + inst * sB + r * cols;
+  const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= rows) return;
+  const int64_t inst = blockIdx.y;
+  const float* a = A + inst * sA + int64_t(r) * cols;
+  float* b = B + inst * sB + int64_t(r) * cols;
   if constexpr (kV > 0) {
     float4 v[kV];
     float m = -INFINITY;
@@ -246,13 +278,13 @@ __global__ void concat_kernel(ConcatSrc src, float* __restrict__ Y, int64_t sY, 
   float* y = Y + inst * sY + int64_t(i) * cols_each;
   const int64_t row_len = int64_t(cols_each) * count;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  if (kVec) {
+  if (kVec) {  // 32-bit index math (rows * cols_each < 2^31 per member, checked by the launcher)
     const int c4 = cols_each >> 2;
-    const int64_t n4 = int64_t(rows) * c4;
-    for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < n4; t += stride) {
-      int64_t r = t / c4, c = t % c4;
-      float4 v = __ldg(reinterpret_cast<const float4*>(z + r * cols_each) + c);
-      *reinterpret_cast<float4*>(y + r * row_len + c * 4) = v;
+    const int n4 = rows * c4;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n4; t += int(stride)) {
+      const int r = t / c4, c = t - r * c4;
+      float4 v = __ldg(reinterpret_cast<const float4*>(z + int64_t(r) * cols_each) + c);
+      *reinterpret_cast<float4*>(y + int64_t(r) * row_len + c * 4) = v;
     }
   } else {
     const int64_t n = int64_t(rows) * cols_each;
@@ -266,8 +298,13 @@ __global__ void concat_kernel(ConcatSrc src, float* __restrict__ Y, int64_t sY, 
 }  // namespace
 
 cudaError_t transpose(const float* A, int64_t sA, float* B, int64_t sB, int R, int C, int batch, cudaStream_t s) {
-  dim3 grid((C + 31) / 32, (R + 31) / 32, batch), block(32, 8);
-  transpose_kernel<<<grid, block, 0, s>>>(A, sA, B, sB, R, C);
+  if (C % 4 == 0 && sA % 4 == 0 && aligned16(A)) {
+    dim3 grid((C + 127) / 128, (R + 31) / 32, batch), block(32, 8);
+    transpose_wide_kernel<<<grid, block, 0, s>>>(A, sA, B, sB, R, C);
+  } else {
+    dim3 grid((C + 31) / 32, (R + 31) / 32, batch), block(32, 8);
+    transpose_kernel<<<grid, block, 0, s>>>(A, sA, B, sB, R, C);
+  }
   return cudaGetLastError();
 }
 
@@ -290,18 +327,17 @@ cudaError_t add(const float* A, int64_t sA, const float* B, int64_t sB, float* C
 
 cudaError_t softmax(const float* A, int64_t sA, float* B, int64_t sB, int rows, int cols, float f, int batch,
                     cudaStream_t s) {
-  if (cols > 1024 || cols < 1) return cudaErrorInvalidValue;
-  const int64_t total = int64_t(rows) * batch;
+  if (cols > 1024 || cols < 1 || batch > 65535) return cudaErrorInvalidValue;
   const int rows_per_block = kThreads / 32;
-  dim3 grid(unsigned((total + rows_per_block - 1) / rows_per_block));
+  dim3 grid(unsigned((rows + rows_per_block - 1) / rows_per_block), unsigned(batch));
   bool vec = cols % 128 == 0 && sA % 4 == 0 && sB % 4 == 0 && aligned16(A) && aligned16(B);
   int v = vec ? cols / 128 : 0;
   switch (v) {
-    case 1: softmax_kernel<1><<<grid, kThreads, 0, s>>>(A, sA, B, sB, rows, cols, f, total); break;
-    case 2: softmax_kernel<2><<<grid, kThreads, 0, s>>>(A, sA, B, sB, rows, cols, f, total); break;
-    case 4: softmax_kernel<4><<<grid, kThreads, 0, s>>>(A, sA, B, sB, rows, cols, f, total); break;
-    case 8: softmax_kernel<8><<<grid, kThreads, 0, s>>>(A, sA, B, sB, rows, cols, f, total); break;
-    default: softmax_kernel<0><<<grid, kThreads, 0, s>>>(A, sA, B, sB, rows, cols, f, total); break;
+    case 1: softmax_kernel<1><<<grid, kThreads, 0, s>>>(A, sA, B, sB, rows, cols, f); break;
+    case 2: softmax_kernel<2><<<grid, kThreads, 0, s>>>(A, sA, B, sB, rows, cols, f); break;
+    case 4: softmax_kernel<4><<<grid, kThreads, 0, s>>>(A, sA, B, sB, rows, cols, f); break;
+    case 8: softmax_kernel<8><<<grid, kThreads, 0, s>>>(A, sA, B, sB, rows, cols, f); break;
+    default: softmax_kernel<0><<<grid, kThreads, 0, s>>>(A, sA, B, sB, rows, cols, f); break;
   }
   return cudaGetLastError();
 }
@@ -336,6 +372,7 @@ cudaError_t concat(const float* const* Z, const int64_t* sZ, int count, float* Y
     src.s[i] = sZ[i];
     vec = vec && sZ[i] % 4 == 0 && aligned16(Z[i]);
   }
+  vec = vec && int64_t(rows) * cols_each < (int64_t(1) << 31);
   const int64_t work = vec ? int64_t(rows) * (cols_each / 4) : int64_t(rows) * cols_each;
   dim3 grid(blocks_for(work, kThreads), count, batch);
   if (vec) concat_kernel<true><<<grid, kThreads, 0, s>>>(src, Y, sY, rows, cols_each, count);
