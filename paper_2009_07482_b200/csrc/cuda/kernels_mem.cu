@@ -9,7 +9,7 @@
 // instances; per-instance strides of 0 express shared operands.
 //
 // Numerics follow the CPU oracle (oracle/kernels.c): softmax = exp(s*x - max)
-// / sum with accurate expf and IEEE division; LayerNorm is two-pass
+// with accurate expf, times 1/sum (one IEEE division per row); LayerNorm is two-pass
 // (mean, then centred variance), eps added before 1/sqrt. transpose, concat
 // and scale by a power of two are bit-exact.
 #include <cuda_runtime.h>
@@ -160,10 +160,10 @@ __global__ void softmax_kernel(const float* __restrict__ A, int64_t sA, float* _
       v[j].z = expf(v[j].z - m); v[j].w = expf(v[j].w - m);
       s += (v[j].x + v[j].y) + (v[j].z + v[j].w);
     }
-    s = warp_sum(s);
+    const float inv = 1.f / warp_sum(s);  // one division per row, then multiplies
 #pragma unroll
     for (int j = 0; j < kV; ++j) {
-      v[j].x = v[j].x / s; v[j].y = v[j].y / s; v[j].z = v[j].z / s; v[j].w = v[j].w / s;
+      v[j].x *= inv; v[j].y *= inv; v[j].z *= inv; v[j].w *= inv;
       reinterpret_cast<float4*>(b)[lane + 32 * j] = v[j];
     }
   } else {
