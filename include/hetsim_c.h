@@ -190,7 +190,10 @@ typedef struct hs_engine* hs_engine_t;
  *   "batch": B, "slots": 2, "math": "tf32x3"|"tf32"|"simt",
  *   "cpu_devices": [..], "trace": false, "fuse": 3}
  * fuse (graph mode launch lowering): 0 one launch per ndrange,
- * 1 + grouped sibling GEMMs, 2 + chain rewrites, 3 (default) + whole-head launches. */
+ * 1 + grouped sibling GEMMs, 2 + chain rewrites, 3 (default) + whole-head launches.
+ * Optional: "device_gpus": {"<logical device>": ordinal} (components across GPUs),
+ * "domain_per_device": 0|1, "ramp": 1|0 (batch/4 first and last chunks when the
+ * bindings are host memory). */
 int hs_engine_create(const char* config_json, hs_engine_t* out);
 int hs_engine_destroy(hs_engine_t e);
 

@@ -157,6 +157,7 @@ Engine::~Engine() {
   clear_trace();
   for (auto& sl : slots_) {
     hs_graph_destroy(sl.graph);
+    hs_graph_destroy(sl.graph_small);
     for (auto& [k, e] : sl.events) hs_event_destroy(e);
     for (auto& [k, e] : sl.group_event) hs_event_destroy(e);
     for (auto& [k, e] : sl.din) hs_event_destroy(e);
@@ -505,7 +506,7 @@ void Engine::launch_node(Slot& sl, hs_stream_t s, int kernel) {
   for (const auto& in : nd.inputs) {
     auto io = io_copy_.find(in);
     if (io != io_copy_.end())
-      hs_ok(hs_memcpy_d2d(s, sl.buf.at(in), sl.buf.at(io->second), size_t(bytes_.at(in) * cfg_.batch)), "io copy");
+      hs_ok(hs_memcpy_d2d(s, sl.buf.at(in), sl.buf.at(io->second), size_t(bytes_.at(in) * nb())), "io copy");
   }
   hs_op_args a{};
   a.n_in = int(nd.inputs.size());
@@ -531,7 +532,7 @@ void Engine::launch_node(Slot& sl, hs_stream_t s, int kernel) {
     a.in_stride[1] = 0;
     a.aux = head_qkv_planes_.at(kernel);
   }
-  hs_ok(hs_launch(s, nd.op, &a, cfg_.math, cfg_.batch), "hs_launch");
+  hs_ok(hs_launch(s, nd.op, &a, cfg_.math, int(nb())), "hs_launch");
 }
 
 void Engine::issue(Slot& sl, const TaskComponent& t, const CommandQueueStructure& q, int prev_comp,
@@ -587,11 +588,11 @@ void Engine::issue(Slot& sl, const TaskComponent& t, const CommandQueueStructure
           auto io = io_copy_.find(key);
           auto pr = peer_in_.find(key);
           if (io != io_copy_.end())
-            hs_ok(hs_memcpy_d2d(s, sl.buf.at(key), sl.buf.at(io->second), size_t(bytes_.at(key) * cfg_.batch)),
+            hs_ok(hs_memcpy_d2d(s, sl.buf.at(key), sl.buf.at(io->second), size_t(bytes_.at(key) * nb())),
                   "dependent write");
           else if (pr != peer_in_.end())  // producer in another memory domain: one peer copy (NVLink)
             hs_ok(hs_memcpy_peer(s, sl.buf.at(key), dom_gpu_[size_t(kdom(key.first))], sl.buf.at(pr->second),
-                                 dom_gpu_[size_t(kdom(pr->second.first))], size_t(bytes_.at(key) * cfg_.batch)),
+                                 dom_gpu_[size_t(kdom(pr->second.first))], size_t(bytes_.at(key) * nb())),
                   "dependent write (peer)");
         } else if (!graph) {
           const int gi = group_of_.at(key);
@@ -652,7 +653,7 @@ void Engine::issue(Slot& sl, const TaskComponent& t, const CommandQueueStructure
             a.outs[m] = sl.buf.at(okey);
             a.out_strides[m] = bytes_.at(okey) / 4;
           }
-          hs_ok(hs_launch(s, nd.op, &a, cfg_.math, cfg_.batch), "hs_launch (grouped)");
+          hs_ok(hs_launch(s, nd.op, &a, cfg_.math, int(nb())), "hs_launch (grouped)");
           record = true;
         } else if (member != fuse_member_.end()) {
           // computed by the group's leader launch: order this queue after it
@@ -983,6 +984,13 @@ void Engine::capture(Slot& sl) {
   hs_ok(hs_capture_begin(sl.origin), "capture begin");
   emit_plan(sl);
   hs_ok(hs_capture_end(sl.origin, &sl.graph), "capture end");
+  if (ramp_ > 0) {  // the same plan for ramp_ instances (first and last chunks of a host-fed stream)
+    cur_batch_ = ramp_;
+    hs_ok(hs_capture_begin(sl.origin), "capture begin");
+    emit_plan(sl);
+    hs_ok(hs_capture_end(sl.origin, &sl.graph_small), "capture end");
+    cur_batch_ = 0;
+  }
 }
 
 void Engine::clear_trace() {
@@ -1050,6 +1058,16 @@ void Engine::run(int64_t first, int64_t n, int64_t* elapsed_ns) {
     if (cfg_.graph_mode) {
       if (cfg_.fuse >= 1 && cfg_.math != HS_MATH_FP32_SIMT) plan_fusion();
       if (cfg_.fuse >= 2 && cfg_.math != HS_MATH_FP32_SIMT) plan_chain_rewrites();
+      // Ramp (host-fed streams): the first and last chunks of a run are ramp_ =
+      // batch/4 instances, so the copy-in before the first graph and the copy-out
+      // after the last one are short; the copies of every other chunk overlap
+      // the graphs of the other slots.
+      bool host_io = false;
+      for (const auto& gr : groups_)
+        if (!gr.resident && !gr.b.on_device) host_io = true;
+      for (const auto& key : outputs_)
+        if (!bindings_.at(key).on_device) host_io = true;
+      if (cfg_.ramp && host_io && !cfg_.trace && cfg_.batch >= 8 && slots_.size() > 1) ramp_ = cfg_.batch / 4;
       if (capture_ok_)
         for (auto& sl : slots_) capture(sl);
     }
@@ -1064,9 +1082,24 @@ void Engine::run(int64_t first, int64_t n, int64_t* elapsed_ns) {
   for (size_t i = 1; i < slots_.size(); ++i) hs_ok(hs_stream_wait(slots_[i].origin, s0.t_start), "start wait");
   if (cfg_.trace) clear_trace();
   if (cfg_.graph_mode) {
-    for (int64_t b = 0; b < nb; ++b) {
+    // chunks of the stream: (offset, count, small graph?)
+    std::vector<std::tuple<int64_t, int64_t, bool>> chunks;
+    if (ramp_ > 0 && capture_ok_ && n >= 4 * B) {
+      const int64_t R = ramp_;
+      const int64_t full = (n - 2 * R) / B;
+      int64_t off = 0;
+      chunks.emplace_back(off, R, true);
+      off += R;
+      for (int64_t i = 0; i < full; ++i, off += B) chunks.emplace_back(off, B, false);
+      for (; off < n; off += R) chunks.emplace_back(off, std::min(R, n - off), true);
+    } else {
+      for (int64_t b = 0; b < nb; ++b) chunks.emplace_back(b * B, std::min(B, n - b * B), false);
+    }
+    for (size_t ci = 0; ci < chunks.size(); ++ci) {
+      const auto [off, cnt, small] = chunks[ci];
+      const int64_t b = int64_t(ci);
       Slot& sl = slots_[size_t(b % int64_t(slots_.size()))];
-      const int64_t f = first + b * B, cnt = std::min(B, n - b * B);
+      const int64_t f = first + off;
       copies(sl, f, cnt, true);
       if ((cfg_.trace && b == 0) || !capture_ok_) {
         // traced batch: the same plan issued directly (not replayed) with a
@@ -1078,10 +1111,11 @@ void Engine::run(int64_t first, int64_t n, int64_t* elapsed_ns) {
         emit_plan(sl);
         tracing_ = false;
       } else {
-        hs_ok(hs_graph_launch(sl.graph, sl.origin), "graph launch");
+        hs_ok(hs_graph_launch(small ? sl.graph_small : sl.graph, sl.origin), "graph launch");
       }
       copies(sl, f, cnt, false);
     }
+    batches_run_ += int64_t(chunks.size()) - nb;  // counted below as nb
   } else {
     for (auto& [k, s] : s0.streams) hs_ok(hs_stream_wait(s, s0.t_start), "start wait");
     for (int64_t b = 0; b < nb; ++b) {
@@ -1144,6 +1178,7 @@ std::string Engine::info(const std::string& what) const {
     out.set("domain_gpus", std::move(gpus));
     out.set("peer_copies_per_batch", Value::of(static_cast<long long>(peer_in_.size())));
     out.set("captured", Value::of(static_cast<long long>(capture_ok_ && cfg_.graph_mode ? 1 : 0)));
+    out.set("ramp_batch", Value::of(static_cast<long long>(ramp_)));
     out.set("aliased_inputs", Value::of(static_cast<long long>(alias_.size())));
     out.set("grouped_launches", Value::of(static_cast<long long>(fuse_groups_.size())));
     Value rw = Value::make_object();
@@ -1255,6 +1290,7 @@ int hs_engine_create(const char* config_json, hs_engine_t* out) {
     if (const json::Value* v = c.find("device_gpus"))
       for (const auto& [k, g] : v->object_items()) cfg.device_gpus[std::stoi(k)] = g.as_int();
     if (const json::Value* v = c.find("domain_per_device")) cfg.domain_per_device = v->as_int() != 0;
+    if (const json::Value* v = c.find("ramp")) cfg.ramp = v->as_int() != 0;
     if (const json::Value* v = c.find("fuse")) {
       cfg.fuse = v->as_int();
       if (cfg.fuse < 0 || cfg.fuse > 3) fail(Errc::invalid_param, "fuse must be 0, 1, 2 or 3");

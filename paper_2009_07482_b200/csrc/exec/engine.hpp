@@ -57,6 +57,9 @@ struct EngineConfig {
   // own domain even on one GPU (exercises the peer path on a 1-GPU machine).
   std::map<int, int> device_gpus;
   bool domain_per_device = false;
+  // Graph mode with host-memory inputs/outputs: first and last chunks of a run
+  // use a second graph of batch/4 instances (shorter exposed copies).
+  bool ramp = true;
 };
 
 class Engine {
@@ -109,6 +112,7 @@ class Engine {
     std::map<int, hs_event_t> group_event;
     std::set<int> group_done;
     hs_graph_t graph = nullptr;
+    hs_graph_t graph_small = nullptr;  // the plan at ramp_ instances
     hs_event_t t_start = nullptr, t_end = nullptr;
     // several memory domains: per-domain copy streams joined to `origin`
     std::map<int, hs_stream_t> dorigin;
@@ -195,6 +199,9 @@ class Engine {
   std::map<hs_stream_t, int> stream_dom_;
   std::map<std::pair<int, int>, std::pair<int, int>> peer_in_;  // input fed across domains -> producer
   bool capture_ok_ = true;           // one physical GPU: the plan is captured into graphs
+  int64_t ramp_ = 0;                 // small-graph batch (0: no ramp)
+  int64_t cur_batch_ = 0;            // instances of the plan being emitted (0: cfg_.batch)
+  int64_t nb() const { return cur_batch_ ? cur_batch_ : cfg_.batch; }
   std::vector<Slot> slots_;
   bool planned_ = false;
   bool resident_uploaded_ = false;

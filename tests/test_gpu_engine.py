@@ -259,3 +259,32 @@ def test_ragged_encoder_through_all_rewrites(S, D, DFF, oracle_mod):
         assert plan["chain_rewrites"].get("head_fused", 0) == 2 * (D // 64)
         for i in range(n):
             assert _normwise(outs[key][i], ref[key][i]) <= TOL, (n, i)
+
+
+def test_ramp_chunks_match_full_batches(oracle_mod):
+    """Host-fed graph runs start and end with batch/4-instance chunks (a second
+    captured graph) so the exposed copies are short; every instance is computed
+    exactly as in the full-batch plan (bit-identical to the device-resident run,
+    which has no ramp)."""
+    import torch
+    text, params, meta = workloads.encoder(layers=1)
+    n, batch = 40, 8
+    arrays = _encoder_arrays(meta, params, n)
+    key = (meta["output"]["kernel"], meta["output"]["pos"])
+    host, _, plan = _run_gpu(text, params, arrays, n, mode="graph", batch=batch, slots=3)
+    assert plan["ramp_batch"] == 2
+    x = torch.from_numpy(arrays[(meta["x_inputs"][0]["kernel"], meta["x_inputs"][0]["pos"])]).cuda()
+    out = torch.zeros(n, params["S"] * params["D"], device="cuda")
+    torch.cuda.synchronize()
+    with Engine(text, params, mode="graph", batch=batch, slots=3) as eng:
+        for i in meta["x_inputs"]:
+            eng.bind(i["kernel"], i["pos"], x)
+        for k, w in workloads.encoder_weights(meta).items():
+            eng.bind(*k, w.reshape(-1), shared=True)
+        eng.bind(*key, out)
+        eng.run(0, n)
+        assert eng.info("plan")["ramp_batch"] == 0
+    assert np.array_equal(host[key], out.cpu().numpy())
+    ref = oracle_mod.run_dag(text, params, {k: (v[:2] if v.ndim == 2 else v) for k, v in arrays.items()}, 2)
+    for i in range(2):
+        assert _normwise(host[key][i], ref[key][i]) <= TOL
