@@ -163,7 +163,6 @@ Engine::~Engine() {
     for (auto& [k, e] : sl.din) hs_event_destroy(e);
     for (auto& [k, e] : sl.dout) hs_event_destroy(e);
     hs_event_destroy(sl.copy_fork);
-    hs_event_destroy(sl.copy_join);
     hs_event_destroy(sl.t_start);
     hs_event_destroy(sl.t_end);
     for (auto& [k, s] : sl.streams) hs_stream_destroy(s);
@@ -382,7 +381,6 @@ void Engine::plan_buffers() {
     hs_ok(hs_event_create(ctx_, 1, &sl.t_end), "hs_event_create");
     if (dctx_.size() > 1) {
       hs_ok(hs_event_create(ctx_, 0, &sl.copy_fork), "hs_event_create");
-      hs_ok(hs_event_create(ctx_, 0, &sl.copy_join), "hs_event_create");
       for (size_t d = 1; d < dctx_.size(); ++d) dstream(sl, int(d));
     }
   }

@@ -117,7 +117,7 @@ class Engine {
     // several memory domains: per-domain copy streams joined to `origin`
     std::map<int, hs_stream_t> dorigin;
     std::map<int, hs_event_t> din, dout;
-    hs_event_t copy_fork = nullptr, copy_join = nullptr;
+    hs_event_t copy_fork = nullptr;
   };
 
   void build_nodes();
