@@ -71,8 +71,17 @@ using namespace tc;
 
 constexpr int kS = 128, kDK = 64, kN = 3 * kDK;  // rows, head width, projection width
 constexpr int kThreads = 512;
-constexpr int kNS = 4;  // X staging stages
-constexpr int kNO = 4;  // W operand stages = TMEM A stages
+// Variant (measured slower, kept for A/B): three converter groups (warps 12-15
+// convert too) with 6 X / 3 W+A stages. The projection drops from ~21k to ~19.6k
+// cycles per pair, but stage 0 can be pre-converted for only a third of the
+// pairs, and the first K-blocks of a pair wait for O_FULL: 105 vs 99 us per
+// 512-instance launch (profiles/README.md).
+#ifndef HS_HEAD_CONV3
+#define HS_HEAD_CONV3 0
+#endif
+constexpr int kConv = HS_HEAD_CONV3 ? 3 : 2;  // converter groups (each takes every kConv-th K-block)
+constexpr int kNS = HS_HEAD_CONV3 ? 6 : 4;    // X staging stages
+constexpr int kNO = HS_HEAD_CONV3 ? 3 : 4;    // W operand stages = TMEM A stages
 constexpr uint32_t kStaging = BM * BK * 4;            // 16 KB X tile
 constexpr uint32_t kPlaneB = (kN / 2) * 128;          // 96 rows x 128 B: this CTA's half of N
 constexpr uint32_t kOperand = 2 * kPlaneB;            // hi + lo
@@ -256,8 +265,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         // X stages share the K operand's smem: free once the last pair's S = Q Kᵀ is done
         if (lt > 0) mbar_wait(bar(S_FULL), (lt - 1) & 1u);
         const int inst = 2 * t + int(rank);  // >= batch: zero-filled box
+        bool o_waited = lt == 0;
         for (int kb = 0; kb < nk; ++kb, ++it) {
           const int s = int(it % kNS);
+          if (s >= 4 && !o_waited) {  // stages 4-5 share the Vᵀ operand's smem: wait for P·V
+            mbar_wait(bar(O_FULL), (lt - 1) & 1u);
+            o_waited = true;
+          }
           mbar_wait(bar(ST_EMPTY + s), ((it / kNS) & 1u) ^ 1u);
           mbar_expect_tx(bar(ST_FULL + s), kStaging);
           tma_load_3d(base + kU + uint32_t(s) * kStaging, &tmX, bar(ST_FULL + s), kb * BK, 0, inst);
@@ -385,6 +399,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int col0 = int(rank) * kS;  // this CTA's block of S (its own keys)
     // one K-block of X rows -> TMEM A stage (iteration `i` of the stage rings)
     auto convert = [&](uint32_t i, int kb) {
+      (void)g;
       const int s = int(i % kNS), o = int(i % kNO);
       mbar_wait(bar(ST_FULL + s), (i / kNS) & 1u);
       mbar_wait(bar(OP_EMPTY + o), ((i / kNO) & 1u) ^ 1u);
@@ -416,11 +431,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t it = 0, lt = 0;
     // K-blocks of the current pair this group converted during the last pair's phase 2
     bool pre0 = false, pre3 = false;
+    int pre0k = 0;  // which K-block went to stage 0 early
     for (int t = pair0; t < p.pairs; t += npairs, ++lt) {
       const uint32_t ph = lt & 1u;
       // ---- phase 1: split this CTA's X rows into the TMEM A stages (every other K-block)
       for (int kb = 0; kb < nk; ++kb, ++it) {
-        if (int(it & 1u) != g || (kb == 0 && pre0) || (kb == 3 && pre3)) continue;
+        if (int(it % kConv) != g || (kb == pre0k && pre0) || (kb == 3 && pre3)) continue;
         convert(it, kb);
       }
       pre0 = pre3 = false;
@@ -503,9 +519,24 @@ __global__ void __launch_bounds__(kThreads, 1)
       // free once every warp of this lane quarter has read S (both passed the
       // exchange barriers above). Convert it while P·V runs (its X tile was loaded
       // after S_FULL into the K operand's smem).
-      if (t + npairs < p.pairs && int(it & 1u) == g && it % kNO == 0) {
-        convert(it, 0);
-        pre0 = true;
+      if constexpr (kConv == 2) {
+        if (t + npairs < p.pairs && int(it & 1u) == g && it % kNO == 0) {
+          convert(it, 0);
+          pre0 = true;
+          pre0k = 0;
+        }
+      } else {
+        // the first of the next pair's K-blocks 0-2 that maps to stage 0 (group 0 owns
+        // it, as kNO == kConv), if its X stage lies in the K operand's smem
+        for (uint32_t j = 0; j < 3 && int(j) < nk; ++j)
+          if ((it + j) % kNO == 0) {
+            if (t + npairs < p.pairs && g == 0 && (it + j) % kNS < 4) {
+              convert(it + j, int(j));
+              pre0 = true;
+              pre0k = int(j);
+            }
+            break;
+          }
       }
       // ---- (C) C columns [64r + 32g, +32) -> tf32 hi [256, 320) / lo [320, 384)
       mbar_wait(bar(O_FULL), ph);
@@ -529,9 +560,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       // The next pair's K-block 3 goes to A stage 3 = TMEM [384, 448), P lo's
       // columns: free once P·V has run (O_FULL, waited above). Its X tile was
       // loaded after S_FULL like the first ones.
-      if (t + npairs < p.pairs && nk > 3 && int((it + 3u) & 1u) == g && it % kNO == 0) {
-        convert(it + 3u, 3);
-        pre3 = true;
+      if constexpr (kConv == 2) {
+        if (t + npairs < p.pairs && nk > 3 && int((it + 3u) & 1u) == g && it % kNO == 0) {
+          convert(it + 3u, 3);
+          pre3 = true;
+        }
       }
       // The next pair's A stages 1-2 overlap C hi/lo [256, 384): convert only after
       // the Z MMA has read them. The Z accumulator is drained by warps 12-15.
@@ -540,13 +573,47 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 12) {
     // ------------------------------------------------------------ operand / Z warps (phase 2)
+    // (HS_HEAD_CONV3: also converter group 2 in phase 1)
     const int q = warp & 3;
     const uint32_t lane_base = tmem + (uint32_t(q * 32) << 16);
     const uint32_t stage = base + kEpi + uint32_t(q) * 8192u;
-    uint32_t lt = 0;
+    uint32_t lt = 0, it = 0;
+    const int row = q * 32 + lane;
+    (void)row;
     for (int t = pair0; t < p.pairs; t += npairs, ++lt) {
       const uint32_t ph = lt & 1u;
       const int inst = 2 * t + int(rank);
+      if constexpr (kConv == 3) {
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          if (it % 3u != 2u) continue;
+          const int s = int(it % kNS), o = int(it % kNO);
+          mbar_wait(bar(ST_FULL + s), (it / kNS) & 1u);
+          mbar_wait(bar(OP_EMPTY + o), ((it / kNO) & 1u) ^ 1u);
+          tc_fence_after();
+          const uint32_t sa = base + kU + uint32_t(s) * kStaging;
+          const uint32_t ta = lane_base + kTStage + uint32_t(o) * 64u;
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            uint32_t x[16], hi[16], lo[16];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              const float4 v = lds128(sa + sw128(row, 4 * hh + c));
+              x[4 * c] = __float_as_uint(v.x); x[4 * c + 1] = __float_as_uint(v.y);
+              x[4 * c + 2] = __float_as_uint(v.z); x[4 * c + 3] = __float_as_uint(v.w);
+            }
+            split_row16<kTerms>(x, hi, lo);
+            tmem_st16(ta + uint32_t(16 * hh), hi);
+            if constexpr (kTerms > 1) tmem_st16(ta + 32u + uint32_t(16 * hh), lo);
+          }
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            mbar_arrive(bar(ST_EMPTY + s));
+            mbar_arrive_cluster(leader(OP_FULL + o));
+          }
+        }
+      }
       mbar_wait(bar(ACC_FULL), ph);
       tc_fence_after();
       if (warp == 12 && lane == 0) TL(lt, 12);
