@@ -288,3 +288,18 @@ def test_ramp_chunks_match_full_batches(oracle_mod):
     ref = oracle_mod.run_dag(text, params, {k: (v[:2] if v.ndim == 2 else v) for k, v in arrays.items()}, 2)
     for i in range(2):
         assert _normwise(host[key][i], ref[key][i]) <= TOL
+
+
+def test_full_depth_c5_dag_matches_oracle(oracle_mod):
+    """The C5 DAG at full depth (12 layers, 828 kernels) through the default plan,
+    five instances in batches of two (a ragged last batch, three slots, ramp chunks
+    off since n < 4 batches), every instance within 1e-4 of the CPU oracle."""
+    text, params, meta = workloads.encoder(layers=12)
+    n = 5
+    arrays = _encoder_arrays(meta, params, n)
+    ref = oracle_mod.run_dag(text, params, arrays, n)
+    key = (meta["output"]["kernel"], meta["output"]["pos"])
+    outs, _, plan = _run_gpu(text, params, arrays, n, mode="graph", batch=2, slots=3)
+    assert plan["kernels"] == 828 and plan["launches_per_batch"] == 144
+    for i in range(n):
+        assert _normwise(outs[key][i], ref[key][i]) <= TOL, i
