@@ -1,3 +1,5 @@
+"""Host cost of one hs_launch call (GEMM, GEMM_NT, add) and of an event create/record/wait/
+destroy cycle, from Python through ctypes: the per-command cost behind dynamic-mode dispatch."""
 import ctypes, sys, time
 sys.path.insert(0, ".")
 import torch
