@@ -303,3 +303,29 @@ def test_full_depth_c5_dag_matches_oracle(oracle_mod):
     assert plan["kernels"] == 828 and plan["launches_per_batch"] == 144
     for i in range(n):
         assert _normwise(outs[key][i], ref[key][i]) <= TOL, i
+
+
+def test_single_term_tf32_plan(oracle_mod):
+    """math='tf32' (one MMA per product, ~1e-3): the same plan (whole-head kernels,
+    single-term pair GEMMs) runs and stays within its looser tolerance."""
+    text, params, meta = workloads.encoder(layers=2)
+    n = 3
+    arrays = _encoder_arrays(meta, params, n)
+    ref = oracle_mod.run_dag(text, params, arrays, n)
+    key = (meta["output"]["kernel"], meta["output"]["pos"])
+    outs, _, plan = _run_gpu(text, params, arrays, n, mode="graph", batch=2, math="tf32")
+    assert plan["chain_rewrites"].get("head_fused") == 16
+    for i in range(n):
+        assert _normwise(outs[key][i], ref[key][i]) <= 5e-3
+
+
+def test_peer_enable_same_gpu_is_a_noop():
+    import ctypes
+    from paper_2009_07482_b200 import _native
+    L = _native.lib()
+    a, b = ctypes.c_void_p(), ctypes.c_void_p()
+    _native.check(L.hs_ctx_create(0, ctypes.byref(a)))
+    _native.check(L.hs_ctx_create(0, ctypes.byref(b)))
+    _native.check(L.hs_ctx_enable_peer(a, b))
+    L.hs_ctx_destroy(a)
+    L.hs_ctx_destroy(b)
