@@ -189,6 +189,40 @@ def cpu_sample(layers, n_inst=1, reps=1):
     return n_inst / t, O.max_threads(), t
 
 
+def host_path_timing(layers, reps=5):
+    """The host half of the path on the C5 template (828 kernels, 1103 edges): parse_spec +
+    derive_components + classify_edges + bottom_level_ranks, timed single-threaded for
+    the reference's own compiled L0-L2 (oracle/_ref) and for this repo's C++ runtime
+    (hs_query), same JSON in, best of `reps`. The reference has no setup_cq /
+    scheduler; ours adds the full Alg. 1 clustering plan (setup_cq per dispatch)."""
+    from oracle import oracle as O
+    from paper_2009_07482_b200 import _native, workloads
+    text, params, _ = workloads.encoder(layers=layers)
+    times = {}
+    reqs = {"analyze": {"op": "analyze", "spec": text, "params": params},
+            "ranks": {"op": "ranks", "spec": text, "params": params,
+                      "times": {str(k): "1" for k in range(69 * layers)}}}
+    for name, req in reqs.items():
+        for who, fn in (("reference", O.ref_query if O.ref_available() else None), ("ours", _native.query)):
+            if fn is None:
+                continue
+            best = 1e9
+            for _ in range(reps):
+                t0 = time.perf_counter()
+                fn(req)
+                best = min(best, time.perf_counter() - t0)
+            times[f"{who}_{name}_ms"] = best * 1e3
+    best = 1e9
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        _native.query({"op": "schedule", "spec": text, "params": params, "policy": "clustering"})
+        best = min(best, time.perf_counter() - t0)
+    times["ours_schedule_ms"] = best * 1e3
+    times["note"] = ("single thread, JSON spec in; reference = /root/reference L0-L2 compiled unmodified "
+                     "(oracle/_ref); 'schedule' = Alg. 1 clustering with setup_cq for every component")
+    return times
+
+
 def run_reference(args, world, rank):
     if rank != 0:
         return
@@ -625,7 +659,8 @@ def run_ours(args, world, rank, local):
             v, threads, t = cpu_sample(args.layers, n_inst=12)
             cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
                    "sample": f"12 instances of the {args.layers}-layer DAG ({t:.1f} s; oracle port: clustering "
-                             f"scheduler + fp32 kernels on all host threads)"}
+                             f"scheduler + fp32 kernels on all host threads)",
+                   "host_path": host_path_timing(args.layers)}
         makespans = None if args.no_makespans else config_makespans()
         others = kernel_rooflines(args.batch, peak, pk["hbm_gbs"]) if args.math in ("tf32x3", "tf32") else None
         flop_per_inst = 782.2e6 * args.layers
