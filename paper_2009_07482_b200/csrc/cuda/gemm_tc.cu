@@ -63,6 +63,9 @@ using namespace tc;
 #ifndef HS_SPLIT_K  // split-K with red.global.add for latency-bound single-CTA launches
 #define HS_SPLIT_K 1
 #endif
+#ifndef HS_SPLIT_MIN_KB  // K-blocks per split at least
+#define HS_SPLIT_MIN_KB 1
+#endif
 #ifndef HS_DBG_EARLYREL
 #define HS_DBG_EARLYREL 0
 #endif
@@ -978,10 +981,10 @@ cudaError_t launch(const GemmArgs& a, cudaStream_t s) {
   // launches never split.
   const int nk = (a.K + BK - 1) / BK;
   int split = 1;
-  if (HS_SPLIT_K && a.batch == 1 && !a.relu && !a.softmax && p.n_out == 0 && !a.ldc && nk >= 8 &&
+  if (HS_SPLIT_K && a.batch == 1 && !a.relu && !a.softmax && p.n_out == 0 && !a.ldc && nk >= 2 * HS_SPLIT_MIN_KB &&
       4 * base <= slots) {
     split = slots / base;
-    if (split > nk / 4) split = nk / 4;
+    if (split > nk / HS_SPLIT_MIN_KB) split = nk / HS_SPLIT_MIN_KB;
     if (split > 16) split = 16;
     if (split < 2) split = 1;
   }
