@@ -615,8 +615,9 @@ void Engine::issue(Slot& sl, const TaskComponent& t, const CommandQueueStructure
         break;
       }
       case CmdKind::ndrange: {
-        auto lead = graph ? fuse_leader_.find({t.id, ev}) : fuse_leader_.end();
-        auto member = graph ? fuse_member_.find({t.id, ev}) : fuse_member_.end();
+        const bool fused = graph || dyn_fused_;
+        auto lead = fused ? fuse_leader_.find({t.id, ev}) : fuse_leader_.end();
+        auto member = fused ? fuse_member_.find({t.id, ev}) : fuse_member_.end();
         if (lead != fuse_leader_.end()) {
           // Grouped launch for every member: first make this stream wait for the
           // other members' inter-edge inputs (their dependent writes come later
@@ -1047,12 +1048,23 @@ void Engine::run_dynamic(Slot& sl, int64_t first, int64_t n) {
 void Engine::run(int64_t first, int64_t n, int64_t* elapsed_ns) {
   if (n < 1) fail(Errc::invalid_param, "n_instances must be >= 1");
   if (!planned_) {
-    if (cfg_.graph_mode) {
+    // Dynamic mode launches one kernel per ndrange, unless dynamic_fuse asks for the
+    // graph plan's launch lowering: the rewrites are per component and keyed by
+    // (component, event), and setup_cq numbers a component's events the same on
+    // every device when all devices have the same queue count.
+    bool uniform_queues = true;
+    for (const auto& d : platform_.devices) uniform_queues = uniform_queues && d.queues == platform_.devices[0].queues;
+    dyn_fused_ = !cfg_.graph_mode && cfg_.dynamic_fuse && uniform_queues && cfg_.math != HS_MATH_FP32_SIMT;
+    if (cfg_.graph_mode || dyn_fused_) {
       PlanExecutor pe;
       plan_ = sched_->run(pe);
       place_components();
     }
     plan_buffers();
+    if (dyn_fused_) {
+      if (cfg_.fuse >= 1) plan_fusion();
+      if (cfg_.fuse >= 2) plan_chain_rewrites();
+    }
     if (cfg_.graph_mode) {
       if (cfg_.fuse >= 1 && cfg_.math != HS_MATH_FP32_SIMT) plan_fusion();
       if (cfg_.fuse >= 2 && cfg_.math != HS_MATH_FP32_SIMT) plan_chain_rewrites();
@@ -1177,6 +1189,7 @@ std::string Engine::info(const std::string& what) const {
     out.set("peer_copies_per_batch", Value::of(static_cast<long long>(peer_in_.size())));
     out.set("captured", Value::of(static_cast<long long>(capture_ok_ && cfg_.graph_mode ? 1 : 0)));
     out.set("ramp_batch", Value::of(static_cast<long long>(ramp_)));
+    out.set("dynamic_fused", Value::of(static_cast<long long>(dyn_fused_ ? 1 : 0)));
     out.set("aliased_inputs", Value::of(static_cast<long long>(alias_.size())));
     out.set("grouped_launches", Value::of(static_cast<long long>(fuse_groups_.size())));
     Value rw = Value::make_object();
@@ -1289,6 +1302,7 @@ int hs_engine_create(const char* config_json, hs_engine_t* out) {
       for (const auto& [k, g] : v->object_items()) cfg.device_gpus[std::stoi(k)] = g.as_int();
     if (const json::Value* v = c.find("domain_per_device")) cfg.domain_per_device = v->as_int() != 0;
     if (const json::Value* v = c.find("ramp")) cfg.ramp = v->as_int() != 0;
+    if (const json::Value* v = c.find("dynamic_fuse")) cfg.dynamic_fuse = v->as_int() != 0;
     if (const json::Value* v = c.find("fuse")) {
       cfg.fuse = v->as_int();
       if (cfg.fuse < 0 || cfg.fuse > 3) fail(Errc::invalid_param, "fuse must be 0, 1, 2 or 3");

@@ -60,6 +60,9 @@ struct EngineConfig {
   // Graph mode with host-memory inputs/outputs: first and last chunks of a run
   // use a second graph of batch/4 instances (shorter exposed copies).
   bool ramp = true;
+  // Dynamic mode with the graph plan's launch lowering (grouped / fused launches per
+  // component); off by default: Alg. 1 as written launches one kernel per ndrange.
+  bool dynamic_fuse = false;
 };
 
 class Engine {
@@ -200,6 +203,7 @@ class Engine {
   std::map<std::pair<int, int>, std::pair<int, int>> peer_in_;  // input fed across domains -> producer
   bool capture_ok_ = true;           // one physical GPU: the plan is captured into graphs
   int64_t ramp_ = 0;                 // small-graph batch (0: no ramp)
+  bool dyn_fused_ = false;           // dynamic mode issues the fused launches
   int64_t cur_batch_ = 0;            // instances of the plan being emitted (0: cfg_.batch)
   int64_t nb() const { return cur_batch_ ? cur_batch_ : cfg_.batch; }
   std::vector<Slot> slots_;

@@ -30,7 +30,7 @@ class Engine:
     def __init__(self, spec_text: str, params: dict | None = None, *, gpu: int = 0, policy: str = "clustering",
                  mode: str = "graph", batch: int = 1, slots: int = 2, math: str = "tf32x3", cpu_devices=(),
                  fuse: int | bool = 3, trace: bool = False, device_gpus: dict | None = None,
-                 domain_per_device: bool = False):
+                 domain_per_device: bool = False, dynamic_fuse: bool = False):
         """fuse (graph mode): 0 = one launch per ndrange; 1 = + grouped sibling GEMMs;
         2 = + chain rewrites (transpose -> gemm_nt, softmax as a GEMM epilogue, concat
         inputs written in place, fused attention heads); 3 (default, also True) = + each
@@ -41,11 +41,14 @@ class Engine:
         device_gpus: {logical device id: GPU ordinal} places components on several GPUs
         (graph mode); an inter edge between GPUs becomes one peer copy over NVLink.
         domain_per_device: every logical device gets its own memory (test hook: the peer
-        path on one GPU)."""
+        path on one GPU).
+        dynamic_fuse: dynamic mode issues the graph plan's fused launches (per component)
+        instead of one kernel per ndrange."""
         fuse = 3 if fuse is True else int(fuse)
         cfg = {"spec": spec_text, "params": dict(params or {}), "gpu": gpu, "policy": policy, "mode": mode,
                "batch": batch, "slots": slots, "math": math, "cpu_devices": list(cpu_devices), "fuse": int(fuse),
-               "trace": int(bool(trace)), "domain_per_device": int(bool(domain_per_device))}
+               "trace": int(bool(trace)), "domain_per_device": int(bool(domain_per_device)),
+               "dynamic_fuse": int(bool(dynamic_fuse))}
         if device_gpus:
             cfg["device_gpus"] = {str(k): int(v) for k, v in device_gpus.items()}
         self._lib = lib()

@@ -329,3 +329,20 @@ def test_peer_enable_same_gpu_is_a_noop():
     _native.check(L.hs_ctx_enable_peer(a, b))
     L.hs_ctx_destroy(a)
     L.hs_ctx_destroy(b)
+
+
+@pytest.mark.parametrize("policy", ["clustering", "eager", "heft"])
+def test_dynamic_mode_with_fused_launches(policy, oracle_mod):
+    """dynamic_fuse: Alg. 1 with host callbacks, but each dispatched component issues
+    the graph plan's fused launches (whole heads, grouped / chained GEMMs). Same
+    kernels as graph mode, so the outputs are bit-identical to it."""
+    text, params, meta = workloads.encoder(layers=2, devices=3)
+    n = 3
+    arrays = _encoder_arrays(meta, params, n)
+    key = (meta["output"]["kernel"], meta["output"]["pos"])
+    graph, _, _ = _run_gpu(text, params, arrays, n, mode="graph", batch=3)
+    dyn, info, plan = _run_gpu(text, params, arrays, n, mode="dynamic", batch=3, policy=policy, dynamic_fuse=True)
+    assert plan["dynamic_fused"] == 1 and plan["chain_rewrites"].get("head_fused") == 16
+    assert np.array_equal(dyn[key], graph[key])
+    ref = oracle_mod.run_dag(text, params, arrays, 1)
+    assert _normwise(dyn[key][0], ref[key][0]) <= TOL
