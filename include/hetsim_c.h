@@ -193,7 +193,8 @@ typedef struct hs_engine* hs_engine_t;
  * 1 + grouped sibling GEMMs, 2 + chain rewrites, 3 (default) + whole-head launches.
  * Optional: "device_gpus": {"<logical device>": ordinal} (components across GPUs),
  * "domain_per_device": 0|1, "ramp": 1|0 (batch/4 first and last chunks when the
- * bindings are host memory). */
+ * bindings are host memory), "dynamic_fuse": 0|1 (dynamic mode issues the graph
+ * plan's fused launches instead of one kernel per ndrange). */
 int hs_engine_create(const char* config_json, hs_engine_t* out);
 int hs_engine_destroy(hs_engine_t e);
 
