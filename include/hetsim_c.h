@@ -144,10 +144,16 @@ typedef struct {
    *         softmax node that consumes it. */
   int64_t out_ld;
   int epilogue;
+  /* HS_FLAG_* bits (0 = defaults). */
+  int flags;
 } hs_op_args;
 
 #define HS_EPI_NONE 0
 #define HS_EPI_SOFTMAX 1
+/* No split-K: single-instance GEMMs otherwise add K-split partial sums with
+ * red.global.add (fast for latency-bound launches, but the fp32 addition order
+ * then varies from run to run). With this flag every launch is bit-reproducible. */
+#define HS_FLAG_DETERMINISTIC 1
 /* HS_OP_ATTN_HEAD ("attn_head"): in = {Q, K, V, W}, Q/K/V [S, dk] per instance,
  * W [dk, dw] shared and pre-split (aux, hs_gemm_split_weights_ex format 0);
  * dims = {S, dk, dw} with S <= 128, dk = dw = 64; fparam[0] = softmax scale;
@@ -194,18 +200,25 @@ typedef struct hs_engine* hs_engine_t;
  * Optional: "device_gpus": {"<logical device>": ordinal} (components across GPUs),
  * "domain_per_device": 0|1, "ramp": 1|0 (batch/4 first and last chunks when the
  * bindings are host memory), "dynamic_fuse": 0|1 (dynamic mode issues the graph
- * plan's fused launches instead of one kernel per ndrange). */
+ * plan's fused launches instead of one kernel per ndrange; InvalidParam when it
+ * cannot apply: devices with different queue counts, or simt math),
+ * "deterministic": 0|1 (HS_FLAG_DETERMINISTIC on every launch),
+ * "liveness": 1|0 (intermediate buffers share one arena per slot wherever the
+ * DAG orders all their accesses; 0 = one allocation per output buffer). */
 int hs_engine_create(const char* config_json, hs_engine_t* out);
 int hs_engine_destroy(hs_engine_t e);
 
 /* Bind the isolated input (or isolated output) buffer (kernel, pos) to memory
- * holding `count` instances laid out `stride_bytes` apart (0 = one copy shared
- * by every instance; such inputs are uploaded once and stay resident).
- * on_device != 0 means `ptr` is device memory on the engine's GPU. */
-int hs_engine_bind(hs_engine_t e, int kernel, int pos, void* ptr, int64_t stride_bytes, int on_device);
+ * holding `count` instances laid out `stride_bytes` apart (stride 0 = one copy
+ * shared by every instance; such inputs are uploaded once and stay resident, and
+ * `count` is ignored). on_device != 0 means `ptr` is device memory on the
+ * engine's GPU. */
+int hs_engine_bind(hs_engine_t e, int kernel, int pos, void* ptr, int64_t stride_bytes, int64_t count,
+                   int on_device);
 
 /* Execute `n_instances` DAG instances (instances [first, first+n) of the
- * bound arrays). Blocks until done. elapsed_ns (optional) = device time
+ * bound arrays; InvalidParam unless 0 <= first and first + n <= count of every
+ * per-instance binding). Blocks until done. elapsed_ns (optional) = device time
  * from the first to the last command, measured with CUDA events. */
 int hs_engine_run(hs_engine_t e, int64_t first, int64_t n_instances, int64_t* elapsed_ns);
 

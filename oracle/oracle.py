@@ -534,6 +534,67 @@ def run_dag(spec_text: str, params: dict, inputs: dict, n: int, keep=False):
     return {key: v for key, v in bufs.items() if key not in feeding}
 
 
+def _node_f64(name, ins, vals, n):
+    """One node in float64 for n instances; ins: [n, elems] or shared [elems] float64."""
+    def rows(a, r, c):
+        return np.broadcast_to(a, (n, a.shape[-1])).reshape(n, r, c)
+    if name in ("gemm", "gemm_nt", "gemm_relu"):
+        M, N, K = vals[:3]
+        A = rows(ins[0], M, K)
+        B = rows(ins[1], N, K).transpose(0, 2, 1) if name == "gemm_nt" else rows(ins[1], K, N)
+        C = A @ B
+        if name == "gemm_relu":
+            C = np.maximum(C, 0.0)
+        return C.reshape(n, -1)
+    if name == "transpose":
+        return rows(ins[0], vals[0], vals[1]).transpose(0, 2, 1).reshape(n, -1)
+    if name == "scale":
+        return np.broadcast_to(ins[0], (n, ins[0].shape[-1])) * (vals[1] / vals[2])
+    if name == "softmax":
+        s = vals[2] / vals[3] if len(vals) >= 4 else 1.0
+        x = rows(ins[0], vals[0], vals[1]) * s
+        e = np.exp(x - x.max(axis=2, keepdims=True))
+        return (e / e.sum(axis=2, keepdims=True)).reshape(n, -1)
+    if name == "add":
+        return np.broadcast_to(ins[0], (n, ins[0].shape[-1])) + ins[1]
+    if name == "add_layernorm":
+        R, C = vals[:2]
+        v = rows(ins[0], R, C) + rows(ins[1], R, C)
+        mu = v.mean(axis=2, keepdims=True)
+        var = ((v - mu) ** 2).mean(axis=2, keepdims=True)
+        return ((v - mu) / np.sqrt(var + 1e-5) * ins[2].reshape(-1)[:C] + ins[3].reshape(-1)[:C]).reshape(n, -1)
+    if name == "concat":
+        R, c = vals[:2]
+        return np.concatenate([rows(z, R, c) for z in ins], axis=2).reshape(n, -1)
+    if name == "attn_head":
+        S, dk, dw = vals[:3]
+        sm = [S, S] + (list(vals[3:5]) if len(vals) >= 5 else [])
+        P = _node_f64("softmax", [_node_f64("gemm_nt", ins[:2], [S, S, dk], n)], sm, n)
+        Cm = _node_f64("gemm", [P, ins[2]], [S, dk, S], n)
+        return _node_f64("gemm", [Cm, ins[3]], [S, dw, dk], n)
+    raise ValueError(name)
+
+
+def run_dag_f64(spec_text: str, params: dict, inputs: dict, n: int):
+    """The same DAG executed entirely in float64 (numpy, exact scale factors): the
+    "truth" against which both the fp32 oracle and the GPU are measured, to report
+    error headroom (fp64-accumulate variant). Returns isolated outputs."""
+    spec = Spec(spec_text, params)
+    producer = {(d, dp): (s, sp) for s, sp, d, dp in spec.edges}
+    feeding = {(s, sp) for s, sp, _, _ in spec.edges}
+    bufs = {}
+    for k in spec.topo_order():
+        kd = spec.kernels[k]
+        ins = []
+        for b in spec.buffers(k, "in"):
+            key = (k, b["pos"])
+            ins.append(bufs[producer[key]] if key in producer else np.asarray(inputs[key], dtype=np.float64))
+        ob = spec.buffers(k, "out")[0]
+        vals = [eval_expr(str(v["value"]), params) for v in sorted(kd.get("varArguments", []), key=lambda v: v["pos"])]
+        bufs[(k, ob["pos"])] = np.ascontiguousarray(_node_f64(kd["name"], ins, vals, n))
+    return {key: v for key, v in bufs.items() if key not in feeding}
+
+
 def max_threads() -> int:
     return int(olib().or_max_threads())
 

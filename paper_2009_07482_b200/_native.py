@@ -48,10 +48,12 @@ class OpArgs(ctypes.Structure):
         ("out_strides", c_int64 * 4),
         ("out_ld", c_int64),
         ("epilogue", c_int),
+        ("flags", c_int),
     ]
 
 
 EPI_NONE, EPI_SOFTMAX = 0, 1
+FLAG_DETERMINISTIC = 1
 
 
 _PROTOS = {
@@ -99,7 +101,7 @@ _PROTOS = {
     "hs_gemm_split_weights_ex": (c_int, [c_void_p, c_void_p, c_int, c_int64, c_int64, c_void_p, c_int64, c_int]),
     "hs_engine_create": (c_int, [c_char_p, ctypes.POINTER(c_void_p)]),
     "hs_engine_destroy": (c_int, [c_void_p]),
-    "hs_engine_bind": (c_int, [c_void_p, c_int, c_int, c_void_p, c_int64, c_int]),
+    "hs_engine_bind": (c_int, [c_void_p, c_int, c_int, c_void_p, c_int64, c_int64, c_int]),
     "hs_engine_run": (c_int, [c_void_p, c_int64, c_int64, ctypes.POINTER(c_int64)]),
     "hs_engine_info": (c_int, [c_void_p, c_char_p, ctypes.POINTER(c_void_p)]),
 }

@@ -981,7 +981,7 @@ cudaError_t launch(const GemmArgs& a, cudaStream_t s) {
   // launches never split.
   const int nk = (a.K + BK - 1) / BK;
   int split = 1;
-  if (HS_SPLIT_K && a.batch == 1 && !a.relu && !a.softmax && p.n_out == 0 && !a.ldc && nk >= 2 * HS_SPLIT_MIN_KB &&
+  if (HS_SPLIT_K && !a.deterministic && a.batch == 1 && !a.relu && !a.softmax && p.n_out == 0 && !a.ldc && nk >= 2 * HS_SPLIT_MIN_KB &&
       4 * base <= slots) {
     split = slots / base;
     if (split > nk / HS_SPLIT_MIN_KB) split = nk / HS_SPLIT_MIN_KB;

@@ -272,6 +272,7 @@ int hs_launch(hs_stream_t st, int op, const hs_op_args* a, int math, int batch) 
       if (a->out_ld < 0 || (a->out_ld > 0 && a->out_ld < a->dims[1])) return invalid("gemm out_ld < N");
       if (a->epilogue != HS_EPI_NONE && a->epilogue != HS_EPI_SOFTMAX) return invalid("unknown GEMM epilogue");
       g.ldc = a->out_ld;
+      g.deterministic = (a->flags & HS_FLAG_DETERMINISTIC) != 0;
       if (a->epilogue == HS_EPI_SOFTMAX) {
         if (math == HS_MATH_FP32_SIMT || op == HS_OP_GEMM_RELU || a->n_out > 1 || a->dims[1] > 128)
           return invalid("softmax epilogue needs tcgen05 math, a plain GEMM and N <= 128");

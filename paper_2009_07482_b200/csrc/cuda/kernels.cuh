@@ -36,6 +36,8 @@ struct GemmArgs {
   // 1 = row softmax of (A·B)·escale over the N columns (N <= 128, one tile row).
   int softmax = 0;
   float escale = 1.f;
+  // no split-K (HS_FLAG_DETERMINISTIC): bit-reproducible single-instance launches
+  bool deterministic = false;
 };
 
 // planes: hi at planes[n*K + k], lo at planes[plane_stride + n*K + k]

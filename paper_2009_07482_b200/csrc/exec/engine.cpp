@@ -260,13 +260,14 @@ void Engine::build_nodes() {
   }
 }
 
-void Engine::bind(int kernel, int pos, void* ptr, int64_t stride_bytes, bool on_device) {
+void Engine::bind(int kernel, int pos, void* ptr, int64_t stride_bytes, int64_t count, bool on_device) {
   if (planned_) fail(Errc::invalid_param, "bindings are frozen after the first run");
   const BufferSpec* b = g_.kernel(kernel).buffer_at(pos);
   if (!b) fail(Errc::invalid_param, "kernel " + std::to_string(kernel) + " has no buffer at position " + std::to_string(pos));
   if (!ptr) fail(Errc::invalid_param, "null binding");
   if (stride_bytes < 0) fail(Errc::invalid_param, "negative stride");
-  bindings_[{kernel, pos}] = Binding{ptr, stride_bytes, on_device};
+  if (stride_bytes > 0 && count < 1) fail(Errc::invalid_param, "a per-instance binding needs count >= 1");
+  bindings_[{kernel, pos}] = Binding{ptr, stride_bytes, stride_bytes > 0 ? count : 0, on_device};
 }
 
 void Engine::plan_buffers() {
@@ -356,11 +357,155 @@ void Engine::plan_buffers() {
       node_planes_[kid] = it->second.ptr;
     }
   }
+  launches_per_batch_ = int64_t(g_.kernels.size());
+}
+
+// Which launch of the plan touches which buffer, after the launch rewrites.
+// Returns, for every output-side buffer (kernel,pos), the kernels whose
+// launches (or dependent-write copies) read or write it. An accessor stands for
+// the position of that kernel's ndrange in the plan; a grouped launch counts as
+// every member (it starts after all members' inputs are ready, and every
+// member's event completes after it). Buffers no launch touches (outputs of
+// elided nodes, absorbed intermediates) get no entry.
+std::map<std::pair<int, int>, std::set<int>> Engine::buffer_accessors() const {
+  std::map<std::pair<int, int>, std::set<int>> acc;
+  auto phys = [&](std::pair<int, int> key) {
+    auto al = alias_.find(key);
+    return al == alias_.end() ? key : al->second;
+  };
+  const bool fused = cfg_.graph_mode || dyn_fused_;
+  std::set<int> grouped_members;
+  if (fused)
+    for (const auto& fg : fuse_groups_) {
+      grouped_members.insert(fg.kernels.begin(), fg.kernels.end());
+      if (fg.absorbed) continue;
+      const Node& lead = nodes_.at(fg.kernels[0]);
+      for (int m : fg.kernels) {
+        acc[phys(lead.inputs[0])].insert(fg.kernels.begin(), fg.kernels.end());
+        acc[nodes_.at(m).output].insert(fg.kernels.begin(), fg.kernels.end());
+      }
+    }
+  for (const auto& [kid, nd] : nodes_) {
+    if (grouped_members.count(kid) || nd.elided) continue;
+    for (const auto& in : nd.inputs) {
+      acc[phys(in)].insert(kid);
+      auto io = io_copy_.find(in);
+      if (io != io_copy_.end()) acc[io->second].insert(kid);
+    }
+    acc[nd.output].insert(kid);
+  }
+  // dependent-write copies (io inputs, peer copies) run on the consumer's queue
+  for (const auto& [key, src] : io_copy_) {
+    acc[key].insert(key.first);
+    acc[src].insert(key.first);
+  }
+  for (const auto& [key, src] : peer_in_) acc[src].insert(key.first);
+  return acc;
+}
+
+// Per-slot device memory with buffer liveness (graph and dynamic mode alike).
+// Fixed allocations: per-instance input groups (written by copy-in before the
+// plan), bound isolated outputs (read by copy-out after it), io buffers and
+// peer-copy targets. Every other output buffer lives in one arena per (slot,
+// memory domain), at an offset chosen first-fit in plan order: two buffers may
+// share bytes only when every launch touching one is a proper DAG ancestor of
+// every launch touching the other. DAG edges are exactly what the plan
+// enforces (same-queue order, E_Q events, inter-edge events), so the earlier
+// buffer's last access completes before the later buffer's first write, in any
+// interleaving of the streams.
+void Engine::place_slot_buffers() {
   const int64_t B = cfg_.batch;
+  const auto acc = buffer_accessors();
+  // proper-ancestor bitsets over kernel indices
+  const size_t K = g_.kernels.size(), W = (K + 63) / 64;
+  std::vector<std::vector<uint64_t>> anc(K, std::vector<uint64_t>(W, 0));
+  std::map<int, int> topo_pos;
+  {
+    const auto order = g_.topo_order();
+    for (size_t i = 0; i < order.size(); ++i) topo_pos[order[i]] = int(i);
+    const auto preds = g_.kernel_predecessors();
+    for (int v : order) {
+      auto& av = anc[size_t(g_.index_of(v))];
+      auto pit = preds.find(v);
+      if (pit == preds.end()) continue;
+      for (int u : pit->second) {
+        const size_t ui = size_t(g_.index_of(u));
+        av[ui / 64] |= uint64_t(1) << (ui % 64);
+        for (size_t w = 0; w < W; ++w) av[w] |= anc[ui][w];
+      }
+    }
+  }
+  auto before = [&](const std::set<int>& a, const std::set<int>& b) {  // every a strictly precedes every b
+    for (int y : b) {
+      const auto& ay = anc[size_t(g_.index_of(y))];
+      for (int x : a) {
+        const size_t xi = size_t(g_.index_of(x));
+        if (!(ay[xi / 64] >> (xi % 64) & 1)) return false;
+      }
+    }
+    return true;
+  };
+  std::set<std::pair<int, int>> fixed(outputs_.begin(), outputs_.end());
+  for (const auto& k : g_.kernels)
+    for (const auto* b : k.output_side())
+      if (b->kind == BufferKind::io) fixed.insert({k.id, b->pos});
+  for (const auto& [key, gi] : group_of_) fixed.insert(key);
+  for (const auto& [key, src] : peer_in_) fixed.insert(key);
+  struct Placed {
+    std::pair<int, int> key;
+    const std::set<int>* acc;
+    int64_t off, size;  // per-instance units
+    int dom;
+  };
+  std::vector<Placed> pooled;
+  for (const auto& k : g_.kernels)
+    for (const auto* b : k.output_side()) {
+      const std::pair<int, int> key{k.id, b->pos};
+      auto it = acc.find(key);
+      if (!cfg_.liveness) fixed.insert(key);  // one allocation per output buffer
+      if (fixed.count(key) || it == acc.end()) continue;
+      pooled.push_back({key, &it->second, 0, (bytes_.at(key) + 127) / 128 * 128, kdom(k.id)});
+    }
+  auto first_pos = [&](const Placed& p) {
+    int m = 1 << 30;
+    for (int x : *p.acc) m = std::min(m, topo_pos.at(x));
+    return m;
+  };
+  std::stable_sort(pooled.begin(), pooled.end(),
+                   [&](const Placed& a, const Placed& b) { return first_pos(a) < first_pos(b); });
+  std::map<int, int64_t> arena;  // domain -> per-instance units
+  for (size_t i = 0; i < pooled.size(); ++i) {
+    Placed& p = pooled[i];
+    std::vector<std::pair<int64_t, int64_t>> busy;
+    for (size_t j = 0; j < i; ++j) {
+      const Placed& q = pooled[j];
+      if (q.dom == p.dom && !before(*q.acc, *p.acc) && !before(*p.acc, *q.acc)) busy.push_back({q.off, q.off + q.size});
+    }
+    std::sort(busy.begin(), busy.end());
+    int64_t off = 0;
+    for (auto [lo, hi] : busy) {
+      if (off + p.size <= lo) break;
+      off = std::max(off, hi);
+    }
+    p.off = off;
+    arena[p.dom] = std::max(arena[p.dom], off + p.size);
+  }
+  int64_t unpooled = 0;
+  for (const auto& k : g_.kernels)
+    for (const auto* b : k.output_side()) unpooled += bytes_.at({k.id, b->pos});
+  pooled_bytes_per_instance_ = 0;
+  for (const auto& [d, units] : arena) pooled_bytes_per_instance_ += units;
+  unpooled_bytes_per_instance_ = unpooled;
   slots_.resize(size_t(cfg_.slots));
   for (auto& sl : slots_) {
+    std::map<int, char*> base;
+    for (const auto& [d, units] : arena) base[d] = static_cast<char*>(dalloc(d, units * B));
+    for (const auto& p : pooled) sl.buf[p.key] = base.at(p.dom) + p.off * B;
     for (const auto& k : g_.kernels)
-      for (const auto* b : k.output_side()) sl.buf[{k.id, b->pos}] = dalloc(kdom(k.id), bytes_.at({k.id, b->pos}) * B);
+      for (const auto* b : k.output_side()) {
+        const std::pair<int, int> key{k.id, b->pos};
+        if (fixed.count(key)) sl.buf[key] = dalloc(kdom(k.id), bytes_.at(key) * B);
+      }
     for (const auto& [key, gi] : group_of_) {
       const Group& gr = groups_[size_t(gi)];
       const int dom = kdom(key.first);
@@ -372,7 +517,10 @@ void Engine::plan_buffers() {
       else if (!sl.group_buf.count({gi, dom})) sl.group_buf[{gi, dom}] = dalloc(dom, gr.bytes * B);
       sl.buf[key] = sl.group_buf.at({gi, dom});
     }
-    for (const auto& [key, src] : alias_) sl.buf[key] = sl.buf.at(src);
+    for (const auto& [key, src] : alias_) {
+      auto it = sl.buf.find(src);
+      if (it != sl.buf.end()) sl.buf[key] = it->second;  // (no entry: read by no launch)
+    }
     for (const auto& [key, src] : peer_in_)
       if (!sl.buf.count(key)) sl.buf[key] = dalloc(kdom(key.first), bytes_.at(key) * B);  // io inputs reuse their output
     hs_ok(hs_stream_create(ctx_, 0, &sl.origin), "hs_stream_create");
@@ -384,7 +532,6 @@ void Engine::plan_buffers() {
       for (size_t d = 1; d < dctx_.size(); ++d) dstream(sl, int(d));
     }
   }
-  launches_per_batch_ = int64_t(g_.kernels.size());
 }
 
 void Engine::upload_resident() {
@@ -530,6 +677,7 @@ void Engine::launch_node(Slot& sl, hs_stream_t s, int kernel) {
     a.in_stride[1] = 0;
     a.aux = head_qkv_planes_.at(kernel);
   }
+  a.flags = cfg_.deterministic ? HS_FLAG_DETERMINISTIC : 0;
   hs_ok(hs_launch(s, nd.op, &a, cfg_.math, int(nb())), "hs_launch");
 }
 
@@ -639,7 +787,11 @@ void Engine::issue(Slot& sl, const TaskComponent& t, const CommandQueueStructure
           hs_op_args a{};
           a.n_in = 2;
           a.in[0] = sl.buf.at(nd.inputs[0]);
-          a.in_stride[0] = bytes_.at(nd.inputs[0]) / 4;
+          {  // a resident A (one shared copy) is read by every instance: stride 0
+            auto agi = group_of_.find(nd.inputs[0]);
+            const bool shared = agi != group_of_.end() && groups_[size_t(agi->second)].resident;
+            a.in_stride[0] = shared ? 0 : bytes_.at(nd.inputs[0]) / 4;
+          }
           a.in[1] = sl.buf.at(nd.inputs[1]);
           a.in_stride[1] = 0;
           a.out = sl.buf.at(nd.output);
@@ -652,6 +804,7 @@ void Engine::issue(Slot& sl, const TaskComponent& t, const CommandQueueStructure
             a.outs[m] = sl.buf.at(okey);
             a.out_strides[m] = bytes_.at(okey) / 4;
           }
+          a.flags = cfg_.deterministic ? HS_FLAG_DETERMINISTIC : 0;
           hs_ok(hs_launch(s, nd.op, &a, cfg_.math, int(nb())), "hs_launch (grouped)");
           record = true;
         } else if (member != fuse_member_.end()) {
@@ -765,6 +918,9 @@ void Engine::plan_chain_rewrites() {
     if (it == consumers.end() || it->second.size() != 1) return false;
     const DagEdge& e = g_.edges[size_t(it->second.front())];
     if (io_copy_.count({e.dst_kernel, e.dst_pos})) return false;  // io inputs are copies, not aliases
+    // an edge between memory domains is a peer copy: no rewrite may let one side
+    // address the other side's buffer directly
+    if (peer_in_.count({e.dst_kernel, e.dst_pos}) || kdom(e.src_kernel) != kdom(e.dst_kernel)) return false;
     *dst_kernel = e.dst_kernel;
     *dst_pos = e.dst_pos;
     return true;
@@ -1047,6 +1203,12 @@ void Engine::run_dynamic(Slot& sl, int64_t first, int64_t n) {
 
 void Engine::run(int64_t first, int64_t n, int64_t* elapsed_ns) {
   if (n < 1) fail(Errc::invalid_param, "n_instances must be >= 1");
+  if (first < 0) fail(Errc::invalid_param, "first must be >= 0");
+  for (const auto& [key, b] : bindings_)
+    if (b.stride > 0 && first + n > b.count)
+      fail(Errc::invalid_param, "instances [" + std::to_string(first) + ", " + std::to_string(first + n) +
+                                    ") exceed the " + std::to_string(b.count) + " bound at (" +
+                                    std::to_string(key.first) + "," + std::to_string(key.second) + ")");
   if (!planned_) {
     // Dynamic mode launches one kernel per ndrange, unless dynamic_fuse asks for the
     // graph plan's launch lowering: the rewrites are per component and keyed by
@@ -1054,7 +1216,10 @@ void Engine::run(int64_t first, int64_t n, int64_t* elapsed_ns) {
     // every device when all devices have the same queue count.
     bool uniform_queues = true;
     for (const auto& d : platform_.devices) uniform_queues = uniform_queues && d.queues == platform_.devices[0].queues;
-    dyn_fused_ = !cfg_.graph_mode && cfg_.dynamic_fuse && uniform_queues && cfg_.math != HS_MATH_FP32_SIMT;
+    if (!cfg_.graph_mode && cfg_.dynamic_fuse && (!uniform_queues || cfg_.math == HS_MATH_FP32_SIMT))
+      fail(Errc::invalid_param, uniform_queues ? "dynamic_fuse needs tcgen05 math (not simt)"
+                                               : "dynamic_fuse needs the same queue count on every device");
+    dyn_fused_ = !cfg_.graph_mode && cfg_.dynamic_fuse;
     if (cfg_.graph_mode || dyn_fused_) {
       PlanExecutor pe;
       plan_ = sched_->run(pe);
@@ -1068,6 +1233,9 @@ void Engine::run(int64_t first, int64_t n, int64_t* elapsed_ns) {
     if (cfg_.graph_mode) {
       if (cfg_.fuse >= 1 && cfg_.math != HS_MATH_FP32_SIMT) plan_fusion();
       if (cfg_.fuse >= 2 && cfg_.math != HS_MATH_FP32_SIMT) plan_chain_rewrites();
+    }
+    place_slot_buffers();
+    if (cfg_.graph_mode) {
       // Ramp (host-fed streams): the first and last chunks of a run are ramp_ =
       // batch/4 instances, so the copy-in before the first graph and the copy-out
       // after the last one are short; the copies of every other chunk overlap
@@ -1173,11 +1341,20 @@ std::string Engine::info(const std::string& what) const {
     out.set("kernels", Value::of(static_cast<long long>(g_.kernels.size())));
     out.set("edges", Value::of(static_cast<long long>(g_.edges.size())));
     out.set("components", Value::of(static_cast<long long>(sched_->components().size())));
-    out.set("dispatches", pairs(plan_.dispatches, &DispatchRecord::component, &DispatchRecord::device));
+    // graph mode: the captured plan; dynamic mode: what Alg. 1 dispatched in the
+    // last batch of the last run (timing-dependent for eager / HEFT)
+    const bool dyn = !cfg_.graph_mode;
+    out.set("dispatches", pairs(dyn ? last_dispatches_ : plan_.dispatches, &DispatchRecord::component,
+                                &DispatchRecord::device));
+    out.set("dispatches_source", Value::of(std::string(dyn ? "last dynamic run" : "captured plan")));
     long long streams = 0;
     for (const auto& sl : slots_) streams += static_cast<long long>(sl.streams.size());
     out.set("streams", Value::of(streams));
     out.set("device_bytes", Value::of(static_cast<long long>(device_bytes_)));
+    // liveness planner: bytes per instance per slot of the pooled (arena) buffers,
+    // against one allocation per output buffer
+    out.set("arena_bytes_per_instance", Value::of(static_cast<long long>(pooled_bytes_per_instance_)));
+    out.set("all_outputs_bytes_per_instance", Value::of(static_cast<long long>(unpooled_bytes_per_instance_)));
     long long resident_groups = 0;
     for (const auto& gr : groups_) resident_groups += gr.resident ? 1 : 0;
     out.set("resident_groups", Value::of(resident_groups));
@@ -1303,6 +1480,8 @@ int hs_engine_create(const char* config_json, hs_engine_t* out) {
     if (const json::Value* v = c.find("domain_per_device")) cfg.domain_per_device = v->as_int() != 0;
     if (const json::Value* v = c.find("ramp")) cfg.ramp = v->as_int() != 0;
     if (const json::Value* v = c.find("dynamic_fuse")) cfg.dynamic_fuse = v->as_int() != 0;
+    if (const json::Value* v = c.find("deterministic")) cfg.deterministic = v->as_int() != 0;
+    if (const json::Value* v = c.find("liveness")) cfg.liveness = v->as_int() != 0;
     if (const json::Value* v = c.find("fuse")) {
       cfg.fuse = v->as_int();
       if (cfg.fuse < 0 || cfg.fuse > 3) fail(Errc::invalid_param, "fuse must be 0, 1, 2 or 3");
@@ -1315,10 +1494,11 @@ int hs_engine_destroy(hs_engine_t e) {
   return guarded([&] { delete reinterpret_cast<hetsim::Engine*>(e); });
 }
 
-int hs_engine_bind(hs_engine_t e, int kernel, int pos, void* ptr, int64_t stride_bytes, int on_device) {
+int hs_engine_bind(hs_engine_t e, int kernel, int pos, void* ptr, int64_t stride_bytes, int64_t count,
+                   int on_device) {
   return guarded([&] {
     if (!e) hetsim::fail(hetsim::Errc::invalid_param, "null engine");
-    reinterpret_cast<hetsim::Engine*>(e)->bind(kernel, pos, ptr, stride_bytes, on_device != 0);
+    reinterpret_cast<hetsim::Engine*>(e)->bind(kernel, pos, ptr, stride_bytes, count, on_device != 0);
   });
 }
 

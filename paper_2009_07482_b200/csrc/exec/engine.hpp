@@ -63,6 +63,12 @@ struct EngineConfig {
   // Dynamic mode with the graph plan's launch lowering (grouped / fused launches per
   // component); off by default: Alg. 1 as written launches one kernel per ndrange.
   bool dynamic_fuse = false;
+  // HS_FLAG_DETERMINISTIC on every node launch (no split-K: bit-reproducible
+  // single-instance GEMMs).
+  bool deterministic = false;
+  // Buffer-liveness planner: intermediates share one arena per slot when the DAG
+  // orders all their accesses (false: one allocation per output buffer).
+  bool liveness = true;
 };
 
 class Engine {
@@ -72,7 +78,8 @@ class Engine {
   Engine(const Engine&) = delete;
   Engine& operator=(const Engine&) = delete;
 
-  void bind(int kernel, int pos, void* ptr, int64_t stride_bytes, bool on_device);
+  // count = instances the memory holds (ignored when stride_bytes == 0)
+  void bind(int kernel, int pos, void* ptr, int64_t stride_bytes, int64_t count, bool on_device);
   void run(int64_t first, int64_t n, int64_t* elapsed_ns);
   std::string info(const std::string& what) const;
 
@@ -97,6 +104,7 @@ class Engine {
   struct Binding {
     void* ptr = nullptr;
     int64_t stride = 0;  // bytes between instances; 0 = shared
+    int64_t count = 0;   // instances held (per-instance bindings)
     bool on_device = false;
   };
   struct Group {  // one device allocation fed by one isolated binding (deduplicated)
@@ -125,6 +133,9 @@ class Engine {
 
   void build_nodes();
   void plan_buffers();
+  std::map<std::pair<int, int>, std::set<int>> buffer_accessors() const;
+  void place_slot_buffers();
+  int64_t pooled_bytes_per_instance_ = 0, unpooled_bytes_per_instance_ = 0;
   void upload_resident();
   void capture(Slot& sl);
   void emit_plan(Slot& sl);

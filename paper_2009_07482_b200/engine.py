@@ -30,7 +30,8 @@ class Engine:
     def __init__(self, spec_text: str, params: dict | None = None, *, gpu: int = 0, policy: str = "clustering",
                  mode: str = "graph", batch: int = 1, slots: int = 2, math: str = "tf32x3", cpu_devices=(),
                  fuse: int | bool = 3, trace: bool = False, device_gpus: dict | None = None,
-                 domain_per_device: bool = False, dynamic_fuse: bool = False):
+                 domain_per_device: bool = False, dynamic_fuse: bool = False, deterministic: bool = False,
+                 liveness: bool = True):
         """fuse (graph mode): 0 = one launch per ndrange; 1 = + grouped sibling GEMMs;
         2 = + chain rewrites (transpose -> gemm_nt, softmax as a GEMM epilogue, concat
         inputs written in place, fused attention heads); 3 (default, also True) = + each
@@ -43,12 +44,17 @@ class Engine:
         domain_per_device: every logical device gets its own memory (test hook: the peer
         path on one GPU).
         dynamic_fuse: dynamic mode issues the graph plan's fused launches (per component)
-        instead of one kernel per ndrange."""
+        instead of one kernel per ndrange.
+        deterministic: no split-K in single-instance GEMMs, so every output is
+        bit-reproducible from run to run (split-K adds K-split partials atomically).
+        liveness: intermediate buffers share one arena per slot wherever the DAG orders
+        all their accesses (False: one device allocation per output buffer)."""
         fuse = 3 if fuse is True else int(fuse)
         cfg = {"spec": spec_text, "params": dict(params or {}), "gpu": gpu, "policy": policy, "mode": mode,
                "batch": batch, "slots": slots, "math": math, "cpu_devices": list(cpu_devices), "fuse": int(fuse),
                "trace": int(bool(trace)), "domain_per_device": int(bool(domain_per_device)),
-               "dynamic_fuse": int(bool(dynamic_fuse))}
+               "dynamic_fuse": int(bool(dynamic_fuse)), "deterministic": int(bool(deterministic)),
+               "liveness": int(bool(liveness))}
         if device_gpus:
             cfg["device_gpus"] = {str(k): int(v) for k, v in device_gpus.items()}
         self._lib = lib()
@@ -67,7 +73,9 @@ class Engine:
             else:
                 shape = tuple(arr.shape)
                 stride_bytes = nbytes // shape[0] if shape and shape[0] else nbytes
-        check(self._lib.hs_engine_bind(self._h, kernel, pos, ctypes.c_void_p(ptr), stride_bytes, int(on_dev)),
+        # instances the array holds: run() rejects [first, first+n) beyond it
+        count = nbytes // stride_bytes if stride_bytes else 0
+        check(self._lib.hs_engine_bind(self._h, kernel, pos, ctypes.c_void_p(ptr), stride_bytes, count, int(on_dev)),
               "hs_engine_bind")
         self._keep.append(arr)
 

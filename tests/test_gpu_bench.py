@@ -26,22 +26,36 @@ def test_bench_single_rank():
     assert p.returncode == 0, p.stderr[-2000:]
     line = _line(p.stdout)
     assert line["n_gpus"] == 1 and line["value"] > 0 and line["gpu_launches"] > 0
-    assert line["parity"]["normwise_err_vs_cpu_oracle"] <= 1e-4
+    par = line["parity"]
+    assert par["pass"] and par["normwise_vs_oracle"] <= 1e-4 and par["instances_checked"] >= 16
+    assert par["normwise_vs_f64"] <= 1e-4 and par["e2e_bit_identical_all_instances"]
+    # every batch's first and last instance is among the checked ones
+    assert {0, 63, 64, 127} <= set(par["per_rank"][0]["instances"])
     assert line["e2e"]["h2d_bytes_per_step"] == 128 * 128 * 512 * 4
 
 
 @pytest.mark.gpu
-def test_bench_two_ranks_partition_the_stream():
+@pytest.mark.parametrize("launcher", ["torchrun", "self"])
+def test_bench_two_ranks_partition_the_stream(launcher):
+    """`torchrun ... bench.py --gpus 2` (the driver's launch) and plain `bench.py --gpus 2`
+    (bench re-launches itself as two ranks) both time two ranks and check both
+    partitions against the oracle."""
     env = dict(os.environ, HS_BENCH_SHARED_GPU="1")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
-           "127.0.0.1", "--master-port", "29561", "bench.py", "--gpus", "2", *ARGS]
+    env.pop("WORLD_SIZE", None)
+    if launcher == "torchrun":
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+               "127.0.0.1", "--master-port", "29561", "bench.py", "--gpus", "2", *ARGS]
+    else:
+        cmd = [sys.executable, "bench.py", "--gpus", "2", *ARGS]
     p = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
     assert p.returncode == 0, p.stderr[-3000:]
     line = _line(p.stdout)
-    assert line["n_gpus"] == 2 and line["value"] > 0
+    assert line["n_gpus"] == 2 and line["value"] > 0 and line["e2e"]["value"] > 0
     assert line["config"]["parallelism"] == "instance partition x2"
-    # rank 0 checks its own first instance (instance 0) against the oracle
-    assert line["parity"]["instance"] == 0 and line["parity"]["normwise_err_vs_cpu_oracle"] <= 1e-4
+    par = line["parity"]
+    assert par["ranks"] == 2 and par["pass"] and par["e2e_bit_identical_all_instances"]
+    firsts = sorted(min(r["instances"]) for r in par["per_rank"])
+    assert firsts == [0, 64] and all(len(r["instances"]) >= 16 for r in par["per_rank"])
 
 
 @pytest.mark.gpu

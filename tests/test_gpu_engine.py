@@ -305,6 +305,60 @@ def test_full_depth_c5_dag_matches_oracle(oracle_mod):
         assert _normwise(outs[key][i], ref[key][i]) <= TOL, i
 
 
+def test_production_stream_c5_sampled_parity(oracle_mod):
+    """The bench's production configuration — 12 layers, batch 512, 3 slots — over
+    2100 instances: device-resident (4 full batches and a ragged one rotating over
+    the 3 slots) and host-fed through pinned memory (ramp chunks of 128 at both
+    ends). Host-fed equals device-resident bit for bit on every instance; the first
+    and last instance of every batch and ramp chunk, plus evenly spaced ones, are
+    within 1e-4 of the fp32 CPU oracle and of the fp64 truth."""
+    import torch
+    text, params, meta = workloads.encoder(layers=12)
+    n, batch = 2100, 512
+    S, D = params["S"], params["D"]
+    key = (meta["output"]["kernel"], meta["output"]["pos"])
+    x = workloads.encoder_inputs(meta, params, n).reshape(n, -1)
+    weights = workloads.encoder_weights(meta)
+
+    def run(xb, out):
+        with Engine(text, params, mode="graph", batch=batch, slots=3) as eng:
+            for i in meta["x_inputs"]:
+                eng.bind(i["kernel"], i["pos"], xb)
+            for k, w in weights.items():
+                eng.bind(*k, w.reshape(-1), shared=True)
+            eng.bind(*key, out)
+            eng.run(0, n)
+            eng.run(0, n)  # a second pass through the same slots
+            return eng.info("plan")
+
+    x_dev = torch.from_numpy(x).cuda()
+    out_dev = torch.zeros(n, S * D, device="cuda")
+    torch.cuda.synchronize()
+    plan = run(x_dev, out_dev)
+    assert plan["ramp_batch"] == 0 and plan["launches_per_batch"] == 144
+    dev = out_dev.cpu().numpy()
+    del x_dev, out_dev
+    torch.cuda.empty_cache()
+    x_host = torch.from_numpy(x).pin_memory()
+    out_host = torch.zeros(n, S * D).pin_memory()
+    plan = run(x_host, out_host)
+    assert plan["ramp_batch"] == 128
+    assert np.array_equal(out_host.numpy(), dev)
+    # batches of the device run: [0,512) .. [2048,2100); chunks of the host run:
+    # [0,128), then 512-wide from 128, then 128-wide tail chunks from 1664
+    edges = {0, 511, 512, 1023, 1024, 1535, 1536, 2047, 2048, 2099, 127, 128, 639, 640, 1663, 1664, 1791, 1792, 2047}
+    idx = sorted(edges | set(np.linspace(0, n - 1, 8).round().astype(int).tolist()))
+    xs = x[idx]
+    arrays = {(i["kernel"], i["pos"]): xs for i in meta["x_inputs"]}
+    for k, w in weights.items():
+        arrays[k] = w.reshape(-1)
+    ref = oracle_mod.run_dag(text, params, arrays, len(idx))[key]
+    truth = oracle_mod.run_dag_f64(text, params, arrays, len(idx))[key]
+    for j, i in enumerate(idx):
+        assert _normwise(dev[i], ref[j]) <= TOL, i
+        assert _normwise(dev[i], truth[j]) <= TOL, i
+
+
 def test_single_term_tf32_plan(oracle_mod):
     """math='tf32' (one MMA per product, ~1e-3): the same plan (whole-head kernels,
     single-term pair GEMMs) runs and stays within its looser tolerance."""

@@ -1,0 +1,133 @@
+"""Engine guards and corner cases (round-1 advisor findings), checked on the B200
+against the CPU oracle:
+  * grouped sibling GEMMs whose shared A is a resident (stride-0) buffer read by
+    every instance of a batch;
+  * run() ranges checked against the instance count of every binding;
+  * deterministic mode (no split-K) is bit-reproducible for single instances;
+  * dynamic_fuse is refused when it cannot apply.
+"""
+import numpy as np
+import pytest
+
+from paper_2009_07482_b200 import workloads
+from paper_2009_07482_b200.engine import Engine, HetsimError
+
+pytestmark = pytest.mark.gpu
+
+
+def _normwise(y, ref):
+    y, ref = np.asarray(y, np.float64), np.asarray(ref, np.float64)
+    return float(np.max(np.abs(y - ref)) / max(np.max(np.abs(ref)), 1e-30))
+
+
+def _siblings_on_shared_a(m=128, k=256, members=3):
+    """`members` gemms C_i = X W_i in one component; X and every W_i are shared."""
+    b = workloads.SpecBuilder()
+    ids = [b.gemm(m, 64, k) for _ in range(members)]
+    return b.doc([ids], workloads.cq_list(1, 3)), {}, ids
+
+
+@pytest.mark.parametrize("members", [2, 3])
+def test_grouped_siblings_with_resident_a(members, oracle_mod):
+    text, params, ids = _siblings_on_shared_a(members=members)
+    n = 5
+    x = workloads.uniform(1, 99, 128 * 256)
+    arrays = {(kid, 0): x for kid in ids}
+    for kid in ids:
+        arrays[(kid, 1)] = workloads.uniform(2 + kid, 100 + kid, 256 * 64) / 16
+    ref = oracle_mod.run_dag(text, params, arrays, 1)
+    outs = {(kid, 2): np.zeros((n, 128 * 64), np.float32) for kid in ids}
+    with Engine(text, params, batch=4, slots=2, mode="graph") as eng:
+        for key, a in arrays.items():
+            eng.bind(*key, a, shared=True)
+        for key, a in outs.items():
+            eng.bind(*key, a)
+        eng.run(0, n)
+        assert eng.info("plan")["grouped_launches"] == 1
+    for key, o in outs.items():
+        for i in range(n):
+            assert _normwise(o[i], ref[key][0]) <= 1e-4, (key, i)
+
+
+def test_run_range_is_checked_against_bound_instances():
+    text, params = workloads.fork_join(n=64)
+    arrays = workloads.generic_inputs(text, params, 2)
+    outs = {(k, p): np.zeros((2, e), np.float32) for k, p, e in workloads.isolated_outputs(text, params)}
+    with Engine(text, params, batch=2, mode="graph") as eng:
+        for key, a in list(arrays.items()) + list(outs.items()):
+            eng.bind(*key, a)
+        eng.run(0, 2)
+        for first, n in ((1, 2), (-1, 1), (0, 3)):
+            with pytest.raises(HetsimError) as ei:
+                eng.run(first, n)
+            assert ei.value.errc == "InvalidParam"
+
+
+def test_deterministic_mode_is_bit_reproducible(oracle_mod):
+    """One instance of the encoder layer: split-K would add K-split partials with
+    atomics; deterministic=True launches without it, run after run bit-identical."""
+    text, params, meta = workloads.encoder(layers=1)
+    x = workloads.encoder_inputs(meta, params, 1).reshape(1, -1)
+    arrays = {(i["kernel"], i["pos"]): x for i in meta["x_inputs"]}
+    for key, w in workloads.encoder_weights(meta).items():
+        arrays[key] = w.reshape(-1)
+    ref = oracle_mod.run_dag(text, params, arrays, 1)
+    key = (meta["output"]["kernel"], meta["output"]["pos"])
+    runs = []
+    for _ in range(3):
+        out = np.zeros((1, params["S"] * params["D"]), np.float32)
+        with Engine(text, params, batch=1, mode="graph", deterministic=True) as eng:
+            for k, a in arrays.items():
+                eng.bind(*k, a, shared=a.ndim == 1)
+            eng.bind(*key, out)
+            eng.run(0, 1)
+            eng.run(0, 1)
+        runs.append(out.copy())
+    assert all(np.array_equal(runs[0], r) for r in runs[1:])
+    assert _normwise(runs[0][0], ref[key][0]) <= 1e-4
+
+
+def test_dynamic_fuse_refused_when_it_cannot_apply():
+    text, params = workloads.fork_join(n=64)
+    arrays = workloads.generic_inputs(text, params, 1)
+    outs = {(k, p): np.zeros((1, e), np.float32) for k, p, e in workloads.isolated_outputs(text, params)}
+    with Engine(text, params, mode="dynamic", math="simt", dynamic_fuse=True) as eng:
+        for key, a in list(arrays.items()) + list(outs.items()):
+            eng.bind(*key, a)
+        with pytest.raises(HetsimError) as ei:
+            eng.run(0, 1)
+        assert ei.value.errc == "InvalidParam"
+
+
+def _encoder_run(layers, n, **kw):
+    text, params, meta = workloads.encoder(layers=layers, queues=kw.pop("queues", 3))
+    x = workloads.encoder_inputs(meta, params, n).reshape(n, -1)
+    key = (meta["output"]["kernel"], meta["output"]["pos"])
+    out = np.zeros((n, params["S"] * params["D"]), np.float32)
+    with Engine(text, params, **kw) as eng:
+        for i in meta["x_inputs"]:
+            eng.bind(i["kernel"], i["pos"], x)
+        for k, w in workloads.encoder_weights(meta).items():
+            eng.bind(*k, w.reshape(-1), shared=True)
+        eng.bind(*key, out)
+        eng.run(0, n)
+        plan = eng.info("plan")
+    return out, plan
+
+
+@pytest.mark.parametrize("mode,fuse", [("graph", 0), ("graph", 3), ("dynamic", 0)])
+def test_liveness_arena_is_bit_identical(mode, fuse):
+    """Intermediates sharing one arena per slot (accesses ordered by DAG edges)
+    compute exactly what one allocation per buffer computes, in less memory."""
+    pooled, p1 = _encoder_run(2, 5, mode=mode, fuse=fuse, batch=3, slots=2)
+    plain, p0 = _encoder_run(2, 5, mode=mode, fuse=fuse, batch=3, slots=2, liveness=False)
+    assert np.array_equal(pooled, plain)
+    assert p1["device_bytes"] < p0["device_bytes"]
+    assert p1["arena_bytes_per_instance"] < p1["all_outputs_bytes_per_instance"]
+
+
+def test_c5_production_plan_fits_in_10_gb():
+    """C5 (12 layers) at batch 512 with 3 slots: the arena holds what the plan touches
+    (whole-head launches leave Q/K/V/S/P/C unallocated), under 10 GB in all."""
+    _, plan = _encoder_run(12, 1, mode="graph", batch=512, slots=3)
+    assert plan["device_bytes"] < 10e9, plan["device_bytes"]
