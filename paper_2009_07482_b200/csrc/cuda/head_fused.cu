@@ -5,38 +5,42 @@
 //
 // which is the head component of the encoder DAG (SURVEY.md §8 C3:
 // three projection GEMMs, transpose, QKᵀ, softmax, P·V, C·W_h) after the engine's
-// launch rewrites: the grouped Q/K/V projection (gemm_tc.cu, gemm_pair_kernel<192>)
-// and the fused attention chain (attn_head.cu) in one kernel, so Q, K, V never
-// leave the SM. Each product is 3xTF32 with the operand split and the MMA order of
-// those two kernels.
+// launch rewrites. Q, K, V, S, P and C never leave the SM. Every product is 3xTF32
+// on tcgen05 (hi/lo splits, lo·hi + hi·lo + hi·hi).
 //
-// CTA pair (cluster of 2 on one TPC) per pair of instances, persistent over pairs.
-// Phase 1 (projection): the pair GEMM main loop with M = 256 (each CTA its own
-// instance's 128 rows), N = 192, K = D: X tiles by TMA into staging, split hi/lo
-// into TMEM by the converter warps, W planes by TMA (each CTA half of N).
-// Phase 2 (attention), all MMAs still cta_group::2 with M = 256:
-//   S  = [Q0;Q1] [K0;K1]ᵀ   N = 256: B rows 0-127 are CTA 0's keys, 128-255 CTA 1's;
-//                           CTA r keeps its own block, columns [128r, 128r+128)
-//   C  = [P0;P1] [V0 V1]    N = 128: B = Vᵀ, rows 0-63 CTA 0's, 64-127 CTA 1's;
-//                           CTA r keeps columns [64r, 64r+64)
-//   Z  = [C0;C1] Wh         N = 64: each CTA holds half of Whᵀ's rows
-// The off-diagonal blocks of S and C are computed and discarded (2x the QKᵀ and
-// P·V flops, 14 % of the head's): the price of one cta_group for the whole kernel.
+// A cluster of two CTAs (one TPC) per pair of instances, persistent over pairs,
+// and two pairs in flight: while the tensor cores run the Q/K/V projection of
+// pair i+1, the attention of pair i runs beside it.
+//   projection  cta_group::2, M = 256 (each CTA its own instance's 128 rows), N = 192,
+//               K-blocks of 16 X columns: X tile -> tf32 hi/lo in a TMEM A stage (32
+//               columns) by the converter warps; W planes K-major SWIZZLE_128B in
+//               K-blocks of 32, each CTA holding half of N (96 rows): the pair halves
+//               each SM's shared-memory traffic for W, which a single CTA at N = 192
+//               cannot sustain
+//   attention   cta_group::1 per CTA on its own instance (no cross-instance blocks):
+//               S = Q Kᵀ (N = 128, Q hi/lo in TMEM, K hi/lo in smem), softmax in
+//               registers, C = P V (N = 64, P hi/lo in TMEM, Vᵀ hi/lo in smem),
+//               Z = C Wh (N = 64, C hi/lo in TMEM, Wh planes in smem)
+// The leader's issuer interleaves its own attention MMAs into the projection's MMA
+// stream as their operands become ready; the other CTA's issuer runs only its own
+// attention. (profiles/mix_probe.cu: cta_group::1 and ::2 MMAs side by side in one
+// cluster kernel are exact.)
 //
-// Warp roles (512 threads):
-//   warp 0      TMA: X tiles (phase 1)
-//   warp 1      MMA issuer (leader CTA, one lane)
-//   warp 2      TMEM allocator (512 columns, cta_group::2)
-//   warp 3      TMA: W planes (phase 1, this CTA's half of N), Wh half once
-//   warps 4-11  phase 1: converters, group g = (w-4)/4 takes every other K-block
-//               phase 2: row warps, TMEM lane quarter q = w%4, column half g:
-//               Q split -> TMEM; softmax (S in registers, row max / sum exchanged
-//               with the partner warp); C split -> TMEM; Z -> TMA store
-//   warps 12-15 phase 2: K -> K-major smem hi/lo; V -> Vᵀ K-major smem hi/lo
+// Warp roles (512 threads per CTA):
+//   warp 0      TMA: this CTA's X tiles (+ L2 prefetch of its next instance's X)
+//   warp 1      MMA issuer (leader: projection + own attention; other: own attention)
+//   warp 2      TMEM allocator (512 columns, cta_group::2); then TMA: Wh planes
+//   warp 3      TMA: this CTA's half of the Wq|Wk|Wv planes
+//   warps 4-7   converters: X tile -> tf32 hi/lo -> TMEM A stage (lane quarter = warp % 4)
+//   warps 8-15  attention (quarter q = warp % 4, half g = (warp - 8) / 4): extraction
+//               (Q -> TMEM hi/lo, K / Vᵀ -> smem hi/lo), softmax, P -> TMEM, C -> TMEM
+//               hi/lo, Z -> global
 //
-// TMEM columns: phase 1: QKV accumulator [0,192) | A stages [192,448).
-// phase 2: S [0,256) -> C acc [0,128) + Z acc [128,192); A operand [256,512):
-// Q hi/lo [256,384) -> P hi/lo [256,512) -> C hi/lo [256,384).
+// TMEM columns (each CTA): [0,192) projection accumulator Q|K|V · [192,256) 2 A
+// stages · [256,384) Q hi|lo, then P hi (128 keys), then C hi|lo · [384,512) S, then
+// P lo of keys 0-63 [384,448) + C accumulator [448,512), then the Z accumulator
+// [384,448). P lo of keys 64-127 replaces [384,448) once the MMAs reading keys
+// 0-63's have run.
 #include <mutex>
 
 #include "kernels.cuh"
@@ -45,24 +49,36 @@
 #ifndef HS_DBG_TIMELINE
 #define HS_DBG_TIMELINE 0
 #endif
-#ifndef HS_DBG_HEAD_NOCONV  // timing experiment only (wrong results): skip the X split in phase 1
+// timing experiments only (wrong results): skip the X split (converters only signal),
+// or the attention (no QKᵀ / P·V / softmax / Z; the accumulator is released at once)
+#ifndef HS_DBG_HEAD_NOCONV
 #define HS_DBG_HEAD_NOCONV 0
+#endif
+#ifndef HS_DBG_HEAD_NOATT
+#define HS_DBG_HEAD_NOATT 0
 #endif
 
 namespace hs {
 
 #if HS_DBG_TIMELINE
-// timing experiment only (profiles/head_timeline.py): clock64 stamps of cluster 0,
-// CTA 0, first 8 pairs x 16 points
+// timing experiment only (profiles/head_timeline.py): CTA 0, first 8 pair iterations
+// x 16 slots: clock64 stamps, and cycles spent in selected waits (summed)
 __device__ long long g_head_timeline[8 * 16];
-#define TL(t, k)                                                             \
-  do {                                                                       \
-    if (pair0 == 0 && rank == 0 && (t) < 8) g_head_timeline[(t) * 16 + (k)] = clock64(); \
+#define TL(t, k)                                                                                   \
+  do {                                                                                             \
+    if (blockIdx.x == 0 && (t) < 8) g_head_timeline[(t) * 16 + (k)] = clock64();                   \
+  } while (0)
+#define TW(t, k, expr)                                                                             \
+  do {                                                                                             \
+    const long long _c0 = clock64();                                                               \
+    expr;                                                                                          \
+    if (blockIdx.x == 0 && (t) < 8 && lane == 0) g_head_timeline[(t) * 16 + (k)] += clock64() - _c0; \
   } while (0)
 #else
 #define TL(t, k) \
   do {           \
   } while (0)
+#define TW(t, k, expr) expr
 #endif
 
 namespace {
@@ -71,52 +87,54 @@ using namespace tc;
 
 constexpr int kS = 128, kDK = 64, kN = 3 * kDK;  // rows, head width, projection width
 constexpr int kThreads = 512;
-// Variant (measured slower, kept for A/B): three converter groups (warps 12-15
-// convert too) with 6 X / 3 W+A stages. The projection drops from ~21k to ~19.6k
-// cycles per pair, but stage 0 can be pre-converted for only a third of the
-// pairs, and the first K-blocks of a pair wait for O_FULL: 105 vs 99 us per
-// 512-instance launch (profiles/README.md).
-#ifndef HS_HEAD_CONV3
-#define HS_HEAD_CONV3 0
+constexpr int kXK = 16;                          // X tile / A stage: 16 columns (SWIZZLE_64B)
+constexpr int kWK = 32;                          // W stage: 32 columns (SWIZZLE_128B) = 2 A stages
+#ifndef HS_HEAD_NA
+#define HS_HEAD_NA 2
 #endif
-constexpr int kConv = HS_HEAD_CONV3 ? 3 : 2;  // converter groups (each takes every kConv-th K-block)
-constexpr int kNS = HS_HEAD_CONV3 ? 6 : 4;    // X staging stages
-constexpr int kNO = HS_HEAD_CONV3 ? 3 : 4;    // W operand stages = TMEM A stages
-constexpr uint32_t kStaging = BM * BK * 4;            // 16 KB X tile
-constexpr uint32_t kPlaneB = (kN / 2) * 128;          // 96 rows x 128 B: this CTA's half of N
-constexpr uint32_t kOperand = 2 * kPlaneB;            // hi + lo
+#ifndef HS_HEAD_NX
+#define HS_HEAD_NX 3
+#endif
+constexpr int kNX = HS_HEAD_NX, kNW = 3, kNA = HS_HEAD_NA;  // ring depths
+constexpr uint32_t kXTile = kS * kXK * 4;        // 8 KB
+constexpr uint32_t kWPlane = (kN / 2) * 128;     // 12 KB: this CTA's 96 rows
+constexpr uint32_t kWStage = 2 * kWPlane;        // hi + lo
 // shared memory (bytes from the 1024-aligned base)
-constexpr uint32_t kU = 0;                            // union: phase 1 stages | phase 2 operands
-constexpr uint32_t kOpB = kU + kNS * kStaging;        // phase 1 W operand ring
-constexpr uint32_t kKop = kU;                         // phase 2: K hi/lo, 2 planes x 2 k-blocks x [128][128 B]
-constexpr uint32_t kVop = kU + 65536;                 // phase 2: Vᵀ hi/lo, 2 planes x 4 k-blocks x [64][128 B]
-constexpr uint32_t kUEnd = kOpB + kNO * kOperand;     // 160 KB
-constexpr uint32_t kWh = kUEnd;                       // Whᵀ half: 2 planes x 2 k-blocks x [32][128 B] (16 KB)
-constexpr uint32_t kEpi = kWh + 16384;                // Z staging: 4 warps x 2 x [32][32] fp32 (32 KB)
-constexpr uint32_t kExch = kEpi + 32768;              // softmax row max / sum exchange: 8 warps x 2 x 32 fp32
-constexpr uint32_t kBar = kExch + 2048;
+constexpr uint32_t kXs = 0;
+constexpr uint32_t kWs = kXs + kNX * kXTile;     // 24 KB
+constexpr uint32_t kKop = kWs + kNW * kWStage;   // 96 KB: K hi/lo, 2 planes x 2 k-blocks x [128 keys][128 B]
+constexpr uint32_t kVop = kKop + 65536;          // 160 KB: Vᵀ hi/lo, 2 planes x 4 k-blocks x [64 d][128 B]
+constexpr uint32_t kBar = HS_DBG_HEAD_NOATT ? kKop : kVop + 65536;  // 224 KB
+constexpr uint32_t kXch = kKop;                  // softmax row max / sum exchange (K consumed by then)
+constexpr uint32_t kWh = kKop + 4096;            // Whᵀ hi/lo, 2 planes x 2 k-blocks x [64][128 B] (after S)
 constexpr int kSmem = int(kBar) + 512 + 1024;
-static_assert(kVop + 65536 <= kUEnd, "phase 2 operands exceed the union");
 static_assert(kSmem <= 227 * 1024, "shared memory budget exceeded");
 
-constexpr uint32_t kTQ = 256;  // TMEM A-operand region (phase 2)
-constexpr uint32_t kTZ = 448;  // Z accumulator: P lo's columns, free after P·V; outside the projection's TMEM
-constexpr uint32_t kTStage = 192;
+// TMEM columns
+constexpr uint32_t kTQ = 0, kTK = 64, kTV = 128;  // projection accumulator
+constexpr uint32_t kTA = 192;                     // A stages, 32 columns each (hi 16 | lo 16)
+constexpr uint32_t kTOp = 256;                    // Q hi/lo -> P hi -> C hi/lo
+constexpr uint32_t kTS = 384;                     // S -> P lo (keys 0-63 / 64-127) -> Z accumulator
+constexpr uint32_t kTC = 448;                     // C accumulator
 
 enum Bar : uint32_t {
-  ST_FULL = 0,             // [kNS] local
-  ST_EMPTY = ST_FULL + kNS,  // [kNS] local, 4 converter warps
-  OP_FULL = ST_EMPTY + kNS,  // [kNO] leader: 2 x 4 converter warps + expect_tx
-  OP_EMPTY = OP_FULL + kNO,  // [kNO] each CTA (commit multicast)
-  ACC_FULL = OP_EMPTY + kNO,
-  A_READY,   // leader: Q split + K operand, 2 x 8 warps (S = Q Kᵀ may start)
-  V_READY,   // leader: Vᵀ operand, 2 x 8 warps (P·V may start)
-  S_FULL,    // each CTA
-  P_READY,   // leader: 2 x 8
-  O_FULL,    // each CTA
-  C_READY,   // leader: 2 x 8
-  Z_FULL,    // each CTA
-  WH_FULL,   // leader: expect_tx
+  XF = 0,               // [kNX] X tile landed (TMA tx)
+  XE = XF + kNX,        // [kNX] X tile converted (4 local converter warps)
+  WF = XE + kNX,        // [kNW] leader: both CTAs' W halves landed (TMA tx)
+  WE = WF + kNW,        // [kNW] W stage consumed (leader's commit, multicast)
+  AF = WE + kNW,        // [kNA] leader: both CTAs' A stages written (2 x 4 converter warps)
+  AE = AF + kNA,        // [kNA] A stage consumed (leader's commit, multicast)
+  ACC_FULL = AE + kNA,  // projection done (leader's commit, multicast)
+  EXT_PAIR,             // leader: both CTAs extracted (2 x 8 attention warps)
+  EXT,                  // this CTA extracted (8 warps): Q hi/lo in TMEM, K / Vᵀ in smem
+  S_FULL,               // S = Q Kᵀ done
+  WH_FULL,              // Wh planes landed (TMA tx)
+  P_READY,              // P hi + P lo of keys 0-63 in TMEM, S read (8 warps)
+  PLO_FREE,             // the MMAs reading P lo of keys 0-63 are done
+  P2_READY,             // P lo of keys 64-127 in TMEM (4 warps)
+  C_FULL,               // C = P V done
+  C_READY,              // C hi/lo in TMEM (8 warps)
+  Z_FULL,               // Z = C Wh done
   TMEM_SLOT,
   kNumBars
 };
@@ -125,22 +143,43 @@ static_assert(kNumBars * 8 <= 512, "barrier area");
 struct HeadParams {
   int S, D, batch, pairs;
   float scale;
+  float* Z;
+  int64_t sZ, ldz;  // elements
 };
 
-template <int kTerms>
-__device__ __forceinline__ void mma3(uint32_t d, uint32_t a_hi, uint32_t a_lo, uint32_t b_hi, uint32_t b_lo,
+// non-blocking test of an mbarrier phase (warp-uniform: lane 0 decides)
+__device__ __forceinline__ bool mbar_test_warp(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  if ((threadIdx.x & 31) == 0)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  return __shfl_sync(0xffffffffu, done, 0) != 0;
+}
+
+// D (+)= A·B with A = a_hi + a_lo in TMEM, B = b_hi + b_lo in smem: lo·hi, hi·lo, hi·hi
+template <int kTerms, bool kPair>
+__device__ __forceinline__ void mma3(uint32_t d, uint32_t a_hi, uint32_t a_lo, uint64_t b_hi, uint64_t b_lo,
                                      uint32_t idesc, uint32_t first) {
+  auto mma = [&](uint32_t a, uint64_t b, uint32_t acc) {
+    if constexpr (kPair) mma_pair_tf32_ts(d, a, b, idesc, acc);
+    else mma_tf32_ts(d, a, b, idesc, acc);
+  };
   if constexpr (kTerms > 1) {
-    mma_pair_tf32_ts(d, a_lo, smem_desc(b_hi), idesc, first);
-    mma_pair_tf32_ts(d, a_hi, smem_desc(b_lo), idesc, 1u);
-    mma_pair_tf32_ts(d, a_hi, smem_desc(b_hi), idesc, 1u);
+    mma(a_lo, b_hi, first);
+    mma(a_hi, b_lo, 1u);
+    mma(a_hi, b_hi, 1u);
   } else {
-    mma_pair_tf32_ts(d, a_hi, smem_desc(b_hi), idesc, first);
+    mma(a_hi, b_hi, first);
   }
 }
 
 template <int kTerms>
-__device__ __forceinline__ void split_row16(const uint32_t* r, uint32_t (&hi)[16], uint32_t (&lo)[16]) {
+__device__ __forceinline__ void split16(const uint32_t* r, uint32_t (&hi)[16], uint32_t (&lo)[16]) {
 #pragma unroll
   for (int e = 0; e < 16; ++e) {
     const float x = __uint_as_float(r[e]);
@@ -148,6 +187,15 @@ __device__ __forceinline__ void split_row16(const uint32_t* r, uint32_t (&hi)[16
     hi[e] = __float_as_uint(h);
     lo[e] = __float_as_uint(x - h);
   }
+}
+
+// 16 values -> hi / lo TMEM columns (hi at taddr, lo at taddr + lo_off)
+template <int kTerms>
+__device__ __forceinline__ void st_split16(uint32_t taddr, uint32_t lo_off, const uint32_t* r) {
+  uint32_t hi[16], lo[16];
+  split16<kTerms>(r, hi, lo);
+  tmem_st16(taddr, hi);
+  if constexpr (kTerms > 1) tmem_st16(taddr + lo_off, lo);
 }
 
 // Softmax passes over this thread's 64 S values (columns c0.. of its row): the
@@ -182,44 +230,10 @@ __device__ __forceinline__ float row_exp(uint32_t (&r0)[32], uint32_t (&r1)[32],
   return sum;
 }
 
-// K row (this key = TMEM lane) -> K-major SW128 tiles [128 keys][32 d] x 2 (hi at +0, lo at +32 KB)
-__device__ __forceinline__ void store_k_operand(uint32_t base, uint32_t lane_base, int key) {
-#pragma unroll 1
-  for (int kb = 0; kb < 2; ++kb) {
-    uint32_t r[32];
-    tmem_ld32(lane_base + uint32_t(kDK + kb * 32), r);
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      const float4 x = make_float4(__uint_as_float(r[4 * c]), __uint_as_float(r[4 * c + 1]),
-                                   __uint_as_float(r[4 * c + 2]), __uint_as_float(r[4 * c + 3]));
-      const float4 h = make_float4(tf32_rna(x.x), tf32_rna(x.y), tf32_rna(x.z), tf32_rna(x.w));
-      const uint32_t dst = base + kKop + uint32_t(kb) * 16384u + sw128(key, c);
-      sts128(dst, h);
-      sts128(dst + 32768u, make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w));
-    }
-  }
-}
-
-// V row (this key = TMEM lane q*32 + lane), d in [32 half, 32 half + 32) -> Vᵀ K-major
-// SW128 tiles [64 d][32 keys] (k-block = key / 32 = q; hi at +0, lo at +32 KB)
-__device__ __forceinline__ void store_vt_operand(uint32_t base, uint32_t lane_base, int q, int lane, int half) {
-  uint32_t r[32];
-  tmem_ld32(lane_base + uint32_t(2 * kDK + half * 32), r);
-#pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    const int n = half * 32 + j;
-    const float x = __uint_as_float(r[j]);
-    const float h = tf32_rna(x);
-    const uint32_t dst = base + kVop + uint32_t(q) * 8192u + sw128(n, lane >> 2) + uint32_t(lane & 3) * 4u;
-    sts32(dst, h);
-    sts32(dst + 32768u, x - h);
-  }
-}
-
 template <int kTerms>
 __global__ void __launch_bounds__(kThreads, 1)
-    head_pair_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
-                     const __grid_constant__ CUtensorMap tmWh, const __grid_constant__ CUtensorMap tmZ, HeadParams p) {
+    head_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
+                const __grid_constant__ CUtensorMap tmWh, HeadParams p) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
   auto bar = [&](uint32_t b) { return base + kBar + 8u * b; };
@@ -228,24 +242,28 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
   const int pair0 = int(cluster_id_x()), npairs = int(nclusters_x());
-  const int nk = p.D / BK;
+  const int nx = p.D / kXK, nw = p.D / kWK;
   auto leader = [&](uint32_t b) { return mapa_rank(bar(b), 0); };
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kNS; ++s) {
-      mbar_init(bar(ST_FULL + s), 1);
-      mbar_init(bar(ST_EMPTY + s), 4);
+    for (int s = 0; s < kNX; ++s) {
+      mbar_init(bar(XF + s), 1);
+      mbar_init(bar(XE + s), 4);
     }
-    for (int o = 0; o < kNO; ++o) {
-      mbar_init(bar(OP_FULL + o), 2 * 4 + 1);
-      mbar_init(bar(OP_EMPTY + o), 1);
+    for (int s = 0; s < kNW; ++s) {
+      mbar_init(bar(WF + s), 1);
+      mbar_init(bar(WE + s), 1);
     }
-    for (uint32_t b : {ACC_FULL, S_FULL, O_FULL, Z_FULL, WH_FULL}) mbar_init(bar(b), 1);
-    mbar_init(bar(A_READY), 2 * 8);
-    mbar_init(bar(V_READY), 2 * 8);
-    for (uint32_t b : {P_READY, C_READY}) mbar_init(bar(b), 2 * 8);
+    for (int a = 0; a < kNA; ++a) {
+      mbar_init(bar(AF + a), 2 * 4);
+      mbar_init(bar(AE + a), 1);
+    }
+    for (uint32_t b : {ACC_FULL, S_FULL, WH_FULL, PLO_FREE, C_FULL, Z_FULL}) mbar_init(bar(b), 1);
+    mbar_init(bar(EXT_PAIR), 2 * 8);
+    for (uint32_t b : {EXT, P_READY, C_READY}) mbar_init(bar(b), 8);
+    mbar_init(bar(P2_READY), 4);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (const CUtensorMap* m : {&tmX, &tmW, &tmWh, &tmZ})
+    for (const CUtensorMap* m : {&tmX, &tmW, &tmWh})
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
   }
   if (warp == 2) {
@@ -258,398 +276,396 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = *tmem_slot_ptr;
 
   if (warp == 0) {
-    // ------------------------------------------------------------ X producer
+    // ------------------------------------------------------------ X producer (this CTA's instance)
     if (lane == 0) {
       uint32_t it = 0, lt = 0;
       for (int t = pair0; t < p.pairs; t += npairs, ++lt) {
-        // X stages share the K operand's smem: free once the last pair's S = Q Kᵀ is done
-        if (lt > 0) mbar_wait(bar(S_FULL), (lt - 1) & 1u);
         const int inst = 2 * t + int(rank);  // >= batch: zero-filled box
-        bool o_waited = lt == 0;
-        for (int kb = 0; kb < nk; ++kb, ++it) {
-          const int s = int(it % kNS);
-          if (s >= 4 && !o_waited) {  // stages 4-5 share the Vᵀ operand's smem: wait for P·V
-            mbar_wait(bar(O_FULL), (lt - 1) & 1u);
-            o_waited = true;
-          }
-          mbar_wait(bar(ST_EMPTY + s), ((it / kNS) & 1u) ^ 1u);
-          mbar_expect_tx(bar(ST_FULL + s), kStaging);
-          tma_load_3d(base + kU + uint32_t(s) * kStaging, &tmX, bar(ST_FULL + s), kb * BK, 0, inst);
+        // warm L2 with this CTA's next instance: its loads start right after this projection
+        if (2 * (t + npairs) + int(rank) < p.batch)
+          for (int kb = 0; kb < nx; ++kb) tma_prefetch_3d(&tmX, kb * kXK, 0, 2 * (t + npairs) + int(rank));
+        for (int kb = 0; kb < nx; ++kb, ++it) {
+          const int s = int(it % kNX);
+          TW(lt, 12, mbar_wait(bar(XE + s), ((it / kNX) & 1u) ^ 1u));
+          mbar_expect_tx(bar(XF + s), kXTile);
+          tma_load_3d(base + kXs + uint32_t(s) * kXTile, &tmX, bar(XF + s), kb * kXK, 0, inst);
         }
-        // warm L2 with this CTA's rows of the next pair: its loads start only after
-        // phase 2, and would otherwise pay the HBM latency at the head of the pipeline
-        if (t + npairs < p.pairs)
-          for (int kb = 0; kb < nk; ++kb) tma_prefetch_3d(&tmX, kb * BK, 0, 2 * (t + npairs) + int(rank));
       }
     }
   } else if (warp == 3) {
     // ------------------------------------------------------------ W producer (this CTA's half of N)
     if (lane == 0) {
-      if (rank == 0) mbar_expect_tx(bar(WH_FULL), 2u * 16384u);
-      for (int pl = 0; pl < 2; ++pl)
-        for (int kb = 0; kb < 2; ++kb)
-          tma_load_3d_pair(base + kWh + uint32_t(pl) * 8192u + uint32_t(kb) * 4096u, &tmWh, leader(WH_FULL), kb * BK,
-                           int(rank) * 32, pl);
       uint32_t it = 0, lt = 0;
       for (int t = pair0; t < p.pairs; t += npairs, ++lt) {
-        if (lt > 0) mbar_wait(bar(O_FULL), (lt - 1) & 1u);
-        for (int kb = 0; kb < nk; ++kb, ++it) {
-          const int o = int(it % kNO);
-          mbar_wait(bar(OP_EMPTY + o), ((it / kNO) & 1u) ^ 1u);
-          const uint32_t b_hi = base + kOpB + uint32_t(o) * kOperand;
-          if (rank == 0) mbar_expect_tx(bar(OP_FULL + o), 2 * (kTerms > 1 ? 2 : 1) * kPlaneB);
+        for (int kb = 0; kb < nw; ++kb, ++it) {
+          const int s = int(it % kNW);
+          TW(lt, 13, mbar_wait(bar(WE + s), ((it / kNW) & 1u) ^ 1u));
+          if (rank == 0) mbar_expect_tx(bar(WF + s), 2u * (kTerms > 1 ? 2u : 1u) * kWPlane);
+          const uint32_t dst = base + kWs + uint32_t(s) * kWStage;
           const int nrow = int(rank) * (kN / 2);
-          tma_load_3d_pair(b_hi, &tmW, leader(OP_FULL + o), kb * BK, nrow, 0);
-          if constexpr (kTerms > 1) tma_load_3d_pair(b_hi + kPlaneB, &tmW, leader(OP_FULL + o), kb * BK, nrow, 1);
+          tma_load_3d_pair(dst, &tmW, leader(WF + s), kb * kWK, nrow, 0);
+          if constexpr (kTerms > 1) tma_load_3d_pair(dst + kWPlane, &tmW, leader(WF + s), kb * kWK, nrow, 1);
         }
+      }
+    }
+  } else if (warp == 2) {
+    // ------------------------------------------------------------ Wh producer (after each S = Q Kᵀ)
+    if (lane == 0 && !HS_DBG_HEAD_NOATT) {
+      uint32_t lt = 0;
+      for (int t = pair0; t < p.pairs; t += npairs, ++lt) {
+        mbar_wait(bar(S_FULL), lt & 1u);
+        mbar_expect_tx(bar(WH_FULL), (kTerms > 1 ? 2u : 1u) * 16384u);
+        for (int pl = 0; pl < (kTerms > 1 ? 2 : 1); ++pl)
+          for (int kb = 0; kb < 2; ++kb)
+            tma_load_3d(base + kWh + uint32_t(pl) * 16384u + uint32_t(kb) * 8192u, &tmWh, bar(WH_FULL), kb * 32, 0,
+                        pl);
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer (leader)
-    // The whole warp runs the loop (warp-uniform state and descriptors); one
-    // elected lane issues each batch of tcgen05.mma and its commit.
-    if (rank == 0) {
-      constexpr uint32_t m256 = uint32_t(BM >> 4) << 24;
-      constexpr uint32_t idQKV = instr_desc_tf32(kN) + m256, idS = instr_desc_tf32(256) + m256,
-                         idC = instr_desc_tf32(128) + m256, idZ = instr_desc_tf32(kDK) + m256;
-      uint32_t it = 0, lt = 0;
-      bool wh = false;
-      for (int t = pair0; t < p.pairs; t += npairs, ++lt) {
-        const uint32_t ph = lt & 1u;
-        // The last pair's C accumulator [0,128) was drained before C_READY and its Z
-        // accumulator lives at [448,512): the projection may overwrite [0,192) at once
-        // (tcgen05.mma executes in issue order, after the last pair's Z MMA).
-        if (lane == 0) TL(lt, 0);
-        // phase 1: [Q|K|V] = X · W
-        for (int kb = 0; kb < nk; ++kb, ++it) {
-          const int o = int(it % kNO);
-          mbar_wait(bar(OP_FULL + o), (it / kNO) & 1u);
-          if (lane == 0 && kb == 0) TL(lt, 2);
-          tc_fence_after();
-          const uint32_t a_hi = tmem + kTStage + uint32_t(o) * 64u, a_lo = a_hi + 32u;
-          const uint32_t b_hi = base + kOpB + uint32_t(o) * kOperand, b_lo = b_hi + kPlaneB;
-          if (elect_one()) {
+    // ------------------------------------------------------------ MMA issuer
+    // The whole warp runs the loop (warp-uniform state); one elected lane issues.
+    constexpr uint32_t idP = instr_desc_tf32(kN, 256), idS = instr_desc_tf32(kS), idC = instr_desc_tf32(kDK);
+    auto kdesc = [&](int kk, int plane) {  // K operand: k-block kk/4 of d, 8-column step kk%4
+      return smem_desc(base + kKop + uint32_t(plane) * 32768u + uint32_t(kk >> 2) * 16384u + uint32_t(kk & 3) * 32u);
+    };
+    auto vdesc = [&](int kk, int plane) {  // Vᵀ operand: k-block kk/4 of keys
+      return smem_desc(base + kVop + uint32_t(plane) * 32768u + uint32_t(kk >> 2) * 8192u + uint32_t(kk & 3) * 32u);
+    };
+    auto whdesc = [&](int kk, int plane) {  // Whᵀ operand: k-block kk/4 of d
+      return smem_desc(base + kWh + uint32_t(plane) * 16384u + uint32_t(kk >> 2) * 8192u + uint32_t(kk & 3) * 32u);
+    };
+    auto issue_s = [&]() {
+      if (elect_one()) {
 #pragma unroll
-            for (int kk = 0; kk < BK / 8; ++kk)
-              mma3<kTerms>(tmem, a_hi + uint32_t(kk) * 8u, a_lo + uint32_t(kk) * 8u, b_hi + uint32_t(kk) * 32u,
-                           b_lo + uint32_t(kk) * 32u, idQKV, (kb | kk) ? 1u : 0u);
-            mma_commit_pair(bar(OP_EMPTY + o));
+        for (int kk = 0; kk < kDK / 8; ++kk)
+          mma3<kTerms, false>(tmem + kTS, tmem + kTOp + uint32_t(kk) * 8u, tmem + kTOp + 64u + uint32_t(kk) * 8u,
+                              kdesc(kk, 0), kdesc(kk, 1), idS, kk ? 1u : 0u);
+        mma_commit(bar(S_FULL));
+      }
+      __syncwarp();
+    };
+    auto issue_pv_a = [&]() {  // P hi · V (both terms), then P lo · V hi for keys 0-63
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < kS / 8; ++kk) {
+          const uint32_t a_hi = tmem + kTOp + uint32_t(kk) * 8u;
+          if constexpr (kTerms > 1) {
+            mma_tf32_ts(tmem + kTC, a_hi, vdesc(kk, 1), idC, kk ? 1u : 0u);
+            mma_tf32_ts(tmem + kTC, a_hi, vdesc(kk, 0), idC, 1u);
+          } else {
+            mma_tf32_ts(tmem + kTC, a_hi, vdesc(kk, 0), idC, kk ? 1u : 0u);
           }
-          __syncwarp();
         }
-        if (lane == 0) TL(lt, 3);
+        if constexpr (kTerms > 1) {
+#pragma unroll
+          for (int kk = 0; kk < kS / 16; ++kk) mma_tf32_ts(tmem + kTC, tmem + kTS + uint32_t(kk) * 8u, vdesc(kk, 0), idC, 1u);
+        }
+        mma_commit(bar(PLO_FREE));
+      }
+      __syncwarp();
+    };
+    auto issue_pv_b = [&]() {  // P lo · V hi for keys 64-127
+      if (elect_one()) {
+        if constexpr (kTerms > 1) {
+#pragma unroll
+          for (int kk = kS / 16; kk < kS / 8; ++kk)
+            mma_tf32_ts(tmem + kTC, tmem + kTS + uint32_t(kk - kS / 16) * 8u, vdesc(kk, 0), idC, 1u);
+        }
+        mma_commit(bar(C_FULL));
+      }
+      __syncwarp();
+    };
+    auto issue_z = [&]() {
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < kDK / 8; ++kk)
+          mma3<kTerms, false>(tmem + kTS, tmem + kTOp + uint32_t(kk) * 8u, tmem + kTOp + 64u + uint32_t(kk) * 8u,
+                              whdesc(kk, 0), whdesc(kk, 1), idC, kk ? 1u : 0u);
+        mma_commit(bar(Z_FULL));
+      }
+      __syncwarp();
+    };
+    // the attention of one instance as a sequence of steps, each gated by barriers:
+    // 0: S (EXT) 1: P·V a (P_READY) 2: P·V b (P2_READY) 3: Z (WH_FULL, C_READY) 4: done
+    auto step_ready = [&](int st, uint32_t ph, bool block) {
+      auto test = [&](uint32_t b) {
+        if (block) {
+          mbar_wait(bar(b), ph);
+          return true;
+        }
+        return mbar_test_warp(bar(b), ph);
+      };
+      switch (st) {
+        case 0: return test(EXT);
+        case 1: return test(P_READY);
+        case 2: return test(P2_READY);
+        default: return test(WH_FULL) && test(C_READY);
+      }
+    };
+    auto step_issue = [&](int st) {
+      tc_fence_after();
+      if (st == 0) issue_s();
+      else if (st == 1) issue_pv_a();
+      else if (st == 2) issue_pv_b();
+      else issue_z();
+    };
+    uint32_t lt = 0;
+    if (rank != 0) {
+      // only this CTA's attention, in order
+      for (int t = pair0; t < p.pairs && !HS_DBG_HEAD_NOATT; t += npairs, ++lt)
+        for (int st = 0; st < 4; ++st) {
+          step_ready(st, lt & 1u, true);
+          step_issue(st);
+        }
+    } else {
+      uint32_t ia = 0, iw = 0;
+      int st = 4;  // step of the previous pair's attention (4: nothing pending)
+      for (int t = pair0; t < p.pairs; t += npairs, ++lt) {
+        if (lt > 0) {
+          // both CTAs have read the accumulator out: the next projection may overwrite it
+          mbar_wait(bar(EXT_PAIR), (lt - 1) & 1u);
+          st = HS_DBG_HEAD_NOATT ? 4 : 0;
+        }
+        if (lane == 0) TL(lt, 0);
+        for (int kb = 0; kb < nw; ++kb, ++iw) {
+          const int w = int(iw % kNW);
+          TW(lt, 8, mbar_wait(bar(WF + w), (iw / kNW) & 1u));
+#pragma unroll 1
+          for (int h = 0; h < kWK / kXK; ++h, ++ia) {
+            const int a = int(ia % kNA);
+            TW(lt, 9, mbar_wait(bar(AF + a), (ia / kNA) & 1u));
+            tc_fence_after();
+            if (elect_one()) {
+              const uint32_t b = base + kWs + uint32_t(w) * kWStage + uint32_t(h) * 64u;
+              const uint32_t ta = tmem + kTA + uint32_t(a) * 32u;
+#pragma unroll
+              for (int kk = 0; kk < kXK / 8; ++kk)
+                mma3<kTerms, true>(tmem + kTQ, ta + uint32_t(kk) * 8u, ta + 16u + uint32_t(kk) * 8u,
+                                   smem_desc(b + uint32_t(kk) * 32u), smem_desc(b + kWPlane + uint32_t(kk) * 32u), idP,
+                                   (kb | h | kk) ? 1u : 0u);
+              mma_commit_pair(bar(AE + a));
+              if (h == kWK / kXK - 1) mma_commit_pair(bar(WE + w));
+            }
+            __syncwarp();
+            // interleave the previous pair's attention MMAs as their operands become ready
+            while (st < 4 && step_ready(st, (lt - 1) & 1u, false)) step_issue(st++);
+          }
+        }
         if (elect_one()) mma_commit_pair(bar(ACC_FULL));
         __syncwarp();
-        // S = Q Kᵀ (K = 64)
-        mbar_wait(bar(A_READY), ph);
-        if (lane == 0) TL(lt, 4);
+        if (lane == 0) TL(lt, 1);
+        // the next extraction reuses the attention operands: finish the previous pair first
+        while (st < 4) {
+          step_ready(st, (lt - 1) & 1u, true);
+          step_issue(st++);
+        }
+      }
+      if (lt > 0 && !HS_DBG_HEAD_NOATT)  // the last pair's attention
+        for (st = 0; st < 4; ++st) {
+          step_ready(st, (lt - 1) & 1u, true);
+          step_issue(st);
+        }
+    }
+  } else if (warp >= 4 && warp < 8) {
+    // ------------------------------------------------------------ converters: X tile -> TMEM A stage
+    const int q = warp & 3, row = q * 32 + lane;
+    const uint32_t lane_base = tmem + (uint32_t(q * 32) << 16);
+    const uint32_t swz = uint32_t((row >> 1) & 3);
+    uint32_t it = 0, lt = 0;
+    for (int t = pair0; t < p.pairs; t += npairs, ++lt) {
+      for (int kb = 0; kb < nx; ++kb, ++it) {
+        const int x = int(it % kNX), a = int(it % kNA);
+        if (q == 0) {
+          TW(lt, 10, mbar_wait(bar(XF + x), (it / kNX) & 1u));
+          TW(lt, 11, mbar_wait(bar(AE + a), ((it / kNA) & 1u) ^ 1u));
+        } else {
+          mbar_wait(bar(XF + x), (it / kNX) & 1u);
+          mbar_wait(bar(AE + a), ((it / kNA) & 1u) ^ 1u);
+        }
         tc_fence_after();
-        if (elect_one()) {
+#if HS_DBG_TIMELINE
+        const long long c_conv0 = clock64();
+#endif
+        if (!HS_DBG_HEAD_NOCONV) {
+          const uint32_t src = base + kXs + uint32_t(x) * kXTile + uint32_t(row) * 64u;
+          uint32_t v[16];
 #pragma unroll
-          for (int kk = 0; kk < kDK / 8; ++kk) {
-            const uint32_t kbo = uint32_t(kk >> 2) * 16384u + uint32_t(kk & 3) * 32u;
-            mma3<kTerms>(tmem, tmem + kTQ + uint32_t(kk) * 8u, tmem + kTQ + 64u + uint32_t(kk) * 8u,
-                         base + kKop + kbo, base + kKop + 32768u + kbo, idS, kk ? 1u : 0u);
+          for (int c = 0; c < 4; ++c) {  // SWIZZLE_64B: 16-byte chunk c of row r sits at chunk c ^ ((r >> 1) & 3)
+            const float4 f = lds128(src + ((uint32_t(c) ^ swz) << 4));
+            v[4 * c] = __float_as_uint(f.x);
+            v[4 * c + 1] = __float_as_uint(f.y);
+            v[4 * c + 2] = __float_as_uint(f.z);
+            v[4 * c + 3] = __float_as_uint(f.w);
           }
-          mma_commit_pair(bar(S_FULL));
+          st_split16<kTerms>(lane_base + kTA + uint32_t(a) * 32u, 16u, v);
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         }
+#if HS_DBG_TIMELINE
+        const long long c_conv1 = clock64();
+#endif
+        tc_fence_before();
         __syncwarp();
-        // C = P V (K = 128 keys)
-        mbar_wait(bar(V_READY), ph);
-        mbar_wait(bar(P_READY), ph);
-        if (lane == 0) TL(lt, 5);
-        tc_fence_after();
-        if (elect_one()) {
-#pragma unroll
-          for (int kk = 0; kk < kS / 8; ++kk) {
-            const uint32_t kbo = uint32_t(kk >> 2) * 8192u + uint32_t(kk & 3) * 32u;
-            mma3<kTerms>(tmem, tmem + kTQ + uint32_t(kk) * 8u, tmem + kTQ + 128u + uint32_t(kk) * 8u,
-                         base + kVop + kbo, base + kVop + 32768u + kbo, idC, kk ? 1u : 0u);
-          }
-          mma_commit_pair(bar(O_FULL));
+        if (lane == 0) {
+          mbar_arrive(bar(XE + x));
+          // relaxed: the stage's TMEM stores are complete (tcgen05.wait::st above); a
+          // release arrive at cluster scope costs ~1k cycles per stage in this thread
+          asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(leader(AF + a))
+                       : "memory");
         }
-        __syncwarp();
-        // Z = C Wh (K = 64)
-        if (!wh) {
-          mbar_wait(bar(WH_FULL), 0);
-          wh = true;
+#if HS_DBG_TIMELINE
+        if (blockIdx.x == 0 && lt < 8 && lane == 0 && q == 0) {
+          g_head_timeline[lt * 16 + 14] += c_conv1 - c_conv0;
+          g_head_timeline[lt * 16 + 15] += clock64() - c_conv1;
         }
-        mbar_wait(bar(C_READY), ph);
-        if (lane == 0) TL(lt, 6);
-        tc_fence_after();
-        if (elect_one()) {
-#pragma unroll
-          for (int kk = 0; kk < kDK / 8; ++kk) {
-            const uint32_t kbo = uint32_t(kk >> 2) * 4096u + uint32_t(kk & 3) * 32u;
-            mma3<kTerms>(tmem + kTZ, tmem + kTQ + uint32_t(kk) * 8u, tmem + kTQ + 64u + uint32_t(kk) * 8u,
-                         base + kWh + kbo, base + kWh + 8192u + kbo, idZ, kk ? 1u : 0u);
-          }
-          mma_commit_pair(bar(Z_FULL));
-        }
-        __syncwarp();
+#endif
       }
     }
-  } else if (warp >= 4 && warp < 12) {
-    // ------------------------------------------------------------ converters (phase 1) / row warps (phase 2)
-    const int q = warp & 3, g = (warp - 4) >> 2, row = q * 32 + lane;
+  } else if (warp >= 8) {
+    // ------------------------------------------------------------ attention warps (this CTA's instance)
+    const int q = warp & 3, g = (warp - 8) >> 2, row = q * 32 + lane;
     const uint32_t lane_base = tmem + (uint32_t(q * 32) << 16);
-    const uint32_t mine = base + kExch + uint32_t(q * 2 + g) * 256u + uint32_t(lane) * 4u;
-    const uint32_t other = base + kExch + uint32_t(q * 2 + (g ^ 1)) * 256u + uint32_t(lane) * 4u;
+    const uint32_t mine = base + kXch + uint32_t(q * 2 + g) * 256u + uint32_t(lane) * 4u;
+    const uint32_t other = base + kXch + uint32_t(q * 2 + (g ^ 1)) * 256u + uint32_t(lane) * 4u;
     const float sl = p.scale * 1.4426950408889634f;
-    const int col0 = int(rank) * kS;  // this CTA's block of S (its own keys)
-    // one K-block of X rows -> TMEM A stage (iteration `i` of the stage rings)
-    auto convert = [&](uint32_t i, int kb) {
-      (void)g;
-      const int s = int(i % kNS), o = int(i % kNO);
-      mbar_wait(bar(ST_FULL + s), (i / kNS) & 1u);
-      mbar_wait(bar(OP_EMPTY + o), ((i / kNO) & 1u) ^ 1u);
+    const bool full = p.S >= kS;  // uniform: no key masking
+    uint32_t lt = 0;
+    for (int t = pair0; t < p.pairs; t += npairs, ++lt) {
+      const uint32_t ph = lt & 1u;
+      const int inst = 2 * t + int(rank);
+      // ---- extraction (the accumulator is free for the next projection afterwards)
+      mbar_wait(bar(ACC_FULL), ph);
       tc_fence_after();
-      const uint32_t sa = base + kU + uint32_t(s) * kStaging;
-      const uint32_t ta = lane_base + kTStage + uint32_t(o) * 64u;
-      (void)kb;
+      if (warp == 8 && lane == 0) TL(lt, 2);
+      if (!HS_DBG_HEAD_NOATT) {
+        uint32_t r[32];
+        // Q columns [32g, 32g+32) -> tf32 hi [256 + 32g) / lo [320 + 32g)
+        tmem_ld32(lane_base + kTQ + uint32_t(32 * g), r);
+        st_split16<kTerms>(lane_base + kTOp + uint32_t(32 * g), 64u, r);
+        st_split16<kTerms>(lane_base + kTOp + uint32_t(32 * g + 16), 64u, r + 16);
+        // K row (key = row), d in [32g, 32g+32) -> K-major SW128 k-block g (hi, lo at +32 KB)
+        tmem_ld32(lane_base + kTK + uint32_t(32 * g), r);
 #pragma unroll
-      for (int hh = 0; hh < (HS_DBG_HEAD_NOCONV ? 0 : 2); ++hh) {
-        uint32_t x[16], hi[16], lo[16];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const float4 v = lds128(sa + sw128(row, 4 * hh + c));
-          x[4 * c] = __float_as_uint(v.x); x[4 * c + 1] = __float_as_uint(v.y);
-          x[4 * c + 2] = __float_as_uint(v.z); x[4 * c + 3] = __float_as_uint(v.w);
+        for (int c = 0; c < 8; ++c) {
+          const float4 x = make_float4(__uint_as_float(r[4 * c]), __uint_as_float(r[4 * c + 1]),
+                                       __uint_as_float(r[4 * c + 2]), __uint_as_float(r[4 * c + 3]));
+          const float4 h = make_float4(tf32_rna(x.x), tf32_rna(x.y), tf32_rna(x.z), tf32_rna(x.w));
+          const uint32_t dst = base + kKop + uint32_t(g) * 16384u + sw128(row, c);
+          sts128(dst, h);
+          if constexpr (kTerms > 1) sts128(dst + 32768u, make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w));
         }
-        split_row16<kTerms>(x, hi, lo);
-        tmem_st16(ta + uint32_t(16 * hh), hi);
-        if constexpr (kTerms > 1) tmem_st16(ta + 32u + uint32_t(16 * hh), lo);
+        // V row (key = row: k-block q, key lane), d in [32g, 32g+32) -> Vᵀ K-major SW128 [64 d][32 keys]
+        tmem_ld32(lane_base + kTV + uint32_t(32 * g), r);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float x = __uint_as_float(r[j]);
+          const float h = tf32_rna(x);
+          const uint32_t dst = base + kVop + uint32_t(q) * 8192u + sw128(32 * g + j, lane >> 2) + uint32_t(lane & 3) * 4u;
+          sts32(dst, h);
+          if constexpr (kTerms > 1) sts32(dst + 32768u, x - h);
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       }
-      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        mbar_arrive(bar(ST_EMPTY + s));
-        mbar_arrive_cluster(leader(OP_FULL + o));
+        mbar_arrive(bar(EXT));
+        mbar_arrive_cluster(leader(EXT_PAIR));
       }
-    };
-    uint32_t it = 0, lt = 0;
-    // K-blocks of the current pair this group converted during the last pair's phase 2
-    bool pre0 = false, pre3 = false;
-    int pre0k = 0;  // which K-block went to stage 0 early
-    for (int t = pair0; t < p.pairs; t += npairs, ++lt) {
-      const uint32_t ph = lt & 1u;
-      // ---- phase 1: split this CTA's X rows into the TMEM A stages (every other K-block)
-      for (int kb = 0; kb < nk; ++kb, ++it) {
-        if (int(it % kConv) != g || (kb == pre0k && pre0) || (kb == 3 && pre3)) continue;
-        convert(it, kb);
-      }
-      pre0 = pre3 = false;
-      // ---- phase 2 (A): operands of S = Q Kᵀ and C = P V, split across 12 warps:
-      //      g = 0: Q (64 columns) -> tf32 hi [256, 320) / lo [320, 384) in TMEM
-      //      g = 1: K -> K-major smem hi/lo, and Vᵀ for d in [0, 32)
-      //      (warps 12-15: Vᵀ for d in [32, 64))
-      if (warp == 4 && lane == 0) TL(lt, 7);
-      mbar_wait(bar(ACC_FULL), ph);
-      if (warp == 4 && lane == 0) TL(lt, 8);
-      tc_fence_after();
-      if (g == 0) {  // Q -> TMEM A operand
-#pragma unroll 1
-        for (int cb = 0; cb < 2; ++cb) {
-          uint32_t r[32], hi[16], lo[16];
-          tmem_ld32(lane_base + uint32_t(cb * 32), r);
-#pragma unroll
-          for (int hh = 0; hh < 2; ++hh) {
-            split_row16<kTerms>(r + 16 * hh, hi, lo);
-            const uint32_t col = kTQ + uint32_t(cb * 32 + hh * 16);
-            tmem_st16(lane_base + col, hi);
-            tmem_st16(lane_base + col + 64u, lo);
-          }
-        }
-        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(leader(A_READY));
-      } else {  // K, then half of Vᵀ
-        store_k_operand(base, lane_base, row);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(leader(A_READY));
-        store_vt_operand(base, lane_base, q, lane, 0);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(leader(V_READY));
-      }
-      // ---- (B) softmax over this CTA's S block, columns [col0 + 64g, +64) in registers
+      if (HS_DBG_HEAD_NOATT) continue;
+      // ---- softmax over keys [64g, 64g+64) of this row, S in registers
       mbar_wait(bar(S_FULL), ph);
-      if (warp == 4 && lane == 0) TL(lt, 9);
       tc_fence_after();
+      if (warp == 8 && lane == 0) TL(lt, 3);
       uint32_t r0[32], r1[32];
-      tmem_ld32_nowait(lane_base + uint32_t(col0 + g * 64), r0);
-      tmem_ld32_nowait(lane_base + uint32_t(col0 + g * 64 + 32), r1);
+      tmem_ld32_nowait(lane_base + kTS + uint32_t(64 * g), r0);
+      tmem_ld32_nowait(lane_base + kTS + uint32_t(64 * g + 32), r1);
       tmem_ld_wait(r0);
       tmem_ld_dep(r1);
-      const bool full = p.S >= kS;  // warp-uniform: no key masking
-      float mx = full ? row_max<false>(r0, r1, 0, p.S, p.scale) : row_max<true>(r0, r1, g * 64, p.S, p.scale);
+      float mx = full ? row_max<false>(r0, r1, 0, p.S, p.scale) : row_max<true>(r0, r1, 64 * g, p.S, p.scale);
       sts32(mine, mx);
       named_bar(1u + uint32_t(q), 64u);
       mx = fmaxf(mx, lds32(other));
       const float ml = mx * 1.4426950408889634f;
-      const float sum = full ? row_exp<false>(r0, r1, 0, p.S, sl, ml) : row_exp<true>(r0, r1, g * 64, p.S, sl, ml);
+      const float sum = full ? row_exp<false>(r0, r1, 0, p.S, sl, ml) : row_exp<true>(r0, r1, 64 * g, p.S, sl, ml);
       sts32(mine + 128u, sum);
       named_bar(1u + uint32_t(q), 64u);
       const float s_other = lds32(other + 128u);
       const float inv = 1.f / (g == 0 ? sum + s_other : s_other + sum);
-#pragma unroll
-      for (int hh = 0; hh < 4; ++hh) {
+      // P = e · inv -> hi to [256 + 64g); lo kept in r0/r1 (keys 0-63 also stored now)
+      auto p_chunk = [&](uint32_t(&r)[32], int off, int hh) {
         uint32_t hi[16], lo[16];
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
-          const float x = __uint_as_float(hh < 2 ? r0[(hh & 1) * 16 + e] : r1[(hh & 1) * 16 + e]) * inv;
+          const float x = __uint_as_float(r[off + e]) * inv;
           const float h = tf32_rna(x);
           hi[e] = __float_as_uint(h);
           lo[e] = __float_as_uint(x - h);
+          r[off + e] = lo[e];
         }
-        const uint32_t col = kTQ + uint32_t(g * 64 + hh * 16);
-        tmem_st16(lane_base + col, hi);
-        tmem_st16(lane_base + col + 128u, lo);
-      }
+        tmem_st16(lane_base + kTOp + uint32_t(64 * g + 16 * hh), hi);
+        if (kTerms > 1 && g == 0) tmem_st16(lane_base + kTS + uint32_t(16 * hh), lo);
+      };
+      p_chunk(r0, 0, 0);
+      p_chunk(r0, 16, 1);
+      p_chunk(r1, 0, 2);
+      p_chunk(r1, 16, 3);
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(leader(P_READY));
-      // The next pair's first K-block goes to A stage 0 = TMEM [192, 256), part of S:
-      // free once every warp of this lane quarter has read S (both passed the
-      // exchange barriers above). Convert it while P·V runs (its X tile was loaded
-      // after S_FULL into the K operand's smem).
-      if constexpr (kConv == 2) {
-        if (t + npairs < p.pairs && int(it & 1u) == g && it % kNO == 0) {
-          convert(it, 0);
-          pre0 = true;
-          pre0k = 0;
-        }
-      } else {
-        // the first of the next pair's K-blocks 0-2 that maps to stage 0 (group 0 owns
-        // it, as kNO == kConv), if its X stage lies in the K operand's smem
-        for (uint32_t j = 0; j < 3 && int(j) < nk; ++j)
-          if ((it + j) % kNO == 0) {
-            if (t + npairs < p.pairs && g == 0 && (it + j) % kNS < 4) {
-              convert(it + j, int(j));
-              pre0 = true;
-              pre0k = int(j);
-            }
-            break;
-          }
-      }
-      // ---- (C) C columns [64r + 32g, +32) -> tf32 hi [256, 320) / lo [320, 384)
-      mbar_wait(bar(O_FULL), ph);
-      if (warp == 4 && lane == 0) TL(lt, 10);
-      tc_fence_after();
-      {
-        uint32_t r[32], hi[16], lo[16];
-        tmem_ld32(lane_base + uint32_t(int(rank) * kDK + g * 32), r);
-#pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          split_row16<kTerms>(r + 16 * hh, hi, lo);
-          const uint32_t col = kTQ + uint32_t(g * 32 + hh * 16);
-          tmem_st16(lane_base + col, hi);
-          tmem_st16(lane_base + col + 64u, lo);
-        }
-      }
-      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(leader(C_READY));
-      // The next pair's K-block 3 goes to A stage 3 = TMEM [384, 448), P lo's
-      // columns: free once P·V has run (O_FULL, waited above). Its X tile was
-      // loaded after S_FULL like the first ones.
-      if constexpr (kConv == 2) {
-        if (t + npairs < p.pairs && nk > 3 && int((it + 3u) & 1u) == g && it % kNO == 0) {
-          convert(it + 3u, 3);
-          pre3 = true;
-        }
-      }
-      // The next pair's A stages 1-2 overlap C hi/lo [256, 384): convert only after
-      // the Z MMA has read them. The Z accumulator is drained by warps 12-15.
-      mbar_wait(bar(Z_FULL), ph);
-      if (warp == 4 && lane == 0) TL(lt, 11);
-    }
-  } else if (warp >= 12) {
-    // ------------------------------------------------------------ operand / Z warps (phase 2)
-    // (HS_HEAD_CONV3: also converter group 2 in phase 1)
-    const int q = warp & 3;
-    const uint32_t lane_base = tmem + (uint32_t(q * 32) << 16);
-    const uint32_t stage = base + kEpi + uint32_t(q) * 8192u;
-    uint32_t lt = 0, it = 0;
-    const int row = q * 32 + lane;
-    (void)row;
-    for (int t = pair0; t < p.pairs; t += npairs, ++lt) {
-      const uint32_t ph = lt & 1u;
-      const int inst = 2 * t + int(rank);
-      if constexpr (kConv == 3) {
-        for (int kb = 0; kb < nk; ++kb, ++it) {
-          if (it % 3u != 2u) continue;
-          const int s = int(it % kNS), o = int(it % kNO);
-          mbar_wait(bar(ST_FULL + s), (it / kNS) & 1u);
-          mbar_wait(bar(OP_EMPTY + o), ((it / kNO) & 1u) ^ 1u);
+      if (lane == 0) mbar_arrive(bar(P_READY));
+      if (g == 1) {
+        // keys 64-127: P lo replaces keys 0-63's once the MMAs reading those are done
+        if constexpr (kTerms > 1) {
+          mbar_wait(bar(PLO_FREE), ph);
           tc_fence_after();
-          const uint32_t sa = base + kU + uint32_t(s) * kStaging;
-          const uint32_t ta = lane_base + kTStage + uint32_t(o) * 64u;
+          auto lo_chunk = [&](const uint32_t(&r)[32], int off, int hh) {
+            uint32_t lo[16];
 #pragma unroll
-          for (int hh = 0; hh < 2; ++hh) {
-            uint32_t x[16], hi[16], lo[16];
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              const float4 v = lds128(sa + sw128(row, 4 * hh + c));
-              x[4 * c] = __float_as_uint(v.x); x[4 * c + 1] = __float_as_uint(v.y);
-              x[4 * c + 2] = __float_as_uint(v.z); x[4 * c + 3] = __float_as_uint(v.w);
-            }
-            split_row16<kTerms>(x, hi, lo);
-            tmem_st16(ta + uint32_t(16 * hh), hi);
-            if constexpr (kTerms > 1) tmem_st16(ta + 32u + uint32_t(16 * hh), lo);
-          }
+            for (int e = 0; e < 16; ++e) lo[e] = r[off + e];
+            tmem_st16(lane_base + kTS + uint32_t(16 * hh), lo);
+          };
+          lo_chunk(r0, 0, 0);
+          lo_chunk(r0, 16, 1);
+          lo_chunk(r1, 0, 2);
+          lo_chunk(r1, 16, 3);
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
           tc_fence_before();
-          __syncwarp();
-          if (lane == 0) {
-            mbar_arrive(bar(ST_EMPTY + s));
-            mbar_arrive_cluster(leader(OP_FULL + o));
-          }
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar(P2_READY));
       }
-      mbar_wait(bar(ACC_FULL), ph);
+      // ---- C columns [32g, 32g+32) -> tf32 hi [256 + 32g) / lo [320 + 32g) (P is consumed)
+      mbar_wait(bar(C_FULL), ph);
       tc_fence_after();
-      if (warp == 12 && lane == 0) TL(lt, 12);
-      store_vt_operand(base, lane_base, q, lane, 1);
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      if (warp == 8 && lane == 0) TL(lt, 4);
+      {
+        uint32_t c[32];
+        tmem_ld32(lane_base + kTC + uint32_t(32 * g), c);
+        st_split16<kTerms>(lane_base + kTOp + uint32_t(32 * g), 64u, c);
+        st_split16<kTerms>(lane_base + kTOp + uint32_t(32 * g + 16), 64u, c + 16);
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
       __syncwarp();
-      if (warp == 12 && lane == 0) TL(lt, 13);
-      if (lane == 0) mbar_arrive_cluster(leader(V_READY));
-      // Z accumulator [448, 512) -> SW128 staging (2 x [32 rows][32 cols]) -> TMA store
+      if (lane == 0) mbar_arrive(bar(C_READY));
+      // ---- Z columns [32g, 32g+32) -> global
       mbar_wait(bar(Z_FULL), ph);
       tc_fence_after();
-#pragma unroll 1
-      for (int cb = 0; cb < 2; ++cb) {
-        uint32_t r[32];
-        tmem_ld32(lane_base + kTZ + uint32_t(cb * 32), r);
-        const uint32_t buf = stage + uint32_t(cb) * 4096u;
-        if (lt > 0) {  // the last pair's store of this buffer has read it
-          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-          __syncwarp();
-        }
+      if (warp == 8 && lane == 0) TL(lt, 5);
+      {
+        uint32_t z[32];
+        tmem_ld32(lane_base + kTS + uint32_t(32 * g), z);
+        if (inst < p.batch && row < p.S) {
+          float4* out = reinterpret_cast<float4*>(p.Z + int64_t(inst) * p.sZ + int64_t(row) * p.ldz + 32 * g);
 #pragma unroll
-        for (int c = 0; c < 8; ++c)
-          sts128(buf + uint32_t(lane) * 128u + (uint32_t(c ^ (lane & 7)) << 4),
-                 make_float4(__uint_as_float(r[4 * c]), __uint_as_float(r[4 * c + 1]), __uint_as_float(r[4 * c + 2]),
-                             __uint_as_float(r[4 * c + 3])));
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) {
-          if (inst < p.batch) tma_store_3d(&tmZ, buf, cb * 32, q * 32, inst);
-          else asm volatile("cp.async.bulk.commit_group;" ::: "memory");  // keep the group count per buffer
+          for (int j4 = 0; j4 < 8; ++j4)
+            out[j4] = make_float4(__uint_as_float(z[4 * j4]), __uint_as_float(z[4 * j4 + 1]),
+                                  __uint_as_float(z[4 * j4 + 2]), __uint_as_float(z[4 * j4 + 3]));
         }
       }
       tc_fence_before();
     }
-    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   tc_fence_before();
   cluster_sync_all();
@@ -659,11 +675,33 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// 3-D fp32 tensor map with 64-byte swizzle (16-element boxes along the contiguous dim)
+bool make_map_sw64(CUtensorMap* m, const void* ptr, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1, uint64_t s2,
+                   uint32_t b0, uint32_t b1) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {d0, d1, d2};
+  cuuint64_t strides[2] = {s1, s2};
+  cuuint32_t box[3] = {b0, b1, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(ptr), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 }  // namespace
 
 }  // namespace hs
 
-// timing experiment only: copy the debug timeline (8 x 16 clock64 stamps) to host
+// timing experiment only: reset / copy the debug timeline (8 x 16 slots)
+extern "C" int hs_debug_head_timeline_reset(void) {
+#if HS_DBG_TIMELINE
+  static const long long zeros[128] = {};
+  return cudaMemcpyToSymbol(hs::g_head_timeline, zeros, sizeof(zeros)) == cudaSuccess ? 0 : 1;
+#else
+  return 1;
+#endif
+}
 extern "C" int hs_debug_head_timeline(long long* out) {
 #if HS_DBG_TIMELINE
   return cudaMemcpyFromSymbol(out, hs::g_head_timeline, sizeof(long long) * 128) == cudaSuccess ? 0 : 1;
@@ -676,17 +714,17 @@ extern "C" int hs_debug_head_timeline(long long* out) {
 namespace hs {
 
 bool head_fused_supported(const HeadArgs& a) {
-  if (a.S < 1 || a.S > kS || a.dk != kDK || a.D < BK || a.D % BK || a.batch < 1 || !a.Wqkv || !a.Wh) return false;
+  if (a.S < 1 || a.S > kS || a.dk != kDK || a.D < kWK || a.D % kWK || a.batch < 1 || !a.Wqkv || !a.Wh) return false;
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
   if (!al16(a.X) || !al16(a.Z) || !al16(a.Wqkv) || !al16(a.Wh)) return false;
   const int64_t ld = a.ldz ? a.ldz : kDK;
   if ((a.sX | a.sZ | ld) & 3) return false;
-  return encode_fn() != nullptr;
+  return tc::encode_fn() != nullptr;
 }
 
 cudaError_t head_fused(const HeadArgs& a, int terms, cudaStream_t s) {
   if (!head_fused_supported(a)) return cudaErrorInvalidValue;
-  auto kernel = terms > 1 ? head_pair_kernel<3> : head_pair_kernel<1>;
+  auto kernel = terms > 1 ? head_kernel<3> : head_kernel<1>;
   static std::once_flag once3, once1;
   static cudaError_t err3 = cudaSuccess, err1 = cudaSuccess;
   std::call_once(terms > 1 ? once3 : once1, [&] {
@@ -694,15 +732,14 @@ cudaError_t head_fused(const HeadArgs& a, int terms, cudaStream_t s) {
   });
   if (cudaError_t e = terms > 1 ? err3 : err1) return e;
   const uint64_t S = uint64_t(a.S), D = uint64_t(a.D), B = uint64_t(a.batch);
-  const uint64_t ldz = uint64_t(a.ldz ? a.ldz : kDK);
-  CUtensorMap mX, mW, mWh, mZ;
-  bool ok = make_map(&mX, a.X, D, S, B, D * 4, uint64_t(a.sX ? a.sX : S * D) * 4, BK, BM, true) &&
-            make_map(&mW, a.Wqkv, D, kN, 2, D * 4, uint64_t(kN) * D * 4, BK, kN / 2, true) &&
-            make_map(&mWh, a.Wh, kDK, kDK, 2, kDK * 4, uint64_t(kDK * kDK) * 4, BK, kDK / 2, true) &&
-            make_map(&mZ, a.Z, kDK, S, B, ldz * 4, uint64_t(a.sZ ? a.sZ : S * ldz) * 4, 32, 32, true);
+  CUtensorMap mX, mW, mWh;
+  const bool ok = make_map_sw64(&mX, a.X, D, S, B, D * 4, uint64_t(a.sX ? a.sX : S * D) * 4, kXK, kS) &&
+                  tc::make_map(&mW, a.Wqkv, D, kN, 2, D * 4, uint64_t(kN) * D * 4, kWK, kN / 2, true) &&
+                  tc::make_map(&mWh, a.Wh, kDK, kDK, 2, kDK * 4, uint64_t(kDK * kDK) * 4, 32, kDK, true);
   if (!ok) return cudaErrorInvalidValue;
-  HeadParams p{a.S, a.D, a.batch, (a.batch + 1) / 2, a.scale};
-  const int max_pairs = num_sms() / 2;
+  const int64_t ldz = a.ldz ? a.ldz : kDK;
+  HeadParams p{a.S, a.D, a.batch, (a.batch + 1) / 2, a.scale, a.Z, a.sZ ? a.sZ : int64_t(S) * ldz, ldz};
+  const int max_pairs = tc::num_sms() / 2;
   const int pairs = p.pairs < max_pairs ? p.pairs : max_pairs;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2 * pairs);
@@ -716,7 +753,7 @@ cudaError_t head_fused(const HeadArgs& a, int terms, cudaStream_t s) {
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kernel, mX, mW, mWh, mZ, p);
+  return cudaLaunchKernelEx(&cfg, kernel, mX, mW, mWh, p);
 }
 
 }  // namespace hs

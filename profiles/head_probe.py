@@ -2,6 +2,7 @@
 vs the two launches it replaces (grouped Q/K/V pair GEMM -> attn_head), per batch.
 usage: python profiles/head_probe.py [batch ...]"""
 import ctypes
+import os
 import sys
 
 import numpy as np
@@ -77,7 +78,7 @@ for batch in [int(b) for b in sys.argv[1:]] or (64, 148, 296, 512):
     torch.cuda.synchronize()
     t_qkv = timed(lambda: _native.check(L.hs_launch(st, 0, ctypes.byref(g), 0, batch)))
     t_att = timed(lambda: _native.check(L.hs_launch(st, 9, ctypes.byref(aa), 0, batch)))
-    t_head = timed(lambda: _native.check(L.hs_launch(st, 10, ctypes.byref(h), 0, batch)))
+    t_head = timed(lambda: _native.check(L.hs_launch(st, 10, ctypes.byref(h), int(os.environ.get('HEAD_MATH', '0')), batch)))
     flops = batch * (2.0 * S * 192 * D + 2.0 * S * S * 64 * 2 + 2.0 * S * 64 * 64)
     print(f"batch={batch:4d}  grouped QKV {t_qkv:7.2f} us + attn_head {t_att:6.2f} us = {t_qkv + t_att:7.2f} us | "
           f"head {t_head:7.2f} us  ({flops / t_head / 1e6:6.1f} TFLOP/s algorithmic)", flush=True)

@@ -1,7 +1,7 @@
-"""Per-pair phase timeline of the whole-head kernel (needs a library built with
--DHS_DBG_TIMELINE=1, e.g. variants/build.sh timeline "-DHS_DBG_TIMELINE=1" and
-HETSIM_LIB=variants/lib_timeline.so). clock64 cycles relative to pair 0's start.
-usage: python profiles/head_timeline.py [batch=296]"""
+"""Per-instance phase timeline of the whole-head kernel, CTA 0 (needs a library built
+with -DHS_DBG_TIMELINE=1, e.g. variants/build.sh timeline "-DHS_DBG_TIMELINE=1" and
+HETSIM_LIB=variants/lib_timeline.so). clock64 cycles relative to instance 0's start.
+usage: python profiles/head_timeline.py [batch=592]"""
 import ctypes
 import sys
 
@@ -15,7 +15,7 @@ from tests.test_gpu_kernels import _qkv_planes  # noqa: E402
 
 L = _native.lib()
 S, D = 128, 512
-batch = int(sys.argv[1]) if len(sys.argv) > 1 else 296
+batch = int(sys.argv[1]) if len(sys.argv) > 1 else 592
 X = torch.randn(batch, S * D, device="cuda")
 Ws = [torch.randn(D * 64, device="cuda") / np.sqrt(D) for _ in range(3)]
 Wh = torch.randn(64 * 64, device="cuda") / 8
@@ -33,13 +33,18 @@ torch.cuda.synchronize()
 for _ in range(3):
     _native.check(L.hs_launch(stream(), 10, ctypes.byref(h), 0, batch))
 _native.check(L.hs_stream_sync(stream()))
+assert L.hs_debug_head_timeline_reset() == 0, "library built without HS_DBG_TIMELINE"
+_native.check(L.hs_launch(stream(), 10, ctypes.byref(h), 0, batch))
+_native.check(L.hs_stream_sync(stream()))
 buf = (ctypes.c_longlong * 128)()
 L.hs_debug_head_timeline.argtypes = [ctypes.c_void_p]
 assert L.hs_debug_head_timeline(ctypes.cast(buf, ctypes.c_void_p)) == 0, "library built without HS_DBG_TIMELINE"
 tl = np.array(buf[:], dtype=np.int64).reshape(8, 16)
-names = ["mma:start", "mma:z_done", "mma:op_full0", "mma:qkv_issued", "mma:a_ready", "mma:p_ready", "mma:c_ready",
-         "row:tile_start", "row:acc_full", "row:s_full", "row:o_full", "row:z_full", "kv:acc_full", "kv:done"]
+names = ["mma:proj_start", "mma:proj_issued", "att:acc_full", "att:s_full", "att:c_full", "att:z_stored"]
+waits = {8: "mma_wait_W", 9: "mma_wait_A", 10: "conv_wait_X", 11: "conv_wait_Aempty", 12: "xtma_wait_empty",
+         13: "wtma_wait_empty", 14: "conv_work", 15: "conv_signal"}
 t0 = tl[0, 0]
-tiles = (batch + 1) // 2 // 74 + (1 if ((batch + 1) // 2) % 74 else 0)
-for t in range(min(tiles, 8)):
-    print(f"pair-tile {t}: " + "  ".join(f"{n}={tl[t, k] - t0}" for k, n in enumerate(names)))
+per_cta = -(-batch // 148)
+for t in range(min(per_cta, 8)):
+    print(f"instance {t}: " + "  ".join(f"{n}={tl[t, k] - t0}" for k, n in enumerate(names)))
+    print("    waits: " + "  ".join(f"{n}={tl[t, k]}" for k, n in waits.items()))

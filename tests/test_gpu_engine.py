@@ -127,12 +127,15 @@ def test_chain_rewrites_match_oracle(math, oracle_mod):
         assert _normwise(chained[key][i], ref[key][i]) <= TOL
         assert _normwise(chained[key][i], grouped[key][i]) <= 1e-5
     # fuse=3: each head's grouped Q/K/V launch is absorbed into a whole-head launch
-    # (tf32 planes only); HS_OP_HEAD is bit-identical to the two launches it replaces
+    # (tf32 planes only); HS_OP_HEAD accumulates the P·V terms in another order, so it
+    # agrees with the two launches it replaces to fp32 rounding
     whole, _, plan3 = _run_gpu(text, params, arrays, n, mode="graph", batch=2, fuse=3, math=math)
     heads = 16 if math == "tf32x3" else 0
     assert plan3["chain_rewrites"].get("head_fused", 0) == heads
     assert plan3["launches_per_batch"] == plan["launches_per_batch"] - heads
-    assert np.array_equal(whole[key], chained[key])
+    for i in range(n):
+        assert _normwise(whole[key][i], ref[key][i]) <= TOL
+        assert _normwise(whole[key][i], chained[key][i]) <= 1e-5
 
 
 @pytest.mark.parametrize("mode", ["graph", "dynamic"])

@@ -354,12 +354,15 @@ def _grouped_qkv(X, Ws, planes, outs, S, D, batch):
 
 
 @pytest.mark.parametrize("S,batch,D", [(128, 1, 512), (128, 4, 512), (128, 7, 512), (100, 3, 512), (128, 300, 512),
-                                       (128, 5, 256), (128, 3, 96), (64, 9, 1024)])
-def test_head_fused_bit_identical_to_grouped_qkv_and_attn_head(S, batch, D):
-    """HS_OP_HEAD (projection + attention in one CTA-pair kernel, Q/K/V never leave
-    the SM) equals the two launches it replaces: the grouped Q/K/V pair GEMM writing
-    Q, K, V to HBM, then the fused attention head."""
-    from tests.gpu_util import launch, split_weights
+                                       (128, 5, 256), (128, 3, 96), (64, 9, 1024), (128, 149, 512), (128, 445, 512)])
+def test_head_fused_matches_grouped_qkv_and_attn_head(S, batch, D, oracle_mod):
+    """HS_OP_HEAD (projection + attention of two instances in flight per SM, Q/K/V
+    never leave the SM) against the two launches it replaces — the grouped Q/K/V
+    GEMM writing Q, K, V to HBM, then the fused attention head — and, on sampled
+    instances (first, last, and both sides of the 148-CTA wrap), the CPU oracle.
+    The P·V terms are accumulated in another order, so the two agree to fp32
+    rounding, not bit for bit."""
+    from tests.gpu_util import launch, normwise, split_weights
     import torch
     X = _t(_rand(80, (batch, S * D)))
     Ws = [_t((_rand(81 + m, (D * 64,)) * np.float32(1 / np.sqrt(D))).astype(np.float32)) for m in range(3)]
@@ -372,8 +375,19 @@ def test_head_fused_bit_identical_to_grouped_qkv_and_attn_head(S, batch, D):
     launch("attn_head", [Q, K, V, Wh], Z0, [S, 64, 64], fparam=(0.125, 1e-5), batch=batch, aux=ph)
     Z1 = torch.full((batch, S * 64), -7.0, device="cuda")
     _head_launch(X, pq, ph, Z1, S, D, batch)
-    diff = (Z0 - Z1).abs().max().item()
-    assert torch.equal(Z0, Z1), f"max |diff| {diff:.3e}"
+    z0, z1 = Z0.cpu().numpy(), Z1.cpu().numpy()
+    for b in range(batch):
+        assert normwise(z1[b], z0[b]) <= 1e-5, b
+    idx = sorted({0, batch - 1, min(batch - 1, 147), min(batch - 1, 148)})
+    x = X.cpu().numpy()[idx]
+    proj = []
+    for W in Ws:
+        out = np.empty((len(idx), S * 64), np.float32)
+        oracle_mod.run_node("gemm", [x, W.cpu().numpy()], [S * D, 0], out, S * 64, [S, 64, D], len(idx))
+        proj.append(out)
+    ref = _attn_ref(oracle_mod, proj[0], proj[1], proj[2], Wh.cpu().numpy(), S, len(idx))
+    for j, b in enumerate(idx):
+        assert normwise(z1[b], ref[j]) <= TOL_TF32X3, b
 
 
 @pytest.mark.parametrize("math,ld", [("tf32x3", 0), ("tf32x3", 512), ("tf32", 0)])
