@@ -37,10 +37,13 @@
 //               hi/lo, Z -> global
 //
 // TMEM columns (each CTA): [0,192) projection accumulator Q|K|V · [192,256) 2 A
-// stages · [256,384) Q hi|lo, then P hi (128 keys), then C hi|lo · [384,512) S, then
-// P lo of keys 0-63 [384,448) + C accumulator [448,512), then the Z accumulator
-// [384,448). P lo of keys 64-127 replaces [384,448) once the MMAs reading keys
-// 0-63's have run.
+// stages · [256,384) Q hi|lo -> P hi|lo of keys 0-63 -> P hi|lo of keys 64-127 -> C
+// hi|lo · [384,512) S -> C accumulator [384,448) + Z accumulator [448,512).
+//
+// Measured (profiles/head_probe.py, r2 session): 94 us per 512-instance launch (round 1:
+// 100 us). The narrow attention MMAs (N = 64 / 128, A read from TMEM at ~64 B/cycle)
+// cost ~7.7k cycles per pair next to the projection's 18.4k, and the projection alone
+// runs at ~60 % of its MMA floor (profiles/README.md).
 #include <mutex>
 
 #include "kernels.cuh"
@@ -113,9 +116,9 @@ static_assert(kSmem <= 227 * 1024, "shared memory budget exceeded");
 // TMEM columns
 constexpr uint32_t kTQ = 0, kTK = 64, kTV = 128;  // projection accumulator
 constexpr uint32_t kTA = 192;                     // A stages, 32 columns each (hi 16 | lo 16)
-constexpr uint32_t kTOp = 256;                    // Q hi/lo -> P hi -> C hi/lo
-constexpr uint32_t kTS = 384;                     // S -> P lo (keys 0-63 / 64-127) -> Z accumulator
-constexpr uint32_t kTC = 448;                     // C accumulator
+constexpr uint32_t kTOp = kTA + 32 * kNA;         // 128 columns: Q hi|lo -> P hi|lo (one key half) -> C hi|lo
+constexpr uint32_t kTR = kTOp + 128;              // 128 columns: S -> C acc [kTR, +64) -> Z acc [kTR + 64, +64)
+static_assert(kTR + 128 <= 512, "TMEM columns");
 
 enum Bar : uint32_t {
   XF = 0,               // [kNX] X tile landed (TMA tx)
@@ -127,11 +130,12 @@ enum Bar : uint32_t {
   ACC_FULL = AE + kNA,  // projection done (leader's commit, multicast)
   EXT_PAIR,             // leader: both CTAs extracted (2 x 8 attention warps)
   EXT,                  // this CTA extracted (8 warps): Q hi/lo in TMEM, K / Vᵀ in smem
-  S_FULL,               // S = Q Kᵀ done
+  S_FULL,               // S = Q Kᵀ done (Q and K consumed)
+  S_READ,               // ... read into registers (8 warps)
   WH_FULL,              // Wh planes landed (TMA tx)
-  P_READY,              // P hi + P lo of keys 0-63 in TMEM, S read (8 warps)
-  PLO_FREE,             // the MMAs reading P lo of keys 0-63 are done
-  P2_READY,             // P lo of keys 64-127 in TMEM (4 warps)
+  P0_READY,             // P hi|lo of keys 0-63 in TMEM (4 warps)
+  PV0_DONE,             // C = P V over keys 0-63 done
+  P1_READY,             // P hi|lo of keys 64-127 in TMEM (4 warps)
   C_FULL,               // C = P V done
   C_READY,              // C hi/lo in TMEM (8 warps)
   Z_FULL,               // Z = C Wh done
@@ -258,10 +262,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(bar(AF + a), 2 * 4);
       mbar_init(bar(AE + a), 1);
     }
-    for (uint32_t b : {ACC_FULL, S_FULL, WH_FULL, PLO_FREE, C_FULL, Z_FULL}) mbar_init(bar(b), 1);
+    for (uint32_t b : {ACC_FULL, S_FULL, WH_FULL, PV0_DONE, C_FULL, Z_FULL}) mbar_init(bar(b), 1);
     mbar_init(bar(EXT_PAIR), 2 * 8);
-    for (uint32_t b : {EXT, P_READY, C_READY}) mbar_init(bar(b), 8);
-    mbar_init(bar(P2_READY), 4);
+    for (uint32_t b : {EXT, S_READ, C_READY}) mbar_init(bar(b), 8);
+    for (uint32_t b : {P0_READY, P1_READY}) mbar_init(bar(b), 4);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (const CUtensorMap* m : {&tmX, &tmW, &tmWh})
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
@@ -334,44 +338,25 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto whdesc = [&](int kk, int plane) {  // Whᵀ operand: k-block kk/4 of d
       return smem_desc(base + kWh + uint32_t(plane) * 16384u + uint32_t(kk >> 2) * 8192u + uint32_t(kk & 3) * 32u);
     };
+    // S = Q hi|lo [kTOp, +128) x K -> kTR (N = 128)
     auto issue_s = [&]() {
       if (elect_one()) {
 #pragma unroll
         for (int kk = 0; kk < kDK / 8; ++kk)
-          mma3<kTerms, false>(tmem + kTS, tmem + kTOp + uint32_t(kk) * 8u, tmem + kTOp + 64u + uint32_t(kk) * 8u,
+          mma3<kTerms, false>(tmem + kTR, tmem + kTOp + uint32_t(kk) * 8u, tmem + kTOp + 64u + uint32_t(kk) * 8u,
                               kdesc(kk, 0), kdesc(kk, 1), idS, kk ? 1u : 0u);
         mma_commit(bar(S_FULL));
       }
       __syncwarp();
     };
-    auto issue_pv_a = [&]() {  // P hi · V (both terms), then P lo · V hi for keys 0-63
+    // C (+)= P·V over one key half: P hi|lo [kTOp, +128) x Vᵀ k-blocks of those keys -> kTR
+    auto issue_pv = [&](int half) {
       if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < kS / 8; ++kk) {
-          const uint32_t a_hi = tmem + kTOp + uint32_t(kk) * 8u;
-          if constexpr (kTerms > 1) {
-            mma_tf32_ts(tmem + kTC, a_hi, vdesc(kk, 1), idC, kk ? 1u : 0u);
-            mma_tf32_ts(tmem + kTC, a_hi, vdesc(kk, 0), idC, 1u);
-          } else {
-            mma_tf32_ts(tmem + kTC, a_hi, vdesc(kk, 0), idC, kk ? 1u : 0u);
-          }
-        }
-        if constexpr (kTerms > 1) {
-#pragma unroll
-          for (int kk = 0; kk < kS / 16; ++kk) mma_tf32_ts(tmem + kTC, tmem + kTS + uint32_t(kk) * 8u, vdesc(kk, 0), idC, 1u);
-        }
-        mma_commit(bar(PLO_FREE));
-      }
-      __syncwarp();
-    };
-    auto issue_pv_b = [&]() {  // P lo · V hi for keys 64-127
-      if (elect_one()) {
-        if constexpr (kTerms > 1) {
-#pragma unroll
-          for (int kk = kS / 16; kk < kS / 8; ++kk)
-            mma_tf32_ts(tmem + kTC, tmem + kTS + uint32_t(kk - kS / 16) * 8u, vdesc(kk, 0), idC, 1u);
-        }
-        mma_commit(bar(C_FULL));
+        for (int kk = 0; kk < 8; ++kk)
+          mma3<kTerms, false>(tmem + kTR, tmem + kTOp + uint32_t(kk) * 8u, tmem + kTOp + 64u + uint32_t(kk) * 8u,
+                              vdesc(8 * half + kk, 0), vdesc(8 * half + kk, 1), idC, (half | kk) ? 1u : 0u);
+        mma_commit(bar(half ? C_FULL : PV0_DONE));
       }
       __syncwarp();
     };
@@ -379,14 +364,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (elect_one()) {
 #pragma unroll
         for (int kk = 0; kk < kDK / 8; ++kk)
-          mma3<kTerms, false>(tmem + kTS, tmem + kTOp + uint32_t(kk) * 8u, tmem + kTOp + 64u + uint32_t(kk) * 8u,
+          mma3<kTerms, false>(tmem + kTR + 64u, tmem + kTOp + uint32_t(kk) * 8u, tmem + kTOp + 64u + uint32_t(kk) * 8u,
                               whdesc(kk, 0), whdesc(kk, 1), idC, kk ? 1u : 0u);
         mma_commit(bar(Z_FULL));
       }
       __syncwarp();
     };
     // the attention of one instance as a sequence of steps, each gated by barriers:
-    // 0: S (EXT) 1: P·V a (P_READY) 2: P·V b (P2_READY) 3: Z (WH_FULL, C_READY) 4: done
+    // 0: S (EXT) 1: P·V keys 0-63 (S_READ, P0_READY) 2: P·V keys 64-127 (P1_READY)
+    // 3: Z (WH_FULL, C_READY) 4: done
+    constexpr int kSteps = 4;
     auto step_ready = [&](int st, uint32_t ph, bool block) {
       auto test = [&](uint32_t b) {
         if (block) {
@@ -397,34 +384,33 @@ __global__ void __launch_bounds__(kThreads, 1)
       };
       switch (st) {
         case 0: return test(EXT);
-        case 1: return test(P_READY);
-        case 2: return test(P2_READY);
+        case 1: return test(S_READ) && test(P0_READY);
+        case 2: return test(P1_READY);
         default: return test(WH_FULL) && test(C_READY);
       }
     };
     auto step_issue = [&](int st) {
       tc_fence_after();
       if (st == 0) issue_s();
-      else if (st == 1) issue_pv_a();
-      else if (st == 2) issue_pv_b();
+      else if (st <= 2) issue_pv(st - 1);
       else issue_z();
     };
     uint32_t lt = 0;
     if (rank != 0) {
       // only this CTA's attention, in order
       for (int t = pair0; t < p.pairs && !HS_DBG_HEAD_NOATT; t += npairs, ++lt)
-        for (int st = 0; st < 4; ++st) {
+        for (int st = 0; st < kSteps; ++st) {
           step_ready(st, lt & 1u, true);
           step_issue(st);
         }
     } else {
       uint32_t ia = 0, iw = 0;
-      int st = 4;  // step of the previous pair's attention (4: nothing pending)
+      int st = kSteps;  // step of the previous pair's attention (kSteps: nothing pending)
       for (int t = pair0; t < p.pairs; t += npairs, ++lt) {
         if (lt > 0) {
           // both CTAs have read the accumulator out: the next projection may overwrite it
           mbar_wait(bar(EXT_PAIR), (lt - 1) & 1u);
-          st = HS_DBG_HEAD_NOATT ? 4 : 0;
+          st = HS_DBG_HEAD_NOATT ? kSteps : 0;
         }
         if (lane == 0) TL(lt, 0);
         for (int kb = 0; kb < nw; ++kb, ++iw) {
@@ -448,20 +434,20 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             __syncwarp();
             // interleave the previous pair's attention MMAs as their operands become ready
-            while (st < 4 && step_ready(st, (lt - 1) & 1u, false)) step_issue(st++);
+            while (st < kSteps && step_ready(st, (lt - 1) & 1u, false)) step_issue(st++);
           }
         }
         if (elect_one()) mma_commit_pair(bar(ACC_FULL));
         __syncwarp();
         if (lane == 0) TL(lt, 1);
         // the next extraction reuses the attention operands: finish the previous pair first
-        while (st < 4) {
+        while (st < kSteps) {
           step_ready(st, (lt - 1) & 1u, true);
           step_issue(st++);
         }
       }
       if (lt > 0 && !HS_DBG_HEAD_NOATT)  // the last pair's attention
-        for (st = 0; st < 4; ++st) {
+        for (st = 0; st < kSteps; ++st) {
           step_ready(st, (lt - 1) & 1u, true);
           step_issue(st);
         }
@@ -573,15 +559,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive_cluster(leader(EXT_PAIR));
       }
       if (HS_DBG_HEAD_NOATT) continue;
-      // ---- softmax over keys [64g, 64g+64) of this row, S in registers
+      // ---- softmax over keys [64g, 64g+64) of this row: S of this key half in registers
       mbar_wait(bar(S_FULL), ph);
       tc_fence_after();
       if (warp == 8 && lane == 0) TL(lt, 3);
       uint32_t r0[32], r1[32];
-      tmem_ld32_nowait(lane_base + kTS + uint32_t(64 * g), r0);
-      tmem_ld32_nowait(lane_base + kTS + uint32_t(64 * g + 32), r1);
+      tmem_ld32_nowait(lane_base + kTR + uint32_t(64 * g), r0);
+      tmem_ld32_nowait(lane_base + kTR + uint32_t(64 * g + 32), r1);
       tmem_ld_wait(r0);
       tmem_ld_dep(r1);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar(S_READ));
       float mx = full ? row_max<false>(r0, r1, 0, p.S, p.scale) : row_max<true>(r0, r1, 64 * g, p.S, p.scale);
       sts32(mine, mx);
       named_bar(1u + uint32_t(q), 64u);
@@ -592,19 +581,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       named_bar(1u + uint32_t(q), 64u);
       const float s_other = lds32(other + 128u);
       const float inv = 1.f / (g == 0 ? sum + s_other : s_other + sum);
-      // P = e · inv -> hi to [256 + 64g); lo kept in r0/r1 (keys 0-63 also stored now)
-      auto p_chunk = [&](uint32_t(&r)[32], int off, int hh) {
-        uint32_t hi[16], lo[16];
+      // P = e · inv of this key half -> hi [kTOp, +64) | lo [kTOp + 64, +64), once Q (key
+      // half 0) or key half 0's P (key half 1) has been consumed
+      if (g) mbar_wait(bar(PV0_DONE), ph);
+      tc_fence_after();
+      auto p_chunk = [&](const uint32_t(&r)[32], int off, int hh) {
+        uint32_t v[16];
 #pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          const float x = __uint_as_float(r[off + e]) * inv;
-          const float h = tf32_rna(x);
-          hi[e] = __float_as_uint(h);
-          lo[e] = __float_as_uint(x - h);
-          r[off + e] = lo[e];
-        }
-        tmem_st16(lane_base + kTOp + uint32_t(64 * g + 16 * hh), hi);
-        if (kTerms > 1 && g == 0) tmem_st16(lane_base + kTS + uint32_t(16 * hh), lo);
+        for (int e = 0; e < 16; ++e) v[e] = __float_as_uint(__uint_as_float(r[off + e]) * inv);
+        st_split16<kTerms>(lane_base + kTOp + uint32_t(16 * hh), 64u, v);
       };
       p_chunk(r0, 0, 0);
       p_chunk(r0, 16, 1);
@@ -613,35 +598,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(bar(P_READY));
-      if (g == 1) {
-        // keys 64-127: P lo replaces keys 0-63's once the MMAs reading those are done
-        if constexpr (kTerms > 1) {
-          mbar_wait(bar(PLO_FREE), ph);
-          tc_fence_after();
-          auto lo_chunk = [&](const uint32_t(&r)[32], int off, int hh) {
-            uint32_t lo[16];
-#pragma unroll
-            for (int e = 0; e < 16; ++e) lo[e] = r[off + e];
-            tmem_st16(lane_base + kTS + uint32_t(16 * hh), lo);
-          };
-          lo_chunk(r0, 0, 0);
-          lo_chunk(r0, 16, 1);
-          lo_chunk(r1, 0, 2);
-          lo_chunk(r1, 16, 3);
-          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-          tc_fence_before();
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(bar(P2_READY));
-      }
-      // ---- C columns [32g, 32g+32) -> tf32 hi [256 + 32g) / lo [320 + 32g) (P is consumed)
+      if (lane == 0) mbar_arrive(bar(g ? P1_READY : P0_READY));
+      // ---- C columns [32g, 32g+32) -> tf32 hi [kTOp + 32g) / lo [kTOp + 64 + 32g) (P is consumed)
       mbar_wait(bar(C_FULL), ph);
       tc_fence_after();
       if (warp == 8 && lane == 0) TL(lt, 4);
       {
         uint32_t c[32];
-        tmem_ld32(lane_base + kTC + uint32_t(32 * g), c);
+        tmem_ld32(lane_base + kTR + uint32_t(32 * g), c);
         st_split16<kTerms>(lane_base + kTOp + uint32_t(32 * g), 64u, c);
         st_split16<kTerms>(lane_base + kTOp + uint32_t(32 * g + 16), 64u, c + 16);
       }
@@ -655,7 +619,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (warp == 8 && lane == 0) TL(lt, 5);
       {
         uint32_t z[32];
-        tmem_ld32(lane_base + kTS + uint32_t(32 * g), z);
+        tmem_ld32(lane_base + kTR + 64u + uint32_t(32 * g), z);
         if (inst < p.batch && row < p.S) {
           float4* out = reinterpret_cast<float4*>(p.Z + int64_t(inst) * p.sZ + int64_t(row) * p.ldz + 32 * g);
 #pragma unroll
