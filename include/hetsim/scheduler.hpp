@@ -8,7 +8,8 @@
 //   * PlanExecutor    — deterministic completion model (dispatch order); used to
 //                       derive the static plan that is captured as a CUDA graph.
 //   * ReplayExecutor  — replays a recorded completion log (scheduling parity).
-//   * CudaExecutor    — real streams/events/kernels (exec/cuda_executor.hpp).
+//   * CudaExecutor    — real streams/events/kernels on the B200
+//                       (include/hetsim/cuda_executor.hpp).
 #pragma once
 
 #include <deque>

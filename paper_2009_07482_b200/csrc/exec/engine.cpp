@@ -58,22 +58,16 @@ std::vector<long long> var_values(const KernelSpec& k, const ParamMap& params) {
 
 }  // namespace
 
-// Executor used in dynamic mode: Alg. 1 dispatch -> Engine::issue.
+// Executor used in dynamic mode: Alg. 1 dispatch -> Engine::issue (the same
+// path a caller-driven hetsim::CudaExecutor takes through ext_dispatch).
 class CudaDispatch : public Executor {
  public:
-  CudaDispatch(Engine& e, Engine::Slot& sl, int64_t first, int64_t n) : e_(e), sl_(sl), first_(first), n_(n) {}
-  void dispatch(const TaskComponent& t, const CommandQueueStructure& q) override {
-    const auto t0 = std::chrono::steady_clock::now();
-    e_.issue(sl_, t, q, -1, nullptr, false, first_, n_);
-    e_.host_dispatch_ns_ += std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count();
-    ++e_.host_dispatches_;
-  }
-  Completion wait_next() override { return e_.wait_completion(); }
+  explicit CudaDispatch(Engine& e) : e_(e) {}
+  void dispatch(const TaskComponent& t, const CommandQueueStructure& q) override { e_.ext_dispatch(t, q); }
+  Completion wait_next() override { return e_.ext_wait(); }
 
  private:
   Engine& e_;
-  Engine::Slot& sl_;
-  int64_t first_, n_;
 };
 
 Engine::Engine(EngineConfig cfg) : cfg_(std::move(cfg)) {
@@ -1185,23 +1179,38 @@ Completion Engine::wait_completion() {
   return c;
 }
 
-void Engine::run_dynamic(Slot& sl, int64_t first, int64_t n) {
+void Engine::reset_dynamic_state(Slot& sl) {
   sl.group_done.clear();
   sl.edge_event.clear();
   last_log_.clear();
-  {
-    std::lock_guard<std::mutex> lk(mu_);
-    done_q_.clear();
-    pending_.store(0, std::memory_order_relaxed);
-  }
-  CudaDispatch ex(*this, sl, first, n);
+  std::lock_guard<std::mutex> lk(mu_);
+  done_q_.clear();
+  pending_.store(0, std::memory_order_relaxed);
+}
+
+void Engine::run_dynamic(Slot& sl, int64_t first, int64_t n) {
+  reset_dynamic_state(sl);
+  ext_first_ = first;
+  ext_n_ = n;
+  CudaDispatch ex(*this);
   ScheduleResult r = sched_->run(ex);
   last_dispatches_ = r.dispatches;
   if (tracing_)
     for (const auto& rec : r.dispatches) trace_dispatch_.push_back({rec.component, rec.device});
 }
 
-void Engine::run(int64_t first, int64_t n, int64_t* elapsed_ns) {
+void Engine::ext_dispatch(const TaskComponent& t, const CommandQueueStructure& q) {
+  if (cfg_.graph_mode) fail(Errc::invalid_param, "external dispatch needs a dynamic-mode engine");
+  const auto t0 = std::chrono::steady_clock::now();
+  issue(slots_.front(), t, q, -1, nullptr, false, ext_first_, ext_n_);
+  host_dispatch_ns_ +=
+      std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count();
+  ++host_dispatches_;
+}
+
+Completion Engine::ext_wait() { return wait_completion(); }
+
+void Engine::check_range(int64_t first, int64_t n) const {
   if (n < 1) fail(Errc::invalid_param, "n_instances must be >= 1");
   if (first < 0) fail(Errc::invalid_param, "first must be >= 0");
   for (const auto& [key, b] : bindings_)
@@ -1209,48 +1218,97 @@ void Engine::run(int64_t first, int64_t n, int64_t* elapsed_ns) {
       fail(Errc::invalid_param, "instances [" + std::to_string(first) + ", " + std::to_string(first + n) +
                                     ") exceed the " + std::to_string(b.count) + " bound at (" +
                                     std::to_string(key.first) + "," + std::to_string(key.second) + ")");
-  if (!planned_) {
-    // Dynamic mode launches one kernel per ndrange, unless dynamic_fuse asks for the
-    // graph plan's launch lowering: the rewrites are per component and keyed by
-    // (component, event), and setup_cq numbers a component's events the same on
-    // every device when all devices have the same queue count.
-    bool uniform_queues = true;
-    for (const auto& d : platform_.devices) uniform_queues = uniform_queues && d.queues == platform_.devices[0].queues;
-    if (!cfg_.graph_mode && cfg_.dynamic_fuse && (!uniform_queues || cfg_.math == HS_MATH_FP32_SIMT))
-      fail(Errc::invalid_param, uniform_queues ? "dynamic_fuse needs tcgen05 math (not simt)"
-                                               : "dynamic_fuse needs the same queue count on every device");
-    dyn_fused_ = !cfg_.graph_mode && cfg_.dynamic_fuse;
-    if (cfg_.graph_mode || dyn_fused_) {
-      PlanExecutor pe;
-      plan_ = sched_->run(pe);
-      place_components();
-    }
-    plan_buffers();
-    if (dyn_fused_) {
-      if (cfg_.fuse >= 1) plan_fusion();
-      if (cfg_.fuse >= 2) plan_chain_rewrites();
-    }
-    if (cfg_.graph_mode) {
-      if (cfg_.fuse >= 1 && cfg_.math != HS_MATH_FP32_SIMT) plan_fusion();
-      if (cfg_.fuse >= 2 && cfg_.math != HS_MATH_FP32_SIMT) plan_chain_rewrites();
-    }
-    place_slot_buffers();
-    if (cfg_.graph_mode) {
-      // Ramp (host-fed streams): the first and last chunks of a run are ramp_ =
-      // batch/4 instances, so the copy-in before the first graph and the copy-out
-      // after the last one are short; the copies of every other chunk overlap
-      // the graphs of the other slots.
-      bool host_io = false;
-      for (const auto& gr : groups_)
-        if (!gr.resident && !gr.b.on_device) host_io = true;
-      for (const auto& key : outputs_)
-        if (!bindings_.at(key).on_device) host_io = true;
-      if (cfg_.ramp && host_io && !cfg_.trace && cfg_.batch >= 8 && slots_.size() > 1) ramp_ = cfg_.batch / 4;
-      if (capture_ok_)
-        for (auto& sl : slots_) capture(sl);
-    }
-    planned_ = true;
+}
+
+void Engine::join_dynamic_streams(Slot& s0) {
+  int j = 0;
+  for (auto& [k, s] : s0.streams) {
+    hs_event_t e = event(s0, -3, j++);
+    hs_ok(hs_event_record(e, s), "join record");
+    hs_ok(hs_stream_wait(s0.origin, e), "join wait");
   }
+}
+
+// A caller-driven run: the caller's scheduler dispatches each component of one
+// batch of n instances through ext_dispatch and drains completions with ext_wait.
+void Engine::ext_begin(int64_t first, int64_t n) {
+  if (cfg_.graph_mode) fail(Errc::invalid_param, "external dispatch needs a dynamic-mode engine");
+  if (ext_open_) fail(Errc::invalid_param, "begin() called twice without end()");
+  check_range(first, n);
+  if (n > cfg_.batch) fail(Errc::invalid_param, "n exceeds the executor's batch");
+  plan_once();
+  upload_resident();
+  Slot& s0 = slots_.front();
+  reset_dynamic_state(s0);
+  ext_first_ = first;
+  ext_n_ = n;
+  hs_ok(hs_event_record(s0.t_start, s0.origin), "start record");
+  for (auto& [k, s] : s0.streams) hs_ok(hs_stream_wait(s, s0.t_start), "start wait");
+  ext_open_ = true;
+}
+
+int64_t Engine::ext_end() {
+  if (!ext_open_) fail(Errc::invalid_param, "end() without begin()");
+  ext_open_ = false;
+  Slot& s0 = slots_.front();
+  join_dynamic_streams(s0);
+  hs_ok(hs_event_record(s0.t_end, s0.origin), "end record");
+  hs_ok(hs_event_sync(s0.t_end), "end sync");
+  int64_t ns = 0;
+  hs_ok(hs_event_elapsed_ns(s0.t_start, s0.t_end, &ns), "elapsed");
+  ++runs_;
+  ++batches_run_;
+  return ns;
+}
+
+void Engine::plan_once() {
+  if (planned_) return;
+  // Dynamic mode launches one kernel per ndrange, unless dynamic_fuse asks for the
+  // graph plan's launch lowering: the rewrites are per component and keyed by
+  // (component, event), and setup_cq numbers a component's events the same on
+  // every device when all devices have the same queue count.
+  bool uniform_queues = true;
+  for (const auto& d : platform_.devices) uniform_queues = uniform_queues && d.queues == platform_.devices[0].queues;
+  if (!cfg_.graph_mode && cfg_.dynamic_fuse && (!uniform_queues || cfg_.math == HS_MATH_FP32_SIMT))
+    fail(Errc::invalid_param, uniform_queues ? "dynamic_fuse needs tcgen05 math (not simt)"
+                                             : "dynamic_fuse needs the same queue count on every device");
+  dyn_fused_ = !cfg_.graph_mode && cfg_.dynamic_fuse;
+  if (cfg_.graph_mode || dyn_fused_) {
+    PlanExecutor pe;
+    plan_ = sched_->run(pe);
+    place_components();
+  }
+  plan_buffers();
+  if (dyn_fused_) {
+    if (cfg_.fuse >= 1) plan_fusion();
+    if (cfg_.fuse >= 2) plan_chain_rewrites();
+  }
+  if (cfg_.graph_mode) {
+    if (cfg_.fuse >= 1 && cfg_.math != HS_MATH_FP32_SIMT) plan_fusion();
+    if (cfg_.fuse >= 2 && cfg_.math != HS_MATH_FP32_SIMT) plan_chain_rewrites();
+  }
+  place_slot_buffers();
+  if (cfg_.graph_mode) {
+    // Ramp (host-fed streams): the first and last chunks of a run are ramp_ =
+    // batch/4 instances, so the copy-in before the first graph and the copy-out
+    // after the last one are short; the copies of every other chunk overlap
+    // the graphs of the other slots.
+    bool host_io = false;
+    for (const auto& gr : groups_)
+      if (!gr.resident && !gr.b.on_device) host_io = true;
+    for (const auto& key : outputs_)
+      if (!bindings_.at(key).on_device) host_io = true;
+    if (cfg_.ramp && host_io && !cfg_.trace && cfg_.batch >= 8 && slots_.size() > 1) ramp_ = cfg_.batch / 4;
+    if (capture_ok_)
+      for (auto& sl : slots_) capture(sl);
+  }
+  planned_ = true;
+}
+
+void Engine::run(int64_t first, int64_t n, int64_t* elapsed_ns) {
+  check_range(first, n);
+  if (ext_open_) fail(Errc::invalid_param, "run() inside an open begin()/end() pair");
+  plan_once();
   upload_resident();
   const int64_t B = cfg_.batch;
   const int64_t nb = (n + B - 1) / B;
@@ -1302,13 +1360,7 @@ void Engine::run(int64_t first, int64_t n, int64_t* elapsed_ns) {
       run_dynamic(s0, f, cnt);
       tracing_ = false;
     }
-    // join every queue stream back into the origin
-    int j = 0;
-    for (auto& [k, s] : s0.streams) {
-      hs_event_t e = event(s0, -3, j++);
-      hs_ok(hs_event_record(e, s), "join record");
-      hs_ok(hs_stream_wait(s0.origin, e), "join wait");
-    }
+    join_dynamic_streams(s0);  // every queue stream back into the origin
   }
   for (size_t i = 1; i < slots_.size(); ++i) {
     hs_ok(hs_event_record(slots_[i].t_end, slots_[i].origin), "end record");

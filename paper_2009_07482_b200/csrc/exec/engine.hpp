@@ -86,6 +86,13 @@ class Engine {
   // Completion delivery from CUDA host callbacks (any thread).
   void push_completion(const Completion& c);
 
+  // Alg. 1 driven from outside (hetsim::CudaExecutor, include/hetsim/cuda_executor.hpp):
+  // one scheduler run per ext_begin / ext_end over n <= batch instances, dynamic mode.
+  void ext_begin(int64_t first, int64_t n);
+  void ext_dispatch(const TaskComponent& t, const CommandQueueStructure& q);
+  Completion ext_wait();
+  int64_t ext_end();
+
  private:
   struct Node {
     int op = -1;
@@ -153,9 +160,14 @@ class Engine {
   void* dalloc(int dom, int64_t bytes);
   hs_stream_t dstream(Slot& sl, int dom);
   void run_dynamic(Slot& sl, int64_t first, int64_t n);
+  void check_range(int64_t first, int64_t n) const;
+  void plan_once();
+  void reset_dynamic_state(Slot& sl);
+  void join_dynamic_streams(Slot& sl);
+  int64_t ext_first_ = 0, ext_n_ = 0;
+  bool ext_open_ = false;
   Completion wait_completion();
 
-  friend class CudaDispatch;
 
   EngineConfig cfg_;
   DagSpec g_;

@@ -145,3 +145,45 @@ def test_spec_examples():
         "depends": [[0, 0, 1, 0]], "tc": [[0], [1]], "cq": [{"device": 0, "queues": 1}]}
     r = same({"op": "ranks", "spec": json.dumps(chain), "times": {"0": "10", "1": "10"}})[0]
     assert r["ranks"] == {"0": "20", "1": "10"}
+
+
+def _random_exprs(seed, count):
+    """Random well-formed and malformed expressions: nested sums/products/divisions,
+    unary minus, long literals, unbound names, stray characters and truncations —
+    whichever problem comes first from the left must decide the Errc."""
+    import random
+    rng = random.Random(seed)
+    atoms = ["M", "N", "a_b1", "Z", "0", "1", "2", "3", "7", "12", "64", "999999999999999999",
+             "1234567890123456789", "4611686018427387904", "3037000499"]
+
+    def gen(d):
+        r = rng.random()
+        if d > 3 or r < 0.3:
+            return rng.choice(atoms)
+        if r < 0.4:
+            return "-" + gen(d + 1)
+        if r < 0.5:
+            return "(" + gen(d + 1) + ")"
+        return gen(d + 1) + rng.choice(["+", "-", "*", "/", " * ", " / "]) + gen(d + 1)
+
+    out = []
+    for _ in range(count):
+        e = gen(0)
+        m = rng.random()
+        if m < 0.15 and e:
+            i = rng.randrange(len(e))
+            e = e[:i] + rng.choice(["$", ")", "(", "+", "  ", "x", "9"]) + e[i:]
+        elif m < 0.25:
+            e = e[:rng.randrange(len(e) + 1)]
+        out.append(e)
+    return out
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_expr_random_against_reference(seed):
+    """The Pratt evaluator (csrc/core/expr.cpp) against the reference's recursive
+    descent (proj/src/expr.cpp), 250 random expressions per seed x three modes:
+    identical values, identical Errc for every malformed or overflowing input."""
+    for e in _random_exprs(seed, 250):
+        for mode in ("eval", "positive", "validate"):
+            same({"op": "expr", "expr": e, "mode": mode, "params": {"M": 4, "N": 6, "a_b1": 3}})
