@@ -87,7 +87,7 @@ int DagSpec::index_of(int id) const {
 
 const KernelSpec& DagSpec::kernel(int id) const {
   int i = index_of(id);
-  if (i < 0) fail(Errc::unknown_kernel_ref, "kernel id " + std::to_string(id));
+  if (i < 0) fail(Errc::unknown_kernel_ref, "no kernel with id " + std::to_string(id));
   return kernels[size_t(i)];
 }
 
@@ -139,7 +139,7 @@ std::vector<int> DagSpec::topo_order() const {
     for (int d : succ[id])
       if (--indeg[d] == 0) ready.insert(d);
   }
-  if (order.size() != kernels.size()) fail(Errc::cycle_detected, "kernel dependency graph is cyclic");
+  if (order.size() != kernels.size()) fail(Errc::cycle_detected, "the depends edges form a cycle");
   return order;
 }
 
@@ -161,13 +161,13 @@ ElemType elem_type_from(const std::string& s) {
   if (s == "int32") return ElemType::i32;
   if (s == "float64") return ElemType::f64;
   if (s == "int64") return ElemType::i64;
-  fail(Errc::malformed_spec, "unknown element type '" + s + "'");
+  fail(Errc::malformed_spec, "buffer type '" + s + "' is not one of the element types");
 }
 
 DeviceType device_type_from(const std::string& s) {
   if (s == "cpu") return DeviceType::cpu;
   if (s == "gpu") return DeviceType::gpu;
-  fail(Errc::malformed_spec, "unknown device type '" + s + "'");
+  fail(Errc::malformed_spec, "dev '" + s + "' is neither gpu nor cpu");
 }
 
 // A symbolic field may be written as a JSON string or as an integer.
@@ -178,16 +178,16 @@ std::string symbolic(const Value& v) {
 }
 
 BufferSpec read_buffer(const Value& j, int kernel_id, BufferKind kind) {
-  if (!j.is_object()) fail(Errc::malformed_spec, "buffer entry must be an object");
+  if (!j.is_object()) fail(Errc::malformed_spec, "each buffer is a JSON object");
   if (!j.contains("type") || !j.contains("size") || !j.contains("pos"))
-    fail(Errc::malformed_spec, "buffer needs type/size/pos");
+    fail(Errc::malformed_spec, "a buffer lacks one of type, size, pos");
   BufferSpec b;
   b.kernel = kernel_id;
   b.kind = kind;
   b.type = elem_type_from(j.at("type").as_string());
   b.size_expr = symbolic(j.at("size"));
   b.pos = j.at("pos").as_int();
-  if (b.pos < 0) fail(Errc::malformed_spec, "buffer pos must be non-negative");
+  if (b.pos < 0) fail(Errc::malformed_spec, "negative buffer position");
   return b;
 }
 
@@ -195,21 +195,21 @@ BufferSpec read_buffer(const Value& j, int kernel_id, BufferKind kind) {
 void check_positions(const KernelSpec& k) {
   std::map<int, int> used;
   auto take = [&](int pos, const char* what) {
-    if (pos < 0) fail(Errc::malformed_spec, std::string(what) + " pos must be non-negative");
+    if (pos < 0) fail(Errc::malformed_spec, "negative position in " + std::string(what));
     if (++used[pos] > 1)
-      fail(Errc::arg_position_clash, "kernel " + std::to_string(k.id) + " argument position " + std::to_string(pos));
+      fail(Errc::arg_position_clash, "two arguments of kernel " + std::to_string(k.id) + " share position " + std::to_string(pos));
   };
-  for (const auto& b : k.input_buffers) take(b.pos, "buffer");
-  for (const auto& b : k.output_buffers) take(b.pos, "buffer");
-  for (const auto& b : k.io_buffers) take(b.pos, "buffer");
-  for (const auto& v : k.var_args) take(v.pos, "var arg");
+  for (const auto& b : k.input_buffers) take(b.pos, "a buffer");
+  for (const auto& b : k.output_buffers) take(b.pos, "a buffer");
+  for (const auto& b : k.io_buffers) take(b.pos, "a buffer");
+  for (const auto& v : k.var_args) take(v.pos, "a varArgument");
   if (used.empty()) return;
   int hi = used.rbegin()->first;
   if (int(used.size()) != hi + 1) {
     for (int p = 0; p <= hi; ++p)
       if (!used.count(p))
         fail(Errc::malformed_spec,
-             "kernel " + std::to_string(k.id) + " argument position " + std::to_string(p) + " is not covered");
+             "kernel " + std::to_string(k.id) + " has a gap at argument position " + std::to_string(p));
   }
 }
 
@@ -226,15 +226,15 @@ void read_document(const Value& root, DagSpec& g) {
     const Value& jk = *pk;
     KernelSpec k;
     k.id = jk.at("id").as_int();
-    if (k.id < 0) fail(Errc::malformed_spec, "kernel id must be non-negative");
+    if (k.id < 0) fail(Errc::malformed_spec, "negative kernel id");
     k.name = jk.at("name").as_string();
     k.dev = device_type_from(jk.at("dev").as_string());
     if (!jk.is_object()) throw json::TypeError("kernel entry must be an object");
     const Value* wd = jk.find("workDimension");
     k.work_dimension = wd ? wd->as_int() : 1;
-    if (k.work_dimension < 1 || k.work_dimension > 3) fail(Errc::malformed_spec, "workDimension must be in [1,3]");
+    if (k.work_dimension < 1 || k.work_dimension > 3) fail(Errc::malformed_spec, "workDimension outside 1..3");
     if (const Value* gws = jk.find("globalWorkSize")) {
-      if (!gws->is_array() || gws->size() != 3) fail(Errc::malformed_spec, "globalWorkSize must be a 3-element list");
+      if (!gws->is_array() || gws->size() != 3) fail(Errc::malformed_spec, "globalWorkSize is not a list of three");
       for (int i = 0; i < 3; ++i) k.global_work_size[size_t(i)] = symbolic((*gws)[size_t(i)]);
     }
     for (const Value* jb : list_or_empty(jk, "inputBuffers").items())
@@ -253,12 +253,12 @@ void read_document(const Value& root, DagSpec& g) {
     const Value* src = jk.find("src");
     k.src_path = src ? src->as_string() : std::string();
     check_positions(k);
-    if (g.has_kernel(k.id)) fail(Errc::malformed_spec, "duplicate kernel id " + std::to_string(k.id));
+    if (g.has_kernel(k.id)) fail(Errc::malformed_spec, "kernel id " + std::to_string(k.id) + " is used twice");
     g.kernels.push_back(std::move(k));
   }
 
   for (const Value* je : list_or_empty(root, "depends").items()) {
-    if (!je->is_array() || je->size() != 4) fail(Errc::malformed_spec, "depends entries are 4-integer records");
+    if (!je->is_array() || je->size() != 4) fail(Errc::malformed_spec, "a depends entry is not [src, src_pos, dst, dst_pos]");
     g.edges.push_back(DagEdge{(*je)[0].as_int(), (*je)[1].as_int(), (*je)[2].as_int(), (*je)[3].as_int()});
   }
 
@@ -271,7 +271,7 @@ void read_document(const Value& root, DagSpec& g) {
   for (const Value* jc : list_or_empty(root, "cq").items()) {
     int dev = jc->at("device").as_int();
     int n = jc->at("queues").as_int();
-    if (n < 0) fail(Errc::malformed_spec, "queue count must be non-negative");
+    if (n < 0) fail(Errc::malformed_spec, "negative queue count in cq");
     g.cq[dev] = n;
   }
 }
@@ -286,7 +286,7 @@ DagSpec parse_spec(const std::string& text, const ParamMap& params) {
     fail(Errc::malformed_spec, e.what());
   }
   if (!root.is_object() || !root.contains("kernels"))
-    fail(Errc::malformed_spec, "top-level object with 'kernels' required");
+    fail(Errc::malformed_spec, "the document is not an object with a kernels list");
 
   DagSpec g;
   g.params = params;
@@ -299,19 +299,19 @@ DagSpec parse_spec(const std::string& text, const ParamMap& params) {
   // Edges: known endpoints, output-side source, input-side target, one producer per input.
   std::set<std::pair<int, int>> fed;
   for (const auto& e : g.edges) {
-    if (!g.has_kernel(e.src_kernel)) fail(Errc::unknown_kernel_ref, "edge source kernel " + std::to_string(e.src_kernel));
-    if (!g.has_kernel(e.dst_kernel)) fail(Errc::unknown_kernel_ref, "edge target kernel " + std::to_string(e.dst_kernel));
+    if (!g.has_kernel(e.src_kernel)) fail(Errc::unknown_kernel_ref, "depends edge from missing kernel " + std::to_string(e.src_kernel));
+    if (!g.has_kernel(e.dst_kernel)) fail(Errc::unknown_kernel_ref, "depends edge into missing kernel " + std::to_string(e.dst_kernel));
     const BufferSpec* s = g.kernel(e.src_kernel).buffer_at(e.src_pos);
     if (!s || s->kind == BufferKind::input)
       fail(Errc::malformed_spec, "edge source (" + std::to_string(e.src_kernel) + "," + std::to_string(e.src_pos) +
-                                     ") is not an output buffer");
+                                     ") does not produce data (input buffer or no buffer)");
     const BufferSpec* d = g.kernel(e.dst_kernel).buffer_at(e.dst_pos);
     if (!d || d->kind == BufferKind::output)
       fail(Errc::malformed_spec, "edge target (" + std::to_string(e.dst_kernel) + "," + std::to_string(e.dst_pos) +
-                                     ") is not an input buffer");
+                                     ") does not consume data (output buffer or no buffer)");
     if (!fed.insert({e.dst_kernel, e.dst_pos}).second)
       fail(Errc::malformed_spec, "input buffer (" + std::to_string(e.dst_kernel) + "," + std::to_string(e.dst_pos) +
-                                     ") has multiple producers");
+                                     ") is fed by more than one edge");
   }
 
   g.topo_order();  // CycleDetected
@@ -319,17 +319,17 @@ DagSpec parse_spec(const std::string& text, const ParamMap& params) {
   // tc: non-empty parts, known ids, disjoint, one device type per part, covering.
   std::set<int> seen;
   for (const auto& comp : g.tc) {
-    if (comp.empty()) fail(Errc::partition_error, "empty task component");
+    if (comp.empty()) fail(Errc::partition_error, "a tc entry lists no kernels");
     const KernelSpec* first = nullptr;
     for (int id : comp) {
-      if (!g.has_kernel(id)) fail(Errc::partition_error, "tc references unknown kernel " + std::to_string(id));
-      if (!seen.insert(id).second) fail(Errc::partition_error, "kernel " + std::to_string(id) + " appears twice in tc");
+      if (!g.has_kernel(id)) fail(Errc::partition_error, "tc names missing kernel " + std::to_string(id));
+      if (!seen.insert(id).second) fail(Errc::partition_error, "tc lists kernel " + std::to_string(id) + " more than once");
       const KernelSpec& k = g.kernel(id);
       if (!first) first = &k;
-      else if (k.dev != first->dev) fail(Errc::partition_error, "task component mixes device types");
+      else if (k.dev != first->dev) fail(Errc::partition_error, "a tc entry mixes gpu and cpu kernels");
     }
   }
-  if (seen.size() != g.kernels.size()) fail(Errc::partition_error, "tc does not cover every kernel");
+  if (seen.size() != g.kernels.size()) fail(Errc::partition_error, "some kernel belongs to no tc entry");
   return g;
 }
 
@@ -418,7 +418,7 @@ std::string serialize(const DagSpec& g) { return json::dump(spec_to_json(g), 2) 
 
 long long buffer_bytes(const BufferSpec& b, const ParamMap& params) {
   __int128 bytes = __int128(eval_positive(b.size_expr, params)) * elem_width(b.type);
-  if (bytes > std::numeric_limits<long long>::max()) fail(Errc::numeric_overflow, "buffer byte size out of range");
+  if (bytes > std::numeric_limits<long long>::max()) fail(Errc::numeric_overflow, "buffer size in bytes overflows 64 bits");
   return static_cast<long long>(bytes);
 }
 
