@@ -67,6 +67,7 @@ class PlatformSim : public Executor {
 
   const std::vector<SimEvent>& trace() const { return trace_; }
   Ratio now() const { return now_; }
+  std::optional<Ratio> clock() const override { return now_; }
   Ratio makespan() const;  // EmptyTrace
 
   /// Scheduler profiles (per device type) implied by the device profiles.
@@ -107,6 +108,6 @@ struct SimResult {
   Ratio makespan;
 };
 SimResult simulate(const DagSpec& g, const Platform& p, const std::vector<DeviceProfile>& profiles, Policy policy,
-                   Ratio callback_delay = Ratio(0));
+                   Ratio callback_delay = Ratio(0), bool heft_waits = false);
 
 }  // namespace hetsim

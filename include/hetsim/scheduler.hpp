@@ -69,6 +69,9 @@ class Executor {
   /// Blocks until the next callback-marked event completes (Alg. 1
   /// sleep_till_cb_update + cb delivery). Raises Deadlock if none can.
   virtual Completion wait_next() = 0;
+  /// The executor's clock (ms), when it has one (the platform simulator); HEFT's
+  /// busy-device mode estimates release times from it.
+  virtual std::optional<Ratio> clock() const { return std::nullopt; }
 };
 
 struct DispatchRecord {
@@ -88,6 +91,11 @@ class Scheduler {
   Scheduler(const DagSpec& g, Platform platform, Profiles profiles, Policy policy);
 
   ScheduleResult run(Executor& ex);
+
+  /// HEFT busy-device mode (`--heft-waits`): select() also weighs
+  /// busy devices, EFT(k, d) = remaining time of d's component + t(k, d), and
+  /// waits for a busy device that wins. Default off (strict availability).
+  void set_heft_waits(bool on) { heft_waits_ = on; }
 
   const std::vector<TaskComponent>& components() const { return comps_; }
   const EdgeClasses& edge_classes() const { return ec_; }
@@ -113,6 +121,11 @@ class Scheduler {
   std::vector<std::vector<int>> cross_preds_;  // per component: kernels of other components it waits for
   std::map<int, int> comp_of_;
 
+  // HEFT with busy devices: the max-rank component's device by EFT over every
+  // device at time `now` (none if that device is busy: wait for it)
+  std::optional<std::pair<int, int>> select_heft_waits(const Ratio& now) const;
+  bool heft_waits_ = false;
+
   // run state
   std::vector<State> state_;
   std::set<int> finished_;
@@ -121,11 +134,13 @@ class Scheduler {
     int device = -1;
     CommandQueueStructure q;
     std::set<int> done_events;
+    Ratio release;  // dispatch time + profiled component time (heft_waits)
   };
   std::map<int, Live> live_;
 };
 
-ScheduleResult run_schedule(const DagSpec& g, const Platform& p, const Profiles& prof, Policy policy, Executor& ex);
+ScheduleResult run_schedule(const DagSpec& g, const Platform& p, const Profiles& prof, Policy policy, Executor& ex,
+                            bool heft_waits = false);
 
 /// Completion model used to build static (graph-captured) plans: components
 /// complete in dispatch order, each reporting its callback events in event order.

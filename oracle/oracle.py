@@ -334,11 +334,15 @@ def setup_cq(spec: Spec, comp_id: int, device: int, device_type: str, r: int) ->
 
 # ============================================================================ scheduler
 
-def schedule(spec: Spec, policy="clustering", times=None, cpu_devices=(), replay=None, executor=None) -> dict:
+def schedule(spec: Spec, policy="clustering", times=None, cpu_devices=(), replay=None, executor=None,
+             heft_waits=False) -> dict:
     """Alg. 1. Completions come from `replay` (a recorded log), from `executor`
     (an object with dispatch(component, device, q) and wait_next() -> (c, ev),
     e.g. oracle/platform_sim.py), or else from the plan model: components
-    complete in dispatch order, callback events in event order."""
+    complete in dispatch order, callback events in event order.
+    heft_waits: HEFT weighs busy devices too, EFT(k, d) =
+    residual time of d's component (dispatch time + profiled time - now, clock from
+    executor.now()) + t(k, d), ties to the lower id; a busy winner is waited for."""
     comps = components(spec)
     devices = sorted(spec.cq)
     dtype = {d: ("cpu" if d in cpu_devices else "gpu") for d in devices}
@@ -378,6 +382,15 @@ def schedule(spec: Spec, policy="clustering", times=None, cpu_devices=(), replay
             return order[0], min(A)
         c = order[0]   # heft: minimal EFT over idle devices, ties lower id
         best = None
+        if heft_waits:
+            now = executor.now() if executor is not None else Fraction(0)
+            release = {L["device"]: L["release"] for L in live.values()}
+            for d in devices:
+                residual = max(Fraction(0), release[d] - now) if d not in A else Fraction(0)
+                eft = residual + sum(t_of(k, dtype[d]) for k in comps[c]["kernels"])
+                if best is None or eft < best[0]:
+                    best = (eft, d)
+            return (c, best[1]) if best[1] in A else None
         for d in sorted(A):
             eft = sum(t_of(k, dtype[d]) for k in comps[c]["kernels"])
             if best is None or eft < best[0]:
@@ -400,7 +413,9 @@ def schedule(spec: Spec, policy="clustering", times=None, cpu_devices=(), replay
             F.discard(c)
             A.discard(d)
             state[c] = "dispatched"
-            live[c] = {"device": d, "q": q, "done": set()}
+            now = executor.now() if executor is not None and hasattr(executor, "now") else Fraction(0)
+            live[c] = {"device": d, "q": q, "done": set(),
+                       "release": now + sum(t_of(k, dtype[d]) for k in comps[c]["kernels"])}
             dispatches.append([c, d])
             if executor is not None:
                 executor.dispatch(c, d, q)

@@ -133,13 +133,16 @@ class Sim:
             if c["callback"]:
                 self.deliver.append((self.t + self.delay, len(self.trace), (c["comp"], c["ev"])))
 
+    def now(self):
+        return self.t
+
     def makespan(self):
         if not self.trace:
             raise OracleError("EmptyTrace")
         return max(e["finish"] for e in self.trace) - min(e["start"] for e in self.trace)
 
 
-def simulate(spec_text, params, profiles, policy="clustering", cpu_devices=(), callback_delay=0):
+def simulate(spec_text, params, profiles, policy="clustering", cpu_devices=(), callback_delay=0, heft_waits=False):
     """Alg. 1 (oracle.schedule) over the restated simulator. profiles: list of
     {"device", "type", "kernel_times", "kernel_share", "copy_channels", "bandwidth",
     "transfer_latency"}; the scheduler's per-type kernel times come from the first
@@ -151,5 +154,6 @@ def simulate(spec_text, params, profiles, policy="clustering", cpu_devices=(), c
         for k, v in p["kernel_times"].items():
             per.setdefault(int(k), F(v))
     sim = Sim(profiles, callback_delay)
-    sched = schedule(spec, policy=policy, times=times or None, cpu_devices=cpu_devices, executor=sim)
+    sched = schedule(spec, policy=policy, times=times or None, cpu_devices=cpu_devices, executor=sim,
+                     heft_waits=heft_waits)
     return {"schedule": sched, "trace": sim.trace, "makespan": sim.makespan()}

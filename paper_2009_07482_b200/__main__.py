@@ -4,6 +4,7 @@ compare / sweep over the host API, the platform simulator and the B200 engine.
   python -m paper_2009_07482_b200 validate --spec dag.json [--params N=256 ...]
   python -m paper_2009_07482_b200 simulate --spec dag.json --profiles prof.json [--policy clustering]
                                            [--gantt text|svg|none] [--callback-delay MS] [--cpu-devices 1]
+                                           [--heft-waits]
   python -m paper_2009_07482_b200 run      --spec dag.json [--policy P] [--mode graph|dynamic] [--instances N]
                                            [--gantt text|svg|none] [--out DIR]          (B200)
   python -m paper_2009_07482_b200 compare  --spec dag.json --profiles prof.json --policies clustering,eager,heft
@@ -76,10 +77,10 @@ def _emit(out_dir, name, text):
         (p / name).write_text(text)
 
 
-def _sim(spec_text, params, profiles, policy, delay, cpu_devices):
+def _sim(spec_text, params, profiles, policy, delay, cpu_devices, heft_waits=False):
     return _native.query({"op": "simulate", "spec": spec_text, "params": params, "policy": policy,
                           "cpu_devices": cpu_devices, "device_profiles": profiles,
-                          "callback_delay": _frac(delay)})["simulate"]
+                          "callback_delay": _frac(delay), "heft_waits": int(bool(heft_waits))})["simulate"]
 
 
 def _float_trace(tr):
@@ -97,7 +98,8 @@ def cmd_validate(a):
 
 def cmd_simulate(a):
     text = pathlib.Path(a.spec).read_text()
-    s = _sim(text, _params(a.params), _profiles(a.profiles), a.policy, a.callback_delay, a.cpu_devices)
+    s = _sim(text, _params(a.params), _profiles(a.profiles), a.policy, a.callback_delay, a.cpu_devices,
+             a.heft_waits)
     tr = _float_trace(s["trace"])
     print(f"makespan_ms {s['makespan_ms']:.6f}")
     if a.gantt != "none":
@@ -113,7 +115,8 @@ def cmd_compare(a):
         raise UsageError("--policies is empty")
     runs = []
     for pol in policies:
-        s = _sim(text, _params(a.params), _profiles(a.profiles), pol, a.callback_delay, a.cpu_devices)
+        s = _sim(text, _params(a.params), _profiles(a.profiles), pol, a.callback_delay, a.cpu_devices,
+                 a.heft_waits)
         runs.append((pol, _float_trace(s["trace"])))
     csv = reporting.compare_csv(runs)
     print(csv, end="")
@@ -180,6 +183,8 @@ def main(argv=None) -> int:
             p.add_argument("--profiles", required=True)
             p.add_argument("--callback-delay", type=float, default=0.0)
             p.add_argument("--cpu-devices", type=int, nargs="*", default=[])
+            # SPEC.md:358 / :551: HEFT weighs busy devices by their release time
+            p.add_argument("--heft-waits", action="store_true")
 
     p = sub.add_parser("validate")
     common(p)

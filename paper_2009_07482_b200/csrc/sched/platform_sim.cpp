@@ -214,7 +214,7 @@ Ratio PlatformSim::makespan() const {
 }
 
 SimResult simulate(const DagSpec& g, const Platform& p, const std::vector<DeviceProfile>& profiles, Policy policy,
-                   Ratio callback_delay) {
+                   Ratio callback_delay, bool heft_waits) {
   for (const auto& d : p.devices) {
     auto it = std::find_if(profiles.begin(), profiles.end(), [&](const DeviceProfile& x) { return x.device_id == d.id; });
     if (it == profiles.end()) fail(Errc::missing_profile_entry, "no profile for device " + std::to_string(d.id));
@@ -222,6 +222,7 @@ SimResult simulate(const DagSpec& g, const Platform& p, const std::vector<Device
       fail(Errc::invalid_param, "device " + std::to_string(d.id) + ": profile type does not match the platform");
   }
   Scheduler sched(g, p, PlatformSim::scheduler_profiles(profiles), policy);
+  sched.set_heft_waits(heft_waits);
   PlatformSim sim(profiles, callback_delay);
   SimResult r;
   r.schedule = sched.run(sim);

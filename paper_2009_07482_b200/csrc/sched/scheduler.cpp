@@ -13,7 +13,10 @@
 //    queue completed;
 //  * clustering: max rank, ties lower component id then lower device id;
 //    eager: max rank on the lowest-id available device;
-//    heft: max rank on the available device with minimal EFT, ties lower id.
+//    heft: max rank on the available device with minimal EFT, ties lower id;
+//    heft with heft_waits: EFT over every device, a busy one counting the residual
+//    time of its component (release = dispatch time + profiled time), and a busy
+//    winner is waited for.
 #include "hetsim/scheduler.hpp"
 
 #include <algorithm>
@@ -125,6 +128,28 @@ std::optional<std::pair<int, int>> Scheduler::select(const std::set<int>& fronti
   return std::nullopt;
 }
 
+std::optional<std::pair<int, int>> Scheduler::select_heft_waits(const Ratio& now) const {
+  if (frontier_.empty()) return std::nullopt;
+  int c = *frontier_.begin();
+  for (int f : frontier_)
+    if (comp_rank_[size_t(c)] < comp_rank_[size_t(f)]) c = f;  // max rank, ties lower id
+  std::optional<int> best;
+  Ratio best_eft = 0;
+  for (const auto& dev : platform_.devices) {  // ascending id: ties go to the lower id
+    Ratio residual = 0;
+    if (!available_.count(dev.id))
+      for (const auto& [comp, live] : live_)
+        if (live.device == dev.id && now < live.release) residual = live.release - now;
+    const Ratio eft = residual + component_time(c, dev.type);
+    if (!best || eft < best_eft) {
+      best = dev.id;
+      best_eft = eft;
+    }
+  }
+  if (!available_.count(*best)) return std::nullopt;  // the best device is busy: wait for it
+  return std::make_pair(c, *best);
+}
+
 void Scheduler::mark_finished(int kernel, ScheduleResult& out) {
   if (finished_.insert(kernel).second) out.kernel_finish_order.push_back(kernel);
 }
@@ -193,7 +218,8 @@ ScheduleResult Scheduler::run(Executor& ex) {
   const size_t total = g_.kernels.size();
   while (finished_.size() < total) {
     while (!available_.empty() && !frontier_.empty()) {
-      auto pick = select(frontier_, available_);
+      const bool waits = heft_waits_ && policy_ == Policy::heft;
+      auto pick = waits ? select_heft_waits(ex.clock().value_or(Ratio(0))) : select(frontier_, available_);
       if (!pick) break;  // select blocks until a callback changes F or A
       auto [c, d] = *pick;
       const DeviceInfo& dev = platform_.device(d);
@@ -205,6 +231,7 @@ ScheduleResult Scheduler::run(Executor& ex) {
       Live live;
       live.device = d;
       live.q = q;
+      live.release = ex.clock().value_or(Ratio(0)) + component_time(c, dev.type);
       live_.emplace(c, std::move(live));
       out.dispatches.push_back({c, d});
       out.structures.push_back(q);
@@ -219,8 +246,10 @@ ScheduleResult Scheduler::run(Executor& ex) {
   return out;
 }
 
-ScheduleResult run_schedule(const DagSpec& g, const Platform& p, const Profiles& prof, Policy policy, Executor& ex) {
+ScheduleResult run_schedule(const DagSpec& g, const Platform& p, const Profiles& prof, Policy policy, Executor& ex,
+                            bool heft_waits) {
   Scheduler s(g, p, prof, policy);
+  s.set_heft_waits(heft_waits);
   return s.run(ex);
 }
 

@@ -84,3 +84,20 @@ def test_unknown_policy_is_a_usage_error(forkjoin):
     f, prof = forkjoin
     rc, _, _ = cli("simulate", "--spec", str(f), "--params", "N=64", "--profiles", str(prof), "--policy", "nope")
     assert rc == 2
+
+
+def test_simulate_heft_waits_flag(tmp_path):
+    """--heft-waits: the SPEC.md:338 HEFT example where the busy GPU's
+    EFT (3 + 5) beats the idle CPU's (12): k1 waits for the GPU."""
+    from tests.test_policies import _gpu_cpu, _two_kernels
+    text, _ = _two_kernels()
+    f = tmp_path / "two.json"
+    f.write_text(text)
+    prof = tmp_path / "prof.json"
+    prof.write_text(json.dumps({"devices": _gpu_cpu({0: 3, 1: 5}, {0: 1000, 1: 12})}))
+    base = ["simulate", "--spec", str(f), "--profiles", str(prof), "--policy", "heft", "--cpu-devices", "1"]
+    rc, strict, err = cli(*base)
+    assert rc == 0, err
+    rc, waits, err = cli(*base, "--heft-waits")
+    assert rc == 0, err
+    assert float(waits.split()[1]) < float(strict.split()[1])

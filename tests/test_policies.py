@@ -1,0 +1,161 @@
+"""Scheduler policies on the platform model (acceptance criteria
+7-8 at SPEC.md:566-567):
+  * HEFT's busy-device mode (`heft_waits`): product == restatement
+    (oracle/oracle.py schedule) on random DAGs, and SPEC.md:337-340's EFT examples;
+  * criterion 7: on a 16-head transformer with t_cpu(GEMM) = 20 t_gpu(GEMM) and a
+    callback delay, makespan(clustering, best mc) < makespan(HEFT) < makespan(eager);
+  * criterion 8: every trace conserves work (the integral of each ndrange's rate
+    over its lifetime equals its standalone time, exactly) and repeated runs are
+    bit-identical.
+"""
+import json
+import random
+from fractions import Fraction
+
+import pytest
+
+from oracle import platform_sim as OS
+from paper_2009_07482_b200 import _native, workloads
+from tests.dag_gen import layered_dag
+from tests.test_platform_sim import _random_profiles, _same, kernel
+
+
+def simulate(text, params, profiles, policy, cpu_devices=(), delay="0", heft_waits=False):
+    req = {"op": "simulate", "spec": text, "params": params, "policy": policy, "cpu_devices": list(cpu_devices),
+           "device_profiles": profiles, "callback_delay": str(delay), "heft_waits": int(heft_waits)}
+    return _native.query(req)["simulate"]
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_heft_waits_product_matches_restatement(seed):
+    rng = random.Random(7000 + seed)
+    cpu = seed % 2 == 0
+    text, params = layered_dag(seed + 300, max_kernels=14, devices=2, cpu_frac=0.4 if cpu else 0.0)
+    cpu_devices = [1] if cpu else []
+    profs = _random_profiles(rng, text, 2, cpu_devices)
+    delay = rng.choice(["0", "1/2", "3"])
+    try:
+        orc = OS.simulate(text, params, profs, policy="heft", cpu_devices=cpu_devices, callback_delay=Fraction(delay),
+                          heft_waits=True)
+    except Exception as e:  # the product must fail the same way
+        with pytest.raises(_native.HetsimError) as pe:
+            simulate(text, params, profs, "heft", cpu_devices, delay, heft_waits=True)
+        assert pe.value.errc == getattr(e, "errc", type(e).__name__)
+        return
+    _same(simulate(text, params, profs, "heft", cpu_devices, delay, heft_waits=True), orc)
+
+
+def _two_kernels():
+    """k0 and k1 independent, one component each; device 0 = GPU, device 1 = CPU. k0
+    prefers the CPU, so its rank (its CPU time) puts it first."""
+    ks = [kernel(0, [(0, "1")], [(1, "1")], dev="cpu"), kernel(1, [(0, "1")], [(1, "1")])]
+    doc = {"kernels": ks, "tc": [[0], [1]], "cq": [{"device": 0, "queues": 1}, {"device": 1, "queues": 1}],
+           "depends": []}
+    return json.dumps(doc), {}
+
+
+def _gpu_cpu(gpu_t, cpu_t):
+    fast = {"copy_channels": 1, "bandwidth": "1000000000000", "transfer_latency": "0"}
+    return [{"device": 0, "type": "gpu", "kernel_times": {str(k): str(v) for k, v in gpu_t.items()}, **fast},
+            {"device": 1, "type": "cpu", "kernel_times": {str(k): str(v) for k, v in cpu_t.items()}, **fast}]
+
+
+@pytest.mark.parametrize("gpu_busy,expect_waits", [(10, 1), (3, 0)])
+def test_heft_eft_examples(gpu_busy, expect_waits):
+    """k0 occupies the GPU for `gpu_busy` ms; k1 takes 5 ms on the GPU
+    and 12 on the CPU. Strict availability puts k1 on the idle CPU. With heft_waits,
+    EFT(gpu) = gpu_busy + 5: 15 > 12 -> CPU, 8 < 12 -> wait for the GPU."""
+    text, params = _two_kernels()
+    profs = _gpu_cpu({0: gpu_busy, 1: 5}, {0: 1000, 1: 12})
+    strict = simulate(text, params, profs, "heft", [1])
+    waits = simulate(text, params, profs, "heft", [1], heft_waits=True)
+    assert [list(d) for d in strict["dispatches"]] == [[0, 0], [1, 1]]
+    assert [list(d) for d in waits["dispatches"]] == [[0, 0], [1, expect_waits]]
+    if expect_waits == 0:  # k1 runs after k0 on the GPU
+        assert Fraction(waits["makespan"]) < Fraction(strict["makespan"])
+        ndr = [r for r in waits["trace"] if r["kind"] == "ndrange"]
+        assert Fraction(ndr[1]["start"]) >= Fraction(ndr[0]["finish"])
+
+
+def _criterion7_profiles(doc, cpu_dev, gpu_dev, ratio=20):
+    role = {k["id"]: ("gemm" if k["name"].startswith("gemm") else k["name"]) for k in doc["kernels"]}
+    gpu_t = {"gemm": Fraction(1), "transpose": Fraction(1, 4), "softmax": Fraction(1, 2)}
+    cpu_t = {**gpu_t, "gemm": ratio * gpu_t["gemm"]}
+    fast = {"copy_channels": 2, "bandwidth": "1000000000", "transfer_latency": "1/100"}
+    return [{"device": gpu_dev, "type": "gpu", "kernel_times": {str(k): str(gpu_t[r]) for k, r in role.items()},
+             "kernel_share": {str(k): "1/2" for k in role}, **fast},
+            {"device": cpu_dev, "type": "cpu", "copy_channels": 1, "bandwidth": "1000000000", "transfer_latency": "0",
+             "kernel_times": {str(k): str(cpu_t[r]) for k, r in role.items()}}]
+
+
+def test_acceptance_7_policy_ordering():
+    """SPEC.md:566 / Fig. 12: 16 heads, t_cpu(GEMM) = 20 t_gpu(GEMM) (other nodes
+    equally fast on both), callback delay 1/2 ms. Eager and HEFT see one component per
+    kernel and one queue per device; device 0 is the CPU, so eager's
+    lowest-id rule sends GEMMs there. HEFT is the paper's EFT with busy devices
+    (heft_waits, "the execution time of a kernel currently executing on
+    d"); under strict availability HEFT and eager place the same work and tie.
+    Clustering keeps a head per component; its best mc over q_gpu in 1..4 and 0-1
+    CPU heads is compared."""
+    H, delay = 16, "1/2"
+    text, params = workloads.head_dag(heads=H, beta=64, tc_mode="per_kernel", queues=1)
+    doc = json.loads(text)
+    doc["cq"] = [{"device": 0, "queues": 1}, {"device": 1, "queues": 1}]  # 0 = CPU, 1 = GPU
+    per_kernel = json.dumps(doc)
+    profs = _criterion7_profiles(doc, cpu_dev=0, gpu_dev=1)
+    eager = Fraction(simulate(per_kernel, params, profs, "eager", [0], delay)["makespan"])
+    heft = Fraction(simulate(per_kernel, params, profs, "heft", [0], delay)["makespan"])
+    heft_w = Fraction(simulate(per_kernel, params, profs, "heft", [0], delay, heft_waits=True)["makespan"])
+    best = None
+    for q_gpu in range(1, 5):
+        for h_cpu in (0, 1):
+            t2, p2 = workloads.head_dag(heads=H, beta=64, tc_mode="per_head", queues=q_gpu)
+            d2 = json.loads(t2)
+            per_head = len(d2["kernels"]) // H
+            for k in d2["kernels"]:
+                if k["id"] // per_head < h_cpu:
+                    k["dev"] = "cpu"
+            d2["cq"] = [{"device": 0, "queues": 1}, {"device": 1, "queues": q_gpu}]
+            m = Fraction(simulate(json.dumps(d2), p2, _criterion7_profiles(d2, 0, 1), "clustering", [0],
+                                  delay)["makespan"])
+            best = m if best is None else min(best, m)
+    assert best < heft_w < eager, (float(best), float(heft_w), float(eager))
+    assert heft == eager  # strict availability: the two place the same work
+
+
+def _audit_work(text, params, profiles, trace):
+    """∫ rate dt over each ndrange's lifetime == its standalone time,
+    with rate = 1 / max(1, sigma) and sigma = the summed shares of the ndranges
+    running on the device at that moment."""
+    prof = {p["device"]: p for p in profiles}
+    ndr = [r for r in trace if r["kind"] == "ndrange"]
+    for r in ndr:
+        p = prof[r["device"]]
+        share = lambda k: Fraction(p.get("kernel_share", {}).get(str(k), "1"))  # noqa: E731
+        same_dev = [x for x in ndr if x["device"] == r["device"]]
+        s, f = Fraction(r["start"]), Fraction(r["finish"])
+        cuts = sorted({s, f} | {Fraction(x[e]) for x in same_dev for e in ("start", "finish")
+                                if s < Fraction(x[e]) < f})
+        work = Fraction(0)
+        for a, b in zip(cuts, cuts[1:]):
+            sigma = sum(share(x["kernel"]) for x in same_dev if Fraction(x["start"]) <= a and Fraction(x["finish"]) >= b)
+            work += (b - a) / max(Fraction(1), sigma)
+        assert work == Fraction(p["kernel_times"][str(r["kernel"])]), (r, work)
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_acceptance_8_work_conservation_and_determinism(seed):
+    rng = random.Random(9000 + seed)
+    cpu = seed % 3 == 0
+    text, params = layered_dag(seed + 500, max_kernels=14, devices=2, cpu_frac=0.4 if cpu else 0.0)
+    cpu_devices = [1] if cpu else []
+    profs = _random_profiles(rng, text, 2, cpu_devices)
+    policy = ["clustering", "eager", "heft"][seed % 3]
+    delay = rng.choice(["0", "1/2"])
+    try:
+        a = simulate(text, params, profs, policy, cpu_devices, delay)
+    except _native.HetsimError:
+        return  # e.g. a profile-less device type for the policy: not a trace
+    b = simulate(text, params, profs, policy, cpu_devices, delay)
+    assert a == b  # bit-identical repeated runs
+    _audit_work(text, params, profs, a["trace"])
