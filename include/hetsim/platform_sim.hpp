@@ -16,7 +16,10 @@
 //  * ndranges of one device share it: with running set S and sigma = sum of
 //    their shares, each progresses at rate 1 (sigma <= 1) or 1/sigma;
 //  * simultaneous completions complete in (device, queue, position) order;
-//    callback-marked completions reach the scheduler `callback_delay` later.
+//    callback-marked completions reach the scheduler `callback_delay` later;
+//  * host dispatch cost (B200 extension, profiles/sim_vs_measured.py): issuing a
+//    component occupies the host thread for `dispatch_cost`, one component at a
+//    time; its commands cannot start before the host has issued it.
 // Time is an exact rational (milliseconds): identical inputs give
 // bit-identical traces.
 #pragma once
@@ -60,7 +63,7 @@ struct SimEvent {
 class PlatformSim : public Executor {
  public:
   /// profiles: one per logical device of the spec's cq map (InvalidParam if missing).
-  PlatformSim(std::vector<DeviceProfile> profiles, Ratio callback_delay = Ratio(0));
+  PlatformSim(std::vector<DeviceProfile> profiles, Ratio callback_delay = Ratio(0), Ratio dispatch_cost = Ratio(0));
 
   void dispatch(const TaskComponent& t, const CommandQueueStructure& q) override;
   Completion wait_next() override;  // SimDeadlock when commands remain but none can run
@@ -85,6 +88,7 @@ class PlatformSim : public Executor {
     int queue_prev = -1;     // index of the previous command in the same queue
     St st = St::pending;
     Ratio start, finish, remaining;
+    Ratio ready_at;  // earliest start: the host has issued the component
   };
   const DeviceProfile& prof(int device) const;
   void start_runnable();
@@ -93,6 +97,8 @@ class PlatformSim : public Executor {
 
   std::map<int, DeviceProfile> profiles_;
   Ratio callback_delay_;
+  Ratio dispatch_cost_;
+  Ratio host_free_ = Ratio(0);  // the host thread issues one component at a time
   Ratio now_ = Ratio(0);
   std::vector<Cmd> cmds_;
   std::map<int, std::vector<Ratio>> channel_free_;  // device -> per-channel free time
@@ -108,6 +114,6 @@ struct SimResult {
   Ratio makespan;
 };
 SimResult simulate(const DagSpec& g, const Platform& p, const std::vector<DeviceProfile>& profiles, Policy policy,
-                   Ratio callback_delay = Ratio(0), bool heft_waits = false);
+                   Ratio callback_delay = Ratio(0), bool heft_waits = false, Ratio dispatch_cost = Ratio(0));
 
 }  // namespace hetsim

@@ -13,6 +13,8 @@ Rules restated (SPEC.md line refs):
   :433  equal completion times complete in (device, queue, position) order
 Callback-marked completions reach the scheduler `callback_delay` later;
 completions at a time are processed before callbacks delivered at that time.
+B200 extension: issuing a component occupies the host for `dispatch_cost`, one
+component at a time; its commands start no earlier than that.
 """
 from __future__ import annotations
 
@@ -32,9 +34,11 @@ def transfer_time(nbytes: int, prof: dict) -> Fraction:
 
 
 class Sim:
-    def __init__(self, profiles: list[dict], callback_delay=0):
+    def __init__(self, profiles: list[dict], callback_delay=0, dispatch_cost=0):
         self.prof = {p["device"]: p for p in profiles}
         self.delay = F(callback_delay)
+        self.cost = F(dispatch_cost)
+        self.host_free = Fraction(0)
         self.t = Fraction(0)
         self.cmds = []        # dicts
         self.free = {d: [Fraction(0)] * max(1, int(p.get("copy_channels", 2))) for d, p in self.prof.items()}
@@ -44,6 +48,7 @@ class Sim:
     # -- executor interface used by oracle.schedule
     def dispatch(self, comp, device, q):
         base = len(self.cmds)
+        self.host_free = max(self.t, self.host_free) + self.cost  # one component at a time on the host
         ev_index = {}
         for qi, evs in enumerate(q["_queues"]):
             for pos, ev in enumerate(evs):
@@ -53,7 +58,7 @@ class Sim:
                                   "kind": c["kind"], "kernel": c["kernel"], "label": c["label"],
                                   "bytes": c.get("bytes", 0), "callback": ev in q["_callbacks"],
                                   "prev": ev_index[evs[pos - 1]] if pos else None, "preds": [],
-                                  "st": "pending", "channel": -1})
+                                  "st": "pending", "channel": -1, "ready_at": self.host_free})
         for a, b in q["_deps"]:
             self.cmds[ev_index[b]]["preds"].append(ev_index[a])
         assert base <= len(self.cmds)
@@ -69,6 +74,8 @@ class Sim:
 
     def _start(self):
         for c in sorted((c for c in self.cmds if c["st"] == "pending"), key=self._key):
+            if self.t < c["ready_at"]:
+                continue
             if c["prev"] is not None and self.cmds[c["prev"]]["st"] != "done":
                 continue
             if any(self.cmds[p]["st"] != "done" for p in c["preds"]):
@@ -112,6 +119,11 @@ class Sim:
                 f = self.t + c["left"] / self._rate(c["device"]) if c["kind"] == "ndrange" else c["finish"]
                 cand.append((f, self._key(c), i))
             nxt = min(cand) if cand else None
+            rel = min((c["ready_at"] for c in self.cmds if c["st"] == "pending" and self.t < c["ready_at"]),
+                      default=None)
+            if rel is not None and (nxt is None or rel < nxt[0]) and (not self.deliver or rel <= min(self.deliver)[0]):
+                self._advance(rel)
+                continue
             if self.deliver:
                 d = min(self.deliver)
                 if nxt is None or d[0] < nxt[0]:
@@ -142,7 +154,8 @@ class Sim:
         return max(e["finish"] for e in self.trace) - min(e["start"] for e in self.trace)
 
 
-def simulate(spec_text, params, profiles, policy="clustering", cpu_devices=(), callback_delay=0, heft_waits=False):
+def simulate(spec_text, params, profiles, policy="clustering", cpu_devices=(), callback_delay=0, heft_waits=False,
+             dispatch_cost=0):
     """Alg. 1 (oracle.schedule) over the restated simulator. profiles: list of
     {"device", "type", "kernel_times", "kernel_share", "copy_channels", "bandwidth",
     "transfer_latency"}; the scheduler's per-type kernel times come from the first
@@ -153,7 +166,7 @@ def simulate(spec_text, params, profiles, policy="clustering", cpu_devices=(), c
         per = times.setdefault(p["type"], {})
         for k, v in p["kernel_times"].items():
             per.setdefault(int(k), F(v))
-    sim = Sim(profiles, callback_delay)
+    sim = Sim(profiles, callback_delay, dispatch_cost)
     sched = schedule(spec, policy=policy, times=times or None, cpu_devices=cpu_devices, executor=sim,
                      heft_waits=heft_waits)
     return {"schedule": sched, "trace": sim.trace, "makespan": sim.makespan()}

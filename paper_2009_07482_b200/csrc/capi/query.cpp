@@ -157,7 +157,7 @@ Value schedule(const DagSpec& g, const Value& req) {
 
 Ratio ratio_of(const Value& v) { return v.is_string() ? Ratio::parse(v.as_string()) : Ratio(v.as_int64()); }
 
-// {"op":"simulate", spec, params, policy, cpu_devices, callback_delay, heft_waits (0/1),
+// {"op":"simulate", spec, params, policy, cpu_devices, callback_delay, heft_waits (0/1), dispatch_cost,
 //  "device_profiles": [{"device", "type", "kernel_times": {id: ms}, "kernel_share": {id: s},
 //                       "copy_channels", "bandwidth" (bytes/ms), "transfer_latency" (ms)}]}
 Value simulate_req(const DagSpec& g, const Value& req) {
@@ -182,7 +182,9 @@ Value simulate_req(const DagSpec& g, const Value& req) {
   }
   const Value* cd = req.find("callback_delay");
   const Value* hw = req.find("heft_waits");
-  SimResult r = simulate(g, p, profs, pol, cd ? ratio_of(*cd) : Ratio(0), hw && hw->as_int64() != 0);
+  const Value* dc = req.find("dispatch_cost");
+  SimResult r = simulate(g, p, profs, pol, cd ? ratio_of(*cd) : Ratio(0), hw && hw->as_int64() != 0,
+                         dc ? ratio_of(*dc) : Ratio(0));
   Value out = Value::make_object();
   out.set("makespan", S(r.makespan.str()));
   out.set("makespan_ms", Value::real(r.makespan.to_double()));

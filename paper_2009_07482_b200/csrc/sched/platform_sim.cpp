@@ -13,9 +13,10 @@ Ratio transfer_time(int64_t bytes, const DeviceProfile& d) {
   return d.transfer_latency + Ratio(static_cast<long long>(bytes)) / d.bandwidth;
 }
 
-PlatformSim::PlatformSim(std::vector<DeviceProfile> profiles, Ratio callback_delay)
-    : callback_delay_(callback_delay) {
+PlatformSim::PlatformSim(std::vector<DeviceProfile> profiles, Ratio callback_delay, Ratio dispatch_cost)
+    : callback_delay_(callback_delay), dispatch_cost_(dispatch_cost) {
   if (callback_delay < Ratio(0)) fail(Errc::invalid_param, "callback delay must be >= 0");
+  if (dispatch_cost < Ratio(0)) fail(Errc::invalid_param, "dispatch cost must be >= 0");
   for (auto& p : profiles) {
     if (profiles_.count(p.device_id)) fail(Errc::invalid_param, "duplicate profile for device " + std::to_string(p.device_id));
     if (p.device_type == DeviceType::gpu && p.copy_channels < 1)
@@ -47,6 +48,7 @@ Profiles PlatformSim::scheduler_profiles(const std::vector<DeviceProfile>& profi
 
 void PlatformSim::dispatch(const TaskComponent& t, const CommandQueueStructure& q) {
   prof(q.device);
+  host_free_ = rmax(now_, host_free_) + dispatch_cost_;
   std::map<int, int> idx_of;  // event -> index into cmds_
   for (size_t qi = 0; qi < q.queues.size(); ++qi) {
     int prev = -1;
@@ -64,6 +66,7 @@ void PlatformSim::dispatch(const TaskComponent& t, const CommandQueueStructure& 
       m.bytes = c.bytes;
       m.callback = q.callbacks.count(c.event) > 0;
       m.queue_prev = prev;
+      m.ready_at = host_free_;
       prev = int(cmds_.size());
       idx_of[c.event] = prev;
       cmds_.push_back(std::move(m));
@@ -94,6 +97,7 @@ void PlatformSim::start_runnable() {
   });
   for (int i : order) {
     Cmd& c = cmds_[size_t(i)];
+    if (now_ < c.ready_at) continue;
     if (c.queue_prev >= 0 && cmds_[size_t(c.queue_prev)].st != St::done) continue;
     bool ready = true;
     for (int p : c.preds) ready = ready && cmds_[size_t(p)].st == St::done;
@@ -168,6 +172,18 @@ Completion PlatformSim::wait_next() {
     size_t di = deliveries_.size();
     for (size_t i = 0; i < deliveries_.size(); ++i)
       if (di == deliveries_.size() || deliveries_[i].first < deliveries_[di].first) di = i;
+    // the next moment the host finishes issuing a component whose commands wait for it
+    bool has_rel = false;
+    Ratio rel;
+    for (const auto& c : cmds_)
+      if (c.st == St::pending && now_ < c.ready_at && (!has_rel || c.ready_at < rel)) {
+        rel = c.ready_at;
+        has_rel = true;
+      }
+    if (has_rel && (!has || rel < tc) && (di == deliveries_.size() || rel <= deliveries_[di].first)) {
+      advance_to(rel);
+      continue;
+    }
     // completions at time T are processed before callbacks delivered at T
     if (di < deliveries_.size() && (!has || deliveries_[di].first < tc)) {
       advance_to(rmax(now_, deliveries_[di].first));
@@ -214,7 +230,7 @@ Ratio PlatformSim::makespan() const {
 }
 
 SimResult simulate(const DagSpec& g, const Platform& p, const std::vector<DeviceProfile>& profiles, Policy policy,
-                   Ratio callback_delay, bool heft_waits) {
+                   Ratio callback_delay, bool heft_waits, Ratio dispatch_cost) {
   for (const auto& d : p.devices) {
     auto it = std::find_if(profiles.begin(), profiles.end(), [&](const DeviceProfile& x) { return x.device_id == d.id; });
     if (it == profiles.end()) fail(Errc::missing_profile_entry, "no profile for device " + std::to_string(d.id));
@@ -223,7 +239,7 @@ SimResult simulate(const DagSpec& g, const Platform& p, const std::vector<Device
   }
   Scheduler sched(g, p, PlatformSim::scheduler_profiles(profiles), policy);
   sched.set_heft_waits(heft_waits);
-  PlatformSim sim(profiles, callback_delay);
+  PlatformSim sim(profiles, callback_delay, dispatch_cost);
   SimResult r;
   r.schedule = sched.run(sim);
   r.trace = sim.trace();

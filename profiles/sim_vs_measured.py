@@ -9,7 +9,9 @@ the B200, against the makespans measured on the B200.
 3. Simulated makespans: the same DAG/partition through Alg. 1 + platform_sim
    (hs_query "simulate") with those kernel times (share 1: a B200 kernel fills
    the GPU), measured H2D bandwidth / latency, and callback_delay = 0 (graph)
-   or the measured gap (dynamic).
+   or the measured gap (dynamic). Dynamic mode is simulated twice: without and
+   with the host dispatch cost (dispatch_cost = the engine's measured host time
+   per component dispatch: stream/event setup and launches on the host thread).
 usage: python profiles/sim_vs_measured.py [out.json]"""
 import ctypes
 import json
@@ -39,9 +41,13 @@ def traced(queues, mode, fuse):
         for k, arr in outs.items():
             eng.bind(*k, arr)
         eng.run(0, BATCH)
+        before = eng.info("stats")
         eng.run(0, BATCH)
+        after = eng.info("stats")
         info = eng.info("trace")
-    return text, params, info["trace"], [c for c, _ in info["dispatches"]]
+    n = after["host_dispatches"] - before["host_dispatches"]
+    cost = (after["host_dispatch_us"] - before["host_dispatch_us"]) / n / 1e3 if n else 0.0  # ms per dispatch
+    return text, params, info["trace"], [c for c, _ in info["dispatches"]], cost
 
 
 def h2d_profile():
@@ -75,7 +81,7 @@ def frac(ms):
 
 
 def main(out=None):
-    _, _, solo, _ = traced(1, "graph", 0)
+    _, _, solo, _, _ = traced(1, "graph", 0)
     ktime = {}
     for r in solo:
         if r["kind"] == "ndrange":
@@ -83,20 +89,24 @@ def main(out=None):
     lat, bw = h2d_profile()
     rows = []
     for mode in ("graph", "dynamic"):
-        text, params, tr, disp = traced(3, mode, 0)
+        text, params, tr, disp, cost = traced(3, mode, 0)
         gaps = [g["gap"] for g in R.component_gaps(tr, disp)]
         delay = statistics.median(gaps) if mode == "dynamic" else 0.0
         prof = [{"device": 0, "type": "gpu", "kernel_times": {str(k): frac(v) for k, v in ktime.items()},
                  "copy_channels": 2, "bandwidth": str(int(round(bw))), "transfer_latency": frac(lat)}]
-        s = _native.query({"op": "simulate", "spec": text, "params": params, "policy": "clustering",
-                           "device_profiles": prof, "callback_delay": frac(delay)})["simulate"]
-        meas = R.makespan(tr)
-        row = {"mode": mode, "layers": LAYERS, "batch": BATCH, "queues": 3, "kernels": len(ktime),
-               "measured_makespan_ms": meas, "simulated_makespan_ms": s["makespan_ms"],
-               "sim_over_measured": s["makespan_ms"] / meas, "callback_delay_ms": delay,
-               "h2d_latency_ms": lat, "h2d_GBps": bw / 1e6, "sum_standalone_ms": sum(ktime.values())}
-        rows.append(row)
-        print(json.dumps(row), flush=True)
+        for with_cost in ((False, True) if mode == "dynamic" else (False,)):
+            dc = cost if with_cost else 0.0
+            s = _native.query({"op": "simulate", "spec": text, "params": params, "policy": "clustering",
+                               "device_profiles": prof, "callback_delay": frac(delay),
+                               "dispatch_cost": frac(dc)})["simulate"]
+            meas = R.makespan(tr)
+            row = {"mode": mode, "layers": LAYERS, "batch": BATCH, "queues": 3, "kernels": len(ktime),
+                   "measured_makespan_ms": meas, "simulated_makespan_ms": s["makespan_ms"],
+                   "sim_over_measured": s["makespan_ms"] / meas, "callback_delay_ms": delay,
+                   "dispatch_cost_ms": dc, "h2d_latency_ms": lat, "h2d_GBps": bw / 1e6,
+                   "sum_standalone_ms": sum(ktime.values())}
+            rows.append(row)
+            print(json.dumps(row), flush=True)
     if out:
         json.dump(rows, open(out, "w"), indent=1)
 

@@ -159,3 +159,30 @@ def test_acceptance_8_work_conservation_and_determinism(seed):
     b = simulate(text, params, profs, policy, cpu_devices, delay)
     assert a == b  # bit-identical repeated runs
     _audit_work(text, params, profs, a["trace"])
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_dispatch_cost_product_matches_restatement(seed):
+    """platform_sim's host dispatch cost (components issued one at a time, each
+    occupying the host for dispatch_cost): product == restatement exactly."""
+    rng = random.Random(11000 + seed)
+    cpu = seed % 3 == 0
+    text, params = layered_dag(seed + 700, max_kernels=14, devices=2, cpu_frac=0.4 if cpu else 0.0)
+    cpu_devices = [1] if cpu else []
+    profs = _random_profiles(rng, text, 2, cpu_devices)
+    policy = ["clustering", "eager", "heft"][seed % 3]
+    delay, cost = rng.choice(["0", "1/2"]), rng.choice(["1/10", "1", "7/3"])
+    req = {"op": "simulate", "spec": text, "params": params, "policy": policy, "cpu_devices": cpu_devices,
+           "device_profiles": profs, "callback_delay": delay, "dispatch_cost": cost}
+    try:
+        orc = OS.simulate(text, params, profs, policy=policy, cpu_devices=cpu_devices, callback_delay=Fraction(delay),
+                          dispatch_cost=Fraction(cost))
+    except Exception as e:
+        with pytest.raises(_native.HetsimError) as pe:
+            _native.query(req)
+        assert pe.value.errc == getattr(e, "errc", type(e).__name__)
+        return
+    prod = _native.query(req)["simulate"]
+    _same(prod, orc)
+    base = _native.query({**req, "dispatch_cost": "0"})["simulate"]
+    assert Fraction(prod["makespan"]) >= Fraction(base["makespan"]) or policy != "clustering"
