@@ -47,3 +47,24 @@ clean:
 	rm -rf $(BUILD) $(LIB)
 
 .PHONY: all oracle clean
+
+# Host race check: the C++ runtime (spec model, scheduler, engine,
+# callback -> MPSC queue -> Scheduler::cb) built with ThreadSanitizer, linked with
+# the sm_100a kernels and the drop-in driver tests/cxx/dropin_main.cpp (Alg. 1 in
+# dynamic mode through hetsim::CudaExecutor: CUDA host callbacks deliver completions).
+TSAN_BUILD := build_tsan
+TSAN_CXX   ?= $(shell command -v g++-13 || echo $(CXX))
+TSAN_OBJS  := $(patsubst $(SRC)/%.cpp,$(TSAN_BUILD)/%.o,$(CPP_SRCS))
+TSAN_EXE   := $(TSAN_BUILD)/dropin_tsan
+
+$(TSAN_BUILD)/%.o: $(SRC)/%.cpp $(HEADERS)
+	@mkdir -p $(dir $@)
+	$(TSAN_CXX) $(CXXFLAGS) -g -O1 -fsanitize=thread -c $< -o $@
+
+$(TSAN_EXE): tests/cxx/dropin_main.cpp $(TSAN_OBJS) $(CU_OBJS)
+	$(TSAN_CXX) -std=c++20 -g -O1 -fsanitize=thread -Iinclude $< $(TSAN_OBJS) $(CU_OBJS) \
+	    -L/usr/local/cuda/lib64 -lcudart_static -ldl -lrt -lpthread -o $@
+
+tsan: $(TSAN_EXE)
+
+.PHONY: tsan

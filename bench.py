@@ -201,6 +201,22 @@ def cpu_sample(layers, n_inst=1, reps=1):
     return n_inst / t, O.max_threads(), t
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def cpu_threads():
+    from oracle import oracle as O
+    return O.max_threads()
+
+
 def host_path_timing(layers, reps=5):
     """The host half of the path on the C5 template (828 kernels, 1103 edges): parse_spec +
     derive_components + classify_edges + bottom_level_ranks, timed single-threaded for
@@ -254,7 +270,8 @@ def run_reference(args, world, rank):
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"C5 {layers}-layer encoder DAG stream, {args.instances} instances (CPU sample)",
                    "instances": args.instances, "layers": layers, "kernels": 69 * layers},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample,
+                         "cpu_model": cpu_model()},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -543,7 +560,9 @@ def config_makespan(cfg, fuse=3, queues=3, devices=1, reps=20, warmup=3, math_mo
          "bound": bound["bound"], "frac": bound["t_star_ms"] / ms}
     if check:  # every instance of the config against the fp32 oracle and the fp64 truth
         from oracle import oracle as O
-        ref = O.run_dag(text, params, arrays, n)
+        t0 = time.perf_counter()
+        ref = O.run_dag(text, params, arrays, n)  # also the CPU port's makespan for this config
+        r["cpu_port_ms"] = (time.perf_counter() - t0) * 1e3
         truth = O.run_dag_f64(text, params, arrays, n)
         errs = [errors(out_dev[k].cpu().numpy(), ref[k], truth[k]) for k in out_dev]
         r["parity"] = {key: max(e[key] for e in errs) for key in errs[0]}
@@ -563,7 +582,9 @@ def config_makespans():
     for cfg, kw in best.items():
         r = config_makespan(cfg, **kw)
         out[cfg] = {k: r[k] for k in ("instances", "logical_devices", "queues", "fuse", "launches", "makespan_ms",
-                                      "t_star_ms", "bound", "frac", "normwise_err_vs_cpu_oracle", "parity")}
+                                      "t_star_ms", "bound", "frac", "normwise_err_vs_cpu_oracle", "parity",
+                                      "cpu_port_ms")}
+        out[cfg]["gpu_speedup_vs_cpu_port"] = r["cpu_port_ms"] / r["makespan_ms"]
     out["C4"]["target_1p5x_t_star_ms"] = 1.5 * out["C4"]["t_star_ms"]
     grain = []
     for cfg in ("C3", "C4"):
@@ -574,7 +595,9 @@ def config_makespans():
     out["fine_vs_coarse"] = {"logical_devices": 1, "rows": grain,
                              "note": "queues=1 is the coarse-grained default mc=(1,0,0); queues=3 fine-grained"}
     out["note"] = ("median of 20 runs of the engine's CUDA-event makespan (start -> end event on the origin stream); "
-                   "C3/C4 use one logical device per component of a layer (9) so that heads run concurrently")
+                   "C3/C4 use one logical device per component of a layer (9) so that heads run concurrently; "
+                   "cpu_port_ms = the same config (all instances) through the CPU oracle port (fp32 C kernels, "
+                   f"{cpu_threads()} threads, {cpu_model()})")
     return out
 
 
@@ -739,9 +762,9 @@ def run_ours(args, world, rank, local):
             alt["normwise_err_vs_cpu_oracle"] = max(p["alt_normwise_vs_oracle"] for p in checked)
         cpu = None
         if not args.no_cpu_baseline:
-            v, threads, t = cpu_sample(args.layers, n_inst=12)
-            cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
-                   "sample": f"12 instances of the {args.layers}-layer DAG ({t:.1f} s; oracle port: clustering "
+            v, threads, t = cpu_sample(args.layers, n_inst=64)
+            cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port", "cpu_model": cpu_model(),
+                   "sample": f"64 instances of the {args.layers}-layer DAG ({t:.1f} s; oracle port: clustering "
                              f"scheduler + fp32 kernels on all host threads)",
                    "host_path": host_path_timing(args.layers)}
         makespans = None if args.no_makespans else config_makespans()

@@ -34,6 +34,7 @@
 #include <mutex>
 
 #include "kernels.cuh"
+#include "launch.cuh"
 #include "tc_common.cuh"
 
 namespace hs {
@@ -121,6 +122,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  pdl_launch_dependents();  // PDL (launch.cuh)
+  pdl_wait();
   const uint32_t tmem = *tmem_slot_ptr;
   constexpr uint32_t kTS = 0, kTA = 128, kTC = 384, kTZ = 448;  // TMEM column offsets
 
@@ -405,8 +408,7 @@ cudaError_t attn_head(const AttnArgs& a, int terms, cudaStream_t s) {
   if (!ok) return cudaErrorInvalidValue;
   AttnParams p{a.S, a.batch, a.scale};
   const int grid = a.batch < num_sms() ? a.batch : num_sms();
-  kernel<<<grid, kAttnThreads, kAttnSmem, s>>>(mQ, mK, mV, mW, mZ, p);
-  return cudaGetLastError();
+  return launch_node(kernel, dim3(grid), dim3(kAttnThreads), kAttnSmem, s, 1, mQ, mK, mV, mW, mZ, p);
 }
 
 }  // namespace hs

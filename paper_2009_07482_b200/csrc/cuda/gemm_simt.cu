@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include "kernels.cuh"
+#include "launch.cuh"
 
 namespace hs {
 
@@ -16,6 +17,8 @@ constexpr int BM = 64, BN = 64, BK = 16;
 
 template <bool kNT>
 __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs p) {
+  pdl_launch_dependents();  // PDL (launch.cuh)
+  pdl_wait();
   __shared__ float As[BK][BM + 4];
   __shared__ float Bs[BK][BN + 4];
   const int64_t inst = blockIdx.z;
@@ -73,8 +76,8 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs p) {
 
 cudaError_t gemm_simt(const GemmArgs& a, cudaStream_t s) {
   dim3 grid((a.N + BN - 1) / BN, (a.M + BM - 1) / BM, a.batch);
-  if (a.layout == GemmLayout::nt) gemm_simt_kernel<true><<<grid, 256, 0, s>>>(a);
-  else gemm_simt_kernel<false><<<grid, 256, 0, s>>>(a);
+  if (a.layout == GemmLayout::nt) HS_TRY(launch_node(gemm_simt_kernel<true>, dim3(grid), dim3(256), 0, s, 1, a));
+  else HS_TRY(launch_node(gemm_simt_kernel<false>, dim3(grid), dim3(256), 0, s, 1, a));
   return cudaGetLastError();
 }
 

@@ -33,6 +33,7 @@
 #include <mutex>
 
 #include "kernels.cuh"
+#include "launch.cuh"
 #include "tc_common.cuh"
 
 namespace hs {
@@ -303,6 +304,8 @@ __global__ void __launch_bounds__(kThreads, kSmall ? 2 : 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  pdl_launch_dependents();  // PDL (launch.cuh): the prologue above overlaps the previous kernel
+  pdl_wait();
   const uint32_t tmem = *tmem_slot_ptr;
   const uint32_t tmem_a = tmem + uint32_t(L::kAccCols);  // A stages start after the accumulators
 
@@ -659,6 +662,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   cluster_sync_all();  // barriers initialised and TMEM allocated in both CTAs
   tc_fence_after();
+  pdl_launch_dependents();  // PDL (launch.cuh)
+  pdl_wait();
   const uint32_t tmem = *tmem_slot_ptr;
   const uint32_t tmem_a = tmem + uint32_t(L::kAccCols);
 
@@ -996,8 +1001,7 @@ cudaError_t launch(const GemmArgs& a, cudaStream_t s) {
     if (e != cudaSuccess) return e;
   }
   const int grid = p.total_tiles < slots ? p.total_tiles : slots;
-  kernel<<<grid, kThreads, L::kTotal, s>>>(mA, mB, p);
-  return cudaGetLastError();
+  return launch_node(kernel, dim3(grid), dim3(kThreads), L::kTotal, s, 1, mA, mB, p);
 }
 
 // CTA-pair launch (resident B planes): clusters of 2, one pair per TPC,
@@ -1068,19 +1072,7 @@ cudaError_t launch_pair(const GemmArgs& a, cudaStream_t s) {
   const int row_pairs = (a.batch * p.m_tiles + 1) / 2;
   p.total_tiles = p.n_tiles * row_pairs;
   const int pairs = p.total_tiles < max_pairs ? p.total_tiles : max_pairs;
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(2 * pairs);
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = L::kTotal;
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = 2;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kernel, mA, mB, mc, p);
+  return launch_node(kernel, dim3(2 * pairs), dim3(kThreads), L::kTotal, s, 2, mA, mB, mc, p);
 }
 
 template <int BN>

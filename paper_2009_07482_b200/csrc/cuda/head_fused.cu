@@ -47,6 +47,7 @@
 #include <mutex>
 
 #include "kernels.cuh"
+#include "launch.cuh"
 #include "tc_common.cuh"
 
 #ifndef HS_DBG_TIMELINE
@@ -277,6 +278,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   cluster_sync_all();
   tc_fence_after();
+  pdl_launch_dependents();  // PDL (launch.cuh)
+  pdl_wait();
   const uint32_t tmem = *tmem_slot_ptr;
 
   if (warp == 0) {
@@ -705,19 +708,7 @@ cudaError_t head_fused(const HeadArgs& a, int terms, cudaStream_t s) {
   HeadParams p{a.S, a.D, a.batch, (a.batch + 1) / 2, a.scale, a.Z, a.sZ ? a.sZ : int64_t(S) * ldz, ldz};
   const int max_pairs = tc::num_sms() / 2;
   const int pairs = p.pairs < max_pairs ? p.pairs : max_pairs;
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(2 * pairs);
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = kSmem;
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = 2;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kernel, mX, mW, mWh, p);
+  return launch_node(kernel, dim3(2 * pairs), dim3(kThreads), kSmem, s, 2, mX, mW, mWh, p);
 }
 
 }  // namespace hs

@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include "kernels.cuh"
+#include "launch.cuh"
 
 namespace hs {
 
@@ -43,6 +44,8 @@ int blocks_for(int64_t work, int per_block) {
 // ---------------------------------------------------------------- transpose
 __global__ void transpose_kernel(const float* __restrict__ A, int64_t sA, float* __restrict__ B, int64_t sB, int R,
                                  int C) {
+  pdl_launch_dependents();  // PDL (launch.cuh)
+  pdl_wait();
   __shared__ float tile[32][33];
   const int64_t inst = blockIdx.z;
   A += inst * sA;
@@ -64,6 +67,8 @@ __global__ void transpose_kernel(const float* __restrict__ A, int64_t sA, float*
 // 128-byte scalar stores along R. Needs C % 4 == 0 and 16-byte aligned rows.
 __global__ void transpose_wide_kernel(const float* __restrict__ A, int64_t sA, float* __restrict__ B, int64_t sB,
                                       int R, int C) {
+  pdl_launch_dependents();  // PDL (launch.cuh)
+  pdl_wait();
   __shared__ float tile[32][129];
   const int64_t inst = blockIdx.z;
   A += inst * sA;
@@ -92,6 +97,8 @@ __global__ void transpose_wide_kernel(const float* __restrict__ A, int64_t sA, f
 template <bool kVec>
 __global__ void scale_kernel(const float* __restrict__ A, int64_t sA, float* __restrict__ B, int64_t sB, int64_t n,
                              float f) {
+  pdl_launch_dependents();  // PDL (launch.cuh)
+  pdl_wait();
   const int64_t inst = blockIdx.y;
   A += inst * sA;
   B += inst * sB;
@@ -111,6 +118,8 @@ __global__ void scale_kernel(const float* __restrict__ A, int64_t sA, float* __r
 template <bool kVec>
 __global__ void add_kernel(const float* __restrict__ A, int64_t sA, const float* __restrict__ Bm, int64_t sB,
                            float* __restrict__ C, int64_t sC, int64_t n) {
+  pdl_launch_dependents();  // PDL (launch.cuh)
+  pdl_wait();
   const int64_t inst = blockIdx.y;
   A += inst * sA;
   Bm += inst * sB;
@@ -137,6 +146,8 @@ __global__ void add_kernel(const float* __restrict__ A, int64_t sA, const float*
 template <int kV>
 __global__ void softmax_kernel(const float* __restrict__ A, int64_t sA, float* __restrict__ B, int64_t sB, int rows,
                                int cols, float f) {
+  pdl_launch_dependents();  // PDL (launch.cuh)
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (r >= rows) return;
@@ -198,6 +209,8 @@ template <int kV>
 __global__ void add_ln_kernel(const float* __restrict__ A, int64_t sA, const float* __restrict__ Bm, int64_t sB,
                               const float* __restrict__ G, int64_t sG, const float* __restrict__ Be, int64_t sBe,
                               float* __restrict__ Y, int64_t sY, int rows, int cols, float eps, int64_t total_rows) {
+  pdl_launch_dependents();  // PDL (launch.cuh)
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const int64_t row = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= total_rows) return;
@@ -272,6 +285,8 @@ struct ConcatSrc {
 
 template <bool kVec>
 __global__ void concat_kernel(ConcatSrc src, float* __restrict__ Y, int64_t sY, int rows, int cols_each, int count) {
+  pdl_launch_dependents();  // PDL (launch.cuh)
+  pdl_wait();
   const int64_t inst = blockIdx.z;
   const int i = blockIdx.y;
   const float* z = src.p[i] + inst * src.s[i];
@@ -300,10 +315,10 @@ __global__ void concat_kernel(ConcatSrc src, float* __restrict__ Y, int64_t sY, 
 cudaError_t transpose(const float* A, int64_t sA, float* B, int64_t sB, int R, int C, int batch, cudaStream_t s) {
   if (C % 4 == 0 && sA % 4 == 0 && aligned16(A)) {
     dim3 grid((C + 127) / 128, (R + 31) / 32, batch), block(32, 8);
-    transpose_wide_kernel<<<grid, block, 0, s>>>(A, sA, B, sB, R, C);
+    HS_TRY(launch_node(transpose_wide_kernel, dim3(grid), dim3(block), 0, s, 1, A, sA, B, sB, R, C));
   } else {
     dim3 grid((C + 31) / 32, (R + 31) / 32, batch), block(32, 8);
-    transpose_kernel<<<grid, block, 0, s>>>(A, sA, B, sB, R, C);
+    HS_TRY(launch_node(transpose_kernel, dim3(grid), dim3(block), 0, s, 1, A, sA, B, sB, R, C));
   }
   return cudaGetLastError();
 }
@@ -311,8 +326,8 @@ cudaError_t transpose(const float* A, int64_t sA, float* B, int64_t sB, int R, i
 cudaError_t scale(const float* A, int64_t sA, float* B, int64_t sB, int64_t n, float f, int batch, cudaStream_t s) {
   bool vec = n % 4 == 0 && sA % 4 == 0 && sB % 4 == 0 && aligned16(A) && aligned16(B);
   dim3 grid(blocks_for(vec ? n / 4 : n, kThreads), batch);
-  if (vec) scale_kernel<true><<<grid, kThreads, 0, s>>>(A, sA, B, sB, n, f);
-  else scale_kernel<false><<<grid, kThreads, 0, s>>>(A, sA, B, sB, n, f);
+  if (vec) HS_TRY(launch_node(scale_kernel<true>, dim3(grid), dim3(kThreads), 0, s, 1, A, sA, B, sB, n, f));
+  else HS_TRY(launch_node(scale_kernel<false>, dim3(grid), dim3(kThreads), 0, s, 1, A, sA, B, sB, n, f));
   return cudaGetLastError();
 }
 
@@ -320,8 +335,8 @@ cudaError_t add(const float* A, int64_t sA, const float* B, int64_t sB, float* C
                 cudaStream_t s) {
   bool vec = n % 4 == 0 && sA % 4 == 0 && sB % 4 == 0 && sC % 4 == 0 && aligned16(A) && aligned16(B) && aligned16(C);
   dim3 grid(blocks_for(vec ? n / 4 : n, kThreads), batch);
-  if (vec) add_kernel<true><<<grid, kThreads, 0, s>>>(A, sA, B, sB, C, sC, n);
-  else add_kernel<false><<<grid, kThreads, 0, s>>>(A, sA, B, sB, C, sC, n);
+  if (vec) HS_TRY(launch_node(add_kernel<true>, dim3(grid), dim3(kThreads), 0, s, 1, A, sA, B, sB, C, sC, n));
+  else HS_TRY(launch_node(add_kernel<false>, dim3(grid), dim3(kThreads), 0, s, 1, A, sA, B, sB, C, sC, n));
   return cudaGetLastError();
 }
 
@@ -333,11 +348,11 @@ cudaError_t softmax(const float* A, int64_t sA, float* B, int64_t sB, int rows, 
   bool vec = cols % 128 == 0 && sA % 4 == 0 && sB % 4 == 0 && aligned16(A) && aligned16(B);
   int v = vec ? cols / 128 : 0;
   switch (v) {
-    case 1: softmax_kernel<1><<<grid, kThreads, 0, s>>>(A, sA, B, sB, rows, cols, f); break;
-    case 2: softmax_kernel<2><<<grid, kThreads, 0, s>>>(A, sA, B, sB, rows, cols, f); break;
-    case 4: softmax_kernel<4><<<grid, kThreads, 0, s>>>(A, sA, B, sB, rows, cols, f); break;
-    case 8: softmax_kernel<8><<<grid, kThreads, 0, s>>>(A, sA, B, sB, rows, cols, f); break;
-    default: softmax_kernel<0><<<grid, kThreads, 0, s>>>(A, sA, B, sB, rows, cols, f); break;
+    case 1: HS_TRY(launch_node(softmax_kernel<1>, dim3(grid), dim3(kThreads), 0, s, 1, A, sA, B, sB, rows, cols, f)); break;
+    case 2: HS_TRY(launch_node(softmax_kernel<2>, dim3(grid), dim3(kThreads), 0, s, 1, A, sA, B, sB, rows, cols, f)); break;
+    case 4: HS_TRY(launch_node(softmax_kernel<4>, dim3(grid), dim3(kThreads), 0, s, 1, A, sA, B, sB, rows, cols, f)); break;
+    case 8: HS_TRY(launch_node(softmax_kernel<8>, dim3(grid), dim3(kThreads), 0, s, 1, A, sA, B, sB, rows, cols, f)); break;
+    default: HS_TRY(launch_node(softmax_kernel<0>, dim3(grid), dim3(kThreads), 0, s, 1, A, sA, B, sB, rows, cols, f)); break;
   }
   return cudaGetLastError();
 }
@@ -353,11 +368,11 @@ cudaError_t add_layernorm(const float* A, int64_t sA, const float* B, int64_t sB
              aligned16(A) && aligned16(B) && aligned16(gamma) && aligned16(beta) && aligned16(Y);
   int v = vec ? cols / 128 : 0;
   switch (v) {
-    case 1: add_ln_kernel<1><<<grid, kThreads, 0, s>>>(A, sA, B, sB, gamma, sG, beta, sBt, Y, sY, rows, cols, eps, total); break;
-    case 2: add_ln_kernel<2><<<grid, kThreads, 0, s>>>(A, sA, B, sB, gamma, sG, beta, sBt, Y, sY, rows, cols, eps, total); break;
-    case 4: add_ln_kernel<4><<<grid, kThreads, 0, s>>>(A, sA, B, sB, gamma, sG, beta, sBt, Y, sY, rows, cols, eps, total); break;
-    case 8: add_ln_kernel<8><<<grid, kThreads, 0, s>>>(A, sA, B, sB, gamma, sG, beta, sBt, Y, sY, rows, cols, eps, total); break;
-    default: add_ln_kernel<0><<<grid, kThreads, 0, s>>>(A, sA, B, sB, gamma, sG, beta, sBt, Y, sY, rows, cols, eps, total); break;
+    case 1: HS_TRY(launch_node(add_ln_kernel<1>, dim3(grid), dim3(kThreads), 0, s, 1, A, sA, B, sB, gamma, sG, beta, sBt, Y, sY, rows, cols, eps, total)); break;
+    case 2: HS_TRY(launch_node(add_ln_kernel<2>, dim3(grid), dim3(kThreads), 0, s, 1, A, sA, B, sB, gamma, sG, beta, sBt, Y, sY, rows, cols, eps, total)); break;
+    case 4: HS_TRY(launch_node(add_ln_kernel<4>, dim3(grid), dim3(kThreads), 0, s, 1, A, sA, B, sB, gamma, sG, beta, sBt, Y, sY, rows, cols, eps, total)); break;
+    case 8: HS_TRY(launch_node(add_ln_kernel<8>, dim3(grid), dim3(kThreads), 0, s, 1, A, sA, B, sB, gamma, sG, beta, sBt, Y, sY, rows, cols, eps, total)); break;
+    default: HS_TRY(launch_node(add_ln_kernel<0>, dim3(grid), dim3(kThreads), 0, s, 1, A, sA, B, sB, gamma, sG, beta, sBt, Y, sY, rows, cols, eps, total)); break;
   }
   return cudaGetLastError();
 }
@@ -375,8 +390,8 @@ cudaError_t concat(const float* const* Z, const int64_t* sZ, int count, float* Y
   vec = vec && int64_t(rows) * cols_each < (int64_t(1) << 31);
   const int64_t work = vec ? int64_t(rows) * (cols_each / 4) : int64_t(rows) * cols_each;
   dim3 grid(blocks_for(work, kThreads), count, batch);
-  if (vec) concat_kernel<true><<<grid, kThreads, 0, s>>>(src, Y, sY, rows, cols_each, count);
-  else concat_kernel<false><<<grid, kThreads, 0, s>>>(src, Y, sY, rows, cols_each, count);
+  if (vec) HS_TRY(launch_node(concat_kernel<true>, dim3(grid), dim3(kThreads), 0, s, 1, src, Y, sY, rows, cols_each, count));
+  else HS_TRY(launch_node(concat_kernel<false>, dim3(grid), dim3(kThreads), 0, s, 1, src, Y, sY, rows, cols_each, count));
   return cudaGetLastError();
 }
 

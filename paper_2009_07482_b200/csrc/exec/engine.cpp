@@ -41,10 +41,13 @@ struct CbData {
   Completion c;
 };
 
+// Runs on a CUDA driver thread. The record was written under the engine's mutex
+// before the callback was enqueued and is read under it here: the mutex, not the
+// driver's internal hand-off, orders the two accesses (what ThreadSanitizer checks,
+// `make tsan`).
 void CUDART_CB_trampoline(void* p) {
   auto* d = static_cast<CbData*>(p);
-  d->engine->push_completion(d->c);
-  delete d;
+  d->engine->deliver_callback(d);
 }
 
 std::vector<long long> var_values(const KernelSpec& k, const ParamMap& params) {
@@ -148,6 +151,7 @@ void Engine::place_components() {
 Engine::~Engine() {
   if (!ctx_) return;
   for (hs_ctx_t c : dctx_) hs_ctx_sync(c);
+  { std::lock_guard<std::mutex> lk(mu_); }  // every host callback has left deliver_callback
   clear_trace();
   for (auto& sl : slots_) {
     hs_graph_destroy(sl.graph);
@@ -833,7 +837,7 @@ void Engine::issue(Slot& sl, const TaskComponent& t, const CommandQueueStructure
     }
     if (record) hs_ok(hs_event_record(event(sl, t.id, ev), s), "event record");
     if (!graph && q.callbacks.count(ev))
-      hs_ok(hs_host_callback(s, &CUDART_CB_trampoline, new CbData{this, {t.id, ev}}), "host callback");
+      hs_ok(hs_host_callback(s, &CUDART_CB_trampoline, new_callback({t.id, ev})), "host callback");
   }
 }
 
@@ -1151,12 +1155,27 @@ void Engine::clear_trace() {
   trace_dispatch_.clear();
 }
 
+void* Engine::new_callback(const Completion& c) {
+  std::lock_guard<std::mutex> lk(mu_);
+  return new CbData{this, c};
+}
+
+// Notified under the lock: once this thread releases mu_ it no longer touches the
+// engine, so the scheduler thread may finish the run and destroy it (ThreadSanitizer
+// caught the notify-after-unlock variant racing ~Engine's pthread_cond_destroy).
+void Engine::deliver_callback(void* p) {
+  auto* d = static_cast<CbData*>(p);
+  std::lock_guard<std::mutex> lk(mu_);
+  done_q_.push_back(d->c);
+  pending_.fetch_add(1, std::memory_order_release);
+  delete d;
+  cv_.notify_one();
+}
+
 void Engine::push_completion(const Completion& c) {
-  {
-    std::lock_guard<std::mutex> lk(mu_);
-    done_q_.push_back(c);
-    pending_.fetch_add(1, std::memory_order_release);
-  }
+  std::lock_guard<std::mutex> lk(mu_);
+  done_q_.push_back(c);
+  pending_.fetch_add(1, std::memory_order_release);
   cv_.notify_one();
 }
 

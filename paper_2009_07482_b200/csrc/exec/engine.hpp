@@ -85,6 +85,9 @@ class Engine {
 
   // Completion delivery from CUDA host callbacks (any thread).
   void push_completion(const Completion& c);
+  // host callbacks: the per-callback record is created and consumed under mu_
+  void* new_callback(const Completion& c);
+  void deliver_callback(void* record);
 
   // Alg. 1 driven from outside (hetsim::CudaExecutor, include/hetsim/cuda_executor.hpp):
   // one scheduler run per ext_begin / ext_end over n <= batch instances, dynamic mode.

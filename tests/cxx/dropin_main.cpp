@@ -3,7 +3,7 @@
 // graph_analysis.hpp:27-38 derive_components) plus the scheduler / executor
 // plug-in, linked against libhetsim.so, runs a DAG on the B200.
 //
-//   dropin_main SPEC PARAMS IO_IN IO_OUT N BATCH
+//   dropin_main SPEC PARAMS IO_IN IO_OUT N BATCH [POLICY]
 // PARAMS: "NAME VALUE" lines. IO_IN: records {int32 kernel, int32 pos, int32
 // is_output, int64 stride_bytes, int64 count, int64 nbytes, bytes}; outputs
 // (is_output = 1, zero-filled) are written to IO_OUT in the same format.
@@ -28,8 +28,8 @@ struct Rec {
 };
 
 int main(int argc, char** argv) {
-  if (argc != 7) {
-    std::cerr << "usage: dropin_main SPEC PARAMS IO_IN IO_OUT N BATCH\n";
+  if (argc != 7 && argc != 8) {
+    std::cerr << "usage: dropin_main SPEC PARAMS IO_IN IO_OUT N BATCH [POLICY]\n";
     return 2;
   }
   try {
@@ -65,13 +65,14 @@ int main(int argc, char** argv) {
     hetsim::CudaExecutor ex(g, opts);
     for (auto& r : recs) ex.bind(r.kernel, r.pos, r.data.data(), r.stride, r.count);
     const hetsim::Platform platform = hetsim::Platform::from_spec(g);
+    const hetsim::Policy policy = argc == 8 ? hetsim::policy_from_name(argv[7]) : hetsim::Policy::clustering;
     int64_t total_ns = 0;
     size_t dispatches = 0;
     for (int64_t first = 0; first < n; first += opts.batch) {
       const int64_t cnt = std::min<int64_t>(opts.batch, n - first);
       ex.begin(first, cnt);
       const hetsim::ScheduleResult res =
-          hetsim::run_schedule(g, platform, hetsim::Profiles{}, hetsim::Policy::clustering, ex);
+          hetsim::run_schedule(g, platform, hetsim::Profiles{}, policy, ex);
       total_ns += ex.end();
       dispatches = res.dispatches.size();
     }

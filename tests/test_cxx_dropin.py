@@ -91,3 +91,41 @@ def test_dropin_runs_alg1_on_the_b200(dag, tmp_path, oracle_mod):
     for key, r in ref.items():
         for i in range(n):
             assert _normwise(got[key][i], r[i]) <= 1e-4, (key, i)
+
+
+TSAN_EXE = ROOT / "build_tsan" / "dropin_tsan"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("policy", ["clustering", "eager", "heft"])
+def test_host_runtime_under_threadsanitizer(policy, tmp_path, oracle_mod):
+    """SURVEY.md §4 race detection: the host runtime built with -fsanitize=thread
+    (`make tsan`) drives Alg. 1 in dynamic mode — CUDA host callbacks on driver
+    threads push completions through the MPSC queue to Scheduler::cb on the main
+    thread (the paper's lock()/unlock() region). One component per
+    kernel on three logical devices maximises concurrent callbacks. ThreadSanitizer
+    must report nothing and the outputs must match the oracle."""
+    if not TSAN_EXE.exists():
+        p = subprocess.run(["make", "-C", str(ROOT), "tsan"], capture_output=True, text=True)
+        assert p.returncode == 0, p.stderr[-3000:]
+    text, params, meta = workloads.encoder(layers=1, tc_mode="per_kernel", queues=1, devices=3)
+    n, batch = 2, 2
+    x = workloads.encoder_inputs(meta, params, n).reshape(n, -1)
+    arrays = {(i["kernel"], i["pos"]): x for i in meta["x_inputs"]}
+    for key, w in workloads.encoder_weights(meta).items():
+        arrays[key] = w.reshape(-1)
+    outs = {(k, p): e for k, p, e in workloads.isolated_outputs(text, params)}
+    (tmp_path / "spec.json").write_text(text)
+    (tmp_path / "params.txt").write_text("".join(f"{k} {v}\n" for k, v in params.items()))
+    _write_io(tmp_path / "in.bin", arrays, outs, n)
+    env = dict(os.environ, TSAN_OPTIONS="halt_on_error=0 exitcode=66 report_signal_unsafe=0")
+    p = subprocess.run([str(TSAN_EXE), str(tmp_path / "spec.json"), str(tmp_path / "params.txt"),
+                        str(tmp_path / "in.bin"), str(tmp_path / "out.bin"), str(n), str(batch), policy],
+                       capture_output=True, text=True, timeout=600, env=env)
+    assert "ThreadSanitizer" not in p.stderr, p.stderr[-4000:]
+    assert p.returncode == 0, p.stderr[-3000:]
+    got = _read_out(tmp_path / "out.bin")
+    ref = oracle_mod.run_dag(text, params, arrays, n)
+    for key, r in ref.items():
+        for i in range(n):
+            assert _normwise(got[key][i], r[i]) <= 1e-4, (key, i)
