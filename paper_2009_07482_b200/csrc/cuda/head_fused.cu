@@ -238,7 +238,7 @@ __device__ __forceinline__ float row_exp(uint32_t (&r0)[32], uint32_t (&r1)[32],
 template <int kTerms>
 __global__ void __launch_bounds__(kThreads, 1)
     head_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
-                const __grid_constant__ CUtensorMap tmWh, HeadParams p) {
+                const __grid_constant__ CUtensorMap tmWh, const __grid_constant__ CUtensorMap tmXp, HeadParams p) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
   auto bar = [&](uint32_t b) { return base + kBar + 8u * b; };
@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (uint32_t b : {EXT, S_READ, C_READY}) mbar_init(bar(b), 8);
     for (uint32_t b : {P0_READY, P1_READY}) mbar_init(bar(b), 4);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (const CUtensorMap* m : {&tmX, &tmW, &tmWh})
+    for (const CUtensorMap* m : {&tmX, &tmW, &tmWh, &tmXp})
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
   }
   if (warp == 2) {
@@ -289,8 +289,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int t = pair0; t < p.pairs; t += npairs, ++lt) {
         const int inst = 2 * t + int(rank);  // >= batch: zero-filled box
         // warm L2 with this CTA's next instance: its loads start right after this projection
+        // (whole 128-byte row segments: the 64-byte X tiles then hit L2 instead of each
+        // fetching half of a DRAM line)
         if (2 * (t + npairs) + int(rank) < p.batch)
-          for (int kb = 0; kb < nx; ++kb) tma_prefetch_3d(&tmX, kb * kXK, 0, 2 * (t + npairs) + int(rank));
+          for (int kb = 0; kb < nw; ++kb) tma_prefetch_3d(&tmXp, kb * kWK, 0, 2 * (t + npairs) + int(rank));
         for (int kb = 0; kb < nx; ++kb, ++it) {
           const int s = int(it % kNX);
           TW(lt, 12, mbar_wait(bar(XE + s), ((it / kNX) & 1u) ^ 1u));
@@ -460,21 +462,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q = warp & 3, row = q * 32 + lane;
     const uint32_t lane_base = tmem + (uint32_t(q * 32) << 16);
     const uint32_t swz = uint32_t((row >> 1) & 3);
+    // The X tile is read and split into registers (and its staging slot released)
+    // before waiting for the A stage to free up: only the TMEM stores and the signal
+    // remain between the MMA's release of the stage and its next use.
     uint32_t it = 0, lt = 0;
     for (int t = pair0; t < p.pairs; t += npairs, ++lt) {
       for (int kb = 0; kb < nx; ++kb, ++it) {
         const int x = int(it % kNX), a = int(it % kNA);
-        if (q == 0) {
-          TW(lt, 10, mbar_wait(bar(XF + x), (it / kNX) & 1u));
-          TW(lt, 11, mbar_wait(bar(AE + a), ((it / kNA) & 1u) ^ 1u));
-        } else {
-          mbar_wait(bar(XF + x), (it / kNX) & 1u);
-          mbar_wait(bar(AE + a), ((it / kNA) & 1u) ^ 1u);
-        }
-        tc_fence_after();
-#if HS_DBG_TIMELINE
-        const long long c_conv0 = clock64();
-#endif
+        TW(lt, 10, mbar_wait(bar(XF + x), (it / kNX) & 1u));
+        uint32_t hi[16], lo[16];
         if (!HS_DBG_HEAD_NOCONV) {
           const uint32_t src = base + kXs + uint32_t(x) * kXTile + uint32_t(row) * 64u;
           uint32_t v[16];
@@ -486,7 +482,22 @@ __global__ void __launch_bounds__(kThreads, 1)
             v[4 * c + 2] = __float_as_uint(f.z);
             v[4 * c + 3] = __float_as_uint(f.w);
           }
-          st_split16<kTerms>(lane_base + kTA + uint32_t(a) * 32u, 16u, v);
+          split16<kTerms>(v, hi, lo);
+          // the staging slot goes back to TMA (async proxy) on the arrive below: hold it
+          // until the shared-memory loads have returned (one register of each LDS.128)
+          asm volatile("" ::"r"(hi[0]), "r"(hi[4]), "r"(hi[8]), "r"(hi[12]) : "memory");
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar(XE + x));
+        TW(lt, 11, mbar_wait(bar(AE + a), ((it / kNA) & 1u) ^ 1u));
+        tc_fence_after();
+#if HS_DBG_TIMELINE
+        const long long c_conv0 = clock64();
+#endif
+        if (!HS_DBG_HEAD_NOCONV) {
+          const uint32_t ta = lane_base + kTA + uint32_t(a) * 32u;
+          tmem_st16(ta, hi);
+          if constexpr (kTerms > 1) tmem_st16(ta + 16u, lo);
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         }
 #if HS_DBG_TIMELINE
@@ -495,7 +506,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
-          mbar_arrive(bar(XE + x));
           // relaxed: the stage's TMEM stores are complete (tcgen05.wait::st above); a
           // release arrive at cluster scope costs ~1k cycles per stage in this thread
           asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(leader(AF + a))
@@ -699,8 +709,9 @@ cudaError_t head_fused(const HeadArgs& a, int terms, cudaStream_t s) {
   });
   if (cudaError_t e = terms > 1 ? err3 : err1) return e;
   const uint64_t S = uint64_t(a.S), D = uint64_t(a.D), B = uint64_t(a.batch);
-  CUtensorMap mX, mW, mWh;
+  CUtensorMap mX, mW, mWh, mXp;
   const bool ok = make_map_sw64(&mX, a.X, D, S, B, D * 4, uint64_t(a.sX ? a.sX : S * D) * 4, kXK, kS) &&
+                  tc::make_map(&mXp, a.X, D, S, B, D * 4, uint64_t(a.sX ? a.sX : S * D) * 4, kWK, kS, true) &&
                   tc::make_map(&mW, a.Wqkv, D, kN, 2, D * 4, uint64_t(kN) * D * 4, kWK, kN / 2, true) &&
                   tc::make_map(&mWh, a.Wh, kDK, kDK, 2, kDK * 4, uint64_t(kDK * kDK) * 4, 32, kDK, true);
   if (!ok) return cudaErrorInvalidValue;
@@ -708,7 +719,7 @@ cudaError_t head_fused(const HeadArgs& a, int terms, cudaStream_t s) {
   HeadParams p{a.S, a.D, a.batch, (a.batch + 1) / 2, a.scale, a.Z, a.sZ ? a.sZ : int64_t(S) * ldz, ldz};
   const int max_pairs = tc::num_sms() / 2;
   const int pairs = p.pairs < max_pairs ? p.pairs : max_pairs;
-  return launch_node(kernel, dim3(2 * pairs), dim3(kThreads), kSmem, s, 2, mX, mW, mWh, p);
+  return launch_node(kernel, dim3(2 * pairs), dim3(kThreads), kSmem, s, 2, mX, mW, mWh, mXp, p);
 }
 
 }  // namespace hs
