@@ -38,6 +38,21 @@
 
 namespace hs {
 
+#ifndef HS_DBG_GEMM_TL  // timing experiment only: clock64 stamps of CTA 0 of gemm_tc_kernel
+#define HS_DBG_GEMM_TL 0
+#endif
+#if HS_DBG_GEMM_TL
+__device__ long long g_gemm_tl[16];
+#define GTL(k)                                                                  \
+  do {                                                                          \
+    if (blockIdx.x == 0 && g_gemm_tl[k] == 0) g_gemm_tl[k] = clock64();         \
+  } while (0)
+#else
+#define GTL(k) \
+  do {         \
+  } while (0)
+#endif
+
 namespace {
 
 using namespace tc;
@@ -205,9 +220,6 @@ __device__ __forceinline__ void split_a_to_tmem(uint32_t sa, uint32_t ta, int ro
 // Rows >= M (or the whole chunk when !rows_valid) are not stored.
 __device__ __forceinline__ void epi_store_chunk(const TileParams& p, uint32_t tile, const float (&v)[32], int lane,
                                                 int q, int m0, int inst, int c0, bool rows_valid) {
-#pragma unroll
-  for (int j = 0; j < 32; ++j) sts32(tile + uint32_t(lane * 33 + j) * 4u, v[j]);
-  __syncwarp();
   // destination of this 32-column chunk: the single C, or member m's C;
   // `ncols` valid columns, rows `ld` elements apart
   int ncols = p.N;
@@ -221,6 +233,32 @@ __device__ __forceinline__ void epi_store_chunk(const TileParams& p, uint32_t ti
     cbase = p.C + int64_t(inst) * p.sC;
   }
   const int64_t ld = p.ldc ? p.ldc : ncols;
+  // Latency-bound launches (one instance): each thread stores its own row's 32
+  // columns straight from registers (8 x 16 B, or red.add for a K split) instead of
+  // the coalescing transpose through shared memory, which costs ~2k cycles per tile.
+  if (p.batch == 1 && !HS_DBG_NOEPI) {
+    const int grow = m0 + q * 32 + lane;
+    float* dst = cbase + int64_t(grow) * ld + c0;
+    // warp-uniform choice (the transpose path below synchronises the warp)
+    if (__all_sync(0xffffffffu, c0 + 32 <= ncols && (reinterpret_cast<uintptr_t>(dst) & 15u) == 0)) {
+      if (rows_valid && grow < p.M) {
+#pragma unroll
+        for (int j4 = 0; j4 < 8; ++j4) {
+          if (p.split_k > 1)
+            asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + 4 * j4), "f"(v[4 * j4]),
+                         "f"(v[4 * j4 + 1]), "f"(v[4 * j4 + 2]), "f"(v[4 * j4 + 3])
+                         : "memory");
+          else
+            *reinterpret_cast<float4*>(dst + 4 * j4) =
+                make_float4(v[4 * j4], v[4 * j4 + 1], v[4 * j4 + 2], v[4 * j4 + 3]);
+        }
+      }
+      return;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 32; ++j) sts32(tile + uint32_t(lane * 33 + j) * 4u, v[j]);
+  __syncwarp();
   const int cq = (lane & 7) * 4, rsub = lane >> 3;
   const bool vec = c0 + 32 <= ncols && (ld & 3) == 0;
 #pragma unroll
@@ -274,6 +312,7 @@ __global__ void __launch_bounds__(kThreads, kSmall ? 2 : 1)
   const uint32_t* tmem_slot_ptr = reinterpret_cast<const uint32_t*>(smem_raw + (tmem_slot - smem_u32(smem_raw)));
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) GTL(0);
   const int nk = (p.K + BK - 1) / BK;
   // K-block range of tile t (the whole K unless split-K)
   auto kb_begin = [&](int t) { return (t / p.base_tiles) * nk / p.split_k; };
@@ -304,8 +343,10 @@ __global__ void __launch_bounds__(kThreads, kSmall ? 2 : 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (threadIdx.x == 0) GTL(1);
   pdl_launch_dependents();  // PDL (launch.cuh): the prologue above overlaps the previous kernel
   pdl_wait();
+  if (threadIdx.x == 0) GTL(2);
   const uint32_t tmem = *tmem_slot_ptr;
   const uint32_t tmem_a = tmem + uint32_t(L::kAccCols);  // A stages start after the accumulators
 
@@ -336,6 +377,7 @@ __global__ void __launch_bounds__(kThreads, kSmall ? 2 : 1)
           (void)sa; (void)ia; (void)ib; (void)m0;
 #else
           mbar_expect_tx(st_full(s), L::kStaging);
+          GTL(3);
           tma_load_3d(sa, &tmA, st_full(s), kb * BK, m0, ia);
           if constexpr (kBSrc == 0) tma_load_3d(sa + L::kStageA, &tmB, st_full(s), kb * BK, n0, ib);
           if constexpr (kBSrc == 1) tma_load_3d(sa + L::kStageA, &tmB, st_full(s), n0, kb * BK, ib);
@@ -413,6 +455,7 @@ __global__ void __launch_bounds__(kThreads, kSmall ? 2 : 1)
             }
           }
           mma_commit(op_empty(o));  // operand slot (TMEM A + smem B) free once these MMAs have read it
+          GTL(6);
         }
         mma_commit(acc_full(int(acc)));
       }
@@ -427,6 +470,7 @@ __global__ void __launch_bounds__(kThreads, kSmall ? 2 : 1)
       const uint32_t acc = lt % uint32_t(L::kAccBufs);
       mbar_wait(acc_full(int(acc)), (lt / uint32_t(L::kAccBufs)) & 1u);
       tc_fence_after();
+      if (q == 0 && lane == 0) GTL(7);
       const uint32_t tacc = tmem + (uint32_t(q * 32) << 16) + acc * uint32_t(BN);
       // Softmax epilogue: this thread owns one full row of the tile (N <= BN).
       // Two read passes over TMEM give the row max and the sum of exp(s*x - max);
@@ -480,6 +524,7 @@ __global__ void __launch_bounds__(kThreads, kSmall ? 2 : 1)
         }
         epi_store_chunk(p, scratch + uint32_t(q) * uint32_t(kEpiTileBytes), v, lane, q, m0, inst, n0 + cb * 32, true);
       }
+      if (q == 0 && lane == 0) GTL(8);
     }
   } else if (warp >= 8) {
     // ------------------------------------------------------------ converters
@@ -497,6 +542,7 @@ __global__ void __launch_bounds__(kThreads, kSmall ? 2 : 1)
         if (int(it % kConvGroups) != g) continue;
         const int s = int(it % NS), o = int(it % NO);
         mbar_wait(st_full(s), (it / NS) & 1u);
+        if (q == 0 && lane == 0) GTL(4);
         mbar_wait(op_empty(o), ((it / NO) & 1u) ^ 1u);
         tc_fence_after();
         const uint32_t sa = staging + uint32_t(s) * L::kStaging, sb = sa + L::kStageA;
@@ -529,15 +575,18 @@ __global__ void __launch_bounds__(kThreads, kSmall ? 2 : 1)
         if (lane == 0) {
           mbar_arrive(st_empty(s));
           mbar_arrive(op_full(o));
+          if (q == 0) GTL(5);
         }
       }
     }
   }
+  if (threadIdx.x == 0) GTL(9);
   tc_fence_before();
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(L::kTmemCols));
+    if (lane == 0) GTL(10);
   }
 }
 
@@ -571,6 +620,9 @@ __global__ void __launch_bounds__(kThreads, kSmall ? 2 : 1)
 #endif
 #ifndef HS_PAIR_BN  // pair tile width for N >= 256
 #define HS_PAIR_BN 256
+#endif
+#ifndef HS_PAIR_RELAXED  // converters signal A stages with relaxed (not release) cluster arrives
+#define HS_PAIR_RELAXED 1
 #endif
 #ifndef HS_PAIR_MIN_ASTAGES  // double-buffer the accumulator if this many A stages still fit
 #define HS_PAIR_MIN_ASTAGES 4
@@ -860,7 +912,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (lane == 0) {
           mbar_arrive(st_empty(s));
+#if HS_PAIR_RELAXED
+          // relaxed: the stage's TMEM stores are complete (tcgen05.wait::st above); a
+          // release arrive at cluster scope costs ~1k cycles in this thread (head_fused.cu)
+          asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(mapa_rank(op_full(o), 0))
+                       : "memory");
+#else
           mbar_arrive_cluster(mapa_rank(op_full(o), 0));
+#endif
         }
       }
     }
@@ -1160,3 +1219,16 @@ cudaError_t gemm_split_weights(const float* B, GemmLayout layout, int N, int K, 
 }
 
 }  // namespace hs
+
+// timing experiment only (profiles/gemm_timeline.py): gemm_tc_kernel CTA 0 stamps
+extern "C" int hs_debug_gemm_timeline(long long* out, int reset) {
+#if HS_DBG_GEMM_TL
+  static const long long zeros[16] = {};
+  if (reset) return cudaMemcpyToSymbol(hs::g_gemm_tl, zeros, sizeof(zeros)) == cudaSuccess ? 0 : 1;
+  return cudaMemcpyFromSymbol(out, hs::g_gemm_tl, sizeof(long long) * 16) == cudaSuccess ? 0 : 1;
+#else
+  (void)out;
+  (void)reset;
+  return 1;
+#endif
+}

@@ -161,6 +161,8 @@ Engine::~Engine() {
     for (auto& [k, e] : sl.din) hs_event_destroy(e);
     for (auto& [k, e] : sl.dout) hs_event_destroy(e);
     hs_event_destroy(sl.copy_fork);
+    for (hs_event_t e : sl.copy_join) hs_event_destroy(e);
+    for (hs_stream_t cs : sl.copy_streams) hs_stream_destroy(cs);
     hs_event_destroy(sl.t_start);
     hs_event_destroy(sl.t_end);
     for (auto& [k, s] : sl.streams) hs_stream_destroy(s);
@@ -607,8 +609,35 @@ void Engine::copy_in(Slot& sl, hs_stream_t s, int gi, int64_t first, int64_t n, 
 void Engine::copies(Slot& sl, int64_t first, int64_t n, bool in) {
   if (dctx_.size() == 1) {
     if (in) {
+      // independent input groups are copied side by side: group 0 on the origin
+      // stream, the others on per-slot copy streams forked from and joined to it
+      std::vector<int> gis;
       for (size_t gi = 0; gi < groups_.size(); ++gi)
-        if (!groups_[gi].resident) copy_in(sl, sl.origin, int(gi), first, n, 0);
+        if (!groups_[gi].resident) gis.push_back(int(gi));
+      if (gis.size() > 1) {
+        if (!sl.copy_fork) hs_ok(hs_event_create(ctx_, 0, &sl.copy_fork), "hs_event_create");
+        hs_ok(hs_event_record(sl.copy_fork, sl.origin), "copy fork");
+      }
+      for (size_t i = 0; i < gis.size(); ++i) {
+        if (i == 0) {
+          copy_in(sl, sl.origin, gis[i], first, n, 0);
+          continue;
+        }
+        while (sl.copy_streams.size() < i) {
+          hs_stream_t cs = nullptr;
+          hs_event_t ce = nullptr;
+          hs_ok(hs_stream_create(ctx_, 0, &cs), "hs_stream_create");
+          hs_ok(hs_event_create(ctx_, 0, &ce), "hs_event_create");
+          stream_dom_[cs] = 0;
+          sl.copy_streams.push_back(cs);
+          sl.copy_join.push_back(ce);
+        }
+        hs_stream_t cs = sl.copy_streams[i - 1];
+        hs_ok(hs_stream_wait(cs, sl.copy_fork), "copy fork wait");
+        copy_in(sl, cs, gis[i], first, n, 0);
+        hs_ok(hs_event_record(sl.copy_join[i - 1], cs), "copy join");
+        hs_ok(hs_stream_wait(sl.origin, sl.copy_join[i - 1]), "copy join wait");
+      }
     } else {
       copy_out(sl, sl.origin, first, n, 0);
     }

@@ -139,6 +139,9 @@ class Engine {
     std::map<int, hs_stream_t> dorigin;
     std::map<int, hs_event_t> din, dout;
     hs_event_t copy_fork = nullptr;
+    // one GPU, several per-instance input groups: copy-in streams forked from `origin`
+    std::vector<hs_stream_t> copy_streams;
+    std::vector<hs_event_t> copy_join;
   };
 
   void build_nodes();
