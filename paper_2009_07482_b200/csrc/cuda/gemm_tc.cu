@@ -621,6 +621,15 @@ __global__ void __launch_bounds__(kThreads, kSmall ? 2 : 1)
 #ifndef HS_PAIR_BN  // pair tile width for N >= 256
 #define HS_PAIR_BN 256
 #endif
+#ifndef HS_PAIR_DBL192  // 192-wide pair tiles keep two accumulators
+#define HS_PAIR_DBL192 1
+#endif
+#ifndef HS_PAIR_WIDE192  // FFN1-shaped GEMMs on double-buffered 192-wide pair tiles
+#define HS_PAIR_WIDE192 1
+#endif
+#ifndef HS_PAIR_PRESPLIT  // converters split the A tile into registers before waiting for the A stage
+#define HS_PAIR_PRESPLIT 1
+#endif
 #ifndef HS_PAIR_RELAXED  // converters signal A stages with relaxed (not release) cluster arrives
 #define HS_PAIR_RELAXED 1
 #endif
@@ -637,7 +646,11 @@ struct CfgPair {
   static constexpr int kPlaneB = kHalfN * (kBf16 ? 64 : 128);   // one SW128 tf32 / SW64 bf16 half plane
   static constexpr int kOperand = 2 * kPlaneB;
   static constexpr int kAStage = kBf16 ? 32 : 64;
-  static constexpr int kAccBufs = (2 * BN + HS_PAIR_MIN_ASTAGES * kAStage <= kTmemCols) ? 2 : 1;
+  // BN = 192 keeps two accumulators (384 columns) beside two A stages, so the
+  // epilogue of one tile overlaps the next tile's MMAs; BN = 256 needs all of TMEM
+  // for one accumulator and four A stages.
+  static constexpr int kMinAStages = (BN == 192 && HS_PAIR_DBL192) ? 2 : HS_PAIR_MIN_ASTAGES;
+  static constexpr int kAccBufs = (2 * BN + kMinAStages * kAStage <= kTmemCols) ? 2 : 1;
   static constexpr int kAccCols = kAccBufs * BN;
   static constexpr int kBudget = HS_SMEM_BUDGET_KB * 1024;
   static constexpr int kNOtm = (kTmemCols - kAccCols) / kAStage;
@@ -902,16 +915,49 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (int(it % kConvGroups) != g) continue;
         const int s = int(it % NS), o = int(it % NO);
         mbar_wait(st_full(s), (it / NS) & 1u);
-        mbar_wait(op_empty(o), ((it / NO) & 1u) ^ 1u);
-        tc_fence_after();
         const uint32_t sa = staging + uint32_t(s) * L::kStaging;
         const uint32_t ta = tmem_a + (uint32_t(q * 32) << 16) + uint32_t(o) * uint32_t(L::kAStage);
-        split_a_to_tmem<kTerms, kBf16>(sa, ta, row);
+        bool staged_released = false;
+        if constexpr (!kBf16 && HS_PAIR_PRESPLIT) {
+          // split this row's 32 values into registers and hand the staging tile back
+          // before waiting for the A stage: only the TMEM stores remain between the
+          // MMAs' release of the stage and its reuse (as in head_fused.cu)
+          uint32_t hi[32], lo[32], dep = 0;
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const float4 x = lds128(sa + sw128(row, c));
+            dep ^= __float_as_uint(x.x);  // one register of each LDS.128
+            const float xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float hv = tf32_rna(xs[e]);
+              hi[4 * c + e] = __float_as_uint(hv);
+              lo[4 * c + e] = __float_as_uint(xs[e] - hv);
+            }
+          }
+          // the slot goes back to TMA only once this warp's loads have returned
+          if (lane == 0) mbar_arrive_after(st_empty(s), dep);
+          staged_released = true;
+          mbar_wait(op_empty(o), ((it / NO) & 1u) ^ 1u);
+          tc_fence_after();
+          if (!HS_DBG_NOCONV) {
+            tmem_st16(ta, *reinterpret_cast<const uint32_t(*)[16]>(hi));
+            tmem_st16(ta + 16u, *reinterpret_cast<const uint32_t(*)[16]>(hi + 16));
+            if constexpr (kTerms > 1) {
+              tmem_st16(ta + 32u, *reinterpret_cast<const uint32_t(*)[16]>(lo));
+              tmem_st16(ta + 48u, *reinterpret_cast<const uint32_t(*)[16]>(lo + 16));
+            }
+          }
+        } else {
+          mbar_wait(op_empty(o), ((it / NO) & 1u) ^ 1u);
+          tc_fence_after();
+          split_a_to_tmem<kTerms, kBf16>(sa, ta, row);
+        }
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
-          mbar_arrive(st_empty(s));
+          if (!staged_released) mbar_arrive(st_empty(s));
 #if HS_PAIR_RELAXED
           // relaxed: the stage's TMEM stores are complete (tcgen05.wait::st above); a
           // release arrive at cluster scope costs ~1k cycles in this thread (head_fused.cu)
@@ -1176,6 +1222,10 @@ cudaError_t gemm_tcgen05(const GemmArgs& a, int terms, cudaStream_t s) {
   if (HS_PAIR_GEMM && store_ok && a.Bplanes && !a.softmax && row_blocks >= 2 &&
       !(a.n_out > 1 && a.N / a.n_out % 32)) {
     if (a.N == 192) return launch_pair_bn<192>(a, terms, s);
+    // wide N over a short K (FFN1: N = 2048, K = 512): the per-tile epilogue drain is
+    // ~10 % of a 256-wide tile's MMA time, so double-buffered 192-wide tiles win
+    // despite the ragged last tile
+    if (HS_PAIR_WIDE192 && a.n_out <= 1 && a.N >= 1024 && a.K <= 1024) return launch_pair_bn<192>(a, terms, s);
     if (a.N >= 256 && a.n_out <= 1) return launch_pair_bn<HS_PAIR_BN>(a, terms, s);
   }
   if (a.n_out > 1) {

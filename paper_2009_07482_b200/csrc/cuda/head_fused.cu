@@ -470,7 +470,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int kb = 0; kb < nx; ++kb, ++it) {
         const int x = int(it % kNX), a = int(it % kNA);
         TW(lt, 10, mbar_wait(bar(XF + x), (it / kNX) & 1u));
-        uint32_t hi[16], lo[16];
+        uint32_t hi[16], lo[16], dep = 0;
         if (!HS_DBG_HEAD_NOCONV) {
           const uint32_t src = base + kXs + uint32_t(x) * kXTile + uint32_t(row) * 64u;
           uint32_t v[16];
@@ -481,14 +481,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             v[4 * c + 1] = __float_as_uint(f.y);
             v[4 * c + 2] = __float_as_uint(f.z);
             v[4 * c + 3] = __float_as_uint(f.w);
+            dep ^= v[4 * c];  // one register of each LDS.128
           }
           split16<kTerms>(v, hi, lo);
-          // the staging slot goes back to TMA (async proxy) on the arrive below: hold it
-          // until the shared-memory loads have returned (one register of each LDS.128)
-          asm volatile("" ::"r"(hi[0]), "r"(hi[4]), "r"(hi[8]), "r"(hi[12]) : "memory");
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(bar(XE + x));
+        // the staging slot goes back to TMA once this warp's loads have returned
+        if (lane == 0) mbar_arrive_after(bar(XE + x), dep);
         TW(lt, 11, mbar_wait(bar(AE + a), ((it / kNA) & 1u) ^ 1u));
         tc_fence_after();
 #if HS_DBG_TIMELINE

@@ -27,6 +27,19 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
+// Arrive on a local mbarrier once the shared-memory loads that produced `dep` have
+// returned (lane 0 only). The plain arrive is not ordered behind in-flight LDS:
+// ptxas issues SYNCS.ARRIVE right after the LDS.128s, and a TMA refill it releases
+// can overwrite the slot before the reads land (measured: corrupted rows in the
+// pair GEMM with an early staging release). The arrive count 1 + (dep &
+// %lanemask_lt), which is 1 in lane 0, makes the arrive wait on those loads.
+__device__ __forceinline__ void mbar_arrive_after(uint32_t bar, uint32_t dep) {
+  asm volatile(
+      "{\n .reg .b32 z;\n mov.u32 z, %%lanemask_lt;\n and.b32 z, z, %1;\n add.u32 z, z, 1;\n"
+      " mbarrier.arrive.shared::cta.b64 _, [%0], z;\n}" ::"r"(bar),
+      "r"(dep)
+      : "memory");
+}
 // Watchdog: a pipeline that has not advanced for ~2^34 cycles (several
 // seconds) traps, so a broken barrier protocol surfaces as a launch error
 // (DeviceError) instead of a hung GPU.
