@@ -21,15 +21,17 @@
 //               S = Q Kᵀ (N = 128, Q hi/lo in TMEM, K hi/lo in smem), softmax in
 //               registers, C = P V (N = 64, P hi/lo in TMEM, Vᵀ hi/lo in smem),
 //               Z = C Wh (N = 64, C hi/lo in TMEM, Wh planes in smem)
-// The leader's issuer interleaves its own attention MMAs into the projection's MMA
-// stream as their operands become ready; the other CTA's issuer runs only its own
-// attention. (profiles/mix_probe.cu: cta_group::1 and ::2 MMAs side by side in one
-// cluster kernel are exact.)
+// Two issuer warps per CTA feed one tensor pipe: the leader's warp 1 issues the
+// projection, and warp 2 of each CTA issues that CTA's attention in pair order, so
+// neither stream waits on the other's barriers (profiles/mix_probe.cu: cta_group::1
+// and ::2 MMAs side by side in one cluster kernel, from one thread or from two
+// warps, are exact).
 //
 // Warp roles (512 threads per CTA):
 //   warp 0      TMA: this CTA's X tiles (+ L2 prefetch of its next instance's X)
-//   warp 1      MMA issuer (leader: projection + own attention; other: own attention)
-//   warp 2      TMEM allocator (512 columns, cta_group::2); then TMA: Wh planes
+//   warp 1      MMA issuer: the projection (leader only)
+//   warp 2      TMEM allocator (512 columns, cta_group::2); then MMA issuer of this
+//               CTA's attention (S, P·V, Z) and TMA of the Wh planes
 //   warp 3      TMA: this CTA's half of the Wq|Wk|Wv planes
 //   warps 4-7   converters: X tile -> tf32 hi/lo -> TMEM A stage (lane quarter = warp % 4)
 //   warps 8-15  attention (quarter q = warp % 4, half g = (warp - 8) / 4): extraction
@@ -40,10 +42,13 @@
 // stages · [256,384) Q hi|lo -> P hi|lo of keys 0-63 -> P hi|lo of keys 64-127 -> C
 // hi|lo · [384,512) S -> C accumulator [384,448) + Z accumulator [448,512).
 //
-// Measured (profiles/head_probe.py, r2 session): 94 us per 512-instance launch (round 1:
-// 100 us). The narrow attention MMAs (N = 64 / 128, A read from TMEM at ~64 B/cycle)
-// cost ~7.7k cycles per pair next to the projection's 18.4k, and the projection alone
-// runs at ~60 % of its MMA floor (profiles/README.md).
+// Measured (profiles/head_probe.py): 80 us per 512-instance launch (round 1: 100 us;
+// one issuer warp for both streams: 88 us). Per pair (profiles/head_timeline.py,
+// ~32k cycles): the tensor pipe holds 18.4k cycles of projection and ~3.8k of
+// attention MMAs (the narrow shapes run at full rate, profiles/mma_rate.cu); the rest
+// is the two-stage A ring's converter round trip (~11k cycles of issuer waits) and the
+// accumulator hand-over between pairs (~5k), both bounded by TMEM (512 columns) and
+// shared memory (224 KB) rather than by the X / W rings (deeper rings: no change).
 #include <mutex>
 
 #include "kernels.cuh"
@@ -58,6 +63,9 @@
 #ifndef HS_DBG_HEAD_NOCONV
 #define HS_DBG_HEAD_NOCONV 0
 #endif
+#ifndef HS_DBG_HEAD_NOPROJ  // timing experiment only: no projection MMAs (commits only)
+#define HS_DBG_HEAD_NOPROJ 0
+#endif
 #ifndef HS_DBG_HEAD_NOATT
 #define HS_DBG_HEAD_NOATT 0
 #endif
@@ -66,23 +74,33 @@ namespace hs {
 
 #if HS_DBG_TIMELINE
 // timing experiment only (profiles/head_timeline.py): CTA 0, first 8 pair iterations
-// x 16 slots: clock64 stamps, and cycles spent in selected waits (summed)
-__device__ long long g_head_timeline[8 * 16];
-#define TL(t, k)                                                                                   \
-  do {                                                                                             \
-    if (blockIdx.x == 0 && (t) < 8) g_head_timeline[(t) * 16 + (k)] = clock64();                   \
+// x 32 slots: clock stamps (low 32 bits), and cycles spent in selected waits (summed).
+// Accumulated in shared memory (a global read-modify-write would add its own latency
+// to every measured interval) and copied out at the end.
+__device__ long long g_head_timeline[8 * 32];
+#define TL(t, k)                                                           \
+  do {                                                                     \
+    if (blockIdx.x == 0 && (t) < 8) s_tl[(t) * 32 + (k)] = uint32_t(clock64()); \
   } while (0)
-#define TW(t, k, expr)                                                                             \
-  do {                                                                                             \
-    const long long _c0 = clock64();                                                               \
-    expr;                                                                                          \
-    if (blockIdx.x == 0 && (t) < 8 && lane == 0) g_head_timeline[(t) * 16 + (k)] += clock64() - _c0; \
+#define TW(t, k, expr)                                                          \
+  do {                                                                          \
+    const long long _c0 = clock64();                                            \
+    expr;                                                                       \
+    const long long _c1 = clock64();                                            \
+    if (blockIdx.x == 0 && (t) < 8 && lane == 0) s_tl[(t) * 32 + (k)] += uint32_t(_c1 - _c0); \
+  } while (0)
+#define TADD(t, k, v)                                              \
+  do {                                                             \
+    if (blockIdx.x == 0 && (t) < 8 && lane == 0) s_tl[(t) * 32 + (k)] += uint32_t(v); \
   } while (0)
 #else
 #define TL(t, k) \
   do {           \
   } while (0)
 #define TW(t, k, expr) expr
+#define TADD(t, k, v) \
+  do {                \
+  } while (0)
 #endif
 
 namespace {
@@ -92,16 +110,23 @@ using namespace tc;
 constexpr int kS = 128, kDK = 64, kN = 3 * kDK;  // rows, head width, projection width
 constexpr int kThreads = 512;
 constexpr int kXK = 16;                          // X tile / A stage: 16 columns (SWIZZLE_64B)
-constexpr int kWK = 32;                          // W stage: 32 columns (SWIZZLE_128B) = 2 A stages
+#ifndef HS_HEAD_WK
+#define HS_HEAD_WK 32
+#endif
+#ifndef HS_HEAD_NW
+#define HS_HEAD_NW 3
+#endif
+constexpr int kWK = HS_HEAD_WK;                  // W stage: 32 columns (SWIZZLE_128B) = 2 A stages, or 16 (SWIZZLE_64B)
+static_assert(kWK == 16 || kWK == 32, "W stage width");
 #ifndef HS_HEAD_NA
 #define HS_HEAD_NA 2
 #endif
 #ifndef HS_HEAD_NX
 #define HS_HEAD_NX 3
 #endif
-constexpr int kNX = HS_HEAD_NX, kNW = 3, kNA = HS_HEAD_NA;  // ring depths
+constexpr int kNX = HS_HEAD_NX, kNW = HS_HEAD_NW, kNA = HS_HEAD_NA;  // ring depths
 constexpr uint32_t kXTile = kS * kXK * 4;        // 8 KB
-constexpr uint32_t kWPlane = (kN / 2) * 128;     // 12 KB: this CTA's 96 rows
+constexpr uint32_t kWPlane = (kN / 2) * kWK * 4;  // this CTA's 96 rows (12 KB at kWK = 32)
 constexpr uint32_t kWStage = 2 * kWPlane;        // hi + lo
 // shared memory (bytes from the 1024-aligned base)
 constexpr uint32_t kXs = 0;
@@ -119,7 +144,7 @@ constexpr uint32_t kTQ = 0, kTK = 64, kTV = 128;  // projection accumulator
 constexpr uint32_t kTA = 192;                     // A stages, 32 columns each (hi 16 | lo 16)
 constexpr uint32_t kTOp = kTA + 32 * kNA;         // 128 columns: Q hi|lo -> P hi|lo (one key half) -> C hi|lo
 constexpr uint32_t kTR = kTOp + 128;              // 128 columns: S -> C acc [kTR, +64) -> Z acc [kTR + 64, +64)
-static_assert(kTR + 128 <= 512, "TMEM columns");
+static_assert(HS_DBG_HEAD_NOATT || kTR + 128 <= 512, "TMEM columns");
 
 enum Bar : uint32_t {
   XF = 0,               // [kNX] X tile landed (TMA tx)
@@ -151,20 +176,6 @@ struct HeadParams {
   float* Z;
   int64_t sZ, ldz;  // elements
 };
-
-// non-blocking test of an mbarrier phase (warp-uniform: lane 0 decides)
-__device__ __forceinline__ bool mbar_test_warp(uint32_t bar, uint32_t parity) {
-  uint32_t done = 0;
-  if ((threadIdx.x & 31) == 0)
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(done)
-        : "r"(bar), "r"(parity)
-        : "memory");
-  return __shfl_sync(0xffffffffu, done, 0) != 0;
-}
 
 // D (+)= A·B with A = a_hi + a_lo in TMEM, B = b_hi + b_lo in smem: lo·hi, hi·lo, hi·hi
 template <int kTerms, bool kPair>
@@ -242,6 +253,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
   auto bar = [&](uint32_t b) { return base + kBar + 8u * b; };
+#if HS_DBG_TIMELINE
+  __shared__ uint32_t s_tl[8 * 32];
+  for (int i = threadIdx.x; i < 8 * 32; i += blockDim.x) s_tl[i] = 0;
+#endif
   const uint32_t* tmem_slot_ptr =
       reinterpret_cast<const uint32_t*>(smem_raw + (bar(TMEM_SLOT) - smem_u32(smem_raw)));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -292,7 +307,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // (whole 128-byte row segments: the 64-byte X tiles then hit L2 instead of each
         // fetching half of a DRAM line)
         if (2 * (t + npairs) + int(rank) < p.batch)
-          for (int kb = 0; kb < nw; ++kb) tma_prefetch_3d(&tmXp, kb * kWK, 0, 2 * (t + npairs) + int(rank));
+          for (int kb = 0; kb < p.D / 32; ++kb) tma_prefetch_3d(&tmXp, kb * 32, 0, 2 * (t + npairs) + int(rank));
         for (int kb = 0; kb < nx; ++kb, ++it) {
           const int s = int(it % kNX);
           TW(lt, 12, mbar_wait(bar(XE + s), ((it / kNX) & 1u) ^ 1u));
@@ -317,22 +332,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp == 2) {
-    // ------------------------------------------------------------ Wh producer (after each S = Q Kᵀ)
-    if (lane == 0 && !HS_DBG_HEAD_NOATT) {
-      uint32_t lt = 0;
-      for (int t = pair0; t < p.pairs; t += npairs, ++lt) {
-        mbar_wait(bar(S_FULL), lt & 1u);
-        mbar_expect_tx(bar(WH_FULL), (kTerms > 1 ? 2u : 1u) * 16384u);
-        for (int pl = 0; pl < (kTerms > 1 ? 2 : 1); ++pl)
-          for (int kb = 0; kb < 2; ++kb)
-            tma_load_3d(base + kWh + uint32_t(pl) * 16384u + uint32_t(kb) * 8192u, &tmWh, bar(WH_FULL), kb * 32, 0,
-                        pl);
-      }
-    }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    // The whole warp runs the loop (warp-uniform state); one elected lane issues.
+  } else if (warp == 1 || warp == 2) {
+    // ------------------------------------------------------------ MMA issuers
+    // warp 1 (leader only): the projection; warp 2 (both CTAs): this CTA's attention
+    // and the Wh planes. Each loop runs on the whole warp (warp-uniform state) and one
+    // elected lane issues; every commit tracks the MMAs of its own issuing thread, and
+    // the two streams share the tensor pipe (profiles/mix_probe.cu -DMIX_SPLIT=1).
     constexpr uint32_t idP = instr_desc_tf32(kN, 256), idS = instr_desc_tf32(kS), idC = instr_desc_tf32(kDK);
     auto kdesc = [&](int kk, int plane) {  // K operand: k-block kk/4 of d, 8-column step kk%4
       return smem_desc(base + kKop + uint32_t(plane) * 32768u + uint32_t(kk >> 2) * 16384u + uint32_t(kk & 3) * 32u);
@@ -343,80 +348,70 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto whdesc = [&](int kk, int plane) {  // Whᵀ operand: k-block kk/4 of d
       return smem_desc(base + kWh + uint32_t(plane) * 16384u + uint32_t(kk >> 2) * 8192u + uint32_t(kk & 3) * 32u);
     };
-    // S = Q hi|lo [kTOp, +128) x K -> kTR (N = 128)
-    auto issue_s = [&]() {
-      if (elect_one()) {
-#pragma unroll
-        for (int kk = 0; kk < kDK / 8; ++kk)
-          mma3<kTerms, false>(tmem + kTR, tmem + kTOp + uint32_t(kk) * 8u, tmem + kTOp + 64u + uint32_t(kk) * 8u,
-                              kdesc(kk, 0), kdesc(kk, 1), idS, kk ? 1u : 0u);
-        mma_commit(bar(S_FULL));
-      }
-      __syncwarp();
-    };
-    // C (+)= P·V over one key half: P hi|lo [kTOp, +128) x Vᵀ k-blocks of those keys -> kTR
-    auto issue_pv = [&](int half) {
-      if (elect_one()) {
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          mma3<kTerms, false>(tmem + kTR, tmem + kTOp + uint32_t(kk) * 8u, tmem + kTOp + 64u + uint32_t(kk) * 8u,
-                              vdesc(8 * half + kk, 0), vdesc(8 * half + kk, 1), idC, (half | kk) ? 1u : 0u);
-        mma_commit(bar(half ? C_FULL : PV0_DONE));
-      }
-      __syncwarp();
-    };
-    auto issue_z = [&]() {
-      if (elect_one()) {
-#pragma unroll
-        for (int kk = 0; kk < kDK / 8; ++kk)
-          mma3<kTerms, false>(tmem + kTR + 64u, tmem + kTOp + uint32_t(kk) * 8u, tmem + kTOp + 64u + uint32_t(kk) * 8u,
-                              whdesc(kk, 0), whdesc(kk, 1), idC, kk ? 1u : 0u);
-        mma_commit(bar(Z_FULL));
-      }
-      __syncwarp();
-    };
-    // the attention of one instance as a sequence of steps, each gated by barriers:
-    // 0: S (EXT) 1: P·V keys 0-63 (S_READ, P0_READY) 2: P·V keys 64-127 (P1_READY)
-    // 3: Z (WH_FULL, C_READY) 4: done
-    constexpr int kSteps = 4;
-    auto step_ready = [&](int st, uint32_t ph, bool block) {
-      auto test = [&](uint32_t b) {
-        if (block) {
-          mbar_wait(bar(b), ph);
-          return true;
-        }
-        return mbar_test_warp(bar(b), ph);
-      };
-      switch (st) {
-        case 0: return test(EXT);
-        case 1: return test(S_READ) && test(P0_READY);
-        case 2: return test(P1_READY);
-        default: return test(WH_FULL) && test(C_READY);
-      }
-    };
-    auto step_issue = [&](int st) {
-      tc_fence_after();
-      if (st == 0) issue_s();
-      else if (st <= 2) issue_pv(st - 1);
-      else issue_z();
-    };
+    auto wdesc = [](uint32_t a) { return kWK == 32 ? smem_desc(a) : smem_desc_sw64(a); };
     uint32_t lt = 0;
-    if (rank != 0) {
-      // only this CTA's attention, in order
-      for (int t = pair0; t < p.pairs && !HS_DBG_HEAD_NOATT; t += npairs, ++lt)
-        for (int st = 0; st < kSteps; ++st) {
-          step_ready(st, lt & 1u, true);
-          step_issue(st);
+    if (warp == 2) {
+      // ---------------------------------------------------------- attention, in pair order
+      for (int t = pair0; t < p.pairs && !HS_DBG_HEAD_NOATT; t += npairs, ++lt) {
+        const uint32_t ph = lt & 1u;
+        // S = Q hi|lo [kTOp, +128) x K -> kTR (N = 128), once this CTA has extracted
+        TW(lt, 16, mbar_wait(bar(EXT), ph));
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < kDK / 8; ++kk)
+            mma3<kTerms, false>(tmem + kTR, tmem + kTOp + uint32_t(kk) * 8u, tmem + kTOp + 64u + uint32_t(kk) * 8u,
+                                kdesc(kk, 0), kdesc(kk, 1), idS, kk ? 1u : 0u);
+          mma_commit(bar(S_FULL));
         }
-    } else {
+        __syncwarp();
+        // K consumed: the Wh planes land over the K operand
+        TW(lt, 17, mbar_wait(bar(S_FULL), ph));
+        if (lane == 0) {
+          mbar_expect_tx(bar(WH_FULL), (kTerms > 1 ? 2u : 1u) * 16384u);
+          for (int pl = 0; pl < (kTerms > 1 ? 2 : 1); ++pl)
+            for (int kb = 0; kb < 2; ++kb)
+              tma_load_3d(base + kWh + uint32_t(pl) * 16384u + uint32_t(kb) * 8192u, &tmWh, bar(WH_FULL), kb * 32, 0,
+                          pl);
+        }
+        // C (+)= P·V per key half: P hi|lo [kTOp, +128) x Vᵀ k-blocks of those keys -> kTR
+        for (int half = 0; half < 2; ++half) {
+          if (half == 0) {
+            TW(lt, 18, mbar_wait(bar(S_READ), ph));
+            TW(lt, 18, mbar_wait(bar(P0_READY), ph));
+          } else {
+            TW(lt, 19, mbar_wait(bar(P1_READY), ph));
+          }
+          tc_fence_after();
+          if (elect_one()) {
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk)
+              mma3<kTerms, false>(tmem + kTR, tmem + kTOp + uint32_t(kk) * 8u, tmem + kTOp + 64u + uint32_t(kk) * 8u,
+                                  vdesc(8 * half + kk, 0), vdesc(8 * half + kk, 1), idC, (half | kk) ? 1u : 0u);
+            mma_commit(bar(half ? C_FULL : PV0_DONE));
+          }
+          __syncwarp();
+        }
+        // Z = C hi|lo x Wh -> kTR + 64
+        TW(lt, 20, mbar_wait(bar(WH_FULL), ph));
+        TW(lt, 20, mbar_wait(bar(C_READY), ph));
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < kDK / 8; ++kk)
+            mma3<kTerms, false>(tmem + kTR + 64u, tmem + kTOp + uint32_t(kk) * 8u,
+                                tmem + kTOp + 64u + uint32_t(kk) * 8u, whdesc(kk, 0), whdesc(kk, 1), idC,
+                                kk ? 1u : 0u);
+          mma_commit(bar(Z_FULL));
+        }
+        __syncwarp();
+      }
+    } else if (rank == 0) {
+      // ---------------------------------------------------------- projection (leader)
       uint32_t ia = 0, iw = 0;
-      int st = kSteps;  // step of the previous pair's attention (kSteps: nothing pending)
       for (int t = pair0; t < p.pairs; t += npairs, ++lt) {
-        if (lt > 0) {
-          // both CTAs have read the accumulator out: the next projection may overwrite it
-          mbar_wait(bar(EXT_PAIR), (lt - 1) & 1u);
-          st = HS_DBG_HEAD_NOATT ? kSteps : 0;
-        }
+        // both CTAs have read the accumulator out: the next projection may overwrite it
+        if (lt > 0) TW(lt, 6, mbar_wait(bar(EXT_PAIR), (lt - 1) & 1u));
         if (lane == 0) TL(lt, 0);
         for (int kb = 0; kb < nw; ++kb, ++iw) {
           const int w = int(iw % kNW);
@@ -426,36 +421,30 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int a = int(ia % kNA);
             TW(lt, 9, mbar_wait(bar(AF + a), (ia / kNA) & 1u));
             tc_fence_after();
+#if HS_DBG_TIMELINE
+            const long long c_iss0 = clock64();
+#endif
             if (elect_one()) {
               const uint32_t b = base + kWs + uint32_t(w) * kWStage + uint32_t(h) * 64u;
               const uint32_t ta = tmem + kTA + uint32_t(a) * 32u;
 #pragma unroll
-              for (int kk = 0; kk < kXK / 8; ++kk)
+              for (int kk = 0; kk < kXK / 8 && !HS_DBG_HEAD_NOPROJ; ++kk)
                 mma3<kTerms, true>(tmem + kTQ, ta + uint32_t(kk) * 8u, ta + 16u + uint32_t(kk) * 8u,
-                                   smem_desc(b + uint32_t(kk) * 32u), smem_desc(b + kWPlane + uint32_t(kk) * 32u), idP,
+                                   wdesc(b + uint32_t(kk) * 32u), wdesc(b + kWPlane + uint32_t(kk) * 32u), idP,
                                    (kb | h | kk) ? 1u : 0u);
               mma_commit_pair(bar(AE + a));
               if (h == kWK / kXK - 1) mma_commit_pair(bar(WE + w));
             }
             __syncwarp();
-            // interleave the previous pair's attention MMAs as their operands become ready
-            while (st < kSteps && step_ready(st, (lt - 1) & 1u, false)) step_issue(st++);
+#if HS_DBG_TIMELINE
+            TADD(lt, 7, clock64() - c_iss0);
+#endif
           }
         }
         if (elect_one()) mma_commit_pair(bar(ACC_FULL));
         __syncwarp();
         if (lane == 0) TL(lt, 1);
-        // the next extraction reuses the attention operands: finish the previous pair first
-        while (st < kSteps) {
-          step_ready(st, (lt - 1) & 1u, true);
-          step_issue(st++);
-        }
       }
-      if (lt > 0 && !HS_DBG_HEAD_NOATT)  // the last pair's attention
-        for (st = 0; st < kSteps; ++st) {
-          step_ready(st, (lt - 1) & 1u, true);
-          step_issue(st);
-        }
     }
   } else if (warp >= 4 && warp < 8) {
     // ------------------------------------------------------------ converters: X tile -> TMEM A stage
@@ -469,7 +458,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int t = pair0; t < p.pairs; t += npairs, ++lt) {
       for (int kb = 0; kb < nx; ++kb, ++it) {
         const int x = int(it % kNX), a = int(it % kNA);
-        TW(lt, 10, mbar_wait(bar(XF + x), (it / kNX) & 1u));
+#if HS_DBG_TIMELINE
+        const long long c_x0 = clock64();
+#endif
+        mbar_wait(bar(XF + x), (it / kNX) & 1u);
+#if HS_DBG_TIMELINE
+        if (q == 0) TADD(lt, 10, clock64() - c_x0);
+#endif
         uint32_t hi[16], lo[16], dep = 0;
         if (!HS_DBG_HEAD_NOCONV) {
           const uint32_t src = base + kXs + uint32_t(x) * kXTile + uint32_t(row) * 64u;
@@ -487,7 +482,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         // the staging slot goes back to TMA once this warp's loads have returned
         if (lane == 0) mbar_arrive_after(bar(XE + x), dep);
-        TW(lt, 11, mbar_wait(bar(AE + a), ((it / kNA) & 1u) ^ 1u));
+#if HS_DBG_TIMELINE
+        const long long c_a0 = clock64();
+#endif
+        mbar_wait(bar(AE + a), ((it / kNA) & 1u) ^ 1u);
+#if HS_DBG_TIMELINE
+        if (q == 0) TADD(lt, 11, clock64() - c_a0);
+#endif
         tc_fence_after();
 #if HS_DBG_TIMELINE
         const long long c_conv0 = clock64();
@@ -510,9 +511,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                        : "memory");
         }
 #if HS_DBG_TIMELINE
-        if (blockIdx.x == 0 && lt < 8 && lane == 0 && q == 0) {
-          g_head_timeline[lt * 16 + 14] += c_conv1 - c_conv0;
-          g_head_timeline[lt * 16 + 15] += clock64() - c_conv1;
+        const long long c_conv2 = clock64();
+        if (q == 0) {
+          TADD(lt, 14, c_conv1 - c_conv0);
+          TADD(lt, 15, c_conv2 - c_conv1);
         }
 #endif
       }
@@ -539,6 +541,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld32(lane_base + kTQ + uint32_t(32 * g), r);
         st_split16<kTerms>(lane_base + kTOp + uint32_t(32 * g), 64u, r);
         st_split16<kTerms>(lane_base + kTOp + uint32_t(32 * g + 16), 64u, r + 16);
+        if (warp == 8 && lane == 0) TL(lt, 24);
         // K row (key = row), d in [32g, 32g+32) -> K-major SW128 k-block g (hi, lo at +32 KB)
         tmem_ld32(lane_base + kTK + uint32_t(32 * g), r);
 #pragma unroll
@@ -550,6 +553,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           sts128(dst, h);
           if constexpr (kTerms > 1) sts128(dst + 32768u, make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w));
         }
+        if (warp == 8 && lane == 0) TL(lt, 25);
         // V row (key = row: k-block q, key lane), d in [32g, 32g+32) -> Vᵀ K-major SW128 [64 d][32 keys]
         tmem_ld32(lane_base + kTV + uint32_t(32 * g), r);
 #pragma unroll
@@ -560,6 +564,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           sts32(dst, h);
           if constexpr (kTerms > 1) sts32(dst + 32768u, x - h);
         }
+        if (warp == 8 && lane == 0) TL(lt, 26);
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       }
@@ -569,6 +574,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive(bar(EXT));
         mbar_arrive_cluster(leader(EXT_PAIR));
       }
+      if (lane == 0 && (warp == 8 || warp == 15)) TL(lt, warp == 8 ? 27 : 28);
       if (HS_DBG_HEAD_NOATT) continue;
       // ---- softmax over keys [64g, 64g+64) of this row: S of this key half in registers
       mbar_wait(bar(S_FULL), ph);
@@ -648,6 +654,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
   }
+#if HS_DBG_TIMELINE
+  if (blockIdx.x == 0)
+    for (int i = threadIdx.x; i < 8 * 32; i += blockDim.x) g_head_timeline[i] = s_tl[i];
+#endif
 }
 
 // 3-D fp32 tensor map with 64-byte swizzle (16-element boxes along the contiguous dim)
@@ -668,10 +678,10 @@ bool make_map_sw64(CUtensorMap* m, const void* ptr, uint64_t d0, uint64_t d1, ui
 
 }  // namespace hs
 
-// timing experiment only: reset / copy the debug timeline (8 x 16 slots)
+// timing experiment only: reset / copy the debug timeline (8 x 32 slots)
 extern "C" int hs_debug_head_timeline_reset(void) {
 #if HS_DBG_TIMELINE
-  static const long long zeros[128] = {};
+  static const long long zeros[256] = {};
   return cudaMemcpyToSymbol(hs::g_head_timeline, zeros, sizeof(zeros)) == cudaSuccess ? 0 : 1;
 #else
   return 1;
@@ -679,7 +689,7 @@ extern "C" int hs_debug_head_timeline_reset(void) {
 }
 extern "C" int hs_debug_head_timeline(long long* out) {
 #if HS_DBG_TIMELINE
-  return cudaMemcpyFromSymbol(out, hs::g_head_timeline, sizeof(long long) * 128) == cudaSuccess ? 0 : 1;
+  return cudaMemcpyFromSymbol(out, hs::g_head_timeline, sizeof(long long) * 256) == cudaSuccess ? 0 : 1;
 #else
   (void)out;
   return 1;
@@ -710,7 +720,8 @@ cudaError_t head_fused(const HeadArgs& a, int terms, cudaStream_t s) {
   CUtensorMap mX, mW, mWh, mXp;
   const bool ok = make_map_sw64(&mX, a.X, D, S, B, D * 4, uint64_t(a.sX ? a.sX : S * D) * 4, kXK, kS) &&
                   tc::make_map(&mXp, a.X, D, S, B, D * 4, uint64_t(a.sX ? a.sX : S * D) * 4, kWK, kS, true) &&
-                  tc::make_map(&mW, a.Wqkv, D, kN, 2, D * 4, uint64_t(kN) * D * 4, kWK, kN / 2, true) &&
+                  (kWK == 32 ? tc::make_map(&mW, a.Wqkv, D, kN, 2, D * 4, uint64_t(kN) * D * 4, kWK, kN / 2, true)
+                             : make_map_sw64(&mW, a.Wqkv, D, kN, 2, D * 4, uint64_t(kN) * D * 4, kWK, kN / 2)) &&
                   tc::make_map(&mWh, a.Wh, kDK, kDK, 2, kDK * 4, uint64_t(kDK * kDK) * 4, 32, kDK, true);
   if (!ok) return cudaErrorInvalidValue;
   const int64_t ldz = a.ldz ? a.ldz : kDK;

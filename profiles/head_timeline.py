@@ -36,15 +36,18 @@ _native.check(L.hs_stream_sync(stream()))
 assert L.hs_debug_head_timeline_reset() == 0, "library built without HS_DBG_TIMELINE"
 _native.check(L.hs_launch(stream(), 10, ctypes.byref(h), 0, batch))
 _native.check(L.hs_stream_sync(stream()))
-buf = (ctypes.c_longlong * 128)()
+buf = (ctypes.c_longlong * 256)()
 L.hs_debug_head_timeline.argtypes = [ctypes.c_void_p]
 assert L.hs_debug_head_timeline(ctypes.cast(buf, ctypes.c_void_p)) == 0, "library built without HS_DBG_TIMELINE"
-tl = np.array(buf[:], dtype=np.int64).reshape(8, 16)
-names = ["mma:proj_start", "mma:proj_issued", "att:acc_full", "att:s_full", "att:c_full", "att:z_stored"]
-waits = {8: "mma_wait_W", 9: "mma_wait_A", 10: "conv_wait_X", 11: "conv_wait_Aempty", 12: "xtma_wait_empty",
-         13: "wtma_wait_empty", 14: "conv_work", 15: "conv_signal"}
-t0 = tl[0, 0]
+tl = np.array(buf[:], dtype=np.int64).reshape(8, 32)
+names = ["mma:proj_start", "mma:proj_issued", "att:acc_full", "att:s_full", "att:c_full", "att:z_stored"]  # slots 0-5
+ext = {24: "ext:q", 25: "ext:k", 26: "ext:v_issued", 27: "ext:done_w8", 28: "ext:done_w15"}
+waits = {6: "mma_wait_extpair", 7: "mma_proj_issue", 8: "mma_wait_W", 9: "mma_wait_A", 10: "conv_wait_X",
+         11: "conv_wait_Aempty", 12: "xtma_wait_empty", 13: "wtma_wait_empty", 14: "conv_work", 15: "conv_signal",
+         16: "att_wait_ext", 17: "att_wait_sfull", 18: "att_wait_p0", 19: "att_wait_p1", 20: "att_wait_c"}
+t0 = tl[0, 0]  # stamps are the low 32 bits of clock64
 per_cta = -(-batch // 148)
 for t in range(min(per_cta, 8)):
-    print(f"instance {t}: " + "  ".join(f"{n}={tl[t, k] - t0}" for k, n in enumerate(names)))
+    print(f"pair {t}: " + "  ".join(f"{n}={(tl[t, k] - t0) % 2**32}" for k, n in enumerate(names)))
+    print("    extraction: " + "  ".join(f"{n}={(tl[t, k] - t0) % 2**32}" for k, n in ext.items()))
     print("    waits: " + "  ".join(f"{n}={tl[t, k]}" for k, n in waits.items()))

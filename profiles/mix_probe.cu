@@ -4,7 +4,7 @@
 // into columns [0, 64) while each CTA issues its own cta_group::1 MMAs (M = 128,
 // N = 64) into columns [128, 192), interleaved over many iterations. Inputs are
 // small integers (exact in tf32), so both results are checked exactly.
-//   nvcc -gencode arch=compute_100a,code=sm_100a -O2 -o /tmp/mix_probe profiles/mix_probe.cu -lcuda
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O2 [-DMIX_SPLIT=1] -o /tmp/mix_probe profiles/mix_probe.cu -lcuda
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -62,19 +62,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
   tc_fence_before();
   cluster_sync_all();
   tc_fence_after();
+#ifndef MIX_SPLIT  // MIX_SPLIT=1: the single-CTA MMAs come from another warp (own issuer thread)
+#define MIX_SPLIT 0
+#endif
+  const uint32_t id2 = instr_desc_tf32(64, 256), id1 = instr_desc_tf32(64, 128);
   if (warp == 1) {
-    const uint32_t id2 = instr_desc_tf32(64, 256), id1 = instr_desc_tf32(64, 128);
     for (int it = 0; it < kIters; ++it) {
       if (elect_one()) {
         if (rank == 0) mma_pair_tf32_ts(tmem + 0, tmem + 256, smem_desc(sB2), id2, it ? 1u : 0u);
-        mma_tf32_ts(tmem + 128, tmem + 320, smem_desc(sB1), id1, it ? 1u : 0u);
+        if (!MIX_SPLIT) mma_tf32_ts(tmem + 128, tmem + 320, smem_desc(sB1), id1, it ? 1u : 0u);
       }
       __syncwarp();
     }
     if (elect_one()) {
       if (rank == 0) mma_commit_pair(bar2);
-      mma_commit(bar1);
+      if (!MIX_SPLIT) mma_commit(bar1);
     }
+    __syncwarp();
+  } else if (warp == 2 && MIX_SPLIT) {
+    for (int it = 0; it < kIters; ++it) {
+      if (elect_one()) mma_tf32_ts(tmem + 128, tmem + 320, smem_desc(sB1), id1, it ? 1u : 0u);
+      __syncwarp();
+    }
+    if (elect_one()) mma_commit(bar1);
     __syncwarp();
   }
   mbar_wait(bar2, 0);
