@@ -279,6 +279,19 @@ def run_reference(args, world, rank):
 
 # --------------------------------------------------------------------------- GPU arm
 
+def nominal_tc(achieved, clocks, math):
+    """The tensor pipe's issue-rate ceiling at the run's median SM clock: tcgen05
+    kind::tf32 retires 4096 dense flop/clk/SM and kind::f16 8192 (profiles/mma_rate.cu
+    measures both at full rate, M = 128, N = 64-256), / 3 MMAs per product. The
+    measured-peak P above is lower (cuBLAS bf16 under the power cap)."""
+    mhz = (clocks or {}).get("sm_mhz")
+    if not mhz:
+        return None
+    per_clk = 8192 if math == "bf16x3" else 4096
+    pk = per_clk * 148 * mhz * 1e6 / 1e12 / (1.0 if math == "tf32" else 3.0)
+    return {"peak_at_sm_clock": pk, "sm_mhz": mhz, "flop_per_clk_per_sm": per_clk, "frac": achieved / pk}
+
+
 def gemm_roofline(batch, math_mode, reps=20):
     """Time the dominant kernel exactly as the DAG launches it — FFN1, gemm_relu
     128x2048x512 per instance, batched, resident weight pre-split into planes —
@@ -791,9 +804,11 @@ def run_ours(args, world, rank, local):
                        "l2": "inputs (1 GiB X + 1 GiB out per step) larger than L2"},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": f"gemm_pair_kernel (CTA pair, cta_group::2, BN=256) FFN1 gemm_relu 128x2048x512 "
-                                   f"x{args.batch}, resident pre-split weight, {args.math} ({ms_launch:.3f} ms/launch)",
-                         "peak_note": peak_note, "measured_peaks_file": pk_kind},
+                         "kernel": f"gemm_pair_kernel (CTA pair, cta_group::2, 192-wide tiles, two TMEM accumulators) "
+                                   f"FFN1 gemm_relu 128x2048x512 x{args.batch}, resident pre-split weight, {args.math} "
+                                   f"({ms_launch:.3f} ms/launch)",
+                         "peak_note": peak_note, "measured_peaks_file": pk_kind,
+                         "nominal": nominal_tc(achieved, clocks, args.math)},
             "dag_roofline": {"flop_per_dag": flop_per_inst, "achieved_tflops": flop_per_inst * value / 1e12,
                              "frac_of_peak": flop_per_inst * value / 1e12 / (peak * world),
                              "t_star_ms": args.instances * flop_per_inst / (peak * world * 1e12) * 1e3,
