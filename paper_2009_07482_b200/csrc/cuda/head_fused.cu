@@ -66,6 +66,12 @@
 #ifndef HS_DBG_HEAD_NOPROJ  // timing experiment only: no projection MMAs (commits only)
 #define HS_DBG_HEAD_NOPROJ 0
 #endif
+#ifndef HS_HEAD_PREFETCH_AHEAD  // pairs of X prefetched into L2 ahead of the current one
+#define HS_HEAD_PREFETCH_AHEAD 1
+#endif
+#ifndef HS_DBG_HEAD_XSRC
+#define HS_DBG_HEAD_XSRC 0
+#endif
 #ifndef HS_DBG_HEAD_NOATT
 #define HS_DBG_HEAD_NOATT 0
 #endif
@@ -300,19 +306,32 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     // ------------------------------------------------------------ X producer (this CTA's instance)
     if (lane == 0) {
+      // Warm L2 with whole instances ahead of their X tiles: the tile ring keeps only
+      // kNX x 8 KB in flight, too little to cover DRAM latency, while a prefetch of all
+      // 16 128-byte row segments per row has no such limit (and the 64-byte tiles then
+      // hit L2 instead of each fetching half of a DRAM line). X from L2 instead of DRAM
+      // is worth ~10 % of the launch (profiles/README.md, HS_DBG_HEAD_XSRC).
+      auto prefetch = [&](int t) {
+        const int inst = 2 * t + int(rank);
+        if (t < p.pairs && inst < p.batch)
+          for (int kb = 0; kb < p.D / 32; ++kb) tma_prefetch_3d(&tmXp, kb * 32, 0, inst);
+      };
+      for (int a = 0; a < HS_HEAD_PREFETCH_AHEAD; ++a) prefetch(pair0 + a * npairs);
       uint32_t it = 0, lt = 0;
       for (int t = pair0; t < p.pairs; t += npairs, ++lt) {
         const int inst = 2 * t + int(rank);  // >= batch: zero-filled box
-        // warm L2 with this CTA's next instance: its loads start right after this projection
-        // (whole 128-byte row segments: the 64-byte X tiles then hit L2 instead of each
-        // fetching half of a DRAM line)
-        if (2 * (t + npairs) + int(rank) < p.batch)
-          for (int kb = 0; kb < p.D / 32; ++kb) tma_prefetch_3d(&tmXp, kb * 32, 0, 2 * (t + npairs) + int(rank));
+        prefetch(t + HS_HEAD_PREFETCH_AHEAD * npairs);
         for (int kb = 0; kb < nx; ++kb, ++it) {
           const int s = int(it % kNX);
           TW(lt, 12, mbar_wait(bar(XE + s), ((it / kNX) & 1u) ^ 1u));
+#if HS_DBG_HEAD_XSRC == 2  // timing experiment only: no X loads
+          mbar_arrive(bar(XF + s));
+#else  // timing experiments only: HS_DBG_HEAD_XSRC == 1: every pair reads instance 0's X (L2-resident);
+       // 3: every pair of a CTA re-reads its first instance
           mbar_expect_tx(bar(XF + s), kXTile);
-          tma_load_3d(base + kXs + uint32_t(s) * kXTile, &tmX, bar(XF + s), kb * kXK, 0, inst);
+          tma_load_3d(base + kXs + uint32_t(s) * kXTile, &tmX, bar(XF + s), kb * kXK, 0,
+                      HS_DBG_HEAD_XSRC == 1 ? 0 : HS_DBG_HEAD_XSRC == 3 ? 2 * pair0 + int(rank) : inst);
+#endif
         }
       }
     }
