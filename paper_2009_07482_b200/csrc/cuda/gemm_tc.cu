@@ -624,6 +624,15 @@ __global__ void __launch_bounds__(kThreads, kSmall ? 2 : 1)
 #ifndef HS_PAIR_DBL192  // 192-wide pair tiles keep two accumulators
 #define HS_PAIR_DBL192 1
 #endif
+#ifndef HS_PAIR_WIDE_BN  // tile width of that route (two accumulators fit up to 192)
+#define HS_PAIR_WIDE_BN 192
+#endif
+#ifndef HS_PAIR_WIDE_KMAX
+#define HS_PAIR_WIDE_KMAX 1024
+#endif
+#ifndef HS_PAIR_WIDE_NMIN
+#define HS_PAIR_WIDE_NMIN 1024
+#endif
 #ifndef HS_PAIR_WIDE192  // FFN1-shaped GEMMs on double-buffered 192-wide pair tiles
 #define HS_PAIR_WIDE192 1
 #endif
@@ -742,6 +751,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     m0 = (rb % p.m_tiles) * BM;
     n0 = nt * BN;
   };
+  // Columns the tile's MMAs cover: BN, or for a ragged last tile its valid columns
+  // rounded up to 64 (FFN1: N = 2048 = 10 x 192 + 128), so no MMA work or epilogue
+  // drain is spent on padding. Each CTA holds half of them as its B rows.
+  auto tile_n = [&](int n0) {
+    const int valid = p.N - n0;
+    return valid >= BN ? BN : ((valid + 63) / 64) * 64;
+  };
 
   if (warp == 0) {
     // ------------------------------------------------------------ A producer (local)
@@ -784,7 +800,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           (void)b_hi; (void)full;
 #else
           if (rank == 0) mbar_expect_tx(op_full(o), 2 * (kTerms > 1 ? 2 : 1) * L::kPlaneB);
-          const int nrow = n0 + int(rank) * L::kHalfN;
+          const int nrow = n0 + int(rank) * (tile_n(n0) / 2);
           tma_load_3d_pair(b_hi, &tmB, full, kb * BK, nrow, 0);
           if constexpr (kTerms > 1) tma_load_3d_pair(b_hi + L::kPlaneB, &tmB, full, kb * BK, nrow, 1);
 #endif
@@ -794,13 +810,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (leader only)
     if (lane == 0 && rank == 0) {
-      constexpr uint32_t idesc = (kBf16 ? instr_desc_bf16(BN) : instr_desc_tf32(BN)) + (uint32_t(BM >> 4) << 24);
+      constexpr uint32_t idesc_bn = (kBf16 ? instr_desc_bf16(BN) : instr_desc_tf32(BN)) + (uint32_t(BM >> 4) << 24);
       uint32_t it = 0, lt = 0;
       for (int t = pair0; t < p.total_tiles; t += npairs, ++lt) {
         const uint32_t acc = lt % uint32_t(L::kAccBufs);
         mbar_wait(acc_empty(int(acc)), ((lt / uint32_t(L::kAccBufs)) & 1u) ^ 1u);
         tc_fence_after();
         const uint32_t d = tmem + acc * uint32_t(BN);
+        const uint32_t idesc = (idesc_bn & ~(0x3Fu << 17)) | (uint32_t(tile_n((t % p.n_tiles) * BN) >> 3) << 17);
         for (int kb = 0; kb < nk; ++kb, ++it) {
           const int o = int(it % NO);
           mbar_wait(op_full(o), (it / NO) & 1u);
@@ -888,13 +905,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       // accumulator is released as soon as the last pair is in registers.
       static_assert((BN / 32) % 2 == 0, "pair epilogue drains chunks in pairs");
 #pragma unroll 1
-      for (int cb = 0; cb < BN / 32; cb += 2) {
+      const int nchunks = tile_n(n0) / 32;
+      for (int cb = 0; cb < nchunks; cb += 2) {
         uint32_t r0[32], r1[32];
         tmem_ld32_nowait(tacc + uint32_t(cb * 32), r0);
         tmem_ld32_nowait(tacc + uint32_t(cb * 32 + 32), r1);
         tmem_ld_wait(r0);
         tmem_ld_dep(r1);
-        if (cb + 2 == BN / 32 && !HS_DBG_EARLYREL) {
+        if (cb + 2 == nchunks && !HS_DBG_EARLYREL) {
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive_cluster(mapa_rank(acc_empty(int(acc)), 0));
@@ -1225,7 +1243,8 @@ cudaError_t gemm_tcgen05(const GemmArgs& a, int terms, cudaStream_t s) {
     // wide N over a short K (FFN1: N = 2048, K = 512): the per-tile epilogue drain is
     // ~10 % of a 256-wide tile's MMA time, so double-buffered 192-wide tiles win
     // despite the ragged last tile
-    if (HS_PAIR_WIDE192 && a.n_out <= 1 && a.N >= 1024 && a.K <= 1024) return launch_pair_bn<192>(a, terms, s);
+    if (HS_PAIR_WIDE192 && a.n_out <= 1 && a.N >= HS_PAIR_WIDE_NMIN && a.K <= HS_PAIR_WIDE_KMAX)
+      return launch_pair_bn<HS_PAIR_WIDE_BN>(a, terms, s);
     if (a.N >= 256 && a.n_out <= 1) return launch_pair_bn<HS_PAIR_BN>(a, terms, s);
   }
   if (a.n_out > 1) {
