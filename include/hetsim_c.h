@@ -198,8 +198,8 @@ typedef struct hs_engine* hs_engine_t;
  * fuse (graph mode launch lowering): 0 one launch per ndrange,
  * 1 + grouped sibling GEMMs, 2 + chain rewrites, 3 (default) + whole-head launches.
  * Optional: "device_gpus": {"<logical device>": ordinal} (components across GPUs),
- * "domain_per_device": 0|1, "ramp": 1|0 (batch/4 first and last chunks when the
- * bindings are host memory), "dynamic_fuse": 0|1 (dynamic mode issues the graph
+ * "domain_per_device": 0|1, "ramp": 1|0|R (first and last chunks of batch/4, off,
+ * or R <= batch/2 instances when the bindings are host memory), "dynamic_fuse": 0|1 (dynamic mode issues the graph
  * plan's fused launches instead of one kernel per ndrange; InvalidParam when it
  * cannot apply: devices with different queue counts, or simt math),
  * "deterministic": 0|1 (HS_FLAG_DETERMINISTIC on every launch),

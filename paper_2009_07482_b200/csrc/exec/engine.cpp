@@ -1346,7 +1346,8 @@ void Engine::plan_once() {
       if (!gr.resident && !gr.b.on_device) host_io = true;
     for (const auto& key : outputs_)
       if (!bindings_.at(key).on_device) host_io = true;
-    if (cfg_.ramp && host_io && !cfg_.trace && cfg_.batch >= 8 && slots_.size() > 1) ramp_ = cfg_.batch / 4;
+    if (cfg_.ramp && host_io && !cfg_.trace && cfg_.batch >= 8 && slots_.size() > 1)
+      ramp_ = cfg_.ramp > 1 ? std::min<int64_t>(cfg_.ramp, cfg_.batch / 2) : cfg_.batch / 4;
     if (capture_ok_)
       for (auto& sl : slots_) capture(sl);
   }
@@ -1578,7 +1579,10 @@ int hs_engine_create(const char* config_json, hs_engine_t* out) {
     if (const json::Value* v = c.find("device_gpus"))
       for (const auto& [k, g] : v->object_items()) cfg.device_gpus[std::stoi(k)] = g.as_int();
     if (const json::Value* v = c.find("domain_per_device")) cfg.domain_per_device = v->as_int() != 0;
-    if (const json::Value* v = c.find("ramp")) cfg.ramp = v->as_int() != 0;
+    if (const json::Value* v = c.find("ramp")) {
+      cfg.ramp = int(v->as_int());
+      if (cfg.ramp < 0) fail(Errc::invalid_param, "ramp must be >= 0");
+    }
     if (const json::Value* v = c.find("dynamic_fuse")) cfg.dynamic_fuse = v->as_int() != 0;
     if (const json::Value* v = c.find("deterministic")) cfg.deterministic = v->as_int() != 0;
     if (const json::Value* v = c.find("liveness")) cfg.liveness = v->as_int() != 0;

@@ -58,8 +58,9 @@ struct EngineConfig {
   std::map<int, int> device_gpus;
   bool domain_per_device = false;
   // Graph mode with host-memory inputs/outputs: first and last chunks of a run
-  // use a second graph of batch/4 instances (shorter exposed copies).
-  bool ramp = true;
+  // use a second graph of ramp instances (shorter exposed copies): 1 = batch/4,
+  // 0 = off, > 1 = that many instances (at most batch/2).
+  int ramp = 1;
   // Dynamic mode with the graph plan's launch lowering (grouped / fused launches per
   // component); off by default: Alg. 1 as written launches one kernel per ndrange.
   bool dynamic_fuse = false;

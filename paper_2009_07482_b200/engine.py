@@ -31,7 +31,7 @@ class Engine:
                  mode: str = "graph", batch: int = 1, slots: int = 2, math: str = "tf32x3", cpu_devices=(),
                  fuse: int | bool = 3, trace: bool = False, device_gpus: dict | None = None,
                  domain_per_device: bool = False, dynamic_fuse: bool = False, deterministic: bool = False,
-                 liveness: bool = True):
+                 liveness: bool = True, ramp: int = 1):
         """fuse (graph mode): 0 = one launch per ndrange; 1 = + grouped sibling GEMMs;
         2 = + chain rewrites (transpose -> gemm_nt, softmax as a GEMM epilogue, concat
         inputs written in place, fused attention heads); 3 (default, also True) = + each
@@ -48,13 +48,15 @@ class Engine:
         deterministic: no split-K in single-instance GEMMs, so every output is
         bit-reproducible from run to run (split-K adds K-split partials atomically).
         liveness: intermediate buffers share one arena per slot wherever the DAG orders
-        all their accesses (False: one device allocation per output buffer)."""
+        all their accesses (False: one device allocation per output buffer).
+        ramp (graph mode, host-memory bindings): the first and last chunks of a run are
+        short so their copies are short: 1 = batch/4 instances, 0 = off, R > 1 = R."""
         fuse = 3 if fuse is True else int(fuse)
         cfg = {"spec": spec_text, "params": dict(params or {}), "gpu": gpu, "policy": policy, "mode": mode,
                "batch": batch, "slots": slots, "math": math, "cpu_devices": list(cpu_devices), "fuse": int(fuse),
                "trace": int(bool(trace)), "domain_per_device": int(bool(domain_per_device)),
                "dynamic_fuse": int(bool(dynamic_fuse)), "deterministic": int(bool(deterministic)),
-               "liveness": int(bool(liveness))}
+               "liveness": int(bool(liveness)), "ramp": int(ramp)}
         if device_gpus:
             cfg["device_gpus"] = {str(k): int(v) for k, v in device_gpus.items()}
         self._lib = lib()
