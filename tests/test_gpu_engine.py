@@ -153,18 +153,22 @@ def test_encoder_bf16x3_within_tolerance(mode, oracle_mod):
         assert _normwise(outs[key][i], ref[key][i]) <= TOL
 
 
-def test_dynamic_completion_log_replays_identically(oracle_mod):
-    """Bit-exact scheduling parity: the completion order observed on the GPU,
-    fed back through the CPU scheduler (product and oracle restatement),
-    reproduces the GPU run's dispatch sequence."""
-    text, params, meta = workloads.encoder(layers=1, devices=2)
+@pytest.mark.parametrize("policy,layers,devices", [("clustering", 1, 2), ("eager", 1, 2), ("heft", 1, 2),
+                                                    ("clustering", 2, 3), ("eager", 2, 3), ("heft", 2, 3)])
+def test_dynamic_completion_log_replays_identically(policy, layers, devices, oracle_mod):
+    """Bit-exact scheduling parity for every policy: the completion order observed on
+    the GPU, fed back through the CPU scheduler (product and oracle restatement),
+    reproduces the GPU run's dispatch sequence (eager and HEFT see one component per
+    kernel, so their logs are long and callback-driven)."""
+    text, params, meta = workloads.encoder(layers=layers, devices=devices)
     arrays = _encoder_arrays(meta, params, 1)
-    _, info, _ = _run_gpu(text, params, arrays, 1, mode="dynamic", batch=1)
+    _, info, _ = _run_gpu(text, params, arrays, 1, mode="dynamic", batch=1, policy=policy)
     log = info["completions"]
+    assert log and info["dispatches"]
     spec = hetsim.parse_spec(text, params)
-    replay = hetsim.run_schedule(spec, replay=log)
+    replay = hetsim.run_schedule(spec, policy=policy, replay=log)
     assert replay["dispatches"] == info["dispatches"]
-    o = oracle_mod.schedule(oracle_mod.Spec(text, params), replay=log)
+    o = oracle_mod.schedule(oracle_mod.Spec(text, params), policy=policy, replay=log)
     assert o["dispatches"] == info["dispatches"]
     assert o["kernel_finish_order"] == replay["kernel_finish_order"]
 
