@@ -534,7 +534,7 @@ def config_spec(cfg, queues=3, devices=1):
 
 
 def config_makespan(cfg, fuse=3, queues=3, devices=1, reps=20, warmup=3, math_mode="tf32x3", check=True, batch=None,
-                    slots=1):
+                    slots=1, **engine_kw):
     """Makespan of one whole run of config `cfg` (all its instances in one batch) in graph
     mode with device-resident inputs/outputs: median over `reps` runs of the engine's own
     CUDA-event timing (start event -> end event on the origin stream, which joins every
@@ -555,7 +555,7 @@ def config_makespan(cfg, fuse=3, queues=3, devices=1, reps=20, warmup=3, math_mo
     out_dev = {(k, p): torch.zeros(n, e, device="cuda") for k, p, e in outs}
     torch.cuda.synchronize()
     batch = batch or n
-    with Engine(text, params, batch=batch, slots=slots, mode="graph", fuse=fuse, math=math_mode) as eng:
+    with Engine(text, params, batch=batch, slots=slots, mode="graph", fuse=fuse, math=math_mode, **engine_kw) as eng:
         for key, t in dev.items():
             eng.bind(*key, t, shared=key in shared or t.dim() == 1)
         for key, t in out_dev.items():

@@ -204,7 +204,10 @@ typedef struct hs_engine* hs_engine_t;
  * cannot apply: devices with different queue counts, or simt math),
  * "deterministic": 0|1 (HS_FLAG_DETERMINISTIC on every launch),
  * "liveness": 1|0 (intermediate buffers share one arena per slot wherever the
- * DAG orders all their accesses; 0 = one allocation per output buffer). */
+ * DAG orders all their accesses; 0 = one allocation per output buffer),
+ * "run_graph": 1|0 (graph mode on one GPU: a run of at most `batch` instances
+ * replays one graph holding its copy-in, the plan and its copy-out, captured for
+ * that (first, n) window; 0 = copies issued per run around the plan graph). */
 int hs_engine_create(const char* config_json, hs_engine_t* out);
 int hs_engine_destroy(hs_engine_t e);
 

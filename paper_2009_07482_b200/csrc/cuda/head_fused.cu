@@ -115,13 +115,28 @@ using namespace tc;
 
 constexpr int kS = 128, kDK = 64, kN = 3 * kDK;  // rows, head width, projection width
 constexpr int kThreads = 512;
-constexpr int kXK = 16;                          // X tile / A stage: 16 columns (SWIZZLE_64B)
+// HS_HEAD_RZ: tcgen05 kind::tf32 reads an fp32 operand by truncating its low 13
+// mantissa bits (profiles/tf32_trunc_probe.cu: round-toward-zero, from shared memory
+// and from TMEM alike), so a raw fp32 X tile is already the hi term of an exact
+// split x = rz(x) + (x - rz(x)). The projection's hi·W products read the TMA-landed X
+// tile straight from shared memory; only lo = rna(x - rz(x)) goes through the
+// converters into a TMEM A stage (16 columns instead of 32: half the TMEM stores, and
+// four stages where the hi|lo split fit two). The X slot then stays live until the
+// MMAs that read it complete (their commit frees it).
+#ifndef HS_HEAD_RZ
+#define HS_HEAD_RZ 0
+#endif
 #ifndef HS_HEAD_WK
 #define HS_HEAD_WK 32
 #endif
 #ifndef HS_HEAD_NW
-#define HS_HEAD_NW 3
+#define HS_HEAD_NW (HS_HEAD_RZ ? 2 : 3)
 #endif
+#ifndef HS_HEAD_XK
+#define HS_HEAD_XK (HS_HEAD_RZ ? 32 : 16)
+#endif
+constexpr int kXK = HS_HEAD_XK;                  // X tile / A stage: 16 columns (SWIZZLE_64B) or 32 (SWIZZLE_128B)
+static_assert(kXK == 16 || (kXK == 32 && HS_HEAD_RZ), "X tile width (32 only with lo-only A stages)");
 constexpr int kWK = HS_HEAD_WK;                  // W stage: 32 columns (SWIZZLE_128B) = 2 A stages, or 16 (SWIZZLE_64B)
 static_assert(kWK == 16 || kWK == 32, "W stage width");
 #ifndef HS_HEAD_NA
@@ -147,8 +162,9 @@ static_assert(kSmem <= 227 * 1024, "shared memory budget exceeded");
 
 // TMEM columns
 constexpr uint32_t kTQ = 0, kTK = 64, kTV = 128;  // projection accumulator
-constexpr uint32_t kTA = 192;                     // A stages, 32 columns each (hi 16 | lo 16)
-constexpr uint32_t kTOp = kTA + 32 * kNA;         // 128 columns: Q hi|lo -> P hi|lo (one key half) -> C hi|lo
+constexpr uint32_t kTA = 192;                     // A stages: lo 16 (HS_HEAD_RZ) or hi 16 | lo 16
+constexpr uint32_t kAW = HS_HEAD_RZ ? kXK : 2 * kXK;  // columns per A stage
+constexpr uint32_t kTOp = kTA + kAW * kNA;       // 128 columns: Q hi|lo -> P hi|lo (one key half) -> C hi|lo
 constexpr uint32_t kTR = kTOp + 128;              // 128 columns: S -> C acc [kTR, +64) -> Z acc [kTR + 64, +64)
 static_assert(HS_DBG_HEAD_NOATT || kTR + 128 <= 512, "TMEM columns");
 
@@ -274,7 +290,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < kNX; ++s) {
       mbar_init(bar(XF + s), 1);
-      mbar_init(bar(XE + s), 4);
+      mbar_init(bar(XE + s), HS_HEAD_RZ ? 1 : 4);  // RZ: the leader's commit of the MMAs reading it
     }
     for (int s = 0; s < kNW; ++s) {
       mbar_init(bar(WF + s), 1);
@@ -444,13 +460,33 @@ __global__ void __launch_bounds__(kThreads, 1)
             const long long c_iss0 = clock64();
 #endif
             if (elect_one()) {
-              const uint32_t b = base + kWs + uint32_t(w) * kWStage + uint32_t(h) * 64u;
-              const uint32_t ta = tmem + kTA + uint32_t(a) * 32u;
+              const uint32_t b = base + kWs + uint32_t(w) * kWStage + uint32_t(h) * uint32_t(kXK * 4);
+              const uint32_t ta = tmem + kTA + uint32_t(a) * kAW;
+#if HS_HEAD_RZ
+              // lo·W_hi from the TMEM A stage; hi·W_lo and hi·W_hi read the raw X tile
+              // (each CTA's own 128 rows, same slot offset in both CTAs)
+              const int x = int(ia % kNX);
+              const uint32_t xa = base + kXs + uint32_t(x) * kXTile;
+#pragma unroll
+              for (int kk = 0; kk < kXK / 8 && !HS_DBG_HEAD_NOPROJ; ++kk) {
+                const uint32_t first = (kb | h | kk) ? 1u : 0u;
+                const uint64_t xd = kXK == 32 ? smem_desc(xa + uint32_t(kk) * 32u) : smem_desc_sw64(xa + uint32_t(kk) * 32u);
+                if constexpr (kTerms > 1) {
+                  mma_pair_tf32_ts(tmem + kTQ, ta + uint32_t(kk) * 8u, wdesc(b + uint32_t(kk) * 32u), idP, first);
+                  mma_pair_tf32_ss(tmem + kTQ, xd, wdesc(b + kWPlane + uint32_t(kk) * 32u), idP, 1u);
+                  mma_pair_tf32_ss(tmem + kTQ, xd, wdesc(b + uint32_t(kk) * 32u), idP, 1u);
+                } else {
+                  mma_pair_tf32_ss(tmem + kTQ, xd, wdesc(b + uint32_t(kk) * 32u), idP, first);
+                }
+              }
+              mma_commit_pair(bar(XE + x));
+#else
 #pragma unroll
               for (int kk = 0; kk < kXK / 8 && !HS_DBG_HEAD_NOPROJ; ++kk)
                 mma3<kTerms, true>(tmem + kTQ, ta + uint32_t(kk) * 8u, ta + 16u + uint32_t(kk) * 8u,
                                    wdesc(b + uint32_t(kk) * 32u), wdesc(b + kWPlane + uint32_t(kk) * 32u), idP,
                                    (kb | h | kk) ? 1u : 0u);
+#endif
               mma_commit_pair(bar(AE + a));
               if (h == kWK / kXK - 1) mma_commit_pair(bar(WE + w));
             }
@@ -469,7 +505,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------------------ converters: X tile -> TMEM A stage
     const int q = warp & 3, row = q * 32 + lane;
     const uint32_t lane_base = tmem + (uint32_t(q * 32) << 16);
-    const uint32_t swz = uint32_t((row >> 1) & 3);
+    const uint32_t swz = kXK == 32 ? uint32_t(row & 7) : uint32_t((row >> 1) & 3);
     // The X tile is read and split into registers (and its staging slot released)
     // before waiting for the A stage to free up: only the TMEM stores and the signal
     // remain between the MMA's release of the stage and its next use.
@@ -484,12 +520,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 #if HS_DBG_TIMELINE
         if (q == 0) TADD(lt, 10, clock64() - c_x0);
 #endif
-        uint32_t hi[16], lo[16], dep = 0;
+        uint32_t hi[16], lo[kXK], dep = 0;
         if (!HS_DBG_HEAD_NOCONV) {
-          const uint32_t src = base + kXs + uint32_t(x) * kXTile + uint32_t(row) * 64u;
-          uint32_t v[16];
+          const uint32_t src = base + kXs + uint32_t(x) * kXTile + uint32_t(row) * uint32_t(kXK * 4);
+          uint32_t v[kXK];
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {  // SWIZZLE_64B: 16-byte chunk c of row r sits at chunk c ^ ((r >> 1) & 3)
+          for (int c = 0; c < kXK / 4; ++c) {
+            // SWIZZLE_64B: 16-byte chunk c of row r sits at chunk c ^ ((r >> 1) & 3);
+            // SWIZZLE_128B: at chunk c ^ (r & 7)
             const float4 f = lds128(src + ((uint32_t(c) ^ swz) << 4));
             v[4 * c] = __float_as_uint(f.x);
             v[4 * c + 1] = __float_as_uint(f.y);
@@ -497,10 +535,23 @@ __global__ void __launch_bounds__(kThreads, 1)
             v[4 * c + 3] = __float_as_uint(f.w);
             dep ^= v[4 * c];  // one register of each LDS.128
           }
+#if HS_HEAD_RZ
+#pragma unroll
+          for (int e = 0; e < kXK; ++e) {  // lo of the split the tensor core completes (hi = rz(x))
+            const float xv = __uint_as_float(v[e]);
+            lo[e] = __float_as_uint(tf32_rna(xv - __uint_as_float(v[e] & 0xFFFFE000u)));
+          }
+          (void)hi;
+#else
           split16<kTerms>(v, hi, lo);
+#endif
         }
+#if !HS_HEAD_RZ
         // the staging slot goes back to TMA once this warp's loads have returned
         if (lane == 0) mbar_arrive_after(bar(XE + x), dep);
+#else
+        (void)dep;
+#endif
 #if HS_DBG_TIMELINE
         const long long c_a0 = clock64();
 #endif
@@ -513,9 +564,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         const long long c_conv0 = clock64();
 #endif
         if (!HS_DBG_HEAD_NOCONV) {
-          const uint32_t ta = lane_base + kTA + uint32_t(a) * 32u;
+          const uint32_t ta = lane_base + kTA + uint32_t(a) * kAW;
+#if HS_HEAD_RZ
+          if constexpr (kTerms > 1) {
+            tmem_st16(ta, *reinterpret_cast<const uint32_t(*)[16]>(lo));
+            if constexpr (kXK == 32) tmem_st16(ta + 16u, *reinterpret_cast<const uint32_t(*)[16]>(lo + 16));
+          }
+#else
           tmem_st16(ta, hi);
           if constexpr (kTerms > 1) tmem_st16(ta + 16u, lo);
+#endif
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         }
 #if HS_DBG_TIMELINE
@@ -737,7 +795,8 @@ cudaError_t head_fused(const HeadArgs& a, int terms, cudaStream_t s) {
   if (cudaError_t e = terms > 1 ? err3 : err1) return e;
   const uint64_t S = uint64_t(a.S), D = uint64_t(a.D), B = uint64_t(a.batch);
   CUtensorMap mX, mW, mWh, mXp;
-  const bool ok = make_map_sw64(&mX, a.X, D, S, B, D * 4, uint64_t(a.sX ? a.sX : S * D) * 4, kXK, kS) &&
+  const bool ok = (kXK == 32 ? tc::make_map(&mX, a.X, D, S, B, D * 4, uint64_t(a.sX ? a.sX : S * D) * 4, kXK, kS, true)
+                              : make_map_sw64(&mX, a.X, D, S, B, D * 4, uint64_t(a.sX ? a.sX : S * D) * 4, kXK, kS)) &&
                   tc::make_map(&mXp, a.X, D, S, B, D * 4, uint64_t(a.sX ? a.sX : S * D) * 4, kWK, kS, true) &&
                   (kWK == 32 ? tc::make_map(&mW, a.Wqkv, D, kN, 2, D * 4, uint64_t(kN) * D * 4, kWK, kN / 2, true)
                              : make_map_sw64(&mW, a.Wqkv, D, kN, 2, D * 4, uint64_t(kN) * D * 4, kWK, kN / 2)) &&

@@ -279,6 +279,16 @@ __device__ __forceinline__ void mma_pair_tf32_ts(uint32_t tmem_d, uint32_t tmem_
       "r"(tmem_a), "l"(b), "r"(idesc), "r"(acc), "r"(0u)
       : "memory");
 }
+// A and B both from shared memory (each CTA supplies its own 128 A rows at the same offset)
+__device__ __forceinline__ void mma_pair_tf32_ss(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                                 uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
 __device__ __forceinline__ void mma_pair_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc,
                                                 uint32_t acc) {
   asm volatile(

@@ -70,6 +70,10 @@ struct EngineConfig {
   // Buffer-liveness planner: intermediates share one arena per slot when the DAG
   // orders all their accesses (false: one allocation per output buffer).
   bool liveness = true;
+  // Graph mode, one memory domain: a run that is a single chunk (n <= batch, no ramp)
+  // replays one graph holding its copy-in, the plan and its copy-out (captured per
+  // (first, n) window), so a run costs one host submission.
+  bool run_graph = true;
 };
 
 class Engine {
@@ -135,6 +139,10 @@ class Engine {
     std::set<int> group_done;
     hs_graph_t graph = nullptr;
     hs_graph_t graph_small = nullptr;  // the plan at ramp_ instances
+    // single-chunk runs (n <= batch): copy-in + plan + copy-out captured as one graph for
+    // the run's instance window, so the host submits one launch per run
+    hs_graph_t graph_run = nullptr;
+    int64_t run_first = -1, run_n = -1;
     hs_event_t t_start = nullptr, t_end = nullptr;
     // several memory domains: per-domain copy streams joined to `origin`
     std::map<int, hs_stream_t> dorigin;
