@@ -202,7 +202,9 @@ typedef struct hs_engine* hs_engine_t;
  * or R <= batch/2 instances when the bindings are host memory), "dynamic_fuse": 0|1 (dynamic mode issues the graph
  * plan's fused launches instead of one kernel per ndrange; InvalidParam when it
  * cannot apply: devices with different queue counts, or simt math),
- * "deterministic": 0|1 (HS_FLAG_DETERMINISTIC on every launch),
+ * "deterministic": 0|1 (HS_FLAG_DETERMINISTIC on every launch: no atomic split-K;
+ * single-instance GEMMs use the cluster split-K with its in-order DSMEM reduction
+ * either way, so this only excludes the red.add fallback),
  * "liveness": 1|0 (intermediate buffers share one arena per slot wherever the
  * DAG orders all their accesses; 0 = one allocation per output buffer),
  * "run_graph": 1|0 (graph mode on one GPU: a run of at most `batch` instances

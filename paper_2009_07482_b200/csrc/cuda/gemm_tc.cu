@@ -79,6 +79,9 @@ using namespace tc;
 #ifndef HS_SPLIT_K  // split-K with red.global.add for latency-bound single-CTA launches
 #define HS_SPLIT_K 1
 #endif
+#ifndef HS_CSPLIT_MAX  // cluster split-K: CTAs per cluster at most (0/1: red.add split-K only)
+#define HS_CSPLIT_MAX 8
+#endif
 #ifndef HS_SPLIT_MIN_KB  // K-blocks per split at least
 #define HS_SPLIT_MIN_KB 1
 #endif
@@ -142,6 +145,9 @@ struct Cfg {
   static_assert(kNS % kConvGroups == 0 && kNO % kConvGroups == 0, "stage rings must divide among groups");
   static constexpr int kTotal =
       kNS * kStaging + kNO * kOperand + 1024 /*barriers*/ + kEpiWarps * kEpiTileBytes + 1024 /*align*/;
+  // cluster split-K: the partial tile (128 rows, BN + 4 floats apart) fits the staging ring
+  static constexpr int kRedLd = BN + 4;
+  static constexpr bool kCsplitOk = kNS * kStaging >= BM * kRedLd * 4;
   static_assert(kNS >= 2 && kNO >= 2, "pipeline too shallow");
   static_assert(kTotal * kCtasPerSm <= 227 * 1024, "shared memory budget exceeded");
 };
@@ -168,6 +174,12 @@ struct TileParams {
   // tile t % base_tiles over K-block range split t / base_tiles and adds it into
   // C (zeroed before the launch) with red.global.add; total_tiles = base * split.
   int split_k, base_tiles;
+  // Cluster split-K (csplit > 1, replaces the red.add split): the csplit CTAs of a
+  // cluster compute K-block ranges of one output tile (split = cluster rank), leave
+  // their partial accumulators in shared memory, and reduce them over DSMEM in rank
+  // order (deterministic; no zeroed C, so no memset node before the launch); the
+  // ReLU epilogue applies after the reduction.
+  int csplit;
 };
 
 
@@ -295,7 +307,7 @@ template <int BN, int kBSrc, int kTerms, bool kSmall, bool kBf16>
 __global__ void __launch_bounds__(kThreads, kSmall ? 2 : 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TileParams p) {
   using L = Cfg<BN, kBSrc, kSmall, kBf16>;
-  constexpr int NS = L::kNS, NO = L::kNO;
+  constexpr int NS = L::kNS, NO = L::kNO, kRedLd = L::kRedLd;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
   const uint32_t staging = base;
@@ -317,6 +329,11 @@ __global__ void __launch_bounds__(kThreads, kSmall ? 2 : 1)
   // K-block range of tile t (the whole K unless split-K)
   auto kb_begin = [&](int t) { return (t / p.base_tiles) * nk / p.split_k; };
   auto kb_end = [&](int t) { return (t / p.base_tiles + 1) * nk / p.split_k; };
+  // first tile and stride of this CTA's persistent loop (cluster split-K: exactly one
+  // tile, split = cluster rank, output tile = cluster index)
+  const bool csplit = p.csplit > 1;
+  const int t0 = csplit ? int(cluster_ctarank()) * p.base_tiles + int(blockIdx.x) / p.csplit : int(blockIdx.x);
+  const int tstep = csplit ? p.total_tiles : int(gridDim.x);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
@@ -364,7 +381,7 @@ __global__ void __launch_bounds__(kThreads, kSmall ? 2 : 1)
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
       uint32_t it = 0;
-      for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
+      for (int t = t0; t < p.total_tiles; t += tstep) {
         int m0, inst, n0;
         decode(t, m0, inst, n0);
         const int ia = p.a_batched ? inst : 0, ib = p.b_batched ? inst : 0;
@@ -393,7 +410,7 @@ __global__ void __launch_bounds__(kThreads, kSmall ? 2 : 1)
     if constexpr (L::kBPre) {
       if (lane == 0) {
         uint32_t it = 0;
-        for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
+        for (int t = t0; t < p.total_tiles; t += tstep) {
           int m0, inst, n0;
           decode(t, m0, inst, n0);
           for (int kb = kb_begin(t); kb < kb_end(t); ++kb, ++it) {
@@ -417,7 +434,7 @@ __global__ void __launch_bounds__(kThreads, kSmall ? 2 : 1)
     if (lane == 0) {
       constexpr uint32_t idesc = kBf16 ? instr_desc_bf16(BN) : instr_desc_tf32(BN);
       uint32_t it = 0, lt = 0;
-      for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x, ++lt) {
+      for (int t = t0; t < p.total_tiles; t += tstep, ++lt) {
         const uint32_t acc = lt % uint32_t(L::kAccBufs);
         mbar_wait(acc_empty(int(acc)), ((lt / uint32_t(L::kAccBufs)) & 1u) ^ 1u);
         tc_fence_after();
@@ -464,7 +481,7 @@ __global__ void __launch_bounds__(kThreads, kSmall ? 2 : 1)
     // ------------------------------------------------------------ epilogue
     const int q = warp & 3;  // TMEM lane quarter accessible to this warp
     uint32_t lt = 0;
-    for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x, ++lt) {
+    for (int t = t0; t < p.total_tiles; t += tstep, ++lt) {
       int m0, inst, n0;
       decode(t, m0, inst, n0);
       const uint32_t acc = lt % uint32_t(L::kAccBufs);
@@ -472,6 +489,8 @@ __global__ void __launch_bounds__(kThreads, kSmall ? 2 : 1)
       tc_fence_after();
       if (q == 0 && lane == 0) GTL(7);
       const uint32_t tacc = tmem + (uint32_t(q * 32) << 16) + acc * uint32_t(BN);
+      // the partials overwrite A staging slots whose TMA writes (async proxy) were consumed
+      if (csplit) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       // Softmax epilogue: this thread owns one full row of the tile (N <= BN).
       // Two read passes over TMEM give the row max and the sum of exp(s*x - max);
       // the store pass scales by 1/sum.
@@ -515,6 +534,14 @@ __global__ void __launch_bounds__(kThreads, kSmall ? 2 : 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(acc_empty(int(acc)));
         }
+        if (csplit) {  // this split's partial row chunk -> own smem (reduced after the cluster barrier)
+          const uint32_t dst = staging + uint32_t((q * 32 + lane) * kRedLd + cb * 32) * 4u;
+#pragma unroll
+          for (int j4 = 0; j4 < 8; ++j4)
+            sts128(dst + uint32_t(j4) * 16u, make_float4(__uint_as_float(r[4 * j4]), __uint_as_float(r[4 * j4 + 1]),
+                                                        __uint_as_float(r[4 * j4 + 2]), __uint_as_float(r[4 * j4 + 3])));
+          continue;
+        }
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
@@ -537,7 +564,7 @@ __global__ void __launch_bounds__(kThreads, kSmall ? 2 : 1)
     const int q = warp & 3;
     const int row = q * 32 + lane;
     uint32_t it = 0;
-    for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
+    for (int tile = t0; tile < p.total_tiles; tile += tstep) {
       for (int kb = kb_begin(tile); kb < kb_end(tile); ++kb, ++it) {
         if (int(it % kConvGroups) != g) continue;
         const int s = int(it % NS), o = int(it % NO);
@@ -581,6 +608,45 @@ __global__ void __launch_bounds__(kThreads, kSmall ? 2 : 1)
     }
   }
   if (threadIdx.x == 0) GTL(9);
+  if (csplit) {
+    // every split's partial tile is in its CTA's smem: CTA r reduces rows
+    // [r * 128 / S, (r + 1) * 128 / S) over splits 0..S-1 (fixed order), applies the
+    // ReLU and stores them, consecutive threads on consecutive columns (coalesced).
+    // The cluster barrier is .aligned: every warp must arrive converged (the producer
+    // and MMA warps ran their loops in lane 0 only), hence the CTA barrier first.
+    __syncthreads();
+    cluster_sync_all();
+    int m0, inst, n0;
+    decode(t0, m0, inst, n0);
+    const int S = p.csplit, rows = BM / S, rank = int(cluster_ctarank());
+    const int64_t ld = p.ldc ? p.ldc : p.N;
+    float* cbase = p.C + int64_t(inst) * p.sC;
+    const bool vec = (ld & 3) == 0 && (reinterpret_cast<uintptr_t>(cbase) & 15u) == 0;
+    for (int id = int(threadIdx.x); id < rows * (BN / 4); id += kThreads) {
+      const int rr = rank * rows + id / (BN / 4), c4 = (id % (BN / 4)) * 4;
+      const uint32_t off = staging + uint32_t(rr * kRedLd + c4) * 4u;
+      float4 acc = ld_shared_cluster_v4(mapa_rank(off, 0));
+      for (int sp = 1; sp < S; ++sp) {
+        const float4 x = ld_shared_cluster_v4(mapa_rank(off, uint32_t(sp)));
+        acc.x += x.x;
+        acc.y += x.y;
+        acc.z += x.z;
+        acc.w += x.w;
+      }
+      if (p.relu) acc = make_float4(fmaxf(acc.x, 0.f), fmaxf(acc.y, 0.f), fmaxf(acc.z, 0.f), fmaxf(acc.w, 0.f));
+      const int grow = m0 + rr, gcol = n0 + c4;
+      if (grow >= p.M || gcol >= p.N) continue;
+      float* dst = cbase + int64_t(grow) * ld + gcol;
+      if (vec && gcol + 4 <= p.N) {
+        *reinterpret_cast<float4*>(dst) = acc;
+      } else {
+        const float e[4] = {acc.x, acc.y, acc.z, acc.w};
+        for (int i = 0; i < 4 && gcol + i < p.N; ++i) dst[i] = e[i];
+      }
+    }
+    __syncthreads();
+    cluster_sync_all();  // no CTA leaves while its partial is still being read
+  }
   tc_fence_before();
   __syncthreads();
   if (warp == 2) {
@@ -1103,26 +1169,41 @@ cudaError_t launch(const GemmArgs& a, cudaStream_t s) {
   const int base = p.m_tiles * p.n_tiles * a.batch;
   const int slots = num_sms() * L::kCtasPerSm;
   // Split-K for latency-bound single-instance launches (few output tiles, long K
-  // loop: one instance's FFN2 runs 8 CTAs over 64 K-blocks): each split adds its
-  // partial sum into C with red.global.add, so C is zeroed first and the result
-  // is not bit-reproducible (fp32 addition order across splits). Batched
-  // launches never split.
+  // loop: one instance's FFN2 runs 8 CTAs over 64 K-blocks). Preferred: cluster
+  // split-K (p.csplit): S CTAs of a cluster split the K-blocks of one tile and
+  // reduce their partials over DSMEM in rank order, so the result is deterministic,
+  // ReLU applies after the sum, and C needs no zeroing (no memset node ahead of the
+  // kernel). Otherwise (tiles whose partial does not fit the staging ring) each
+  // split adds its partial into a zeroed C with red.global.add (not bit-
+  // reproducible: fp32 addition order). Batched launches never split.
   const int nk = (a.K + BK - 1) / BK;
-  int split = 1;
-  if (HS_SPLIT_K && !a.deterministic && a.batch == 1 && !a.relu && !a.softmax && p.n_out == 0 && !a.ldc && nk >= 2 * HS_SPLIT_MIN_KB &&
-      4 * base <= slots) {
-    split = slots / base;
-    if (split > nk / HS_SPLIT_MIN_KB) split = nk / HS_SPLIT_MIN_KB;
-    if (split > 16) split = 16;
-    if (split < 2) split = 1;
+  int split = 1, csplit = 0;
+  if (HS_SPLIT_K && a.batch == 1 && !a.softmax && p.n_out == 0 && nk >= 2 * HS_SPLIT_MIN_KB && 4 * base <= slots) {
+    if constexpr (L::kCsplitOk) {
+      if (HS_CSPLIT_MAX >= 2) {
+        int S = slots / base;
+        if (S > nk / HS_SPLIT_MIN_KB) S = nk / HS_SPLIT_MIN_KB;
+        if (S > HS_CSPLIT_MAX) S = HS_CSPLIT_MAX;
+        S = S >= 8 ? 8 : S >= 4 ? 4 : S >= 2 ? 2 : 1;  // rows of the reduction divide evenly
+        if (S >= 2) split = csplit = S;
+      }
+    }
+    if (!csplit && !a.deterministic && !a.relu && !a.ldc) {
+      split = slots / base;
+      if (split > nk / HS_SPLIT_MIN_KB) split = nk / HS_SPLIT_MIN_KB;
+      if (split > 16) split = 16;
+      if (split < 2) split = 1;
+    }
   }
   p.split_k = split;
+  p.csplit = csplit;
   p.base_tiles = base;
   p.total_tiles = base * split;
-  if (split > 1) {
+  if (split > 1 && !csplit) {
     const cudaError_t e = cudaMemsetAsync(a.C, 0, size_t(a.batch) * size_t(a.M) * size_t(a.N) * 4, s);
     if (e != cudaSuccess) return e;
   }
+  if (csplit) return launch_node(kernel, dim3(p.total_tiles), dim3(kThreads), L::kTotal, s, csplit, mA, mB, p);
   const int grid = p.total_tiles < slots ? p.total_tiles : slots;
   return launch_node(kernel, dim3(grid), dim3(kThreads), L::kTotal, s, 1, mA, mB, p);
 }

@@ -45,8 +45,9 @@ class Engine:
         path on one GPU).
         dynamic_fuse: dynamic mode issues the graph plan's fused launches (per component)
         instead of one kernel per ndrange.
-        deterministic: no split-K in single-instance GEMMs, so every output is
-        bit-reproducible from run to run (split-K adds K-split partials atomically).
+        deterministic: no atomic split-K anywhere (HS_FLAG_DETERMINISTIC). Single-instance
+        GEMMs split K over a cluster and reduce in rank order either way; the flag only
+        rules out the red.add fallback for tiles whose partial does not fit on chip.
         liveness: intermediate buffers share one arena per slot wherever the DAG orders
         all their accesses (False: one device allocation per output buffer).
         ramp (graph mode, host-memory bindings): the first and last chunks of a run are

@@ -3,7 +3,8 @@ against the CPU oracle:
   * grouped sibling GEMMs whose shared A is a resident (stride-0) buffer read by
     every instance of a batch;
   * run() ranges checked against the instance count of every binding;
-  * deterministic mode (no split-K) is bit-reproducible for single instances;
+  * single-instance runs are bit-reproducible (cluster split-K reduces in rank order),
+    in the default and the deterministic mode;
   * dynamic_fuse is refused when it cannot apply.
 """
 import numpy as np
@@ -63,9 +64,11 @@ def test_run_range_is_checked_against_bound_instances():
             assert ei.value.errc == "InvalidParam"
 
 
-def test_deterministic_mode_is_bit_reproducible(oracle_mod):
-    """One instance of the encoder layer: split-K would add K-split partials with
-    atomics; deterministic=True launches without it, run after run bit-identical."""
+@pytest.mark.parametrize("deterministic", [True, False])
+def test_single_instance_runs_are_bit_reproducible(deterministic, oracle_mod):
+    """One instance of the encoder layer, run after run and engine after engine bit-
+    identical: single-instance GEMMs split K over a cluster and reduce the partials
+    over DSMEM in rank order (no atomics), in the default mode as in deterministic=True."""
     text, params, meta = workloads.encoder(layers=1)
     x = workloads.encoder_inputs(meta, params, 1).reshape(1, -1)
     arrays = {(i["kernel"], i["pos"]): x for i in meta["x_inputs"]}
@@ -76,7 +79,7 @@ def test_deterministic_mode_is_bit_reproducible(oracle_mod):
     runs = []
     for _ in range(3):
         out = np.zeros((1, params["S"] * params["D"]), np.float32)
-        with Engine(text, params, batch=1, mode="graph", deterministic=True) as eng:
+        with Engine(text, params, batch=1, mode="graph", deterministic=deterministic) as eng:
             for k, a in arrays.items():
                 eng.bind(*k, a, shared=a.ndim == 1)
             eng.bind(*key, out)

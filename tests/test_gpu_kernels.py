@@ -39,11 +39,34 @@ GEMM_CASES = [
     (100, 72, 36, "gemm", 2, False),        # ragged M/N/K tails
     (130, 200, 44, "gemm_nt", 1, False),
     (64, 8, 4, "gemm", 1, False),
-    # single-instance launches with a long K loop run split-K (red.global.add into a zeroed C)
+    # single-instance launches with a long K loop run split-K: a cluster of CTAs per
+    # output tile, partials reduced over DSMEM (ReLU after the sum), ragged tails
     (128, 512, 2048, "gemm", 1, True),
     (256, 256, 256, "gemm", 1, False),
     (100, 64, 1000, "gemm_nt", 1, False),
+    (128, 2048, 512, "gemm_relu", 1, True),
+    (100, 72, 1000, "gemm", 1, False),
+    (200, 130, 600, "gemm_relu", 1, False),
 ]
+
+
+@pytest.mark.parametrize("M,N,K,op,shared", [(256, 256, 256, "gemm", False), (128, 2048, 512, "gemm_relu", True),
+                                             (128, 512, 2048, "gemm", True)])
+def test_single_instance_split_k_is_bit_reproducible(M, N, K, op, shared):
+    """Cluster split-K reduces the K-split partials in rank order over DSMEM: the same
+    launch gives bit-identical outputs every time (no atomics)."""
+    from tests.gpu_util import launch
+    import torch
+    A = _t(_rand(41, (1, M * K)))
+    B = _t((_rand(42, (N * K,) if shared else (1, N * K)) * np.float32(1.0 / np.sqrt(K))).astype(np.float32))
+    outs = []
+    for _ in range(3):
+        out = torch.full((1, M * N), float("nan"), device="cuda")
+        launch(op, [A, B], out, [M, N, K], batch=1)
+        outs.append(out.cpu().numpy())
+    assert np.isfinite(outs[0]).all()
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])
 
 
 @pytest.mark.parametrize("M,N,K,op,batch,shared", GEMM_CASES)
