@@ -209,7 +209,10 @@ typedef struct hs_engine* hs_engine_t;
  * DAG orders all their accesses; 0 = one allocation per output buffer),
  * "run_graph": 1|0 (graph mode on one GPU: a run of at most `batch` instances
  * replays one graph holding its copy-in, the plan and its copy-out, captured for
- * that (first, n) window; 0 = copies issued per run around the plan graph). */
+ * that (first, n) window; 0 = copies issued per run around the plan graph),
+ * "zero_copy": 1|0 (with run_graph and n == batch: per-instance inputs / outputs
+ * bound to dense, non-overlapping memory on this GPU are read / written in place
+ * by the captured kernels instead of copied). */
 int hs_engine_create(const char* config_json, hs_engine_t* out);
 int hs_engine_destroy(hs_engine_t e);
 

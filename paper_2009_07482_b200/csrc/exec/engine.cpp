@@ -594,7 +594,73 @@ hs_event_t Engine::event(Slot& sl, int comp, int ev, int dom) {
   return e;
 }
 
+// Whole-run graph over exactly one batch: per-instance inputs and outputs that are
+// already dense in this GPU's memory are used in place. Every slot pointer inside
+// such a group's / output's own allocation is redirected into the user's buffer at
+// instance `first` (the layouts match: [batch][bytes]); the copy commands of those
+// buffers are skipped during the capture. Not applied when an in-place input and
+// output (or two outputs) overlap, or for io buffers (read and written by the DAG).
+void Engine::zero_copy_remap(Slot& sl, int64_t first, int64_t n) {
+  skip_groups_.clear();
+  skip_outputs_.clear();
+  if (!cfg_.zero_copy || n != cfg_.batch || dctx_.size() != 1) return;
+  struct Range {
+    char *lo, *hi, *to;
+  };
+  std::vector<Range> moves;
+  std::vector<std::pair<char*, char*>> ins, outs;
+  auto aligned = [](const char* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
+  for (size_t gi = 0; gi < groups_.size(); ++gi) {
+    const Group& gr = groups_[gi];
+    if (gr.resident || gr.io || !gr.b.on_device || gr.b.stride != gr.bytes || first + n > gr.b.count) continue;
+    auto it = sl.group_buf.find({int(gi), 0});
+    if (it == sl.group_buf.end()) continue;
+    char* to = static_cast<char*>(gr.b.ptr) + first * gr.b.stride;
+    if (!aligned(to)) continue;
+    char* old = static_cast<char*>(it->second);
+    moves.push_back({old, old + gr.bytes * n, to});
+    ins.emplace_back(to, to + gr.bytes * n);
+    skip_groups_.insert(int(gi));
+  }
+  for (const auto& key : outputs_) {
+    const Binding& b = bindings_.at(key);
+    const int64_t bytes = bytes_.at(key);
+    if (!b.on_device || (b.stride != bytes && n > 1) || first + n > b.count || io_copy_.count(key)) continue;
+    char* to = static_cast<char*>(b.ptr) + first * b.stride;
+    if (!aligned(to)) continue;
+    char* old = static_cast<char*>(sl.buf.at(key));
+    moves.push_back({old, old + bytes * n, to});
+    outs.emplace_back(to, to + bytes * n);
+    skip_outputs_.insert(key);
+  }
+  auto overlap = [](const std::pair<char*, char*>& a, const std::pair<char*, char*>& b) {
+    return a.first < b.second && b.first < a.second;
+  };
+  for (size_t i = 0; i < outs.size(); ++i) {
+    for (const auto& r : ins)
+      if (overlap(outs[i], r)) moves.clear();
+    for (size_t j = i + 1; j < outs.size(); ++j)
+      if (overlap(outs[i], outs[j])) moves.clear();
+  }
+  if (moves.empty()) {
+    skip_groups_.clear();
+    skip_outputs_.clear();
+    return;
+  }
+  auto remap = [&](void*& p) {
+    char* c = static_cast<char*>(p);
+    for (const auto& m : moves)
+      if (c >= m.lo && c < m.hi) {
+        p = m.to + (c - m.lo);
+        return;
+      }
+  };
+  for (auto& [key, p] : sl.buf) remap(p);
+  for (auto& [key, p] : sl.group_buf) remap(p);
+}
+
 void Engine::copy_in(Slot& sl, hs_stream_t s, int gi, int64_t first, int64_t n, int dom) {
+  if (skip_groups_.count(gi)) return;  // read in place (zero_copy_remap)
   const Group& gr = groups_[size_t(gi)];
   auto dst = sl.group_buf.find({gi, dom});
   if (dst == sl.group_buf.end()) return;  // no kernel of this domain reads the group
@@ -664,7 +730,7 @@ void Engine::copies(Slot& sl, int64_t first, int64_t n, bool in) {
 
 void Engine::copy_out(Slot& sl, hs_stream_t s, int64_t first, int64_t n, int dom) {
   for (const auto& key : outputs_) {
-    if (kdom(key.first) != dom) continue;
+    if (kdom(key.first) != dom || skip_outputs_.count(key)) continue;  // skipped: written in place
     const Binding& b = bindings_.at(key);
     const int64_t bytes = bytes_.at(key);
     char* dst = static_cast<char*>(b.ptr) + first * b.stride;
@@ -1390,11 +1456,20 @@ void Engine::run(int64_t first, int64_t n, int64_t* elapsed_ns) {
       if (!sl.graph_run || sl.run_first != first || sl.run_n != n) {
         hs_graph_destroy(sl.graph_run);
         sl.graph_run = nullptr;
+        const auto saved_buf = sl.buf;
+        const auto saved_group_buf = sl.group_buf;
+        zero_copy_remap(sl, first, n);
         hs_ok(hs_capture_begin(sl.origin), "capture begin");
         copies(sl, first, n, true);
         emit_plan(sl);
         copies(sl, first, n, false);
         hs_ok(hs_capture_end(sl.origin, &sl.graph_run), "capture end");
+        sl.buf = saved_buf;
+        sl.group_buf = saved_group_buf;
+        zero_copy_groups_ = int64_t(skip_groups_.size());
+        zero_copy_outputs_ = int64_t(skip_outputs_.size());
+        skip_groups_.clear();
+        skip_outputs_.clear();
         sl.run_first = first;
         sl.run_n = n;
       }
@@ -1504,6 +1579,9 @@ std::string Engine::info(const std::string& what) const {
     out.set("host_wait_us", Value::real(double(host_wait_ns_) / 1e3));
     out.set("runs", Value::of(static_cast<long long>(runs_)));
     out.set("batches", Value::of(static_cast<long long>(batches_run_)));
+    // last whole-run graph capture: input groups / outputs used in place (zero copy)
+    out.set("zero_copy_groups", Value::of(static_cast<long long>(zero_copy_groups_)));
+    out.set("zero_copy_outputs", Value::of(static_cast<long long>(zero_copy_outputs_)));
   } else if (what == "trace") {
     // SPEC.md:435 trace records of the first batch of the last run (times in ms
     // from the run's start event): event id = position in issue order.
@@ -1608,6 +1686,7 @@ int hs_engine_create(const char* config_json, hs_engine_t* out) {
     if (const json::Value* v = c.find("deterministic")) cfg.deterministic = v->as_int() != 0;
     if (const json::Value* v = c.find("liveness")) cfg.liveness = v->as_int() != 0;
     if (const json::Value* v = c.find("run_graph")) cfg.run_graph = v->as_int() != 0;
+    if (const json::Value* v = c.find("zero_copy")) cfg.zero_copy = v->as_int() != 0;
     if (const json::Value* v = c.find("fuse")) {
       cfg.fuse = v->as_int();
       if (cfg.fuse < 0 || cfg.fuse > 3) fail(Errc::invalid_param, "fuse must be 0, 1, 2 or 3");

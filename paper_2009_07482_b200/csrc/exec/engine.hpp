@@ -74,6 +74,10 @@ struct EngineConfig {
   // replays one graph holding its copy-in, the plan and its copy-out (captured per
   // (first, n) window), so a run costs one host submission.
   bool run_graph = true;
+  // With run_graph and n == batch: device-resident per-instance inputs and outputs
+  // (dense, on this GPU, not overlapping) are read and written in place by the
+  // captured kernels instead of being copied into / out of the slot's buffers.
+  bool zero_copy = true;
 };
 
 class Engine {
@@ -153,6 +157,7 @@ class Engine {
     std::vector<hs_event_t> copy_join;
   };
 
+  void zero_copy_remap(Slot& sl, int64_t first, int64_t n);
   void build_nodes();
   void plan_buffers();
   std::map<std::pair<int, int>, std::set<int>> buffer_accessors() const;
@@ -197,6 +202,10 @@ class Engine {
   std::map<std::pair<int, int>, std::pair<int, int>> io_copy_;  // io input fed by an edge -> producer
   std::map<std::pair<int, int>, int64_t> bytes_;                // (kernel,pos) -> bytes per instance
   std::vector<std::pair<int, int>> outputs_;                    // isolated outputs with a binding
+  // zero-copy capture of a whole-run graph: groups / outputs read or written in place
+  std::set<int> skip_groups_;
+  std::set<std::pair<int, int>> skip_outputs_;
+  int64_t zero_copy_groups_ = 0, zero_copy_outputs_ = 0;
   std::map<std::pair<int, int>, void*> resident_;  // (resident group, domain) -> device copy
   // resident GEMM weights pre-split into tf32 hi/lo planes: (group, transposed) -> planes
   struct Planes {

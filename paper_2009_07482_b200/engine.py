@@ -31,7 +31,7 @@ class Engine:
                  mode: str = "graph", batch: int = 1, slots: int = 2, math: str = "tf32x3", cpu_devices=(),
                  fuse: int | bool = 3, trace: bool = False, device_gpus: dict | None = None,
                  domain_per_device: bool = False, dynamic_fuse: bool = False, deterministic: bool = False,
-                 liveness: bool = True, ramp: int = 1, run_graph: bool = True):
+                 liveness: bool = True, ramp: int = 1, run_graph: bool = True, zero_copy: bool = True):
         """fuse (graph mode): 0 = one launch per ndrange; 1 = + grouped sibling GEMMs;
         2 = + chain rewrites (transpose -> gemm_nt, softmax as a GEMM epilogue, concat
         inputs written in place, fused attention heads); 3 (default, also True) = + each
@@ -53,13 +53,17 @@ class Engine:
         ramp (graph mode, host-memory bindings): the first and last chunks of a run are
         short so their copies are short: 1 = batch/4 instances, 0 = off, R > 1 = R.
         run_graph (graph mode, one GPU): a run that fits one batch replays a single graph
-        holding its copies and the plan (one host submission per run)."""
+        holding its copies and the plan (one host submission per run).
+        zero_copy (with run_graph, n == batch): per-instance inputs and outputs bound to
+        dense memory on this GPU are read / written in place by the captured kernels
+        (no copy-in / copy-out commands)."""
         fuse = 3 if fuse is True else int(fuse)
         cfg = {"spec": spec_text, "params": dict(params or {}), "gpu": gpu, "policy": policy, "mode": mode,
                "batch": batch, "slots": slots, "math": math, "cpu_devices": list(cpu_devices), "fuse": int(fuse),
                "trace": int(bool(trace)), "domain_per_device": int(bool(domain_per_device)),
                "dynamic_fuse": int(bool(dynamic_fuse)), "deterministic": int(bool(deterministic)),
-               "liveness": int(bool(liveness)), "ramp": int(ramp), "run_graph": int(bool(run_graph))}
+               "liveness": int(bool(liveness)), "ramp": int(ramp), "run_graph": int(bool(run_graph)),
+               "zero_copy": int(bool(zero_copy))}
         if device_gpus:
             cfg["device_gpus"] = {str(k): int(v) for k, v in device_gpus.items()}
         self._lib = lib()

@@ -5,7 +5,9 @@ against the CPU oracle:
   * run() ranges checked against the instance count of every binding;
   * single-instance runs are bit-reproducible (cluster split-K reduces in rank order),
     in the default and the deterministic mode;
-  * dynamic_fuse is refused when it cannot apply.
+  * dynamic_fuse is refused when it cannot apply;
+  * single-batch runs (one graph with the copies, zero-copy device bindings) are
+    bit-identical to the copying path.
 """
 import numpy as np
 import pytest
@@ -134,3 +136,51 @@ def test_c5_production_plan_fits_in_10_gb():
     (whole-head launches leave Q/K/V/S/P/C unallocated), under 10 GB in all."""
     _, plan = _encoder_run(12, 1, mode="graph", batch=512, slots=3)
     assert plan["device_bytes"] < 10e9, plan["device_bytes"]
+
+
+def _device_run(text, params, arrays, n, batch, **kw):
+    """Run `n` instances from device-resident torch tensors; returns (outputs, stats)."""
+    import torch
+    dev = {k: torch.from_numpy(np.ascontiguousarray(a)).cuda() for k, a in arrays.items()}
+    outs = {(k, p): torch.full((n, e), float("nan"), device="cuda")
+            for k, p, e in workloads.isolated_outputs(text, params)}
+    torch.cuda.synchronize()
+    with Engine(text, params, batch=batch, slots=1, mode="graph", **kw) as eng:
+        for key, t in dev.items():
+            eng.bind(*key, t, shared=t.dim() == 1)
+        for key, t in outs.items():
+            eng.bind(*key, t)
+        for _ in range(2):
+            eng.run(0, n)
+        stats = eng.info("stats")
+    return {k: t.cpu().numpy() for k, t in outs.items()}, stats
+
+
+@pytest.mark.parametrize("cfg", ["fork_join", "encoder"])
+def test_whole_run_graph_and_zero_copy_are_bit_identical(cfg, oracle_mod):
+    """A run of exactly one batch replays one graph (copies + plan); device-resident
+    inputs and outputs are then used in place. Both are bit-identical to the copying
+    path and match the oracle; a run shorter than the batch falls back to copies."""
+    if cfg == "fork_join":
+        text, params = workloads.fork_join()
+        n = 1
+        arrays = workloads.generic_inputs(text, params, n)
+    else:
+        text, params, meta = workloads.encoder(layers=1)
+        n = 2
+        x = workloads.encoder_inputs(meta, params, n).reshape(n, -1)
+        arrays = {(i["kernel"], i["pos"]): x for i in meta["x_inputs"]}
+        for key, w in workloads.encoder_weights(meta).items():
+            arrays[key] = w.reshape(-1)
+    ref = oracle_mod.run_dag(text, params, arrays, n)
+    base, _ = _device_run(text, params, arrays, n, n, run_graph=False)
+    whole, st0 = _device_run(text, params, arrays, n, n, zero_copy=False)
+    zc, st1 = _device_run(text, params, arrays, n, n)
+    assert st0["zero_copy_groups"] == 0 and st1["zero_copy_groups"] >= 1 and st1["zero_copy_outputs"] >= 1
+    short, st2 = _device_run(text, params, {k: a[:1] if a.ndim == 2 else a for k, a in arrays.items()}, 1, n + 1)
+    assert st2["zero_copy_groups"] == 0
+    for key in ref:
+        assert np.array_equal(base[key], whole[key]) and np.array_equal(base[key], zc[key]), key
+        assert _normwise(zc[key], ref[key]) <= 1e-4
+        # (batch 2 launches do not split K: another summation order than batch 1)
+        assert _normwise(short[key][0], ref[key][0]) <= 1e-4
