@@ -534,7 +534,7 @@ def config_spec(cfg, queues=3, devices=1):
 
 
 def config_makespan(cfg, fuse=3, queues=3, devices=1, reps=20, warmup=3, math_mode="tf32x3", check=True, batch=None,
-                    slots=1, **engine_kw):
+                    slots=1, host_io=False, **engine_kw):
     """Makespan of one whole run of config `cfg` (all its instances in one batch) in graph
     mode with device-resident inputs/outputs: median over `reps` runs of the engine's own
     CUDA-event timing (start event -> end event on the origin stream, which joins every
@@ -546,13 +546,17 @@ def config_makespan(cfg, fuse=3, queues=3, devices=1, reps=20, warmup=3, math_mo
     from paper_2009_07482_b200 import roofline
     from paper_2009_07482_b200.engine import Engine
     text, params, arrays, outs, n, shared, io = config_spec(cfg, queues, devices)
+    # host_io: inputs and outputs in pinned host memory (every run copies them in and out,
+    # the paper's isolated writes / reads over PCIe); otherwise device-resident, which a
+    # one-batch run reads and writes in place (engine zero_copy)
+    place = (lambda t: t.pin_memory()) if host_io else (lambda t: t.cuda())
     dev = {}
     x_cache = {}
     for key, a in arrays.items():
         if id(a) not in x_cache:
-            x_cache[id(a)] = torch.from_numpy(np.ascontiguousarray(a)).cuda()
+            x_cache[id(a)] = place(torch.from_numpy(np.ascontiguousarray(a)))
         dev[key] = x_cache[id(a)]
-    out_dev = {(k, p): torch.zeros(n, e, device="cuda") for k, p, e in outs}
+    out_dev = {(k, p): place(torch.zeros(n, e)) for k, p, e in outs}
     torch.cuda.synchronize()
     batch = batch or n
     with Engine(text, params, batch=batch, slots=slots, mode="graph", fuse=fuse, math=math_mode, **engine_kw) as eng:
@@ -599,6 +603,8 @@ def config_makespans():
                                       "t_star_ms", "bound", "frac", "normwise_err_vs_cpu_oracle", "parity",
                                       "cpu_port_ms")}
         out[cfg]["gpu_speedup_vs_cpu_port"] = r["cpu_port_ms"] / r["makespan_ms"]
+        rh = config_makespan(cfg, check=False, host_io=True, **kw)
+        out[cfg]["makespan_host_io_ms"] = rh["makespan_ms"]
     out["C4"]["target_1p5x_t_star_ms"] = 1.5 * out["C4"]["t_star_ms"]
     grain = []
     for cfg in ("C3", "C4"):
@@ -608,7 +614,9 @@ def config_makespans():
                 grain.append({"config": cfg, "fuse": fuse, "queues": queues, "makespan_ms": r["makespan_ms"]})
     out["fine_vs_coarse"] = {"logical_devices": 1, "rows": grain,
                              "note": "queues=1 is the coarse-grained default mc=(1,0,0); queues=3 fine-grained"}
-    out["note"] = ("median of 20 runs of the engine's CUDA-event makespan (start -> end event on the origin stream); "
+    out["note"] = ("median of 20 runs of the engine's CUDA-event makespan (start -> end event on the origin stream) "
+                   "with device-resident inputs and outputs (a one-batch run replays one graph and uses them in place); "
+                   "makespan_host_io_ms = the same with pinned host inputs / outputs copied in and out every run; "
                    "C3/C4 use one logical device per component of a layer (9) so that heads run concurrently; "
                    "cpu_port_ms = the same config (all instances) through the CPU oracle port (fp32 C kernels, "
                    f"{cpu_threads()} threads, {cpu_model()})")
@@ -689,13 +697,6 @@ def run_ours(args, world, rank, local):
     value = args.instances / (ms_per_step / 1e3)
     launches = int(stats["launches_per_batch"]) * math.ceil(n / args.batch) * args.steps
 
-    alt = None
-    if not args.no_alt:
-        alt_math = "bf16x3" if args.math != "bf16x3" else "tf32x3"
-        alt_ms, _, _, alt_out, alt_clk, alt_finite = device_resident(alt_math, True)
-        alt = {"math": alt_math, "value": args.instances / (alt_ms / 1e3), "ms_per_step": alt_ms, "clocks": alt_clk,
-               "finite": alt_finite}
-
     # end-to-end arm through the public API with pinned host buffers
     e2e = None
     e2e_out = None
@@ -717,6 +718,12 @@ def run_ours(args, world, rank, local):
                "ms_per_step": e2e_s / args.steps * 1e3, "ramp_batch": ramp}
         e2e_out = out_host.numpy()
         eng_h.close()
+    alt = None
+    if not args.no_alt:
+        alt_math = "bf16x3" if args.math != "bf16x3" else "tf32x3"
+        alt_ms, _, _, alt_out, alt_clk, alt_finite = device_resident(alt_math, True)
+        alt = {"math": alt_math, "value": args.instances / (alt_ms / 1e3), "ms_per_step": alt_ms, "clocks": alt_clk,
+               "finite": alt_finite}
 
     # Parity of this very run on every rank: sampled instances of the device-resident
     # output (every batch's first and last instance, ramp-chunk instances, >= 16) against
