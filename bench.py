@@ -122,7 +122,9 @@ class ClockSampler:
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
         loaded = [s for s in sm if s > 0.5 * smax] or sm
-        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": smax, "reasons": reasons, "samples": len(rows)}
+        pw = [float(r[3]) for r in rows if r[3].replace(".", "").isdigit() and float(r[1] or 0) > 0.5 * smax]
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": smax, "reasons": reasons, "samples": len(rows),
+                "power_w": statistics.median(pw) if pw else None}
 
 
 def dist_setup():
@@ -760,6 +762,9 @@ def run_ours(args, world, rank, local):
             peak, peak_note = tf32_peak / 3.0, (
                 f"TF32 dense peak = MEASURED_PEAKS.json ({pk_kind}) bf16 {pk['bf16_tflops']:.0f} / 2 = "
                 f"{pk['bf16_tflops'] / 2:.0f} TFLOP/s (cuBLAS TF32 measured in-run: {tf32:.0f}); / 3 MMAs per product")
+        # the same denominator from the sustained (4 s back-to-back, power-capped) bf16 figure
+        bf16_sus = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
+        peak_sus = bf16_sus / 3.0 if args.math == "bf16x3" else bf16_sus / 2.0 / 3.0
         traffic = None
         tf = ROOT / "profiles" / "ffn1_traffic.json"
         if tf.exists():
@@ -819,7 +824,13 @@ def run_ours(args, world, rank, local):
             "dag_roofline": {"flop_per_dag": flop_per_inst, "achieved_tflops": flop_per_inst * value / 1e12,
                              "frac_of_peak": flop_per_inst * value / 1e12 / (peak * world),
                              "t_star_ms": args.instances * flop_per_inst / (peak * world * 1e12) * 1e3,
-                             "note": "T* = instances x flop/DAG / P (compute-bound, SURVEY.md 8d); frac_of_peak = T*/ms_per_step"},
+                             "peak_sustained": peak_sus,
+                             "t_star_sustained_ms": args.instances * flop_per_inst / (peak_sus * world * 1e12) * 1e3,
+                             "frac_of_sustained_peak": flop_per_inst * value / 1e12 / (peak_sus * world),
+                             "note": "T* = instances x flop/DAG / P (compute-bound, SURVEY.md 8d); frac_of_peak = T*/ms_per_step "
+                                     "with P from the burst bf16 peak; the step is a long run under sw_power_cap, for which "
+                                     "MEASURED_PEAKS.json's sustained bf16 figure is the matching denominator "
+                                     "(peak_sustained, t_star_sustained_ms, frac_of_sustained_peak)"},
             "roofline_other_kernels": others,
             "makespans": makespans,
             "parity": parity,

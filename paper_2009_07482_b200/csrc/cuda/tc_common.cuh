@@ -249,7 +249,12 @@ __device__ __forceinline__ uint32_t nclusters_x() {
   asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
   return r;
 }
+// Whole-cluster barrier. The .aligned forms require every lane of the warp to execute
+// them together; warps whose roles ran loops in one lane reconverge first (without it,
+// the cluster split-K reduction in gemm_tc.cu read peers' partials before they were
+// written: profiles/r2_determinism_before_fix.txt).
 __device__ __forceinline__ void cluster_sync_all() {
+  __syncwarp();
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 // shared::cta address of this CTA -> shared::cluster address of the same object in CTA `rank`
