@@ -145,9 +145,10 @@ struct Cfg {
   static_assert(kNS % kConvGroups == 0 && kNO % kConvGroups == 0, "stage rings must divide among groups");
   static constexpr int kTotal =
       kNS * kStaging + kNO * kOperand + 1024 /*barriers*/ + kEpiWarps * kEpiTileBytes + 1024 /*align*/;
-  // cluster split-K: the partial tile (128 rows, BN + 4 floats apart) fits the staging ring
+  // cluster split-K: the partial tile (128 rows, BN + 4 floats apart) fits the staging
+  // and operand rings (both idle once the tile's last MMA has completed)
   static constexpr int kRedLd = BN + 4;
-  static constexpr bool kCsplitOk = kNS * kStaging >= BM * kRedLd * 4;
+  static constexpr bool kCsplitOk = kNS * kStaging + kNO * kOperand >= BM * kRedLd * 4;
   static_assert(kNS >= 2 && kNO >= 2, "pipeline too shallow");
   static_assert(kTotal * kCtasPerSm <= 227 * 1024, "shared memory budget exceeded");
 };
@@ -619,9 +620,13 @@ __global__ void __launch_bounds__(kThreads, kSmall ? 2 : 1)
     int m0, inst, n0;
     decode(t0, m0, inst, n0);
     const int S = p.csplit, rows = BM / S, rank = int(cluster_ctarank());
-    const int64_t ld = p.ldc ? p.ldc : p.N;
-    float* cbase = p.C + int64_t(inst) * p.sC;
-    const bool vec = (ld & 3) == 0 && (reinterpret_cast<uintptr_t>(cbase) & 15u) == 0;
+    // destination of column c: the single C, or member c / Nm of a grouped launch
+    const int64_t ld = p.ldc ? p.ldc : (p.n_out ? p.Nm : p.N);
+    auto dst_of = [&](int grow, int gcol) {
+      if (p.n_out == 0) return p.C + int64_t(inst) * p.sC + int64_t(grow) * ld + gcol;
+      const int m = gcol / p.Nm;
+      return p.Cs[m] + int64_t(inst) * p.sCs[m] + int64_t(grow) * ld + (gcol - m * p.Nm);
+    };
     for (int id = int(threadIdx.x); id < rows * (BN / 4); id += kThreads) {
       const int rr = rank * rows + id / (BN / 4), c4 = (id % (BN / 4)) * 4;
       const uint32_t off = staging + uint32_t(rr * kRedLd + c4) * 4u;
@@ -636,8 +641,8 @@ __global__ void __launch_bounds__(kThreads, kSmall ? 2 : 1)
       if (p.relu) acc = make_float4(fmaxf(acc.x, 0.f), fmaxf(acc.y, 0.f), fmaxf(acc.z, 0.f), fmaxf(acc.w, 0.f));
       const int grow = m0 + rr, gcol = n0 + c4;
       if (grow >= p.M || gcol >= p.N) continue;
-      float* dst = cbase + int64_t(grow) * ld + gcol;
-      if (vec && gcol + 4 <= p.N) {
+      float* dst = dst_of(grow, gcol);
+      if ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0 && gcol + 4 <= p.N && (p.n_out == 0 || p.Nm % 4 == 0)) {
         *reinterpret_cast<float4*>(dst) = acc;
       } else {
         const float e[4] = {acc.x, acc.y, acc.z, acc.w};
@@ -1178,7 +1183,7 @@ cudaError_t launch(const GemmArgs& a, cudaStream_t s) {
   // reproducible: fp32 addition order). Batched launches never split.
   const int nk = (a.K + BK - 1) / BK;
   int split = 1, csplit = 0;
-  if (HS_SPLIT_K && a.batch == 1 && !a.softmax && p.n_out == 0 && nk >= 2 * HS_SPLIT_MIN_KB && 4 * base <= slots) {
+  if (HS_SPLIT_K && a.batch == 1 && !a.softmax && nk >= 2 * HS_SPLIT_MIN_KB && 4 * base <= slots) {
     if constexpr (L::kCsplitOk) {
       if (HS_CSPLIT_MAX >= 2) {
         int S = slots / base;
@@ -1188,7 +1193,7 @@ cudaError_t launch(const GemmArgs& a, cudaStream_t s) {
         if (S >= 2) split = csplit = S;
       }
     }
-    if (!csplit && !a.deterministic && !a.relu && !a.ldc) {
+    if (!csplit && !a.deterministic && !a.relu && !a.ldc && p.n_out == 0) {
       split = slots / base;
       if (split > nk / HS_SPLIT_MIN_KB) split = nk / HS_SPLIT_MIN_KB;
       if (split > 16) split = 16;
