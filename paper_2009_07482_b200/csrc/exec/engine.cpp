@@ -1456,20 +1456,28 @@ void Engine::run(int64_t first, int64_t n, int64_t* elapsed_ns) {
       if (!sl.graph_run || sl.run_first != first || sl.run_n != n) {
         hs_graph_destroy(sl.graph_run);
         sl.graph_run = nullptr;
-        const auto saved_buf = sl.buf;
-        const auto saved_group_buf = sl.group_buf;
+        // the slot's own pointers come back however the capture ends (a failed launch
+        // throws out of emit_plan)
+        struct Restore {
+          Engine* e;
+          Slot& sl;
+          decltype(sl.buf) buf;
+          decltype(sl.group_buf) group_buf;
+          ~Restore() {
+            sl.buf = std::move(buf);
+            sl.group_buf = std::move(group_buf);
+            e->skip_groups_.clear();
+            e->skip_outputs_.clear();
+          }
+        } restore{this, sl, sl.buf, sl.group_buf};
         zero_copy_remap(sl, first, n);
+        zero_copy_groups_ = int64_t(skip_groups_.size());
+        zero_copy_outputs_ = int64_t(skip_outputs_.size());
         hs_ok(hs_capture_begin(sl.origin), "capture begin");
         copies(sl, first, n, true);
         emit_plan(sl);
         copies(sl, first, n, false);
         hs_ok(hs_capture_end(sl.origin, &sl.graph_run), "capture end");
-        sl.buf = saved_buf;
-        sl.group_buf = saved_group_buf;
-        zero_copy_groups_ = int64_t(skip_groups_.size());
-        zero_copy_outputs_ = int64_t(skip_outputs_.size());
-        skip_groups_.clear();
-        skip_outputs_.clear();
         sl.run_first = first;
         sl.run_n = n;
       }
