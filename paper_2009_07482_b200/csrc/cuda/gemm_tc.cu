@@ -713,6 +713,14 @@ __global__ void __launch_bounds__(kThreads, kSmall ? 2 : 1)
 #ifndef HS_PAIR_RELAXED  // converters signal A stages with relaxed (not release) cluster arrives
 #define HS_PAIR_RELAXED 1
 #endif
+// HS_PAIR_RZ: tcgen05 kind::tf32 truncates fp32 operands to tf32 (profiles/tf32_trunc_probe.cu),
+// so the TMA-landed A tile is already the hi term of the split x = rz(x) + (x - rz(x)): the
+// hi·B products read it from shared memory, and the converters write only
+// lo = rna(x - rz(x)) to a 32-column TMEM stage (half the TMEM stores, no hi rounding). The
+// staging slot is then released by the MMAs' commit instead of by the converters.
+#ifndef HS_PAIR_RZ
+#define HS_PAIR_RZ 0
+#endif
 #ifndef HS_PAIR_MIN_ASTAGES  // double-buffer the accumulator if this many A stages still fit
 #define HS_PAIR_MIN_ASTAGES 4
 #endif
@@ -725,7 +733,8 @@ struct CfgPair {
   static constexpr int kHalfN = BN / 2;                          // B rows held by each CTA
   static constexpr int kPlaneB = kHalfN * (kBf16 ? 64 : 128);   // one SW128 tf32 / SW64 bf16 half plane
   static constexpr int kOperand = 2 * kPlaneB;
-  static constexpr int kAStage = kBf16 ? 32 : 64;
+  static constexpr bool kRZ = HS_PAIR_RZ && !kBf16;
+  static constexpr int kAStage = kBf16 || kRZ ? 32 : 64;
   // BN = 192 keeps two accumulators (384 columns) beside two A stages, so the
   // epilogue of one tile overlaps the next tile's MMAs; BN = 256 needs all of TMEM
   // for one accumulator and four A stages.
@@ -785,7 +794,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(st_full(s), 1);
-      mbar_init(st_empty(s), kGroupWarps);
+      mbar_init(st_empty(s), L::kRZ ? 1 : kGroupWarps);  // RZ: the leader's commit (multicast)
     }
     for (int s = 0; s < NO; ++s) {
       mbar_init(op_full(s), 2 * kGroupWarps + 1);
@@ -906,6 +915,24 @@ __global__ void __launch_bounds__(kThreads, 1)
               mma_pair_f16_ts(d, a_hi + kcol, smem_desc_sw64(b_lo + koff), idesc, 1u);
               mma_pair_f16_ts(d, a_hi + kcol, smem_desc_sw64(b_hi + koff), idesc, 1u);
             }
+          } else if constexpr (L::kRZ) {
+            // lo·B_hi from the TMEM stage (lo at the stage's first 32 columns); hi·B_lo and
+            // hi·B_hi read the raw A tile of staging slot s (each CTA its own 128 rows)
+            const uint32_t sa = staging + uint32_t(it % NS) * L::kStaging;
+#pragma unroll
+            for (int kk = 0; kk < BK / 8; ++kk) {
+              const uint32_t kcol = uint32_t(kk) * 8u, koff = uint32_t(kk) * 32u;
+              const uint32_t first = (kb | kk) ? 1u : 0u;
+              const uint64_t ad = smem_desc(sa + koff);
+              if constexpr (kTerms > 1) {
+                mma_pair_tf32_ts(d, a_hi + kcol, smem_desc(b_hi + koff), idesc, first);
+                mma_pair_tf32_ss(d, ad, smem_desc(b_lo + koff), idesc, 1u);
+                mma_pair_tf32_ss(d, ad, smem_desc(b_hi + koff), idesc, 1u);
+              } else {
+                mma_pair_tf32_ss(d, ad, smem_desc(b_hi + koff), idesc, first);
+              }
+            }
+            mma_commit_pair(st_empty(int(it % NS)));
           } else {
 #pragma unroll
             for (int kk = 0; kk < BK / 8; ++kk) {
@@ -1007,7 +1034,26 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t sa = staging + uint32_t(s) * L::kStaging;
         const uint32_t ta = tmem_a + (uint32_t(q * 32) << 16) + uint32_t(o) * uint32_t(L::kAStage);
         bool staged_released = false;
-        if constexpr (!kBf16 && HS_PAIR_PRESPLIT) {
+        if constexpr (L::kRZ) {
+          // lo = rna(x - rz(x)) of this row's 32 values -> the stage's 32 columns; the raw
+          // tile stays in the staging slot for the MMAs (released by their commit)
+          uint32_t lo[32];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const float4 x = lds128(sa + sw128(row, c));
+            const float xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              lo[4 * c + e] = __float_as_uint(tf32_rna(xs[e] - __uint_as_float(__float_as_uint(xs[e]) & 0xFFFFE000u)));
+          }
+          staged_released = true;
+          mbar_wait(op_empty(o), ((it / NO) & 1u) ^ 1u);
+          tc_fence_after();
+          if (kTerms > 1 && !HS_DBG_NOCONV) {
+            tmem_st16(ta, *reinterpret_cast<const uint32_t(*)[16]>(lo));
+            tmem_st16(ta + 16u, *reinterpret_cast<const uint32_t(*)[16]>(lo + 16));
+          }
+        } else if constexpr (!kBf16 && HS_PAIR_PRESPLIT) {
           // split this row's 32 values into registers and hand the staging tile back
           // before waiting for the A stage: only the TMEM stores remain between the
           // MMAs' release of the stage and its reuse (as in head_fused.cu)

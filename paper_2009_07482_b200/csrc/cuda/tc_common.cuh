@@ -250,9 +250,7 @@ __device__ __forceinline__ uint32_t nclusters_x() {
   return r;
 }
 // Whole-cluster barrier. The .aligned forms require every lane of the warp to execute
-// them together; warps whose roles ran loops in one lane reconverge first (without it,
-// the cluster split-K reduction in gemm_tc.cu read peers' partials before they were
-// written: profiles/r2_determinism_before_fix.txt).
+// them together, so warps whose roles ran loops in one lane reconverge first.
 __device__ __forceinline__ void cluster_sync_all() {
   __syncwarp();
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
