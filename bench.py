@@ -579,10 +579,17 @@ def config_makespan(cfg, fuse=3, queues=3, devices=1, reps=20, warmup=3, math_mo
          "bound": bound["bound"], "frac": bound["t_star_ms"] / ms}
     if check:  # every instance of the config against the fp32 oracle and the fp64 truth
         from oracle import oracle as O
+        t0 = time.perf_counter()
         ref = O.run_dag(text, params, arrays, n)
-        t0 = time.perf_counter()  # the CPU port's makespan for this config (second, warm run)
-        O.run_dag(text, params, arrays, n)
-        r["cpu_port_ms"] = (time.perf_counter() - t0) * 1e3
+        first_s = time.perf_counter() - t0
+        # the CPU port's makespan for this config: best of the warm runs (three when a run is
+        # short, where OpenMP wake-ups dominate; one for C4)
+        runs = []
+        for _ in range(3 if first_s < 0.5 else 1):
+            t0 = time.perf_counter()
+            O.run_dag(text, params, arrays, n)
+            runs.append(time.perf_counter() - t0)
+        r["cpu_port_ms"] = min(runs) * 1e3
         truth = O.run_dag_f64(text, params, arrays, n)
         errs = [errors(out_dev[k].cpu().numpy(), ref[k], truth[k]) for k in out_dev]
         r["parity"] = {key: max(e[key] for e in errs) for key in errs[0]}
