@@ -184,3 +184,47 @@ def test_whole_run_graph_and_zero_copy_are_bit_identical(cfg, oracle_mod):
         assert _normwise(zc[key], ref[key]) <= 1e-4
         # (batch 2 launches do not split K: another summation order than batch 1)
         assert _normwise(short[key][0], ref[key][0]) <= 1e-4
+
+
+def test_whole_run_graph_recaptures_per_window(oracle_mod):
+    """A whole-run graph is captured for one (first, n) window: runs over other windows of
+    the same bindings re-capture and compute those instances."""
+    import torch
+    text, params = workloads.fork_join(n=128)
+    N = 4
+    arrays = workloads.generic_inputs(text, params, N)
+    ref = oracle_mod.run_dag(text, params, arrays, N)
+    dev = {k: torch.from_numpy(np.ascontiguousarray(a)).cuda() for k, a in arrays.items()}
+    outs = {(k, p): torch.full((N, e), float("nan"), device="cuda") for k, p, e in workloads.isolated_outputs(text, params)}
+    with Engine(text, params, batch=2, slots=1, mode="graph") as eng:
+        for key, t in dev.items():
+            eng.bind(*key, t, shared=t.dim() == 1)
+        for key, t in outs.items():
+            eng.bind(*key, t)
+        for first in (0, 2, 0, 2):
+            eng.run(first, 2)
+        assert eng.info("stats")["zero_copy_outputs"] >= 1
+    for key, t in outs.items():
+        assert _normwise(t.cpu().numpy(), ref[key]) <= 1e-4, key
+
+
+def test_zero_copy_skipped_when_an_output_aliases_an_input(oracle_mod):
+    """Binding an output to the memory of an input: the in-place path would let a kernel
+    overwrite an input another kernel still reads, so the engine copies instead."""
+    import torch
+    text, params = workloads.fork_join(n=128)
+    arrays = workloads.generic_inputs(text, params, 1)
+    ref = oracle_mod.run_dag(text, params, arrays, 1)
+    dev = {k: torch.from_numpy(np.ascontiguousarray(a)).cuda() for k, a in arrays.items()}
+    ok, op, oelems = workloads.isolated_outputs(text, params)[0]
+    out_key = (ok, op)
+    in_key = next(k for k, t in dev.items() if t.dim() == 2 and t.shape[1] == oelems)
+    with Engine(text, params, batch=1, slots=1, mode="graph") as eng:
+        for key, t in dev.items():
+            eng.bind(*key, t, shared=t.dim() == 1)
+        eng.bind(*out_key, dev[in_key])  # the output lands on an input's memory
+        eng.run(0, 1)
+        st = eng.info("stats")
+        assert st["zero_copy_groups"] == 0 and st["zero_copy_outputs"] == 0
+        got = dev[in_key].cpu().numpy()
+    assert _normwise(got, ref[out_key]) <= 1e-4
