@@ -18,9 +18,13 @@ OPS = {"gemm": 0, "gemm_nt": 1, "gemm_relu": 2}
 MATH = {"tf32x3": 0, "tf32": 1, "simt": 2}
 
 
-def run(M, N, K, batch, op="gemm", math="tf32x3", presplit=True, shared=True, reps=20, epilogue=0):
+def run(M, N, K, batch, op="gemm", math="tf32x3", presplit=True, shared=True, reps=20, epilogue=0, fill=None):
     A = torch.randn(batch, M * K, device="cuda")
     B = torch.randn(N * K if shared else batch * N * K, device="cuda")
+    if fill is not None:  # operand values for data-dependent power experiments ("zeros", "ones")
+        v = {"zeros": 0.0, "ones": 1.0}[fill]
+        A.fill_(v)
+        B.fill_(v)
     C = torch.empty(batch, M * N, device="cuda")
     planes = None
     if presplit and shared:
