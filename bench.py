@@ -745,7 +745,9 @@ def run_ours(args, world, rank, local):
         ref32, ref64 = oracle_rows(args.layers, par["instances"])
         par.update(errors(out_main[idx], ref32, ref64))
         if alt is not None:
-            par["alt_normwise_vs_oracle"] = errors(alt_out[idx], ref32, ref64)["normwise_vs_oracle"]
+            ae = errors(alt_out[idx], ref32, ref64)
+            par["alt_normwise_vs_oracle"] = ae["normwise_vs_oracle"]
+            par["alt_normwise_vs_f64"] = ae["normwise_vs_f64"]
         if e2e_out is not None:
             par["e2e_bit_identical_all_instances"] = bool(np.array_equal(e2e_out, out_main))
             par["e2e_normwise_vs_oracle"] = errors(e2e_out[idx], ref32, ref64)["normwise_vs_oracle"]
@@ -793,6 +795,8 @@ def run_ours(args, world, rank, local):
             parity["e2e_normwise_vs_oracle"] = max(p["e2e_normwise_vs_oracle"] for p in checked)
         if alt is not None:
             alt["normwise_err_vs_cpu_oracle"] = max(p["alt_normwise_vs_oracle"] for p in checked)
+            alt["normwise_err_vs_f64"] = max(p["alt_normwise_vs_f64"] for p in checked)
+            alt["instances_checked"] = sum(len(p["instances"]) for p in checked)
         cpu = None
         if not args.no_cpu_baseline:
             v, threads, t = cpu_sample(args.layers, n_inst=64)
