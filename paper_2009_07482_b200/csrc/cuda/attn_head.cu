@@ -76,7 +76,7 @@ __device__ __forceinline__ void split16(const float (&x)[16], uint32_t (&hi)[16]
   for (int e = 0; e < 16; ++e) {
     const float h = tf32_rna(x[e]);
     hi[e] = __float_as_uint(h);
-    lo[e] = __float_as_uint(x[e] - h);
+    lo[e] = __float_as_uint(tf32_lo(x[e], h));
   }
 }
 
@@ -278,7 +278,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           const float x = __uint_as_float(hh < 2 ? r0[(hh & 1) * 16 + e] : r1[(hh & 1) * 16 + e]) * inv;
           const float h = tf32_rna(x);
           hi[e] = __float_as_uint(h);
-          lo[e] = __float_as_uint(x - h);
+          lo[e] = __float_as_uint(tf32_lo(x, h));
         }
         const uint32_t col = kTA + uint32_t(g * 64 + hh * 16);
         tmem_st16(lane_base + col, hi);
@@ -342,7 +342,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         const float4 x = lds128(base + kKhi + off);
         const float4 h = make_float4(tf32_rna(x.x), tf32_rna(x.y), tf32_rna(x.z), tf32_rna(x.w));
         sts128(base + kKhi + off, h);
-        sts128(base + kKlo + off, make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w));
+        sts128(base + kKlo + off, tf32_lo4(x, h));
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
@@ -359,7 +359,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         const float4 h = make_float4(tf32_rna(x.x), tf32_rna(x.y), tf32_rna(x.z), tf32_rna(x.w));
         const uint32_t dst = base + kVop + uint32_t(kb) * 8192u + sw128(n, kc);
         sts128(dst, h);
-        sts128(dst + 32768u, make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w));
+        sts128(dst + 32768u, tf32_lo4(x, h));
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();

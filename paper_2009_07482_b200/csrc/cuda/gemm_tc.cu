@@ -219,7 +219,7 @@ __device__ __forceinline__ void split_a_to_tmem(uint32_t sa, uint32_t ta, int ro
       for (int e = 0; e < 4; ++e) {
         const float hv = tf32_rna(xs[e]);
         hi[4 * c + e] = __float_as_uint(hv);
-        lo[4 * c + e] = __float_as_uint(xs[e] - hv);
+        lo[4 * c + e] = __float_as_uint(tf32_lo(xs[e], hv));
       }
     }
     tmem_st16(ta + uint32_t(16 * hh), hi);
@@ -1067,7 +1067,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int e = 0; e < 4; ++e) {
               const float hv = tf32_rna(xs[e]);
               hi[4 * c + e] = __float_as_uint(hv);
-              lo[4 * c + e] = __float_as_uint(xs[e] - hv);
+              lo[4 * c + e] = __float_as_uint(tf32_lo(xs[e], hv));
             }
           }
           // the slot goes back to TMA only once this warp's loads have returned
@@ -1160,7 +1160,7 @@ __global__ void split_weights_kernel(const float* __restrict__ B, float* __restr
       float x = tile[i][threadIdx.x];
       float h = tf32_rna(x);
       planes[int64_t(n) * K + k] = h;
-      planes[plane + int64_t(n) * K + k] = x - h;
+      planes[plane + int64_t(n) * K + k] = tf32_lo(x, h);
     }
   }
 }

@@ -223,7 +223,7 @@ __device__ __forceinline__ void split16(const uint32_t* r, uint32_t (&hi)[16], u
     const float x = __uint_as_float(r[e]);
     const float h = tf32_rna(x);
     hi[e] = __float_as_uint(h);
-    lo[e] = __float_as_uint(x - h);
+    lo[e] = __float_as_uint(tf32_lo(x, h));
   }
 }
 
@@ -628,7 +628,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const float4 h = make_float4(tf32_rna(x.x), tf32_rna(x.y), tf32_rna(x.z), tf32_rna(x.w));
           const uint32_t dst = base + kKop + uint32_t(g) * 16384u + sw128(row, c);
           sts128(dst, h);
-          if constexpr (kTerms > 1) sts128(dst + 32768u, make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w));
+          if constexpr (kTerms > 1) sts128(dst + 32768u, tf32_lo4(x, h));
         }
         if (warp == 8 && lane == 0) TL(lt, 25);
         // V row (key = row: k-block q, key lane), d in [32g, 32g+32) -> Vᵀ K-major SW128 [64 d][32 keys]
@@ -639,7 +639,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const float h = tf32_rna(x);
           const uint32_t dst = base + kVop + uint32_t(q) * 8192u + sw128(32 * g + j, lane >> 2) + uint32_t(lane & 3) * 4u;
           sts32(dst, h);
-          if constexpr (kTerms > 1) sts32(dst + 32768u, x - h);
+          if constexpr (kTerms > 1) sts32(dst + 32768u, tf32_lo(x, h));
         }
         if (warp == 8 && lane == 0) TL(lt, 26);
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");

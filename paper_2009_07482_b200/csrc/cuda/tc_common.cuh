@@ -114,6 +114,16 @@ __device__ __forceinline__ void mma_commit(uint32_t bar) {
 __device__ __forceinline__ float tf32_rna(float x) {
   return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
 }
+// lo term of a tf32 hi/lo split, x - hi (exact in fp32). The tensor core reads only its
+// top 11 significant bits (truncating, profiles/tf32_trunc_probe.cu); HS_LO_RNA rounds it
+// to tf32 here instead, so the 13 low bits the MMA ignores are zero rather than random.
+#ifndef HS_LO_RNA
+#define HS_LO_RNA 0
+#endif
+__device__ __forceinline__ float tf32_lo(float x, float h) { return HS_LO_RNA ? tf32_rna(x - h) : x - h; }
+__device__ __forceinline__ float4 tf32_lo4(float4 x, float4 h) {
+  return make_float4(tf32_lo(x.x, h.x), tf32_lo(x.y, h.y), tf32_lo(x.z, h.z), tf32_lo(x.w, h.w));
+}
 __device__ __forceinline__ float4 lds128(uint32_t addr) {
   float4 v;
   asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
@@ -140,7 +150,7 @@ template <int kTerms>
 __device__ __forceinline__ void split_store(uint32_t hi, uint32_t lo, uint32_t off, float4 x) {
   float4 h = make_float4(tf32_rna(x.x), tf32_rna(x.y), tf32_rna(x.z), tf32_rna(x.w));
   sts128(hi + off, h);
-  if constexpr (kTerms > 1) sts128(lo + off, make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w));
+  if constexpr (kTerms > 1) sts128(lo + off, tf32_lo4(x, h));
 }
 
 // D[tmem] (+)= A[tmem] · B[smem]; A is K-major in TMEM (lane = row, column = k).
