@@ -1175,6 +1175,9 @@ cudaError_t launch(const GemmArgs& a, cudaStream_t s) {
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [&] {
     attr_err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal);
+    // cluster split-K may use 16 CTAs per cluster (above the portable 8)
+    if (attr_err == cudaSuccess && HS_CSPLIT_MAX > 8)
+      attr_err = cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   });
   if (attr_err != cudaSuccess) return attr_err;
   const uint64_t M = uint64_t(a.M), N = uint64_t(a.N), K = uint64_t(a.K);
@@ -1235,7 +1238,7 @@ cudaError_t launch(const GemmArgs& a, cudaStream_t s) {
         int S = slots / base;
         if (S > nk / HS_SPLIT_MIN_KB) S = nk / HS_SPLIT_MIN_KB;
         if (S > HS_CSPLIT_MAX) S = HS_CSPLIT_MAX;
-        S = S >= 8 ? 8 : S >= 4 ? 4 : S >= 2 ? 2 : 1;  // rows of the reduction divide evenly
+        S = S >= 16 ? 16 : S >= 8 ? 8 : S >= 4 ? 4 : S >= 2 ? 2 : 1;  // rows of the reduction divide evenly
         if (S >= 2) split = csplit = S;
       }
     }
