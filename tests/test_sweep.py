@@ -51,3 +51,19 @@ def test_all_heads_on_a_slow_cpu_is_worse():
     assert by[(0, 1, 4)] > max(by[(3, 0, 0)], by[(3, 1, 1)])
     csv = sweep.to_csv(t).splitlines()
     assert csv[0].startswith("heads,beta,q_gpu") and len(csv) == 1 + len(t["rows"])
+
+
+def test_acceptance_5_fine_grained_head_beats_coarse():
+    """SPEC acceptance criterion 5 (Figs. 4-5): one whole head on the GPU with the shipped
+    overlap profile, makespan(q_gpu = 3) <= 0.95 x makespan(q_gpu = 1)."""
+    fine = sweep.simulate(1, 256, (3, 0, 0), GPU, CPU_SLOW, SHARE)["makespan_ms"]
+    coarse = sweep.simulate(1, 256, (1, 0, 0), GPU, CPU_SLOW, SHARE)["makespan_ms"]
+    assert fine <= 0.95 * coarse
+
+
+@pytest.mark.parametrize("heads", [4, 8])
+def test_acceptance_6_expt1_speedup(heads):
+    """SPEC acceptance criterion 6 (Expt. 1): over q_gpu in [1, 5] with h_cpu = 0 the best
+    fine-grained configuration is >= 1.10x faster than mc = (1, 0, 0)."""
+    t = sweep.sweep_clustering(heads, 256, GPU, CPU_SLOW, SHARE, q_gpu=range(1, 6), h_cpu=[0])
+    assert t["best_vs_default"] >= 1.10
