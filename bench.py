@@ -850,6 +850,10 @@ def run_ours(args, world, rank, local):
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clocks,
+            # the step runs under sw_power_cap: throughput per watt of board power
+            "energy": ({"power_w": clocks["power_w"], "dags_per_joule": value / clocks["power_w"],
+                        "note": "median nvidia-smi power.draw over the timed region (a moving average)"}
+                       if clocks and clocks.get("power_w") else None),
             "device_bytes": plan["device_bytes"],
         }
     return line
