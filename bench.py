@@ -851,8 +851,9 @@ def run_ours(args, world, rank, local):
             "gpu_launches": launches,
             "clocks": clocks,
             # the step runs under sw_power_cap: throughput per watt of board power
-            "energy": ({"power_w": clocks["power_w"], "dags_per_joule": value / clocks["power_w"],
-                        "note": "median nvidia-smi power.draw over the timed region (a moving average)"}
+            "energy": ({"power_w": clocks["power_w"], "dags_per_joule": value / (clocks["power_w"] * world),
+                        "note": "rank 0's median nvidia-smi power.draw over the timed region (a moving "
+                                "average); DAGs per joule per GPU"}
                        if clocks and clocks.get("power_w") else None),
             "device_bytes": plan["device_bytes"],
         }
