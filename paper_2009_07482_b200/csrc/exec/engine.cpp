@@ -1447,6 +1447,7 @@ void Engine::run(int64_t first, int64_t n, int64_t* elapsed_ns) {
     } else {
       for (int64_t b = 0; b < nb; ++b) chunks.emplace_back(b * B, std::min(B, n - b * B), false);
     }
+    const int64_t n_chunks = int64_t(chunks.size());
     // A run that is one chunk (the latency configs: one DAG, or one batch of them)
     // replays a graph that also holds its copies: one host submission per run instead
     // of the copy commands, their fork/join events and the plan launch. Bindings are
@@ -1504,7 +1505,7 @@ void Engine::run(int64_t first, int64_t n, int64_t* elapsed_ns) {
       }
       copies(sl, f, cnt, false);
     }
-    batches_run_ += int64_t(chunks.size()) - nb;  // counted below as nb
+    batches_run_ += n_chunks - nb;  // counted below as nb
   } else {
     for (auto& [k, s] : s0.streams) hs_ok(hs_stream_wait(s, s0.t_start), "start wait");
     for (int64_t b = 0; b < nb; ++b) {
