@@ -82,6 +82,7 @@ using namespace tc;
 #ifndef HS_CSPLIT_MAX  // cluster split-K: CTAs per cluster at most (0/1: red.add split-K only)
 #define HS_CSPLIT_MAX 8
 #endif
+constexpr int kCsplitCap = HS_CSPLIT_MAX > 8 ? 16 : 8;  // partial registers per reducing thread
 #ifndef HS_SPLIT_MIN_KB  // K-blocks per split at least
 #define HS_SPLIT_MIN_KB 1
 #endif
@@ -148,7 +149,9 @@ struct Cfg {
   // cluster split-K: the partial tile (128 rows, BN + 4 floats apart) fits the staging
   // and operand rings (both idle once the tile's last MMA has completed)
   static constexpr int kRedLd = BN + 4;
-  static constexpr bool kCsplitOk = kNS * kStaging + kNO * kOperand >= BM * kRedLd * 4;
+  static constexpr int kRedTile = BM * kRedLd * 4;  // one CTA's partial tile (bytes)
+  // its own partial + the (S - 1) row slices the peers push to it (at most 15/16 of a tile)
+  static constexpr bool kCsplitOk = kNS * kStaging + kNO * kOperand >= kRedTile + kRedTile / 16 * 15;
   static_assert(kNS >= 2 && kNO >= 2, "pipeline too shallow");
   static_assert(kTotal * kCtasPerSm <= 227 * 1024, "shared memory budget exceeded");
 };
@@ -321,6 +324,7 @@ __global__ void __launch_bounds__(kThreads, kSmall ? 2 : 1)
   auto acc_full = [&](int a) { return bars + 8u * uint32_t(2 * NS + 2 * NO + a); };
   auto acc_empty = [&](int a) { return bars + 8u * uint32_t(2 * NS + 2 * NO + 2 + a); };
   const uint32_t tmem_slot = bars + 8u * uint32_t(2 * NS + 2 * NO + 4);
+  const uint32_t red_full = bars + 8u * uint32_t(2 * NS + 2 * NO + 5);  // cluster split-K: peers' slices landed
   const uint32_t scratch = bars + 1024u;  // epilogue transpose tiles, one per epilogue warp
   const uint32_t* tmem_slot_ptr = reinterpret_cast<const uint32_t*>(smem_raw + (tmem_slot - smem_u32(smem_raw)));
 
@@ -349,6 +353,7 @@ __global__ void __launch_bounds__(kThreads, kSmall ? 2 : 1)
       mbar_init(acc_full(a), 1);
       mbar_init(acc_empty(a), kEpiWarps);
     }
+    mbar_init(red_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
@@ -361,6 +366,7 @@ __global__ void __launch_bounds__(kThreads, kSmall ? 2 : 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+
   if (threadIdx.x == 0) GTL(1);
   pdl_launch_dependents();  // PDL (launch.cuh): the prologue above overlaps the previous kernel
   pdl_wait();
@@ -610,16 +616,44 @@ __global__ void __launch_bounds__(kThreads, kSmall ? 2 : 1)
   }
   if (threadIdx.x == 0) GTL(9);
   if (csplit) {
-    // every split's partial tile is in its CTA's smem: CTA r reduces rows
-    // [r * 128 / S, (r + 1) * 128 / S) over splits 0..S-1 (fixed order), applies the
-    // ReLU and stores them, consecutive threads on consecutive columns (coalesced).
-    // The cluster barrier is .aligned: every warp must arrive converged (the producer
-    // and MMA warps ran their loops in lane 0 only), hence the CTA barrier first.
+    // Every split's partial tile is in its CTA's smem ([128][BN + 4] at `staging`). CTA r
+    // owns rows [r * 128 / S, (r + 1) * 128 / S): once every CTA of the cluster has its
+    // partial written (cluster barrier; the receive areas reuse the rings the mainloop
+    // has then finished with), each CTA pushes the row slice it holds for every peer into
+    // that peer's receive area with one bulk DSMEM copy each (cp.async.bulk shared::cta ->
+    // shared::cluster, completing on the peer's red_full), then sums its own rows over the
+    // S slices in rank order (deterministic), applies the ReLU and stores them,
+    // consecutive threads on consecutive columns (coalesced). A second cluster barrier
+    // phase (arrived once a CTA's incoming slices have landed, waited before exit) keeps
+    // every source slice alive until its copy is done. The barrier is .aligned: warps whose
+    // roles looped in one lane reconverge first.
+    const int S = p.csplit, rows = BM / S, rank = int(cluster_ctarank());
+    const uint32_t slice = uint32_t(rows * kRedLd * 4);
+    const uint32_t recv = staging + uint32_t(L::kRedTile);  // S - 1 slots, sender order
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // partials visible to the bulk copies
     __syncthreads();
     cluster_sync_all();
+    if (threadIdx.x == 0) {
+      GTL(11);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(red_full),
+                   "r"(uint32_t(S - 1) * slice)
+                   : "memory");
+      for (int r = 0; r < S; ++r) {
+        if (r == rank) continue;
+        const uint32_t dst = recv + uint32_t(rank < r ? rank : rank - 1) * slice;
+        asm volatile(
+            "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                mapa_rank(dst, uint32_t(r))),
+            "r"(staging + uint32_t(r) * slice), "r"(slice), "r"(mapa_rank(red_full, uint32_t(r)))
+            : "memory");
+      }
+    }
+    mbar_wait(red_full, 0);
+    if (threadIdx.x == 0) GTL(12);
+    __syncwarp();
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");  // phase 2: my slices landed
     int m0, inst, n0;
     decode(t0, m0, inst, n0);
-    const int S = p.csplit, rows = BM / S, rank = int(cluster_ctarank());
     // destination of column c: the single C, or member c / Nm of a grouped launch
     const int64_t ld = p.ldc ? p.ldc : (p.n_out ? p.Nm : p.N);
     auto dst_of = [&](int grow, int gcol) {
@@ -628,18 +662,26 @@ __global__ void __launch_bounds__(kThreads, kSmall ? 2 : 1)
       return p.Cs[m] + int64_t(inst) * p.sCs[m] + int64_t(grow) * ld + (gcol - m * p.Nm);
     };
     for (int id = int(threadIdx.x); id < rows * (BN / 4); id += kThreads) {
-      const int rr = rank * rows + id / (BN / 4), c4 = (id % (BN / 4)) * 4;
-      const uint32_t off = staging + uint32_t(rr * kRedLd + c4) * 4u;
-      float4 acc = ld_shared_cluster_v4(mapa_rank(off, 0));
-      for (int sp = 1; sp < S; ++sp) {
-        const float4 x = ld_shared_cluster_v4(mapa_rank(off, uint32_t(sp)));
-        acc.x += x.x;
-        acc.y += x.y;
-        acc.z += x.z;
-        acc.w += x.w;
+      const int lr = id / (BN / 4), c4 = (id % (BN / 4)) * 4;
+      const uint32_t in_slice = uint32_t(lr * kRedLd + c4) * 4u;
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int sp = 0; sp < kCsplitCap; ++sp) {
+        if (sp >= S) break;
+        const uint32_t a = sp == rank ? staging + uint32_t(rank) * slice + in_slice
+                                      : recv + uint32_t(sp < rank ? sp : sp - 1) * slice + in_slice;
+        const float4 x = lds128(a);
+        if (sp == 0) {
+          acc = x;
+        } else {
+          acc.x += x.x;
+          acc.y += x.y;
+          acc.z += x.z;
+          acc.w += x.w;
+        }
       }
       if (p.relu) acc = make_float4(fmaxf(acc.x, 0.f), fmaxf(acc.y, 0.f), fmaxf(acc.z, 0.f), fmaxf(acc.w, 0.f));
-      const int grow = m0 + rr, gcol = n0 + c4;
+      const int grow = m0 + rank * rows + lr, gcol = n0 + c4;
       if (grow >= p.M || gcol >= p.N) continue;
       float* dst = dst_of(grow, gcol);
       if ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0 && gcol + 4 <= p.N && (p.n_out == 0 || p.Nm % 4 == 0)) {
@@ -649,8 +691,10 @@ __global__ void __launch_bounds__(kThreads, kSmall ? 2 : 1)
         for (int i = 0; i < 4 && gcol + i < p.N; ++i) dst[i] = e[i];
       }
     }
-    __syncthreads();
-    cluster_sync_all();  // no CTA leaves while its partial is still being read
+    if (threadIdx.x == 0) GTL(13);
+    __syncwarp();
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");  // every copy everywhere done
+    if (threadIdx.x == 0) GTL(14);
   }
   tc_fence_before();
   __syncthreads();

@@ -19,7 +19,8 @@ A = torch.randn(1, M * K, device="cuda")
 B = torch.randn(1, K * N, device="cuda")
 C = torch.empty(1, M * N, device="cuda")
 names = ["entry", "prologue", "pdl_wait", "tma0", "conv_st_full0", "conv_op_full0", "mma_commit0", "epi_acc_full",
-         "epi_done", "pre_exit_sync", "dealloc"]
+         "epi_done", "pre_exit_sync", "dealloc", "csplit_cta_sync", "csplit_cluster_sync", "csplit_reduced",
+         "csplit_cluster_sync2"]
 for rep in range(3):
     assert L.hs_debug_gemm_timeline(None, 1) == 0, "library built without HS_DBG_GEMM_TL"
     launch("gemm", [A, B], C, [M, N, K])
