@@ -268,7 +268,8 @@ def run_reference(args, world, rank):
     sample = f"12 instances of the {layers}-layer encoder DAG per step (CPU oracle port: clustering + fp32 kernels)"
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1000.0 / v, "higher_is_better": True, "scaling": "strong",
+        "warmup": args.warmup, "ms_per_step": 12 * 1000.0 / v,  # one step = the 12-instance sample
+        "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"C5 {layers}-layer encoder DAG stream, {args.instances} instances (CPU sample)",
                    "instances": args.instances, "layers": layers, "kernels": 69 * layers},
